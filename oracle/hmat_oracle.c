@@ -1,0 +1,281 @@
+/*
+ * hmat_oracle.c -- the CPU ORACLE for the weak-admissibility H-matvec y = Hx.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code with the CUDA path (paper_2008_12441_b200/csrc); its only
+ * shared dependency is the seeded input generator gen/hgen.h, used by
+ * oracle_rows_generated() to produce factor entries on demand.
+ *
+ * Plain, slow, obviously correct fp64 loops, written from the paper:
+ *   - structure: Def 2.4 (\label{def:hmat}) on the 2^d-ary
+ *     domain tree of an ideal domain under weak
+ *     admissibility, BASELINE variant (DESIGN.md reading
+ *     R1): every pair of distinct siblings at levels 1..L is a rank-r block
+ *     U_ts V_ts^T, only leaf-diagonal blocks are dense;
+ *   - matvec: y = 0, then for every block y_t += D x_s or y_t += U (V^T x_s),
+ *     eq:hmat-vec-add.
+ * Built with gcc -O2 -ffp-contract=off (no contraction; R11).
+ *
+ * Canonical panel layout (the C-ABI's input format):
+ *   c = 2^d, N = b c^L, m_l = N / c^l, W = (c-1) r, all row-major, Morton rows.
+ *   U_l (N x W): row i, columns [q r, (q+1) r) = row i - t m_l of U_{t, s_q},
+ *                t = i / m_l, s_q = q-th sibling of t (ascending, skip self).
+ *   V_l (N x W): row j, columns [q r, (q+1) r) = row j - s m_l of V_{t_q, s},
+ *                s = j / m_l, t_q = q-th sibling of s.
+ *   D   (N x b): row i = row i - k b of D_k, k = i / b.
+ *   x, y: N x nrhs column-major, leading dimension N.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include "../gen/hgen.h"
+
+/* ---- tree / sibling indexing (R6) ---------- */
+
+/* q-th sibling of node t (siblings of t = the other children of t's parent,
+ * in ascending child order, skipping t itself). */
+int64_t oracle_sibling(int c, int64_t t, int q) {
+  int64_t parent = t / c;
+  int me = (int)(t % c);
+  int child = q < me ? q : q + 1;
+  return parent * c + child;
+}
+
+/* slot of sibling s in t's sibling list: the q with oracle_sibling(t,q) = s. */
+int oracle_slot(int c, int64_t t, int64_t s) {
+  for (int q = 0; q < c - 1; ++q)
+    if (oracle_sibling(c, t, q) == s) return q;
+  return -1;
+}
+
+static int64_t ipow(int64_t a, int e) {
+  int64_t p = 1;
+  while (e-- > 0) p *= a;
+  return p;
+}
+
+/* ---- block enumeration by recursion on Def 2.4 -------------------------
+ * Visits the H-matrix structure of K on Omega x Omega: starting from the root
+ * pair (both domains are the root, level 0), each child pair (t, s) at level
+ * l+1 of a hierarchical pair is
+ *   - admissible (t != s, disjoint domains)  -> low-rank block (kind 1),
+ *   - else (t == s) if l+1 == L (leaf)       -> dense block     (kind 0),
+ *   - else                                   -> hierarchical, recurse.
+ * The callback receives (kind, level, t, s). */
+typedef void (*block_fn)(void* ctx, int kind, int level, int64_t t, int64_t s);
+
+static void visit(int c, int L, int level, int64_t node, block_fn fn, void* ctx) {
+  /* node is a diagonal (hierarchical) pair (node, node) at `level` */
+  for (int a = 0; a < c; ++a) {
+    for (int bb = 0; bb < c; ++bb) {
+      int64_t t = node * c + a, s = node * c + bb;
+      if (t != s) fn(ctx, 1, level + 1, t, s);
+      else if (level + 1 == L) fn(ctx, 0, level + 1, t, s);
+      else visit(c, L, level + 1, t, fn, ctx);
+    }
+  }
+}
+
+static void visit_root(int c, int L, block_fn fn, void* ctx) {
+  if (L == 0) fn(ctx, 0, 0, 0, 0); /* the root is a leaf: one dense block */
+  else visit(c, L, 0, 0, fn, ctx);
+}
+
+typedef struct { int64_t lowrank, dense, lowrank_level1; } census_t;
+
+static void census_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  census_t* cs = (census_t*)ctx;
+  (void)t; (void)s;
+  if (kind == 1) { cs->lowrank++; if (level == 1) cs->lowrank_level1++; }
+  else cs->dense++;
+}
+
+/* Counts blocks by walking the structure (not by formula). */
+void oracle_block_census(int d, int L, int64_t* n_lowrank, int64_t* n_dense, int64_t* n_lowrank_level1) {
+  census_t cs = {0, 0, 0};
+  visit_root(1 << d, L, census_cb, &cs);
+  *n_lowrank = cs.lowrank; *n_dense = cs.dense; *n_lowrank_level1 = cs.lowrank_level1;
+}
+
+typedef struct { int c, L, b; int64_t N; int32_t* count; } cover_t;
+
+static void cover_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  cover_t* cv = (cover_t*)ctx;
+  (void)kind;
+  int64_t m = cv->N / ipow(cv->c, level);
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < m; ++j) cv->count[(t * m + i) * cv->N + (s * m + j)] += 1;
+}
+
+/* count[i*N + j] = number of blocks covering entry (i, j) (must be 1). */
+void oracle_cover_count(int d, int L, int b, int32_t* count) {
+  cover_t cv;
+  cv.c = 1 << d; cv.L = L; cv.b = b; cv.N = (int64_t)b * ipow(cv.c, L); cv.count = count;
+  memset(count, 0, sizeof(int32_t) * (size_t)(cv.N * cv.N));
+  visit_root(cv.c, L, cover_cb, &cv);
+}
+
+/* ---- the matvec, eq:hmat-vec-add ----------------------------------------
+ * y = 0; for every dense block D_k: y_k += D_k x_k; for
+ * every low-rank block (t, s) at level l: z = V_ts^T x_s, y_t += U_ts z.
+ * level_mask bit (l-1) selects level l; dense selects the leaf blocks (test
+ * hook for the per-level decomposition y = y_D + sum_l y_l). */
+void oracle_matvec_masked(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                          const double* D, const double* x, double* y, int nrhs,
+                          uint64_t level_mask, int dense) {
+  const int c = 1 << d;
+  const int64_t N = (int64_t)b * ipow(c, L);
+  const int W = (c - 1) * r;
+  double* z = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  for (int k = 0; k < nrhs; ++k) {
+    const double* xk = x + (int64_t)k * N;
+    double* yk = y + (int64_t)k * N;
+    for (int64_t i = 0; i < N; ++i) yk[i] = 0.0;
+    if (dense) {
+      for (int64_t leaf = 0; leaf < N / b; ++leaf)
+        for (int i = 0; i < b; ++i)
+          for (int j = 0; j < b; ++j)
+            yk[leaf * b + i] += D[(leaf * b + i) * b + j] * xk[leaf * b + j];
+    }
+    for (int l = 1; l <= L; ++l) {
+      if (!((level_mask >> (l - 1)) & 1ull)) continue;
+      const int64_t m = N / ipow(c, l);
+      const double* Ul = U[l - 1];
+      const double* Vl = V[l - 1];
+      for (int64_t t = 0; t < ipow(c, l); ++t) {
+        for (int q = 0; q < c - 1; ++q) {
+          int64_t s = oracle_sibling(c, t, q); /* block (t, s) */
+          int qs = oracle_slot(c, s, t);        /* t's slot in s's list: V_ts columns */
+          for (int a = 0; a < r; ++a) z[a] = 0.0;
+          for (int64_t j = 0; j < m; ++j)       /* z = V_ts^T x_s */
+            for (int a = 0; a < r; ++a)
+              z[a] += Vl[(s * m + j) * W + qs * r + a] * xk[s * m + j];
+          for (int64_t i = 0; i < m; ++i)       /* y_t += U_ts z */
+            for (int a = 0; a < r; ++a)
+              yk[t * m + i] += Ul[(t * m + i) * W + q * r + a] * z[a];
+        }
+      }
+    }
+  }
+  free(z);
+}
+
+void oracle_matvec(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                   const double* D, const double* x, double* y, int nrhs) {
+  oracle_matvec_masked(d, L, b, r, U, V, D, x, y, nrhs, ~0ull, 1);
+}
+
+/* ---- dense assembly + brute-force matvec (small N) --------------------- */
+
+typedef struct {
+  int c, L, b, r, W; int64_t N;
+  const double* const* U; const double* const* V; const double* D; double* A;
+} assemble_t;
+
+static void assemble_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  assemble_t* as = (assemble_t*)ctx;
+  const int64_t N = as->N;
+  if (kind == 0) { /* dense leaf block D_t, t == s */
+    for (int i = 0; i < as->b; ++i)
+      for (int j = 0; j < as->b; ++j)
+        as->A[(t * as->b + i) * N + (s * as->b + j)] = as->D[(t * as->b + i) * as->b + j];
+    return;
+  }
+  const int64_t m = N / ipow(as->c, level);
+  const int q = oracle_slot(as->c, t, s), qs = oracle_slot(as->c, s, t);
+  const double* Ul = as->U[level - 1];
+  const double* Vl = as->V[level - 1];
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      double acc = 0.0; /* (U_ts V_ts^T)[i, j] */
+      for (int a = 0; a < as->r; ++a)
+        acc += Ul[(t * m + i) * as->W + q * as->r + a] * Vl[(s * m + j) * as->W + qs * as->r + a];
+      as->A[(t * m + i) * N + (s * m + j)] = acc;
+    }
+}
+
+/* A (N x N row-major) = the matrix the blocks define. */
+void oracle_assemble(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                     const double* D, double* A) {
+  assemble_t as;
+  as.c = 1 << d; as.L = L; as.b = b; as.r = r; as.W = (as.c - 1) * r;
+  as.N = (int64_t)b * ipow(as.c, L);
+  as.U = U; as.V = V; as.D = D; as.A = A;
+  memset(A, 0, sizeof(double) * (size_t)(as.N * as.N));
+  visit_root(as.c, L, assemble_cb, &as);
+}
+
+/* y = A x by the definition of a matrix-vector product (brute force). */
+void oracle_dense_matvec(int64_t N, const double* A, const double* x, double* y, int nrhs) {
+  for (int k = 0; k < nrhs; ++k)
+    for (int64_t i = 0; i < N; ++i) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < N; ++j) acc += A[i * N + j] * x[(int64_t)k * N + j];
+      y[(int64_t)k * N + i] = acc;
+    }
+}
+
+/* ---- sampled rows at any size, factors generated on demand ---------------
+ * y[rows[n], :] for the H-matrix whose panels are the seeded synthetic inputs
+ * (gen/hgen.h), computed row by row from eq:hmat-vec-add:
+ *   y_i = sum_j D_k[i, j] x_{k b + j}
+ *       + sum_l sum_q U_{t,s_q}[i, :] (V_{t,s_q}^T x_{s_q}),  t = i / m_l.
+ * Only the factor entries these rows touch are generated.  The z vectors of
+ * node t at level l are reused when consecutive sample rows share t; the sum
+ * over j in V^T x may be split across OpenMP threads. */
+void oracle_rows_generated(int d, int L, int b, int r, uint64_t seed, const double* x, int nrhs,
+                           int64_t nrows, const int64_t* rows, double* yrows) {
+  const int c = 1 << d;
+  const int64_t N = (int64_t)b * ipow(c, L);
+  const int W = (c - 1) * r;
+  const uint64_t stD = hgen_stream(seed, HGEN_TAG_D, 0, 0);
+  /* zc[l][(q * nrhs + k) * r + a] = (V_{t,s_q}^T x_{s_q, k})[a] for t = last_t[l] */
+  double* zc = (double*)malloc(sizeof(double) * (size_t)(L + 1) * (size_t)W * (size_t)nrhs + 8);
+  int64_t* last_t = (int64_t*)malloc(sizeof(int64_t) * (size_t)(L + 1));
+  for (int l = 0; l <= L; ++l) last_t[l] = -1;
+  for (int64_t n = 0; n < nrows; ++n) {
+    const int64_t i = rows[n];
+    const int64_t leaf = i / b;
+    for (int k = 0; k < nrhs; ++k) {
+      double acc = 0.0;
+      for (int j = 0; j < b; ++j)
+        acc += hgen_normal(stD, (uint64_t)(i * b + j)) * 0.125 * x[(int64_t)k * N + leaf * b + j];
+      yrows[(int64_t)k * nrows + n] = acc;
+    }
+    for (int l = 1; l <= L; ++l) {
+      const int64_t m = N / ipow(c, l);
+      const double scale = 1.0 / sqrt((double)m);
+      const uint64_t stU = hgen_stream(seed, HGEN_TAG_U, (uint64_t)l, 0);
+      const uint64_t stV = hgen_stream(seed, HGEN_TAG_V, (uint64_t)l, 0);
+      const int64_t t = i / m;
+      double* z = zc + (size_t)l * (size_t)W * (size_t)nrhs;
+      if (last_t[l] != t) {
+        for (int q = 0; q < c - 1; ++q) {
+          const int64_t s = oracle_sibling(c, t, q);
+          const int qs = oracle_slot(c, s, t);
+          for (int k = 0; k < nrhs; ++k)
+            for (int a = 0; a < r; ++a) {
+              double za = 0.0;
+#pragma omp parallel for reduction(+ : za) schedule(static)
+              for (int64_t j = 0; j < m; ++j)
+                za += hgen_normal(stV, (uint64_t)((s * m + j) * W + qs * r + a)) * scale *
+                      x[(int64_t)k * N + s * m + j];
+              z[(q * nrhs + k) * r + a] = za;
+            }
+        }
+        last_t[l] = t;
+      }
+      for (int q = 0; q < c - 1; ++q)
+        for (int k = 0; k < nrhs; ++k) {
+          double acc = 0.0;
+          for (int a = 0; a < r; ++a)
+            acc += hgen_normal(stU, (uint64_t)(i * W + q * r + a)) * scale * z[(q * nrhs + k) * r + a];
+          yrows[(int64_t)k * nrows + n] += acc;
+        }
+    }
+  }
+  free(zc);
+  free(last_t);
+}

@@ -1,0 +1,141 @@
+"""CPU oracle for y = Hx (weak admissibility) -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module.  It wraps oracle/liboracle.so (plain C,
+fp64, -ffp-contract=off), which shares no code with the CUDA path.  See the
+header of oracle/hmat_oracle.c for the paper passages each function follows.
+
+Every function is pinned by tests/test_oracle_pins.py (brute force, closed
+forms, special cases, the paper's block count); see DESIGN.md §5.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run `make` (or __graft_entry__.build())")
+        lib = ctypes.CDLL(path)
+        lib.oracle_sibling.restype = ctypes.c_int64
+        lib.oracle_sibling.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int]
+        lib.oracle_slot.restype = ctypes.c_int
+        lib.oracle_slot.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64]
+        lib.oracle_block_census.restype = None
+        lib.oracle_block_census.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int64)] * 3
+        lib.oracle_cover_count.restype = None
+        lib.oracle_cover_count.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        pp = ctypes.POINTER(_dp)
+        lib.oracle_matvec_masked.restype = None
+        lib.oracle_matvec_masked.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p,
+                                                                 ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64,
+                                                                 ctypes.c_int]
+        lib.oracle_assemble.restype = None
+        lib.oracle_assemble.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_dense_matvec.restype = None
+        lib.oracle_dense_matvec.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_int]
+        lib.oracle_rows_generated.restype = None
+        lib.oracle_rows_generated.argtypes = [ctypes.c_int] * 4 + [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int,
+                                                                  ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        _lib = lib
+    return _lib
+
+
+def _c(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _panel_ptrs(panels):
+    arrs = [_c(p) for p in panels]
+    ptrs = (_dp * max(1, len(arrs)))(*[a.ctypes.data_as(_dp) for a in arrs])
+    return arrs, ptrs
+
+
+def _colmajor(x: np.ndarray) -> np.ndarray:
+    """x as an (N, nrhs) Fortran-order float64 array (column-major, ld = N)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    return np.asfortranarray(x)
+
+
+def sibling(c: int, t: int, q: int) -> int:
+    return _load().oracle_sibling(c, t, q)
+
+
+def slot(c: int, t: int, s: int) -> int:
+    return _load().oracle_slot(c, t, s)
+
+
+def block_census(d: int, L: int):
+    """(#low-rank blocks, #dense blocks, #low-rank blocks at level 1), counted by
+    walking Def 2.4's recursion."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _load().oracle_block_census(d, L, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+    return a.value, b.value, c.value
+
+
+def cover_count(d: int, L: int, b: int) -> np.ndarray:
+    N = b * (1 << d) ** L
+    out = np.zeros((N, N), dtype=np.int32)
+    _load().oracle_cover_count(d, L, b, out.ctypes.data)
+    return out
+
+
+def matvec(d: int, L: int, b: int, r: int, U, V, D, x, level_mask: int = (1 << 64) - 1,
+           dense: bool = True) -> np.ndarray:
+    """y = H x by the block loop of eq:hmat-vec-add.  x: (N,) or (N, nrhs)."""
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    y = np.zeros((N, nrhs), dtype=np.float64, order="F")
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dc = _c(D)
+    _load().oracle_matvec_masked(d, L, b, r, up, vp, Dc.ctypes.data, xc.ctypes.data, y.ctypes.data, nrhs,
+                                 level_mask & ((1 << 64) - 1), int(dense))
+    return y[:, 0] if np.ndim(x) == 1 else y
+
+
+def assemble(d: int, L: int, b: int, r: int, U, V, D) -> np.ndarray:
+    N = b * (1 << d) ** L
+    A = np.zeros((N, N), dtype=np.float64)
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dc = _c(D)
+    _load().oracle_assemble(d, L, b, r, up, vp, Dc.ctypes.data, A.ctypes.data)
+    return A
+
+
+def dense_matvec(A: np.ndarray, x) -> np.ndarray:
+    """y = A x by the definition (plain double loop in C)."""
+    Ac = _c(A)
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    y = np.zeros((N, nrhs), dtype=np.float64, order="F")
+    _load().oracle_dense_matvec(N, Ac.ctypes.data, xc.ctypes.data, y.ctypes.data, nrhs)
+    return y[:, 0] if np.ndim(x) == 1 else y
+
+
+def rows_generated(cfg, x, rows) -> np.ndarray:
+    """y[rows, :] for the seeded synthetic H-matrix of `cfg` (gen/hgen.h), factor
+    entries generated on demand; x: (N,) or (N, nrhs) host array."""
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    assert N == cfg.N
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((len(rows), nrhs), dtype=np.float64, order="F")
+    _load().oracle_rows_generated(cfg.d, cfg.L, cfg.b, cfg.r, cfg.seed, xc.ctypes.data, nrhs, len(rows),
+                                  rows.ctypes.data, out.ctypes.data)
+    return out[:, 0] if np.ndim(x) == 1 else out
