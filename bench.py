@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the weak-admissibility H-matvec y = Hx (arXiv 2008.12441) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One step = one whole matvec (project + on-chip reduction + [exchange] + expand
+with the dense leaf blocks) over one synthetic input vector of BASELINE.json's
+workload.  Default workload: configs[3] ("c4", 2D, N = 2^24, L = 9, b = 64,
+r = 16, 124.55 GB of factors), the configuration BASELINE.json quotes the
+1/2/4/8-GPU metric on; it fits one B200.  Inputs: seeded synthetic panels
+generated in place on the device (gen/), distinct x per step; the working set
+(125 GB) is far larger than L2 (126 MB), so no flush is needed.
+
+N > 1: launched by torch.distributed.run, one rank per GPU; each rank owns the
+Morton rows [g N/P, (g+1) N/P) of every panel (strong scaling of one operator)
+and the library sums the cross-GPU z vectors with NCCL.  Time = max over ranks.
+
+Rank 0 prints one JSON line (see DESIGN.md §7 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from gen import hgen  # noqa: E402
+from gen.hgen import CONFIGS  # noqa: E402
+
+METRIC = "H-matvec GB/s of factor data & matvecs/s vs HBM roofline, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_desc(cfg):
+    return (f"{cfg.name}: {cfg.d}D H-matrix fp64, weak admissibility, N={cfg.N} (Morton), depth L={cfg.L}, "
+            f"leaf b={cfg.b}, rank r={cfg.r} blocks vs each of {cfg.c - 1} siblings at every level, "
+            f"dense {cfg.b}x{cfg.b} leaf-diagonal blocks, nrhs={cfg.nrhs}, seeded synthetic "
+            f"(U,V~N(0,1)/sqrt(m_l), D~N(0,1)/8, x~U[-1,1])")
+
+
+def alg_bytes(cfg, n_rows, nrhs):
+    """Algorithmic bytes of one matvec over n_rows rows:
+    factor panels once + x in + y out.  Split per kernel."""
+    W, L, b = cfg.W, cfg.L, cfg.b
+    project = 8 * n_rows * (W * L) + 8 * n_rows * nrhs
+    expand = 8 * n_rows * (W * L + b) + 16 * n_rows * nrhs
+    factor = 8 * n_rows * (2 * W * L + b)
+    return {"project": project, "expand": expand, "factor": factor, "total": factor + 16 * n_rows * nrhs}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config_name, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d[config_name][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [s.strip() for s in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------
+# CPU oracle baseline: the oracle as it stands, single-threaded, on a bounded sample
+# --------------------------------------------------------------------------------------
+
+def oracle_sample(cfg, budget_bytes):
+    """The leading diagonal sub-H-matrix of `cfg` rooted at level q (rows
+    [0, N/c^q)): exactly the blocks of cfg at levels q+1..L inside that
+    diagonal block plus its dense leaves -- an H-matrix of depth L-q with the
+    same b, r, d.  q is the smallest level whose factor bytes fit the budget."""
+    for q in range(0, cfg.L + 1):
+        n = cfg.N // cfg.c ** q
+        depth = cfg.L - q
+        fb = 8 * n * (2 * cfg.W * depth + cfg.b)
+        if fb <= budget_bytes:
+            return q, n, depth, fb
+    return cfg.L, cfg.b, 0, 8 * cfg.b * cfg.b
+
+
+def run_oracle_sample(cfg, q, n, depth, reps, nrhs):
+    from oracle import oracle
+    # panels of levels q+1..L restricted to rows [0, n): generated from the full
+    # operator's streams (same values as the GPU operator)
+    U = [hgen.panel(cfg, hgen.TAG_U, q + l, 0, n) for l in range(1, depth + 1)]
+    V = [hgen.panel(cfg, hgen.TAG_V, q + l, 0, n) for l in range(1, depth + 1)]
+    D = hgen.panel(cfg, hgen.TAG_D, 0, 0, n)
+    x = hgen.xblock(cfg, nrhs=nrhs, vec=0, row_begin=0, row_end=n)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.matvec(cfg.d, depth, cfg.b, cfg.r, U, V, D, x)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_baseline_record(cfg, budget_bytes=6.5e9, reps=1):
+    q, n, depth, fb = oracle_sample(cfg, budget_bytes)
+    times = run_oracle_sample(cfg, q, n, depth, reps, cfg.nrhs)
+    t = float(np.median(times))
+    gbps = fb / t / 1e9
+    per_matvec = cfg.factor_bytes
+    return {
+        "value": (fb / t) / per_matvec,
+        "unit": "matvec/s",
+        "cores": 1,
+        "kind": "oracle",
+        "host_cores_available": len(os.sched_getaffinity(0)),
+        "sample": (f"oracle block loop (1 thread) over the leading level-{q} diagonal sub-H-matrix of {cfg.name} "
+                   f"(rows [0,{n}), levels {q + 1}..{cfg.L} + dense leaves, {fb / 1e9:.2f} GB of factors, "
+                   f"nrhs={cfg.nrhs}), {reps} rep(s), median {t:.2f} s; value = sample factor GB/s / "
+                   f"{per_matvec / 1e9:.2f} GB per full matvec"),
+        "factor_GBps": gbps,
+    }
+
+
+def run_reference(args):
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    steps, warm = args.steps, args.warmup
+    # size each step so the whole run stays within ~2-3 minutes at ~1.5 GB/s
+    budget = max(64e6, min(6.5e9, 150e9 / (steps + warm)))
+    q, n, depth, fb = oracle_sample(cfg, budget)
+    times = run_oracle_sample(cfg, q, n, depth, warm + steps, cfg.nrhs)[warm:]
+    t = float(np.sum(times))
+    value = steps * fb / t / cfg.factor_bytes
+    cpu = {"value": value, "unit": "matvec/s", "cores": 1, "kind": "oracle",
+           "sample": f"per step: oracle over the leading level-{q} diagonal sub-H-matrix of {cfg.name} "
+                     f"({fb / 1e9:.3f} GB of factors, rows [0,{n})), extrapolated by factor bytes"}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * t / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "parallelism": "1 host thread"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_12441_b200 import hmat as hm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    nrhs = cfg.nrhs
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    nid = None
+    if world > 1:
+        obj = [hm.hmat_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    dd = hm._dist(nranks=world, rank=rank, nccl_unique_id=nid, cuda_stream=sptr, device=local)
+
+    t_setup = time.perf_counter()
+    h = hm.hmat_create_uninit(cfg.L, cfg.d, cfg.b, cfg.r, dd)
+    r0, r1 = hm.hmat_local_rows(h)
+    n = r1 - r0
+    hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, sptr)
+    nvec = max(1, min(args.steps + args.warmup, 8))
+    X = [torch.empty(nrhs, n, dtype=torch.float64, device="cuda") for _ in range(nvec)]
+    for v, xv in enumerate(X):
+        hgen.dev_fill_x(cfg, nrhs, v, r0, r1, xv.data_ptr(), n, sptr)
+    Y = torch.empty(nrhs, n, dtype=torch.float64, device="cuda")
+    xs = [xv.t() for xv in X]
+    ys = Y.t()
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(args.warmup):
+        hm.hmat_matvec(h, xs[i % nvec], ys, nrhs)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device, CUDA events on the launch stream) ----------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    hm.hmat_profile(h, True)
+    hm.hmat_profile_read(h)  # reset
+    barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        hm.hmat_matvec(h, xs[i % nvec], ys, nrhs)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    prof = hm.hmat_profile_read(h)
+    hm.hmat_profile(h, False)
+    ms_total = max_over_ranks(ms_local)
+    ms_step = ms_total / args.steps
+    launches = hm.hmat_launches_per_matvec(h, nrhs) * args.steps
+
+    # ---------------- e2e: C-ABI call with pinned host x / y, copies timed --------------
+    e2e = None
+    if not args.no_e2e:
+        xh = [torch.empty(nrhs, n, dtype=torch.float64).pin_memory() for _ in range(2)]
+        for v, xv in enumerate(xh):
+            xv.copy_(X[v % nvec])
+        yh = torch.empty(nrhs, n, dtype=torch.float64).pin_memory()
+        e2e_steps = max(3, min(args.steps, 16))
+        hm.hmat_matvec(h, xh[0].t(), yh.t(), nrhs)
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(e2e_steps):
+            hm.hmat_matvec(h, xh[i % 2].t(), yh.t(), nrhs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+        e2e = {"value": 1e3 / e2e_ms, "unit": "matvec/s", "h2d_bytes_per_step": 8 * cfg.N * nrhs,
+               "d2h_bytes_per_step": 8 * cfg.N * nrhs, "ms_per_step": e2e_ms, "steps": e2e_steps,
+               "how": "hmat_matvec with pinned host x/y: H2D of x, kernels, D2H of y, all ranks"}
+
+    # ---------------- roofline of the dominant kernel ----------------------------------
+    ab = alg_bytes(cfg, n, nrhs)
+    per_kernel = {}
+    for ph in ("project", "expand"):
+        ms, nl = prof[ph]
+        if nl:
+            per_kernel[ph] = {"avg_ms": ms / nl, "launches": nl, "alg_bytes_per_launch": ab[ph] / max(1, (nl // args.steps)),
+                              "GBps": ab[ph] / (ms / nl * 1e-3) / 1e9 / max(1, (nl // args.steps))}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_ms"])
+    peak, peak_src = measured_peaks()
+    achieved = per_kernel[dom]["GBps"]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, dom), "peak_source": peak_src,
+            "per_kernel": per_kernel, "frac_of_8TBps_nominal": achieved / 8000.0}
+
+    value = 1e3 / ms_step  # matvecs/s of the whole job (one operator across all ranks)
+    factor_gbps = cfg.factor_bytes / (ms_step * 1e-3) / 1e9
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_record(cfg)
+        line = {
+            "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "N": cfg.N, "nrhs": nrhs,
+                       "factor_bytes": cfg.factor_bytes, "parallelism": f"subtree shards x{world} (Morton rows)",
+                       "l2": "working set 1000x L2; no flush needed", "distinct_x": nvec},
+            "factor_GBps": factor_gbps,
+            "alg_GBps": ab["total"] * world / (ms_step * 1e-3) / 1e9,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "phase_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    hm.hmat_destroy(h)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

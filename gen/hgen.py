@@ -190,3 +190,17 @@ def dev_fill_x(cfg: HConfig, nrhs: int, vec: int, row_begin: int, row_end: int, 
     rc = _load_dev().hgen_dev_fill_x(cfg.seed, vec, cfg.N, row_begin, row_end, nrhs, out_ptr, ld, stream)
     if rc != 0:
         raise RuntimeError(f"hgen_dev_fill_x: cuda error {rc}")
+
+
+def dev_fill_operator(cfg: HConfig, panel_fn, row_begin: int, row_end: int, stream: int = 0) -> None:
+    """Fill an operator's device panels in place with the synthetic inputs of
+    rows [row_begin, row_end).  panel_fn(kind, level) -> (ptr, rows, cols, ld)
+    for kind 0 = U_level, 1 = V_level, 2 = D (e.g. paper_2008_12441_b200.hmat.hmat_panel)."""
+    for level in range(1, cfg.L + 1):
+        for kind, tag in ((0, TAG_U), (1, TAG_V)):
+            ptr, rows, cols, ld = panel_fn(kind, level)
+            assert rows == row_end - row_begin and cols == cfg.W
+            dev_fill_panel(cfg, tag, level, row_begin, row_end, ptr, ld, stream)
+    ptr, rows, cols, ld = panel_fn(2, 0)
+    assert rows == row_end - row_begin and cols == cfg.b
+    dev_fill_panel(cfg, TAG_D, 0, row_begin, row_end, ptr, ld, stream)

@@ -1,0 +1,162 @@
+/*
+ * hmat.h -- C ABI of the B200-native weak-admissibility H-matrix-vector
+ * product y = H x (arXiv 2008.12441, Li, Poulson & Ying, "Distributed-memory
+ * H-matrix algebra I").  Implemented by paper_2008_12441_b200/libhmat.so
+ * (sm_100a kernels + host plan; NCCL loaded on demand for nranks > 1).
+ *
+ * The operation (eq:hmat-vec-add): y is initialised to zero
+ * and, for every block K_{t x s} of H holding data, y_t += D_ts x_s (dense) or
+ * y_t += U_ts (V_ts^T x_s) (low rank).  The structure is Def 2.4
+ * on the 2^dim-ary domain tree of an ideal dim-dimensional
+ * domain under weak admissibility, in
+ * the reading of DESIGN.md R1: every node t at levels 1..depth has a rank-`rank`
+ * block U_ts V_ts^T against each of its 2^dim - 1 siblings s; the leaf-diagonal
+ * blocks D_k (leaf_size x leaf_size) are dense; nothing else holds data.
+ *
+ * Notation: c = 2^dim, L = depth, b = leaf_size, r = rank, N = b c^L,
+ * m_l = N / c^l (rows of a level-l node), W = (c-1) r.  Points are in Morton
+ * (Z-) order so every tree node is a contiguous index range: node k of level l
+ * owns rows [k m_l, (k+1) m_l).  Siblings of t are the other children of t's
+ * parent, in ascending child order; slot(t -> s) is s's position in that list.
+ *
+ * CANONICAL PANELS (the input format; row-major, Morton rows):
+ *   U[l-1]  N_loc x W  row i, columns [q r, (q+1) r): row i - t m_l of U_{t,s_q}
+ *           where t = i / m_l and s_q is t's q-th sibling (target-major).
+ *   V[l-1]  N_loc x W  row j, columns [q r, (q+1) r): row j - s m_l of V_{t_q,s}
+ *           where s = j / m_l and t_q is s's q-th sibling (source-major).
+ *   D       N_loc x b  row i: row i - k b of D_k, k = i / b.
+ * Block K_{t x s} = U_ts V_ts^T with U_ts in R^{|t| x r}, V_ts in R^{|s| x r}
+ * (PAPER.md:327-334).  With nranks = P > 1, rank g passes only its Morton
+ * rows [g N/P, (g+1) N/P) of every panel (the paper's block-row placement, U on
+ * the target side, V on the source side; dense blocks on
+ * their single owner).
+ *
+ * VECTORS: x and y are N_loc x nrhs column-major with leading dimension N_loc
+ * (block-row distributed exactly like the panels).  They may
+ * be device pointers (on H's device) or host pointers; host vectors are copied
+ * in/out by the call.  x and y must not alias.  y is overwritten.
+ *
+ * STREAMS AND SYNCHRONISATION: work is enqueued on H's stream.  With device
+ * x/y the call returns without waiting (like a BLAS handle); with a host x or
+ * y it returns after y is complete.  With nranks > 1 hmat_matvec is a
+ * collective: every rank calls it with the same nrhs in the same order.
+ *
+ * ERRORS: every entry point returns HMAT_OK or a negative hmat_status and sets
+ * a thread-local message readable with hmat_last_error().  Argument checks
+ * happen before any device work.  No C++ exception crosses this ABI.
+ * Asynchronous device faults surface as HMAT_ERR_CUDA at a later call.
+ */
+#ifndef HMAT_H
+#define HMAT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hmat_s* hmat_t;
+
+typedef enum {
+  HMAT_OK = 0,
+  HMAT_ERR_INVALID = -1,     /* bad argument (message says which) */
+  HMAT_ERR_NOMEM = -2,       /* device allocation failed */
+  HMAT_ERR_CUDA = -3,        /* CUDA runtime error (incl. asynchronous faults) */
+  HMAT_ERR_NCCL = -4,        /* NCCL load/initialisation/collective error */
+  HMAT_ERR_UNSUPPORTED = -5  /* valid but outside the implemented envelope */
+} hmat_status;
+
+/* Multi-GPU placement of one rank.  NULL => one GPU, the current device,
+ * N_loc = N, a library-owned stream. */
+typedef struct {
+  int nranks;                 /* P: a power of two <= c^L                            */
+  int rank;                   /* 0 <= rank < P; owns Morton rows [rank N/P, ...)     */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId (same on all ranks); P > 1 only */
+  void* cuda_stream;          /* cudaStream_t to enqueue on; NULL => library-owned    */
+  int device;                 /* CUDA ordinal of this rank's GPU                     */
+} hmat_dist_t;
+
+/* Build H from canonical panels (see above).  U and V are arrays of `depth`
+ * pointers (ignored when depth == 0); each panel and D may be host (pageable or
+ * pinned) or device memory; the library copies them into its own 128-byte
+ * aligned per-level device panels, so the caller may free them on return.
+ * dim in {1,2,3}; depth >= 0; leaf_size >= 1; rank >= 1; N < 2^62.
+ * HMAT_ERR_UNSUPPORTED if (2^dim - 1) * rank > 1024. */
+hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                        const double* const* V, const double* D, const hmat_dist_t* dist, hmat_t* out);
+
+/* Same as hmat_create but leaves the panels uninitialised (zero); fill them in
+ * place through hmat_panel() (no second copy of a 125 GB operator). */
+hmat_status hmat_create_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist,
+                               hmat_t* out);
+
+/* Device address of one of H's panels: kind 0 = U_level, 1 = V_level (level in
+ * 1..depth), 2 = D (level ignored).  *rows = N_loc, *cols = W (or b), *ld =
+ * row pitch in doubles (>= cols; padding columns are never read). */
+hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* rows, int64_t* cols,
+                       int64_t* ld);
+
+/* y = H x for nrhs right-hand sides (the whole hot path: project, on-chip
+ * reduction, cross-GPU exchange when P > 1, fused expand + dense). */
+hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
+
+/* Diagnostic form: only the low-rank levels l with bit (l-1) of level_mask set
+ * and, if dense != 0, the dense leaf blocks: y = y_D + sum_{l in mask} y_l. */
+hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, uint64_t level_mask,
+                              int dense);
+
+/* Frees everything H owns (collective when P > 1).  hmat_destroy(NULL) is OK. */
+hmat_status hmat_destroy(hmat_t H);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* hmat_last_error(void);
+
+/* N (global number of points), or -1 if H is NULL. */
+int64_t hmat_num_points(hmat_t H);
+
+/* This rank's Morton rows [begin, end). */
+hmat_status hmat_local_rows(hmat_t H, int64_t* begin, int64_t* end);
+
+/* Make H enqueue on `stream` (a cudaStream_t on H's device) from now on. */
+hmat_status hmat_set_stream(hmat_t H, void* stream);
+
+/* 128 bytes of a fresh ncclUniqueId for hmat_dist_t (call on one rank and
+ * broadcast).  HMAT_ERR_NCCL if NCCL cannot be loaded. */
+hmat_status hmat_nccl_unique_id(void* out128);
+
+/* Kernel timing: when enabled, CUDA events bracket every kernel/collective of
+ * each matvec on H's stream.  hmat_profile_read() synchronises, returns the
+ * accumulated milliseconds and launch counts per phase since the last read
+ * (phase 0 = project, 1 = exchange, 2 = expand, 3 = host<->device copies) and
+ * resets them.  ms and launches point to HMAT_NUM_PHASES entries. */
+#define HMAT_NUM_PHASES 4
+hmat_status hmat_profile(hmat_t H, int enable);
+hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches);
+
+/* Kernel launches one hmat_matvec(nrhs) performs on this rank. */
+int64_t hmat_launches_per_matvec(hmat_t H, int nrhs);
+
+/* Host-only description of a shard's plan (no GPU needed). */
+typedef struct {
+  int64_t N, row_begin, row_end;
+  int c, W, W_pitch;          /* W_pitch: row pitch (doubles) of panels and z rows  */
+  int cross_levels;           /* levels 1..cross_levels go through the exchange     */
+  int64_t exchange_rows;      /* targets in the exchange buffer (sum of c^l, l <= cross) */
+  int64_t level_rows_offset[64]; /* first exchange row of level l (l = 1..cross)    */
+  int Rp, Re, tpr, nstage_p, nstage_e, grid_p, grid_e;
+  int64_t smem_p, smem_e;
+} hmat_plan_info_t;
+
+/* Validates (depth, dim, leaf_size, rank, nranks, rank_id) exactly like
+ * hmat_create and describes the plan a B200 (148 SMs) would use.  The exchange
+ * buffer is level-major, then target-major: row (level_rows_offset[l] + t)
+ * holds, in columns [q r, (q+1) r), z_{t, s_q} = V_{t,s_q}^T x_{s_q}, summed over
+ * all ranks. */
+hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
+                            hmat_plan_info_t* info);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMAT_H */

@@ -1,0 +1,98 @@
+// comm.cpp -- see comm.h.
+#include "comm.h"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
+namespace hmat {
+
+namespace {
+
+struct NcclApi {
+  void* handle = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string error;
+};
+
+NcclApi& api() {
+  static NcclApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      a.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (a.handle) break;
+    }
+    if (!a.handle) {
+      a.error = std::string("cannot dlopen libnccl.so.2: ") + dlerror();
+      return;
+    }
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(a.handle, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(a.handle, "ncclCommInitRank"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.handle, "ncclAllReduce"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.handle, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.handle, "ncclGetErrorString"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.GetErrorString)
+      a.error = "libnccl is missing a required symbol";
+  });
+  return a;
+}
+
+std::string nccl_err(const char* what, ncclResult_t r) {
+  return std::string(what) + ": " + api().GetErrorString(r);
+}
+
+}  // namespace
+
+struct Comm {
+  ncclComm_t comm = nullptr;
+};
+
+std::string comm_unique_id(void* out128) {
+  NcclApi& a = api();
+  if (!a.error.empty()) return a.error;
+  ncclUniqueId id;
+  ncclResult_t r = a.GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_err("ncclGetUniqueId", r);
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(out128, &id, sizeof(id));
+  return "";
+}
+
+std::string comm_create(const void* id128, int nranks, int rank, Comm** out) {
+  NcclApi& a = api();
+  if (!a.error.empty()) return a.error;
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  Comm* c = new Comm;
+  ncclResult_t r = a.CommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_err("ncclCommInitRank", r);
+  }
+  *out = c;
+  return "";
+}
+
+std::string comm_allreduce_sum(Comm* c, double* buf, size_t count, cudaStream_t stream) {
+  if (count == 0) return "";
+  ncclResult_t r = api().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, stream);
+  if (r != ncclSuccess) return nccl_err("ncclAllReduce", r);
+  return "";
+}
+
+void comm_destroy(Comm* c) {
+  if (!c) return;
+  if (c->comm) api().CommDestroy(c->comm);
+  delete c;
+}
+
+}  // namespace hmat

@@ -1,0 +1,518 @@
+// hmat.cpp -- the C ABI (include/hmat.h): validation, device memory, the
+// per-matvec launch sequence and the optional NCCL exchange.
+//
+// One hmat_matvec = for each pass of <= 8 right-hand sides:
+//   [P>1: zero the exchange buffer]
+//   project  (Step 1 + on-chip Step 2)
+//   [P>1: sum-allreduce of the packed exchange buffer = Steps 2-4 across GPUs,
+//         PAPER.md:746-904]
+//   expand   (Step 5, fused with the dense leaf blocks)
+#include "hmat.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "kernels.h"
+#include "plan.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+hmat_status fail(hmat_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+hmat_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? HMAT_ERR_NOMEM : HMAT_ERR_CUDA;
+}
+
+#define CUDA_TRY(expr)                                   \
+  do {                                                   \
+    cudaError_t e_ = (expr);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);  \
+  } while (0)
+
+int env_int(const char* name, int def) {
+  const char* v = getenv(name);
+  if (!v || !*v) return def;
+  return atoi(v);
+}
+
+hmat::PlanOptions options_from_env(int num_sms) {
+  hmat::PlanOptions o;
+  o.num_sms = num_sms;
+  o.ctas_per_sm = env_int("HMAT_CTAS_PER_SM", 1);
+  o.stage_cap_bytes = env_int("HMAT_STAGE_KB", 36) * 1024;
+  o.smem_budget = env_int("HMAT_SMEM_KB", 200) * 1024;
+  o.max_stages = env_int("HMAT_MAX_STAGES", 6);
+  return o;
+}
+
+hmat_status plan_status(const std::string& msg) {
+  if (msg.rfind("unsupported", 0) == 0) return fail(HMAT_ERR_UNSUPPORTED, msg);
+  return fail(HMAT_ERR_INVALID, msg);
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int nr_cap(int nr) { return nr <= 1 ? 1 : nr <= 2 ? 2 : nr <= 4 ? 4 : 8; }
+
+struct EventPair {
+  int phase;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct hmat_s {
+  hmat::Plan plan;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double* U = nullptr;
+  double* V = nullptr;
+  double* D = nullptr;
+  double* zloc = nullptr;
+  double* zex = nullptr;
+  double* part = nullptr;
+  int* cnt = nullptr;
+  double* xbuf = nullptr;
+  double* ybuf = nullptr;
+  size_t xcap = 0, ycap = 0;  // doubles
+  hmat::Comm* comm = nullptr;
+  bool prof = false;
+  std::vector<EventPair> ev;
+  std::vector<cudaEvent_t> pool;
+  double ms[HMAT_NUM_PHASES] = {};
+  int64_t nl[HMAT_NUM_PHASES] = {};
+};
+
+namespace {
+
+void release(hmat_s* H) {
+  if (!H) return;
+  cudaSetDevice(H->device);
+  if (H->stream) cudaStreamSynchronize(H->stream);
+  cudaFree(H->U);
+  cudaFree(H->V);
+  cudaFree(H->D);
+  cudaFree(H->zloc);
+  cudaFree(H->zex);
+  cudaFree(H->part);
+  cudaFree(H->cnt);
+  cudaFree(H->xbuf);
+  cudaFree(H->ybuf);
+  for (auto& e : H->ev) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : H->pool) cudaEventDestroy(e);
+  hmat::comm_destroy(H->comm);
+  if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
+  delete H;
+}
+
+hmat_status validate_dist(const hmat_dist_t* dist, int* P, int* rank) {
+  *P = 1;
+  *rank = 0;
+  if (!dist) return HMAT_OK;
+  *P = dist->nranks;
+  *rank = dist->rank;
+  if (dist->nranks > 1 && !dist->nccl_unique_id) return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1");
+  if (dist->device < 0) return fail(HMAT_ERR_INVALID, "device ordinal must be >= 0");
+  return HMAT_OK;
+}
+
+hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dist_t* dist, hmat_t* out) {
+  if (!out) return fail(HMAT_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  int P, shard;
+  hmat_status st = validate_dist(dist, &P, &shard);
+  if (st != HMAT_OK) return st;
+  hmat::Plan plan;
+  std::string msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, options_from_env(148), &plan);
+  if (!msg.empty()) return plan_status(msg);
+
+  // ---- device work starts here ----
+  int device = 0;
+  if (dist) {
+    device = dist->device;
+    CUDA_TRY(cudaSetDevice(device));
+  } else {
+    CUDA_TRY(cudaGetDevice(&device));
+  }
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, options_from_env(sms), &plan);
+  if (!msg.empty()) return plan_status(msg);
+
+  hmat_s* H = new hmat_s;
+  H->plan = plan;
+  H->device = device;
+  auto bail = [&](hmat_status s) {
+    release(H);
+    return s;
+  };
+  if (dist && dist->cuda_stream) {
+    H->stream = static_cast<cudaStream_t>(dist->cuda_stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
+    H->own_stream = true;
+  }
+  const hmat::Plan& p = H->plan;
+  auto alloc = [&](void** ptr, size_t bytes, const char* what) -> cudaError_t {
+    if (bytes == 0) bytes = 256;
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess) g_err = std::string("cudaMalloc(") + what + ")";
+    return e;
+  };
+  cudaError_t e = cudaSuccess;
+  const size_t panels = size_t(p.L) * size_t(p.panel_stride) * sizeof(double);
+  const size_t zrow = size_t(p.Wp) * hmat::kMaxNR * sizeof(double);
+  if ((e = alloc(reinterpret_cast<void**>(&H->U), panels, "U")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->V), panels, "V")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->D), size_t(p.N_loc) * p.Dp * sizeof(double), "D")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->zloc), size_t(p.z_local_rows) * zrow, "z")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->zex), size_t(p.z_exch_rows) * zrow, "exchange")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->part), size_t(p.grid_p) * 2 * zrow, "partials")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->cnt), size_t(p.grid_p + 1) * sizeof(int), "tickets"))) {
+    std::string what = g_err;
+    return bail(cuda_fail(e, what.c_str()));
+  }
+  if ((e = cudaMemsetAsync(H->cnt, 0, size_t(p.grid_p + 1) * sizeof(int), H->stream)) ||
+      (e = cudaMemsetAsync(H->U, 0, panels ? panels : 256, H->stream)) ||
+      (e = cudaMemsetAsync(H->V, 0, panels ? panels : 256, H->stream)) ||
+      (e = cudaMemsetAsync(H->D, 0, size_t(p.N_loc) * p.Dp * sizeof(double), H->stream)) ||
+      (e = hmat::configure_kernels(p.smem_p, p.smem_e)) || (e = cudaStreamSynchronize(H->stream)))
+    return bail(cuda_fail(e, "initialising device buffers"));
+  if (p.P > 1) {
+    std::string m = hmat::comm_create(dist->nccl_unique_id, p.P, p.rank, &H->comm);
+    if (!m.empty()) return bail(fail(HMAT_ERR_NCCL, m));
+  }
+  *out = H;
+  return HMAT_OK;
+}
+
+cudaEvent_t take_event(hmat_s* H) {
+  if (!H->pool.empty()) {
+    cudaEvent_t e = H->pool.back();
+    H->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(hmat_s* H, int phase, EventPair* ep) {
+  if (!H->prof) return;
+  ep->phase = phase;
+  ep->a = take_event(H);
+  ep->b = take_event(H);
+  cudaEventRecord(ep->a, H->stream);
+}
+
+void prof_end(hmat_s* H, EventPair* ep) {
+  if (!H->prof) return;
+  cudaEventRecord(ep->b, H->stream);
+  H->ev.push_back(*ep);
+}
+
+hmat_status ensure_buf(double** buf, size_t* cap, size_t n) {
+  if (*cap >= n) return HMAT_OK;
+  cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(buf), n * sizeof(double)));
+  *cap = n;
+  return HMAT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hmat_status hmat_create_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist, hmat_t* out) {
+  return create_common(depth, dim, leaf_size, rank, dist, out);
+}
+
+hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const double* const* U, const double* const* V,
+                        const double* D, const hmat_dist_t* dist, hmat_t* out) {
+  if (!out) return fail(HMAT_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (depth > 0 && (!U || !V)) return fail(HMAT_ERR_INVALID, "U or V is NULL");
+  if (!D) return fail(HMAT_ERR_INVALID, "D is NULL");
+  for (int l = 0; depth > 0 && l < depth && l < hmat::kMaxLevels; ++l)
+    if (!U[l] || !V[l]) return fail(HMAT_ERR_INVALID, "a U or V panel pointer is NULL");
+  hmat_t H = nullptr;
+  hmat_status st = create_common(depth, dim, leaf_size, rank, dist, &H);
+  if (st != HMAT_OK) return st;
+  const hmat::Plan& p = H->plan;
+  cudaError_t e = cudaSuccess;
+  for (int l = 1; l <= p.L && e == cudaSuccess; ++l) {
+    e = cudaMemcpy2DAsync(H->U + (l - 1) * p.panel_stride, p.Wp * sizeof(double), U[l - 1], p.W * sizeof(double),
+                          p.W * sizeof(double), p.N_loc, cudaMemcpyDefault, H->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(H->V + (l - 1) * p.panel_stride, p.Wp * sizeof(double), V[l - 1], p.W * sizeof(double),
+                            p.W * sizeof(double), p.N_loc, cudaMemcpyDefault, H->stream);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(H->D, p.Dp * sizeof(double), D, p.b * sizeof(double), p.b * sizeof(double), p.N_loc,
+                          cudaMemcpyDefault, H->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(H->stream);
+  if (e != cudaSuccess) {
+    hmat_status s = cuda_fail(e, "copying panels");
+    release(H);
+    return s;
+  }
+  *out = H;
+  return HMAT_OK;
+}
+
+hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* rows, int64_t* cols, int64_t* ld) {
+  if (!H || !ptr) return fail(HMAT_ERR_INVALID, "NULL argument");
+  const hmat::Plan& p = H->plan;
+  if (kind == 0 || kind == 1) {
+    if (level < 1 || level > p.L) return fail(HMAT_ERR_INVALID, "level out of range [1, depth]");
+    *ptr = (kind == 0 ? H->U : H->V) + (level - 1) * p.panel_stride;
+    if (cols) *cols = p.W;
+    if (ld) *ld = p.Wp;
+  } else if (kind == 2) {
+    *ptr = H->D;
+    if (cols) *cols = p.b;
+    if (ld) *ld = p.Dp;
+  } else {
+    return fail(HMAT_ERR_INVALID, "kind must be 0 (U), 1 (V) or 2 (D)");
+  }
+  if (rows) *rows = p.N_loc;
+  return HMAT_OK;
+}
+
+hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, uint64_t level_mask, int dense) {
+  if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
+  if (!x || !y) return fail(HMAT_ERR_INVALID, "x or y is NULL");
+  if (nrhs < 1) return fail(HMAT_ERR_INVALID, "nrhs must be >= 1");
+  if (static_cast<const void*>(x) == static_cast<const void*>(y)) return fail(HMAT_ERR_INVALID, "x and y alias");
+  const hmat::Plan& p = H->plan;
+  CUDA_TRY(cudaSetDevice(H->device));
+  const int64_t n = p.N_loc;
+  const bool x_dev = is_device_ptr(x), y_dev = is_device_ptr(y);
+  const bool host_io = !x_dev || !y_dev;
+  if (p.L < 64) level_mask &= (p.L == 0 ? 0ull : (~0ull >> (64 - p.L)));
+
+  EventPair ep{};
+  // ---- x: stage when it is host memory, misaligned, or its last column would
+  //      be over-read by the 16-byte-granular bulk copies
+  const double* xd = x;
+  int64_t ldx = n;
+  if (!x_dev || (reinterpret_cast<uintptr_t>(x) & 15) || ((n * nrhs) & 1)) {
+    const int64_t lds = n + (n & 1);
+    hmat_status st = ensure_buf(&H->xbuf, &H->xcap, size_t(lds) * nrhs + 2);
+    if (st != HMAT_OK) return st;
+    prof_begin(H, 3, &ep);
+    CUDA_TRY(cudaMemcpy2DAsync(H->xbuf, lds * sizeof(double), x, n * sizeof(double), n * sizeof(double), nrhs,
+                               cudaMemcpyDefault, H->stream));
+    prof_end(H, &ep);
+    xd = H->xbuf;
+    ldx = lds;
+  }
+  double* yd = y;
+  if (!y_dev) {
+    hmat_status st = ensure_buf(&H->ybuf, &H->ycap, size_t(n) * nrhs);
+    if (st != HMAT_OK) return st;
+    yd = H->ybuf;
+  }
+
+  hmat::StreamArgs a;
+  memset(&a, 0, sizeof a);
+  a.U = H->U;
+  a.V = H->V;
+  a.D = H->D;
+  a.panel_stride = p.panel_stride;
+  a.ldx = ldx;
+  a.ldy = n;
+  a.L = p.L;
+  a.c = p.c;
+  a.r = p.r;
+  a.W = p.W;
+  a.Wp = p.Wp;
+  a.Dp = p.Dp;
+  a.b = p.b;
+  a.N_loc = n;
+  a.row0 = p.row0;
+  a.level_mask = level_mask;
+  a.dense = dense ? 1 : 0;
+  a.Rp = p.Rp;
+  a.nstage_p = p.nstage_p;
+  a.stage_bytes_p = p.stage_bytes_p;
+  a.stages_p = p.stages_p;
+  a.part = H->part;
+  a.cnt = H->cnt;
+  a.Re = p.Re;
+  a.tpr = p.tpr;
+  a.nstage_e = p.nstage_e;
+  a.stage_bytes_e = p.stage_bytes_e;
+  a.items_e = p.items_e;
+  a.xs_p = p.xs_p;
+  a.xs_e = p.xs_e;
+  a.red_off_p = p.red_off_p;
+  a.bar_off_p = p.bar_off_p;
+  a.bar_off_e = p.bar_off_e;
+
+  for (int c0 = 0; c0 < nrhs; c0 += hmat::kMaxNR) {
+    const int nr = nrhs - c0 < hmat::kMaxNR ? nrhs - c0 : hmat::kMaxNR;
+    const int cap = nr_cap(nr);
+    a.nr = nr;
+    a.x = xd + c0 * ldx;
+    a.y = yd + c0 * n;
+    for (int l = 1; l <= p.L; ++l) {
+      hmat::LevelArgs& lv = a.lv[l];
+      lv.m = p.m[l];
+      lv.seg_rows = p.m[l] < n ? p.m[l] : n;
+      lv.zt = (l <= p.cross ? H->zex : H->zloc) + p.zt_off[l] * p.Wp * cap;
+      lv.tbase = p.zt_tbase[l];
+    }
+    const size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
+    if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(H->zex, 0, exch * sizeof(double), H->stream));
+    if (p.grid_p > 0 && level_mask) {
+      prof_begin(H, 0, &ep);
+      CUDA_TRY(hmat::launch_project(a, cap, p.grid_p, p.smem_p, H->stream));
+      prof_end(H, &ep);
+    }
+    if (p.P > 1 && exch) {
+      prof_begin(H, 1, &ep);
+      std::string m = hmat::comm_allreduce_sum(H->comm, H->zex, exch, H->stream);
+      if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+      prof_end(H, &ep);
+    }
+    prof_begin(H, 2, &ep);
+    CUDA_TRY(hmat::launch_expand(a, cap, p.grid_e, p.smem_e, H->stream));
+    prof_end(H, &ep);
+  }
+  if (!y_dev) {
+    prof_begin(H, 3, &ep);
+    CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
+    prof_end(H, &ep);
+  }
+  if (host_io) CUDA_TRY(cudaStreamSynchronize(H->stream));
+  CUDA_TRY(cudaGetLastError());
+  return HMAT_OK;
+}
+
+hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs) {
+  return hmat_matvec_parts(H, x, y, nrhs, ~0ull, 1);
+}
+
+hmat_status hmat_destroy(hmat_t H) {
+  release(H);
+  return HMAT_OK;
+}
+
+const char* hmat_last_error(void) { return g_err.c_str(); }
+
+int64_t hmat_num_points(hmat_t H) { return H ? H->plan.N : -1; }
+
+hmat_status hmat_local_rows(hmat_t H, int64_t* begin, int64_t* end) {
+  if (!H || !begin || !end) return fail(HMAT_ERR_INVALID, "NULL argument");
+  *begin = H->plan.row0;
+  *end = H->plan.row0 + H->plan.N_loc;
+  return HMAT_OK;
+}
+
+hmat_status hmat_set_stream(hmat_t H, void* stream) {
+  if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
+  CUDA_TRY(cudaSetDevice(H->device));
+  CUDA_TRY(cudaStreamSynchronize(H->stream));
+  if (H->own_stream) cudaStreamDestroy(H->stream);
+  H->own_stream = false;
+  H->stream = static_cast<cudaStream_t>(stream);
+  return HMAT_OK;
+}
+
+hmat_status hmat_nccl_unique_id(void* out128) {
+  if (!out128) return fail(HMAT_ERR_INVALID, "out is NULL");
+  std::string m = hmat::comm_unique_id(out128);
+  if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  return HMAT_OK;
+}
+
+hmat_status hmat_profile(hmat_t H, int enable) {
+  if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
+  H->prof = enable != 0;
+  return HMAT_OK;
+}
+
+hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches) {
+  if (!H || !ms || !launches) return fail(HMAT_ERR_INVALID, "NULL argument");
+  CUDA_TRY(cudaSetDevice(H->device));
+  CUDA_TRY(cudaStreamSynchronize(H->stream));
+  for (auto& e : H->ev) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, e.a, e.b));
+    H->ms[e.phase] += t;
+    H->nl[e.phase] += 1;
+    H->pool.push_back(e.a);
+    H->pool.push_back(e.b);
+  }
+  H->ev.clear();
+  for (int i = 0; i < HMAT_NUM_PHASES; ++i) {
+    ms[i] = H->ms[i];
+    launches[i] = H->nl[i];
+    H->ms[i] = 0;
+    H->nl[i] = 0;
+  }
+  return HMAT_OK;
+}
+
+int64_t hmat_launches_per_matvec(hmat_t H, int nrhs) {
+  if (!H || nrhs < 1) return -1;
+  const int64_t passes = (nrhs + hmat::kMaxNR - 1) / hmat::kMaxNR;
+  return passes * ((H->plan.grid_p > 0 ? 1 : 0) + 1);
+}
+
+hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
+                            hmat_plan_info_t* info) {
+  if (!info) return fail(HMAT_ERR_INVALID, "info is NULL");
+  hmat::Plan p;
+  std::string msg = hmat::plan_build(depth, dim, leaf_size, rank, nranks, rank_id, options_from_env(148), &p);
+  if (!msg.empty()) return plan_status(msg);
+  memset(info, 0, sizeof *info);
+  info->N = p.N;
+  info->row_begin = p.row0;
+  info->row_end = p.row0 + p.N_loc;
+  info->c = p.c;
+  info->W = p.W;
+  info->W_pitch = p.Wp;
+  info->cross_levels = p.cross;
+  info->exchange_rows = p.z_exch_rows;
+  for (int l = 1; l <= p.cross && l < 64; ++l) info->level_rows_offset[l] = p.zt_off[l];
+  info->Rp = p.Rp;
+  info->Re = p.Re;
+  info->tpr = p.tpr;
+  info->nstage_p = p.nstage_p;
+  info->nstage_e = p.nstage_e;
+  info->grid_p = p.grid_p;
+  info->grid_e = p.grid_e;
+  info->smem_p = p.smem_p;
+  info->smem_e = p.smem_e;
+  return HMAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// kernels.h -- parameter blocks and launchers of the sm_100a H-matvec kernels.
+//
+//   project  Step 1 + on-chip Step 2: z_ts = V_ts^T x_s for
+//            every sibling block at every level (eq:prod-vx), as per-CTA
+//            contiguous row ranges streamed by bulk TMA, with a deterministic
+//            last-CTA reduction of node sums that cross CTA ranges; results
+//            scattered target-major (Zt_l[t][slot(t->s)]).
+//   expand   Step 5: y_i = sum_l U_l[i,:] . Zt_l[t(i)] +
+//            D_k[i,:] . x_k (eq:prod-yuz, eq:prod-ydz), fused over siblings,
+//            levels and the dense leaf blocks so y is written once.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "plan.h"
+
+namespace hmat {
+
+struct LevelArgs {
+  int64_t m;         // rows per node at this level (global)
+  int64_t seg_rows;  // rows of one local segment = min(m, N_loc)
+  double* zt;        // Zt_l (target-major, pitch Wp*NR), already offset for this pass
+  int64_t tbase;     // global index of zt's first target
+};
+
+struct StreamArgs {
+  // panels
+  const double* U;   // level-major, level l at U + (l-1)*panel_stride, rows pitch Wp
+  const double* V;
+  const double* D;   // N_loc x Dp
+  int64_t panel_stride;
+  // vectors (16-byte aligned base, column-major)
+  const double* x;
+  int64_t ldx;
+  double* y;
+  int64_t ldy;
+  int nr;            // active right-hand sides in this pass (<= NR template)
+  // shape
+  int L, c, r, W, Wp, Dp, b;
+  int64_t N_loc, row0;
+  uint64_t level_mask;
+  int dense;
+  // project schedule
+  int Rp, nstage_p;
+  int64_t stage_bytes_p, stages_p;
+  double* part;      // [grid_p][2][Wp*NR]
+  int* cnt;          // [grid_p]
+  // expand schedule
+  int Re, tpr, nstage_e;
+  int64_t stage_bytes_e, items_e;
+  int xs_p, xs_e;
+  int64_t red_off_p;   // byte offsets inside the dynamic shared memory
+  int64_t bar_off_p, bar_off_e;
+  LevelArgs lv[kMaxLevels + 1];
+};
+
+// Launch one project pass (template NR chosen from args.nr).  grid = plan.grid_p.
+cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
+// Launch one expand pass.  grid = plan.grid_e.
+cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
+// Opt the kernels into large dynamic shared memory (once per device).
+cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e);
+
+}  // namespace hmat

@@ -1,0 +1,198 @@
+// kernels_expand.cu -- Step 5 (target-side local computation) of the
+// H-matvec, fused over all sibling blocks, all levels and
+// the dense leaf-diagonal blocks so that y is written exactly once:
+//
+//   y_i = sum_{l=1..L} U_l[i, :] . Zt_l[t_l(i), :]      (eq:prod-yuz, all q)
+//       + D_k[i, :] . x_k                                (eq:prod-ydz / eq:prod-dx)
+//
+// with t_l(i) = i / m_l, Zt_l[t] = concat_q z_{t, s_q} (written by project),
+// k = i / b the leaf of row i.  (Under weak admissibility the dense blocks are
+// leaf-diagonal and never cross a shard, so their source
+// x_k is local and the paper's z_local = d_p x_p pass-through is not needed.)
+//
+// Structure (persistent, warp-specialised): CTA b owns an even, contiguous
+// range of row tiles ("items") of Re rows (Re | b).  Per item the producer lane
+// streams, by 1-D bulk TMA, U_1 rows + Zt_1 row, ..., U_L rows + Zt_L row,
+// D rows + the leaf's x segment through an nstage-deep smem ring.  Consumer
+// threads own (row, column-subset) pairs: tpr threads per row, interleaved
+// columns visited in a row-rotated order (bank-conflict-free for the row
+// pitches used here), fp64 FMAs into registers, a shuffle reduction across
+// the tpr lanes, one store of y per row and rhs.
+#include "device_utils.cuh"
+#include "kernels.h"
+
+namespace hmat {
+
+cudaError_t configure_project(int64_t smem);
+
+namespace {
+
+constexpr int CT = kConsumerThreads;
+constexpr int NCW = CT / 32;
+
+template <int NR>
+__global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_constant__ StreamArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t G = gridDim.x, bid = blockIdx.x;
+  const int64_t j0 = a.items_e * bid / G, j1 = a.items_e * (bid + 1) / G;
+  const int Re = a.Re, W = a.W, Wp = a.Wp, Dp = a.Dp, b = a.b, L = a.L;
+  const int NS = a.nstage_e;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
+  uint64_t* empty = full + NS;
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], NCW);
+    }
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer ------------------------------------------------
+    if (lane == 0) {
+      const uint64_t pol_stream = dev::policy_evict_first();
+      const uint64_t pol_keep = dev::policy_evict_last();
+      int it = 0;
+      for (int64_t j = j0; j < j1; ++j) {
+        const int64_t i0 = j * Re;
+        for (int l = 1; l <= L + 1; ++l) {
+          const bool is_d = (l == L + 1);
+          if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+          const int slot = it % NS;
+          if (it >= NS) dev::mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
+          unsigned char* st = smem + slot * a.stage_bytes_e;
+          if (!is_d) {
+            const LevelArgs& lv = a.lv[l];
+            const uint32_t ub = static_cast<uint32_t>(Re * Wp * 8);
+            const uint32_t zb = static_cast<uint32_t>(Wp * NR * 8);
+            const int64_t tg = (a.row0 + i0) / lv.m;
+            dev::mbar_arrive_expect_tx(&full[slot], ub + zb);
+            dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
+            dev::bulk_g2s(st + ub, lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR, zb, &full[slot], pol_keep);
+          } else {
+            const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
+            const int64_t leaf0 = (i0 / b) * b;
+            uint32_t total = db;
+            int64_t lo[NR];
+            uint32_t xb[NR];
+#pragma unroll
+            for (int kk = 0; kk < NR; ++kk) {
+              if (kk < a.nr) {
+                const int64_t start = kk * a.ldx + leaf0;
+                lo[kk] = start & ~int64_t(1);
+                xb[kk] = static_cast<uint32_t>((((start + b + 1) & ~int64_t(1)) - lo[kk]) * 8);
+                total += xb[kk];
+              }
+            }
+            dev::mbar_arrive_expect_tx(&full[slot], total);
+            dev::bulk_g2s(st, a.D + i0 * Dp, db, &full[slot], pol_stream);
+#pragma unroll
+            for (int kk = 0; kk < NR; ++kk)
+              if (kk < a.nr)
+                dev::bulk_g2s(st + db + kk * a.xs_e * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
+          }
+          ++it;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ------------------------------------------------
+  const int t = tid - 32;
+  const int tpr = a.tpr;
+  const int ri = t / tpr, p = t - ri * tpr;
+  const bool active = ri < Re;
+  const int njU = (W + tpr - 1) / tpr;
+  const int njD = (b + tpr - 1) / tpr;
+  int it = 0;
+  for (int64_t j = j0; j < j1; ++j) {
+    const int64_t i0 = j * Re;
+    double acc[NR];
+#pragma unroll
+    for (int kk = 0; kk < NR; ++kk) acc[kk] = 0.0;
+    for (int l = 1; l <= L + 1; ++l) {
+      const bool is_d = (l == L + 1);
+      if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+      const int slot = it % NS;
+      dev::mbar_wait(&full[slot], (it / NS) & 1);
+      const unsigned char* st = smem + slot * a.stage_bytes_e;
+      if (active) {
+        if (!is_d) {
+          const double* Us = reinterpret_cast<const double*>(st) + ri * Wp;
+          const double* Zs = reinterpret_cast<const double*>(st + Re * Wp * 8);
+          int jj = ri % njU;
+          for (int n = 0; n < njU; ++n) {
+            const int col = p + tpr * jj;
+            if (col < W) {
+              const double u = Us[col];
+#pragma unroll
+              for (int kk = 0; kk < NR; ++kk) acc[kk] = fma(u, Zs[col * NR + kk], acc[kk]);
+            }
+            if (++jj == njU) jj = 0;
+          }
+        } else {
+          const double* Ds = reinterpret_cast<const double*>(st) + ri * Dp;
+          const double* xs = reinterpret_cast<const double*>(st + Re * Dp * 8);
+          const int64_t leaf0 = (i0 / b) * b;
+          int xo[NR];
+#pragma unroll
+          for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + leaf0) & 1);
+          int jj = ri % njD;
+          for (int n = 0; n < njD; ++n) {
+            const int col = p + tpr * jj;
+            if (col < b) {
+              const double dv = Ds[col];
+#pragma unroll
+              for (int kk = 0; kk < NR; ++kk) acc[kk] = fma(dv, xs[xo[kk] + col], acc[kk]);
+            }
+            if (++jj == njD) jj = 0;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      ++it;
+    }
+#pragma unroll
+    for (int kk = 0; kk < NR; ++kk)
+      for (int off = tpr >> 1; off >= 1; off >>= 1) acc[kk] += __shfl_xor_sync(0xffffffffu, acc[kk], off);
+    if (active && p == 0) {
+#pragma unroll
+      for (int kk = 0; kk < NR; ++kk)
+        if (kk < a.nr) a.y[kk * a.ldy + i0 + ri] = acc[kk];
+    }
+  }
+}
+
+template <int NR>
+cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  expand_kernel<NR><<<grid, kThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s) {
+  switch (nr_cap) {
+    case 1: return launch_nr<1>(a, grid, smem, s);
+    case 2: return launch_nr<2>(a, grid, smem, s);
+    case 4: return launch_nr<4>(a, grid, smem, s);
+    default: return launch_nr<8>(a, grid, smem, s);
+  }
+}
+
+cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e) {
+  cudaError_t e = configure_project(smem_p);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(expand_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
+  if ((e = cudaFuncSetAttribute(expand_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
+  if ((e = cudaFuncSetAttribute(expand_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
+  return cudaFuncSetAttribute(expand_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+}
+
+}  // namespace hmat

@@ -1,0 +1,126 @@
+// plan.cpp -- see plan.h.
+#include "plan.h"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace hmat {
+
+namespace {
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Largest divisor R of b with R <= rmax and R * width_doubles * 8 <= cap (>= 1).
+int pick_rows(int b, int rmax, int64_t width_doubles, int64_t cap) {
+  int best = 1;
+  for (int R = 1; R <= std::min(b, rmax); ++R)
+    if (b % R == 0 && R * width_doubles * 8 <= cap) best = R;
+  return best;
+}
+
+}  // namespace
+
+std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard, const PlanOptions& opt,
+                       Plan* out) {
+  char msg[256];
+  if (dim < 1 || dim > 3) return "dim must be 1, 2 or 3 (ideal domains, PAPER.md:243-246)";
+  if (depth < 0 || depth >= kMaxLevels) {
+    snprintf(msg, sizeof msg, "depth must be in [0, %d]", kMaxLevels - 1);
+    return msg;
+  }
+  if (leaf < 1) return "leaf_size must be >= 1";
+  if (rank < 1) return "rank must be >= 1";
+  Plan p;
+  p.d = dim;
+  p.c = 1 << dim;
+  p.L = depth;
+  p.b = leaf;
+  p.r = rank;
+  p.W = (p.c - 1) * rank;
+  // N = b c^L must stay below 2^62
+  int64_t N = leaf;
+  for (int l = 0; l < depth; ++l) {
+    if (N > (int64_t(1) << 62) / p.c) return "N = leaf_size * 2^(dim*depth) overflows 2^62";
+    N *= p.c;
+  }
+  p.N = N;
+  int64_t cl = 1;
+  for (int l = 0; l <= depth; ++l) {
+    p.m[l] = N / cl;
+    if (l < depth) cl *= p.c;
+  }
+  const int64_t leaves = N / leaf;  // c^L
+  if (P < 1 || (P & (P - 1)) != 0) return "nranks must be a power of two";
+  if (P > leaves) return "nranks must not exceed the number of leaves 2^(dim*depth)";
+  if (shard < 0 || shard >= P) return "rank id out of range [0, nranks)";
+  if (p.W > 4 * kConsumerThreads) return "unsupported: (2^dim - 1) * rank must be <= 1024";
+  p.P = P;
+  p.rank = shard;
+  p.N_loc = N / P;
+  p.row0 = p.N_loc * shard;
+  p.Wp = p.W + (p.W & 1);
+  p.Dp = leaf + (leaf & 1);
+  p.panel_stride = round_up(p.N_loc * p.Wp, 16);
+
+  // Levels whose parent spans more than one shard need the exchange
+  // (Steps 2-4): c^{l-1} < P.
+  p.cross = 0;
+  int64_t cpow = 1;  // c^{l-1}
+  for (int l = 1; l <= depth; ++l) {
+    if (cpow < P) p.cross = l;
+    cpow *= p.c;
+  }
+  int64_t off_loc = 0, off_ex = 0;
+  cpow = p.c;  // c^l
+  for (int l = 1; l <= depth; ++l) {
+    if (l <= p.cross) {
+      p.zt_off[l] = off_ex;
+      p.zt_tbase[l] = 0;
+      p.zt_count[l] = cpow;
+      off_ex += cpow;
+    } else {
+      p.zt_off[l] = off_loc;
+      p.zt_tbase[l] = p.row0 / p.m[l];
+      p.zt_count[l] = p.N_loc / p.m[l];
+      off_loc += p.zt_count[l];
+    }
+    if (l < depth) cpow *= p.c;
+  }
+  p.z_local_rows = off_loc;
+  p.z_exch_rows = off_ex;
+
+  // Pipeline geometry: stages of R rows with R | b, so every stage lies in one
+  // node at every level (m_l = b c^{L-l}).
+  const int64_t cap = opt.stage_cap_bytes;
+  p.Rp = pick_rows(leaf, kConsumerThreads, p.Wp, cap);
+  p.Re = pick_rows(leaf, kConsumerThreads, std::max(p.Wp, p.Dp), cap);
+  p.tpr = 1;
+  while (p.tpr * 2 <= 32 && p.tpr * 2 * p.Re <= kConsumerThreads) p.tpr *= 2;
+  p.xs_p = static_cast<int>(round_up(p.Rp + 2, 2));
+  p.xs_e = static_cast<int>(round_up(leaf + 2, 2));
+  p.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + int64_t(kMaxNR) * p.xs_p * 8, 128);
+  p.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * kMaxNR * 8,
+                                      int64_t(p.Re) * p.Dp * 8 + int64_t(kMaxNR) * p.xs_e * 8),
+                             128);
+  const int rg = p.W <= kConsumerThreads ? kConsumerThreads / p.W : 1;
+  const int64_t red_bytes = round_up(int64_t(rg) * p.Wp * kMaxNR * 8, 128);
+  const int64_t bar_bytes = 256;
+  p.nstage_p = static_cast<int>(std::min<int64_t>(opt.max_stages, (opt.smem_budget - red_bytes - bar_bytes) / p.stage_bytes_p));
+  p.nstage_e = static_cast<int>(std::min<int64_t>(opt.max_stages, (opt.smem_budget - bar_bytes) / p.stage_bytes_e));
+  if (p.nstage_p < 2 || p.nstage_e < 2) return "unsupported: pipeline stages do not fit in shared memory";
+  p.red_off_p = p.nstage_p * p.stage_bytes_p;
+  p.bar_off_p = p.red_off_p + red_bytes;
+  p.bar_off_e = p.nstage_e * p.stage_bytes_e;
+  p.smem_p = p.bar_off_p + bar_bytes;
+  p.smem_e = p.bar_off_e + bar_bytes;
+
+  p.stages_p = int64_t(depth) * (p.N_loc / p.Rp);
+  p.items_e = p.N_loc / p.Re;
+  const int64_t slots = int64_t(opt.num_sms) * std::max(1, opt.ctas_per_sm);
+  p.grid_p = static_cast<int>(std::min<int64_t>(slots, p.stages_p));
+  p.grid_e = static_cast<int>(std::min<int64_t>(slots, p.items_e));
+  *out = p;
+  return "";
+}
+
+}  // namespace hmat

@@ -1,0 +1,78 @@
+// plan.h -- host-side plan of one H-matrix shard: validation, Morton/level
+// arithmetic, device layout, the persistent-kernel schedule and the
+// cross-GPU exchange layout.  Pure host code (testable without a GPU through
+// hmat_plan_query()).
+//
+// Notation: c = 2^d children per node, L levels below the root,
+// b points per leaf, N = b c^L, m_l = N / c^l rows per level-l node, W = (c-1) r
+// panel width.  A shard owns the contiguous Morton rows [row0, row0 + N_loc),
+// N_loc = N / P: whole subtrees at the partition level (PAPER.md:434-448,
+// §3.1 process-tree rules; block-row factor placement PAPER.md:526-531).
+#pragma once
+#include <cstdint>
+#include <string>
+
+namespace hmat {
+
+constexpr int kMaxLevels = 48;   // L <= 47
+constexpr int kMaxNR = 8;        // right-hand sides per streaming pass
+constexpr int kConsumerThreads = 256;
+constexpr int kThreads = 32 + kConsumerThreads;  // 1 producer warp + 8 consumer warps
+
+struct Plan {
+  // problem
+  int d = 0, c = 0, L = 0, b = 0, r = 0, W = 0;
+  int64_t N = 0;
+  int64_t m[kMaxLevels + 1] = {};   // m[l] = N / c^l
+  // shard
+  int P = 1, rank = 0;
+  int64_t N_loc = 0, row0 = 0;
+  // device layout (doubles)
+  int Wp = 0, Dp = 0;               // row pitches of U/V panels and D (even => 16-B rows)
+  int64_t panel_stride = 0;         // doubles between consecutive level panels (128-B multiple)
+  // z storage per level l (target-major, per rhs-pass): Zt_l[t][col][k], pitch Wp*kMaxNR
+  // levels 1..cross live in the exchange buffer (all c^l targets), others in the
+  // local buffer (this shard's targets only).
+  int cross = 0;                    // levels 1..cross need the cross-GPU exchange (c^{l-1} < P)
+  int64_t zt_off[kMaxLevels + 1] = {};    // offset in units of (Wp*kMaxNR) doubles
+  int64_t zt_tbase[kMaxLevels + 1] = {};  // global index of the first stored target
+  int64_t zt_count[kMaxLevels + 1] = {};
+  int64_t z_local_rows = 0;         // targets stored in the local z buffer
+  int64_t z_exch_rows = 0;          // targets stored in the exchange buffer
+  // schedule
+  int Rp = 0, Re = 0;               // rows per pipeline stage: project / expand (both divide b)
+  int tpr = 0;                      // expand: threads per row
+  int nstage_p = 0, nstage_e = 0;   // pipeline depth
+  int64_t stage_bytes_p = 0, stage_bytes_e = 0;
+  int64_t smem_p = 0, smem_e = 0;   // dynamic shared memory per CTA
+  int64_t red_off_p = 0, bar_off_p = 0, bar_off_e = 0;  // byte offsets in it
+  int grid_p = 0, grid_e = 0;       // persistent grid sizes
+  int64_t stages_p = 0;             // L * N_loc / Rp
+  int64_t items_e = 0;              // N_loc / Re
+  int xs_p = 0, xs_e = 0;           // doubles reserved per rhs for x chunks in a stage
+};
+
+struct PlanOptions {
+  int num_sms = 148;
+  int ctas_per_sm = 1;
+  int stage_cap_bytes = 36 * 1024;  // upper bound on the factor bytes of one stage
+  int smem_budget = 200 * 1024;     // dynamic smem per CTA for the pipeline
+  int max_stages = 6;
+};
+
+// Validates arguments and fills `plan`.  Returns "" on success, else a message.
+std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard, const PlanOptions& opt,
+                       Plan* plan);
+
+// q-th sibling of node t (ascending child order, skipping t) and the slot of
+// sibling s in t's list (R6).
+inline int64_t sibling_of(int c, int64_t t, int q) {
+  int me = static_cast<int>(t % c);
+  return (t / c) * c + (q < me ? q : q + 1);
+}
+inline int slot_of(int c, int64_t t, int64_t s) {
+  int me = static_cast<int>(t % c), other = static_cast<int>(s % c);
+  return other < me ? other : other - 1;
+}
+
+}  // namespace hmat

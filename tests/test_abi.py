@@ -1,0 +1,99 @@
+"""The C-ABI library loads, exports every symbol include/hmat.h declares, and
+rejects invalid arguments before touching a device (runs without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2008_12441_b200 import hmat as hm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "hmat.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hmat_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    decl = declared_symbols()
+    assert len(decl) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", hm.LIB_PATH], capture_output=True, text=True, check=True)
+    exported = set(re.findall(r" T (hmat_\w+)", out.stdout))
+    missing = [s for s in decl if s not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    assert set(hm.EXPORTS) == set(decl)
+
+
+def test_binding_names_match_c_names():
+    for s in declared_symbols():
+        assert hasattr(hm, s), s
+
+
+def expect(status, fn, *args):
+    with pytest.raises(hm.HMatError) as ei:
+        fn(*args)
+    assert ei.value.status == status
+    assert hm.hmat_last_error() != ""
+    return str(ei.value)
+
+
+@pytest.mark.parametrize("args,needle", [
+    ((3, 4, 64, 8), "dim"),
+    ((3, 0, 64, 8), "dim"),
+    ((-1, 2, 64, 8), "depth"),
+    ((48, 1, 1, 1), "depth"),
+    ((3, 2, 0, 8), "leaf"),
+    ((3, 2, 64, 0), "rank"),
+    ((40, 2, 64, 1), "overflow"),
+])
+def test_plan_query_rejects_invalid(args, needle):
+    msg = expect(hm.HMAT_ERR_INVALID, hm.hmat_plan_query, *args)
+    assert needle in msg
+
+
+def test_invalid_partitions():
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_plan_query, 3, 2, 64, 8, 3, 0)     # not a power of two
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_plan_query, 1, 2, 64, 8, 8, 0)     # more ranks than leaves
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_plan_query, 3, 2, 64, 8, 2, 2)     # rank id out of range
+    expect(hm.HMAT_ERR_UNSUPPORTED, hm.hmat_plan_query, 3, 3, 64, 147, 1, 0)  # W = 1029 > 1024
+
+
+def test_create_rejects_invalid_before_device_work():
+    # invalid shapes are caught by validation even with real pointers
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_create_uninit, 3, 5, 64, 8, None)
+    # NULL panels
+    h = ctypes.c_void_p()
+    assert hm._lib.hmat_create(2, 2, 4, 2, None, None, None, None, ctypes.byref(h)) == hm.HMAT_ERR_INVALID
+    assert hm._lib.hmat_create(2, 2, 4, 2, None, None, None, None, None) == hm.HMAT_ERR_INVALID
+    # P > 1 needs an NCCL id
+    d = hm._dist(nranks=2, rank=0, device=0)
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_create_uninit, 3, 2, 64, 8, d)
+
+
+def test_null_handles():
+    assert hm._lib.hmat_destroy(None) == hm.HMAT_OK
+    assert hm._lib.hmat_num_points(None) == -1
+    assert hm._lib.hmat_matvec(None, None, None, 1) == hm.HMAT_ERR_INVALID
+    assert "NULL" in hm.hmat_last_error()
+    assert hm._lib.hmat_launches_per_matvec(None, 1) == -1
+
+
+def test_no_gpu_means_error_not_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    # a valid request on a machine without a GPU must fail loudly (no CPU path)
+    status = hm._lib.hmat_create_uninit(1, 1, 2, 1, None, ctypes.byref(ctypes.c_void_p()))
+    assert status == hm.HMAT_ERR_CUDA
+
+
+def test_plan_query_valid():
+    info = hm.hmat_plan_query(9, 2, 64, 16)
+    assert info.N == 2 ** 24 and info.row_begin == 0 and info.row_end == 2 ** 24
+    assert info.W == 48 and info.cross_levels == 0 and info.exchange_rows == 0
+    assert 64 % info.Rp == 0 and 64 % info.Re == 0
+    assert info.smem_p <= 227 * 1024 and info.smem_e <= 227 * 1024

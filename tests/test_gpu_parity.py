@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element, on the same seeded inputs.  Tolerance: rel l2 <= 1e-12
+per right-hand side (BASELINE.json north_star) and |dy_i| <= 1e-12 max|y|."""
+import itertools
+
+import numpy as np
+import pytest
+
+from gen import hgen
+from gen.hgen import CONFIGS, HConfig
+from oracle import oracle
+from tests.helpers import assert_parity, device_operator
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2008_12441_b200 import hmat as hm
+
+
+def gpu_matvec(cfg, U, V, D, x, **kw):
+    """hmat_create from host panels, device x/y, hmat_matvec."""
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        xd = torch.from_numpy(np.asfortranarray(x)).cuda() if x.ndim == 1 else \
+            torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+        yd = torch.empty_like(xd) if x.ndim == 1 else torch.empty(x.shape[1], x.shape[0], dtype=torch.float64,
+                                                                 device="cuda").t()
+        if kw:
+            hm.hmat_matvec_parts(h, xd, yd, **kw)
+        else:
+            hm.hmat_matvec(h, xd, yd)
+        torch.cuda.synchronize()
+        return yd.cpu().numpy()
+    finally:
+        hm.hmat_destroy(h)
+
+
+def host_case(cfg, nrhs=1, vec=0):
+    U, V, D = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs, vec=vec)
+    if nrhs == 1:
+        x = np.ascontiguousarray(x[:, 0])
+    return U, V, D, x
+
+
+SMALL = [HConfig(f"s{d}{L}{b}{r}", d=d, L=L, b=b, r=r, seed=1000 + 97 * d + 13 * L + 7 * b + r)
+         for d, L, b, r in [
+             (1, 0, 5, 1), (2, 0, 64, 3), (1, 1, 1, 1), (1, 3, 2, 2), (1, 6, 4, 3), (1, 9, 8, 5),
+             (2, 1, 4, 2), (2, 2, 3, 3), (2, 3, 64, 8), (2, 4, 16, 16), (2, 3, 7, 5), (2, 5, 8, 1),
+             (3, 1, 8, 4), (3, 2, 2, 2), (3, 2, 64, 32), (3, 3, 5, 3), (3, 2, 1, 7),
+             (2, 3, 64, 86), (3, 2, 8, 146),  # W = 258 (> 256 consumer threads), W = 1022
+         ]]
+
+
+@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_small_shapes(cfg, nrhs):
+    """Ragged leaf sizes (odd b), ranks, depths 0..9, d = 1, 2, 3, W above the
+    consumer-thread count, 1 and 3 right-hand sides."""
+    U, V, D, x = host_case(cfg, nrhs)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    assert_parity(gpu_matvec(cfg, U, V, D, x), ref)
+
+
+def test_c1_against_oracle_and_brute_force():
+    """BASELINE configs[0] (also vs the assembled 4096 x 4096 dense matrix)."""
+    cfg = CONFIGS["c1"]
+    U, V, D, x = host_case(cfg)
+    y = gpu_matvec(cfg, U, V, D, x)
+    assert_parity(y, oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x))
+    A = oracle.assemble(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D)
+    assert_parity(y, oracle.dense_matvec(A, x))
+
+
+@pytest.mark.parametrize("nrhs", [2, 4, 5, 8, 9, 17])
+def test_multi_rhs(nrhs):
+    cfg = HConfig("mr", d=3, L=3, b=64, r=8, seed=4242)  # N = 32768, W = 56
+    U, V, D, x = host_case(cfg, nrhs)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    assert_parity(gpu_matvec(cfg, U, V, D, x), ref)
+
+
+def test_level_parts():
+    """hmat_matvec_parts reproduces the oracle's per-level pieces y_l and y_D."""
+    cfg = HConfig("lp", d=2, L=5, b=16, r=4, seed=77)
+    U, V, D, x = host_case(cfg)
+    for mask, dense in [(0, True), (1, False), (1 << 4, False), (0b10110, False), (0, False), (0b11111, True)]:
+        ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x, level_mask=mask, dense=dense)
+        y = gpu_matvec(cfg, U, V, D, x, level_mask=mask, dense=dense)
+        assert_parity(y, ref)
+
+
+def test_c2_full_parity():
+    """BASELINE configs[1] in full (N = 2^20) against the oracle's block loop."""
+    cfg = CONFIGS["c2"]
+    U, V, D, x = host_case(cfg)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    assert_parity(gpu_matvec(cfg, U, V, D, x), ref)
+
+
+def test_host_io_misaligned_x_and_determinism():
+    cfg = HConfig("io", d=2, L=4, b=64, r=16, seed=99)
+    U, V, D, x = host_case(cfg, nrhs=2)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        # host numpy in/out (the e2e path)
+        yh = np.zeros((cfg.N, 2), order="F")
+        hm.hmat_matvec(h, np.asfortranarray(x), yh)
+        assert_parity(yh, ref)
+        # device, x misaligned by one double (staged internally)
+        big = torch.zeros(2 * cfg.N + 1, dtype=torch.float64, device="cuda")
+        xv = big[1:].view(2, cfg.N).t()
+        xv.copy_(torch.from_numpy(np.asfortranarray(x)))
+        yd = torch.empty(2, cfg.N, dtype=torch.float64, device="cuda").t()
+        hm.hmat_matvec(h, xv, yd)
+        y1 = yd.cpu().numpy()
+        assert np.array_equal(y1, yh)
+        # bitwise reproducible (deterministic reductions, no atomics on values)
+        for _ in range(3):
+            hm.hmat_matvec(h, xv, yd)
+            assert np.array_equal(yd.cpu().numpy(), y1)
+        assert hm.hmat_launches_per_matvec(h, 2) == 2
+    finally:
+        hm.hmat_destroy(h)
+
+
+def test_zero_x_gives_zero():
+    cfg = HConfig("z", d=3, L=2, b=64, r=4, seed=5)
+    U, V, D, _ = host_case(cfg)
+    y = gpu_matvec(cfg, U, V, D, np.zeros(cfg.N))
+    assert np.array_equal(y, np.zeros(cfg.N))
+
+
+def test_device_generator_matches_host_bitwise():
+    """gen/: the device filler writes exactly the host filler's bits."""
+    cfg = CONFIGS["c3"]
+    for tag, level in [(hgen.TAG_U, 1), (hgen.TAG_V, 5), (hgen.TAG_D, 0)]:
+        ncols = cfg.b if tag == hgen.TAG_D else cfg.W
+        r0, r1 = 123456, 123456 + 700
+        dev = torch.empty(r1 - r0, ncols + 2, dtype=torch.float64, device="cuda")
+        hgen.dev_fill_panel(cfg, tag, level, r0, r1, dev.data_ptr(), ncols + 2)
+        host = hgen.panel(cfg, tag, level, r0, r1)
+        assert np.array_equal(dev[:, :ncols].cpu().numpy(), host)
+    xd = torch.empty(3, 1000, dtype=torch.float64, device="cuda")
+    hgen.dev_fill_x(cfg, 3, 7, 5000, 6000, xd.data_ptr(), 1000)
+    assert np.array_equal(xd.cpu().numpy().T, hgen.xblock(cfg, nrhs=3, vec=7, row_begin=5000, row_end=6000))
+
+
+def sample_rows(cfg, rng):
+    """Rows spread over the first and last level-1 nodes plus random ones,
+    grouped so the oracle reuses z of shared ancestors."""
+    N, b = cfg.N, cfg.b
+    rows = [0, 1, b - 1, b, 2 * b + 5] + [N - 1, N - b, N - 2 * b - 3]
+    rows += list(rng.integers(0, N, 4))
+    return np.array(sorted(set(int(r) for r in rows)))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_size_sampled_rows(name):
+    """BASELINE configs at full size, in the bench's launch configuration
+    (device-generated panels, default plan): sampled y rows vs the oracle,
+    which recomputes each row from eq:hmat-vec-add with on-demand factors."""
+    cfg = CONFIGS[name]
+    free, _ = torch.cuda.mem_get_info()
+    if free < cfg.factor_bytes * 1.05:
+        pytest.skip(f"needs {cfg.factor_bytes / 1e9:.0f} GB of device memory")
+    h = device_operator(cfg, hm)
+    try:
+        x = torch.empty(cfg.N, dtype=torch.float64, device="cuda")
+        hgen.dev_fill_x(cfg, 1, 3, 0, cfg.N, x.data_ptr(), cfg.N)
+        y = torch.empty_like(x)
+        hm.hmat_matvec(h, x, y)
+        torch.cuda.synchronize()
+        xh = x.cpu().numpy()
+        assert np.array_equal(xh, hgen.xblock(cfg, nrhs=1, vec=3)[:, 0])
+        rows = sample_rows(cfg, np.random.default_rng(1))
+        ref = oracle.rows_generated(cfg, xh, rows)
+        got = y.cpu().numpy()[rows]
+        # per-row check against the column's scale (the oracle only sees rows)
+        scale = np.abs(y.cpu().numpy()).max()
+        assert np.abs(got - ref).max() <= 1e-12 * scale
+        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    finally:
+        hm.hmat_destroy(h)
+        torch.cuda.empty_cache()
