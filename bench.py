@@ -241,7 +241,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
     nrhs = cfg.nrhs
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()   # one stream for fills, matvecs and the timing events
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
 
     nid = None

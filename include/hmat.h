@@ -67,7 +67,8 @@ typedef enum {
 } hmat_status;
 
 /* Multi-GPU placement of one rank.  NULL => one GPU, the current device,
- * N_loc = N, a library-owned stream. */
+ * N_loc = N, a library-owned stream (a blocking stream, so it is ordered with
+ * work on the legacy default stream). */
 typedef struct {
   int nranks;                 /* P: a power of two <= c^L                            */
   int rank;                   /* 0 <= rank < P; owns Morton rows [rank N/P, ...)     */

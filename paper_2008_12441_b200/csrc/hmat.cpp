@@ -172,7 +172,8 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   if (dist && dist->cuda_stream) {
     H->stream = static_cast<cudaStream_t>(dist->cuda_stream);
   } else {
-    cudaError_t e = cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking);
+    // blocking stream: ordered with work the caller put on the legacy default stream
+    cudaError_t e = cudaStreamCreateWithFlags(&H->stream, cudaStreamDefault);
     if (e != cudaSuccess) return bail(cuda_fail(e, "cudaStreamCreate"));
     H->own_stream = true;
   }

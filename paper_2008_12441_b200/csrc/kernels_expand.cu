@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
       const uint64_t pol_stream = dev::policy_evict_first();
       const uint64_t pol_keep = dev::policy_evict_last();
       int it = 0;
+      const int64_t ipl = b / Re;                        // items per leaf
+      int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
       for (int64_t j = j0; j < j1; ++j) {
         const int64_t i0 = j * Re;
         for (int l = 1; l <= L + 1; ++l) {
@@ -75,7 +77,6 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
             dev::bulk_g2s(st + ub, lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR, zb, &full[slot], pol_keep);
           } else {
             const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
-            const int64_t leaf0 = (i0 / b) * b;
             uint32_t total = db;
             int64_t lo[NR];
             uint32_t xb[NR];
@@ -97,6 +98,10 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
           }
           ++it;
         }
+        if (++in_leaf == ipl) {
+          in_leaf = 0;
+          leaf0 += b;
+        }
       }
     }
     return;
@@ -109,6 +114,9 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
   const bool active = ri < Re;
   const int njU = (W + tpr - 1) / tpr;
   const int njD = (b + tpr - 1) / tpr;
+  const int rotU = ri % njU, rotD = ri % njD;  // row-rotated column order (bank spread)
+  const int64_t ipl = b / Re;
+  int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
   int it = 0;
   for (int64_t j = j0; j < j1; ++j) {
     const int64_t i0 = j * Re;
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
         if (!is_d) {
           const double* Us = reinterpret_cast<const double*>(st) + ri * Wp;
           const double* Zs = reinterpret_cast<const double*>(st + Re * Wp * 8);
-          int jj = ri % njU;
+          int jj = rotU;
           for (int n = 0; n < njU; ++n) {
             const int col = p + tpr * jj;
             if (col < W) {
@@ -138,11 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
         } else {
           const double* Ds = reinterpret_cast<const double*>(st) + ri * Dp;
           const double* xs = reinterpret_cast<const double*>(st + Re * Dp * 8);
-          const int64_t leaf0 = (i0 / b) * b;
           int xo[NR];
 #pragma unroll
           for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + leaf0) & 1);
-          int jj = ri % njD;
+          int jj = rotD;
           for (int n = 0; n < njD; ++n) {
             const int col = p + tpr * jj;
             if (col < b) {
@@ -165,6 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
 #pragma unroll
       for (int kk = 0; kk < NR; ++kk)
         if (kk < a.nr) a.y[kk * a.ldy + i0 + ri] = acc[kk];
+    }
+    if (++in_leaf == ipl) {
+      in_leaf = 0;
+      leaf0 += b;
     }
   }
 }

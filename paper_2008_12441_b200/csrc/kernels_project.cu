@@ -34,15 +34,6 @@ constexpr int CT = kConsumerThreads;
 constexpr int NCW = CT / 32;
 constexpr int MAXCPT = 4;  // columns per consumer thread when W > CT
 
-__device__ __forceinline__ int64_t next_active(int64_t k, int64_t k1, int64_t SL, uint64_t mask) {
-  while (k < k1) {
-    const int64_t l = k / SL + 1;
-    if ((mask >> (l - 1)) & 1ull) return k;
-    k = l * SL;
-  }
-  return k1;
-}
-
 // CTA owning stage k under the even split [S b / G, S (b+1) / G).
 __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { return ((k + 1) * G - 1) / S; }
 
@@ -51,11 +42,11 @@ __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { r
 template <int NR>
 __device__ __forceinline__ void scatter_z(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int col, int kk,
                                           double v) {
-  const int c = a.c;
+  const int d = __ffs(a.c) - 1;  // c = 2^d
   const int q = col / a.r, aa = col - q * a.r;
-  const int me = static_cast<int>(sg % c);
-  const int64_t t = (sg / c) * c + (q < me ? q : q + 1);
-  const int tc = static_cast<int>(t % c);
+  const int me = static_cast<int>(sg & (a.c - 1));
+  const int64_t t = ((sg >> d) << d) + (q < me ? q : q + 1);
+  const int tc = static_cast<int>(t & (a.c - 1));
   const int qt = me < tc ? me : me - 1;
   lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)(qt * a.r + aa) * NR + kk] = v;
 }
@@ -92,12 +83,17 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
       const uint64_t pol_keep = dev::policy_evict_last();
       const uint32_t vbytes = static_cast<uint32_t>(Rp * Wp * 8);
       int it = 0;
-      for (int64_t k = next_active(k0, k1, SL, a.level_mask); k < k1;
-           k = next_active(k + 1, k1, SL, a.level_mask), ++it) {
+      int64_t l = k0 / SL + 1, kl = k0 - (l - 1) * SL;  // level and stage-in-level of k
+      for (int64_t k = k0; k < k1;) {
+        if (!((a.level_mask >> (l - 1)) & 1ull)) {  // masked level: skip it
+          k += SL - kl;
+          ++l;
+          kl = 0;
+          continue;
+        }
         const int slot = it % NS;
         if (it >= NS) dev::mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
-        const int64_t l = k / SL + 1;
-        const int64_t i0 = (k % SL) * Rp;
+        const int64_t i0 = kl * Rp;
         unsigned char* st = smem + slot * a.stage_bytes_p;
         uint32_t total = vbytes;
         int64_t lo[NR];
@@ -117,6 +113,12 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
         for (int kk = 0; kk < NR; ++kk)
           if (kk < a.nr)
             dev::bulk_g2s(st + vbytes + kk * a.xs_p * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
+        ++it;
+        ++k;
+        if (++kl == SL) {
+          kl = 0;
+          ++l;
+        }
       }
     }
     return;
@@ -136,12 +138,28 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
     for (int kk = 0; kk < NR; ++kk) acc[j][kk] = 0.0;
 
   int it = 0;
-  for (int64_t k = next_active(k0, k1, SL, a.level_mask); k < k1;
-       k = next_active(k + 1, k1, SL, a.level_mask), ++it) {
+  int64_t l = k0 / SL + 1, kl = k0 - (l - 1) * SL;
+  // node (segment) cursor of the current level: seg_stages stages per local
+  // node, sl = local node index, pos = stage index inside the node
+  int64_t seg_stages = 0, sl = 0, pos = 0, sg0 = 0;
+  int64_t cur_level = -1;
+  for (int64_t k = k0; k < k1;) {
+    if (!((a.level_mask >> (l - 1)) & 1ull)) {
+      k += SL - kl;
+      ++l;
+      kl = 0;
+      continue;
+    }
+    if (l != cur_level) {  // entering a level: one set of divisions per level
+      cur_level = l;
+      seg_stages = a.lv[l].seg_rows / Rp;
+      sl = kl / seg_stages;
+      pos = kl - sl * seg_stages;
+      sg0 = a.row0 / a.lv[l].m;
+    }
     const int slot = it % NS;
     dev::mbar_wait(&full[slot], (it / NS) & 1);
-    const int64_t l = k / SL + 1;
-    const int64_t i0 = (k % SL) * Rp;
+    const int64_t i0 = kl * Rp;
     const unsigned char* st = smem + slot * a.stage_bytes_p;
     const double* Vs = reinterpret_cast<const double*>(st);
     const double* xs = reinterpret_cast<const double*>(st + Rp * Wp * 8);
@@ -149,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
 #pragma unroll
     for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
     if (active) {
+#pragma unroll 4
       for (int row = rho; row < Rp; row += RG) {
         double xv[NR];
 #pragma unroll
@@ -166,16 +185,27 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
     }
     __syncwarp();
     if (lane == 0) dev::mbar_arrive(&empty[slot]);
+    ++it;
+    const bool node_end = (pos + 1 == seg_stages);
+    const bool range_end = (k + 1 == k1);
+    const int64_t this_l = l, this_sl = sl;
+    // advance the cursors to the next stage
+    ++k;
+    if (++pos == seg_stages) {
+      pos = 0;
+      ++sl;
+    }
+    if (++kl == SL) {
+      kl = 0;
+      ++l;
+    }
+    if (!node_end && !range_end) continue;
 
     // ---- end of a (local) node at this level, or end of this CTA's range ----
-    const LevelArgs& lv = a.lv[l];
-    const int64_t seg_stages = lv.seg_rows / Rp;
-    const int64_t sl = (k % SL) / seg_stages;                 // local node index
-    const int64_t sa = (l - 1) * SL + sl * seg_stages, sb = sa + seg_stages;
-    if (k + 1 != sb && k + 1 != k1) continue;
-
+    const LevelArgs& lv = a.lv[this_l];
+    const int64_t sa = (this_l - 1) * SL + this_sl * seg_stages, sb = sa + seg_stages;
     const bool complete = sa >= k0 && sb <= k1;
-    const int64_t sg = a.row0 / lv.m + sl;                     // global source node
+    const int64_t sg = sg0 + this_sl;                           // global source node
     if (active) {
 #pragma unroll
       for (int j = 0; j < MAXCPT; ++j) {
