@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -50,10 +51,11 @@ int env_int(const char* name, int def) {
 hmat::PlanOptions options_from_env(int num_sms) {
   hmat::PlanOptions o;
   o.num_sms = num_sms;
-  o.ctas_per_sm = env_int("HMAT_CTAS_PER_SM", 1);
+  o.ctas_per_sm = env_int("HMAT_CTAS_PER_SM", 2);
   o.stage_cap_bytes = env_int("HMAT_STAGE_KB", 36) * 1024;
   o.smem_budget = env_int("HMAT_SMEM_KB", 200) * 1024;
-  o.max_stages = env_int("HMAT_MAX_STAGES", 6);
+  o.max_stages_p = env_int("HMAT_MAX_STAGES_P", env_int("HMAT_MAX_STAGES", o.max_stages_p));
+  o.max_stages_e = env_int("HMAT_MAX_STAGES_E", env_int("HMAT_MAX_STAGES", o.max_stages_e));
   return o;
 }
 
@@ -72,6 +74,16 @@ bool is_device_ptr(const void* p) {
 }
 
 int nr_cap(int nr) { return nr <= 1 ? 1 : nr <= 2 ? 2 : nr <= 4 ? 4 : 8; }
+
+cudaError_t configure_all(const hmat::Plan& p) {
+  int64_t sp = 0, se = 0;
+  for (const auto& y : p.lay) {
+    sp = std::max(sp, y.smem_p);
+    se = std::max(se, y.smem_e);
+  }
+  return hmat::configure_kernels(sp, se);
+}
+
 
 struct EventPair {
   int phase;
@@ -192,16 +204,16 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = alloc(reinterpret_cast<void**>(&H->D), size_t(p.N_loc) * p.Dp * sizeof(double), "D")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zloc), size_t(p.z_local_rows) * zrow, "z")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zex), size_t(p.z_exch_rows) * zrow, "exchange")) ||
-      (e = alloc(reinterpret_cast<void**>(&H->part), size_t(p.grid_p) * 2 * zrow, "partials")) ||
-      (e = alloc(reinterpret_cast<void**>(&H->cnt), size_t(p.grid_p + 1) * sizeof(int), "tickets"))) {
+      (e = alloc(reinterpret_cast<void**>(&H->part), size_t(p.grid_p_max) * p.L * 2 * zrow, "partials")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->cnt), size_t(p.grid_p_max) * p.L * sizeof(int) + 256, "tickets"))) {
     std::string what = g_err;
     return bail(cuda_fail(e, what.c_str()));
   }
-  if ((e = cudaMemsetAsync(H->cnt, 0, size_t(p.grid_p + 1) * sizeof(int), H->stream)) ||
+  if ((e = cudaMemsetAsync(H->cnt, 0, size_t(p.grid_p_max) * p.L * sizeof(int) + 256, H->stream)) ||
       (e = cudaMemsetAsync(H->U, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->V, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->D, 0, size_t(p.N_loc) * p.Dp * sizeof(double), H->stream)) ||
-      (e = hmat::configure_kernels(p.smem_p, p.smem_e)) || (e = cudaStreamSynchronize(H->stream)))
+      (e = configure_all(p)) || (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   if (p.P > 1) {
     std::string m = hmat::comm_create(dist->nccl_unique_id, p.P, p.rank, &H->comm);
@@ -361,25 +373,26 @@ hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, ui
   a.level_mask = level_mask;
   a.dense = dense ? 1 : 0;
   a.Rp = p.Rp;
-  a.nstage_p = p.nstage_p;
-  a.stage_bytes_p = p.stage_bytes_p;
   a.stages_p = p.stages_p;
   a.part = H->part;
   a.cnt = H->cnt;
   a.Re = p.Re;
   a.tpr = p.tpr;
-  a.nstage_e = p.nstage_e;
-  a.stage_bytes_e = p.stage_bytes_e;
   a.items_e = p.items_e;
   a.xs_p = p.xs_p;
   a.xs_e = p.xs_e;
-  a.red_off_p = p.red_off_p;
-  a.bar_off_p = p.bar_off_p;
-  a.bar_off_e = p.bar_off_e;
 
   for (int c0 = 0; c0 < nrhs; c0 += hmat::kMaxNR) {
     const int nr = nrhs - c0 < hmat::kMaxNR ? nrhs - c0 : hmat::kMaxNR;
     const int cap = nr_cap(nr);
+    const hmat::Plan::Layout& ly = p.lay[hmat::nr_index(cap)];
+    a.nstage_p = ly.nstage_p;
+    a.stage_bytes_p = ly.stage_bytes_p;
+    a.nstage_e = ly.nstage_e;
+    a.stage_bytes_e = ly.stage_bytes_e;
+    a.red_off_p = ly.red_off_p;
+    a.bar_off_p = ly.bar_off_p;
+    a.bar_off_e = ly.bar_off_e;
     a.nr = nr;
     a.x = xd + c0 * ldx;
     a.y = yd + c0 * n;
@@ -392,9 +405,9 @@ hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, ui
     }
     const size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
     if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(H->zex, 0, exch * sizeof(double), H->stream));
-    if (p.grid_p > 0 && level_mask) {
+    if (ly.grid_p > 0 && level_mask) {
       prof_begin(H, 0, &ep);
-      CUDA_TRY(hmat::launch_project(a, cap, p.grid_p, p.smem_p, H->stream));
+      CUDA_TRY(hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream));
       prof_end(H, &ep);
     }
     if (p.P > 1 && exch) {
@@ -404,7 +417,7 @@ hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, ui
       prof_end(H, &ep);
     }
     prof_begin(H, 2, &ep);
-    CUDA_TRY(hmat::launch_expand(a, cap, p.grid_e, p.smem_e, H->stream));
+    CUDA_TRY(hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream));
     prof_end(H, &ep);
   }
   if (!y_dev) {
@@ -485,7 +498,7 @@ hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches) {
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs) {
   if (!H || nrhs < 1) return -1;
   const int64_t passes = (nrhs + hmat::kMaxNR - 1) / hmat::kMaxNR;
-  return passes * ((H->plan.grid_p > 0 ? 1 : 0) + 1);
+  return passes * ((H->plan.stages_p > 0 ? 1 : 0) + 1);
 }
 
 hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
@@ -507,12 +520,12 @@ hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nra
   info->Rp = p.Rp;
   info->Re = p.Re;
   info->tpr = p.tpr;
-  info->nstage_p = p.nstage_p;
-  info->nstage_e = p.nstage_e;
-  info->grid_p = p.grid_p;
-  info->grid_e = p.grid_e;
-  info->smem_p = p.smem_p;
-  info->smem_e = p.smem_e;
+  info->nstage_p = p.lay[0].nstage_p;
+  info->nstage_e = p.lay[0].nstage_e;
+  info->grid_p = p.lay[0].grid_p;
+  info->grid_e = p.lay[0].grid_e;
+  info->smem_p = p.lay[0].smem_p;
+  info->smem_e = p.lay[0].smem_e;
   return HMAT_OK;
 }
 

@@ -44,8 +44,8 @@ struct StreamArgs {
   // project schedule
   int Rp, nstage_p;
   int64_t stage_bytes_p, stages_p;
-  double* part;      // [grid_p][2][Wp*NR]
-  int* cnt;          // [grid_p]
+  double* part;      // [L][grid_p][2][Wp*NR] partial node sums
+  int* cnt;          // [L][grid_p] arrival tickets
   // expand schedule
   int Re, tpr, nstage_e;
   int64_t stage_bytes_e, items_e;
@@ -60,6 +60,6 @@ cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t sm
 // Launch one expand pass.  grid = plan.grid_e.
 cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
 // Opt the kernels into large dynamic shared memory (once per device).
-cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e);
+cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e);  // max over layouts
 
 }  // namespace hmat

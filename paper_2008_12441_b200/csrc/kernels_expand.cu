@@ -31,7 +31,7 @@ constexpr int CT = kConsumerThreads;
 constexpr int NCW = CT / 32;
 
 template <int NR>
-__global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_constant__ StreamArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_constant__ StreamArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
     if (lane == 0) {
       const uint64_t pol_stream = dev::policy_evict_first();
       const uint64_t pol_keep = dev::policy_evict_last();
-      int it = 0;
+      int slot = 0;
+      uint32_t phase = 0;
       const int64_t ipl = b / Re;                        // items per leaf
       int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
       for (int64_t j = j0; j < j1; ++j) {
@@ -64,8 +65,7 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
         for (int l = 1; l <= L + 1; ++l) {
           const bool is_d = (l == L + 1);
           if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
-          const int slot = it % NS;
-          if (it >= NS) dev::mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
+          dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
           unsigned char* st = smem + slot * a.stage_bytes_e;
           if (!is_d) {
             const LevelArgs& lv = a.lv[l];
@@ -96,7 +96,10 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
               if (kk < a.nr)
                 dev::bulk_g2s(st + db + kk * a.xs_e * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
           }
-          ++it;
+          if (++slot == NS) {
+            slot = 0;
+            phase ^= 1;
+          }
         }
         if (++in_leaf == ipl) {
           in_leaf = 0;
@@ -108,54 +111,72 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
   }
 
   // ---------------- consumers ------------------------------------------------
+  // tpr threads per row; thread p of row ri owns the column pairs
+  // cp = p + tpr*jj (columns 2cp, 2cp+1), visited in a row-rotated order so the
+  // 16-byte smem reads of a warp's rows fall in different bank halves.
   const int t = tid - 32;
   const int tpr = a.tpr;
   const int ri = t / tpr, p = t - ri * tpr;
   const bool active = ri < Re;
-  const int njU = (W + tpr - 1) / tpr;
-  const int njD = (b + tpr - 1) / tpr;
-  const int rotU = ri % njU, rotD = ri % njD;  // row-rotated column order (bank spread)
+  const int NP = Wp >> 1, NPD = Dp >> 1;
+  const int njU = (NP + tpr - 1) / tpr;
+  const int njD = (NPD + tpr - 1) / tpr;
+  const int rotU = ri % njU, rotD = ri % njD;
   const int64_t ipl = b / Re;
   int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
-  int it = 0;
+  int slot = 0;
+  uint32_t phase = 0;
   for (int64_t j = j0; j < j1; ++j) {
     const int64_t i0 = j * Re;
-    double acc[NR];
+    double acc[NR], acc2[NR];  // two chains: even / odd columns
 #pragma unroll
-    for (int kk = 0; kk < NR; ++kk) acc[kk] = 0.0;
+    for (int kk = 0; kk < NR; ++kk) acc[kk] = acc2[kk] = 0.0;
     for (int l = 1; l <= L + 1; ++l) {
       const bool is_d = (l == L + 1);
       if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
-      const int slot = it % NS;
-      dev::mbar_wait(&full[slot], (it / NS) & 1);
+      dev::mbar_wait(&full[slot], phase);
       const unsigned char* st = smem + slot * a.stage_bytes_e;
       if (active) {
         if (!is_d) {
-          const double* Us = reinterpret_cast<const double*>(st) + ri * Wp;
+          const double2* U2 = reinterpret_cast<const double2*>(st) + ri * NP;
           const double* Zs = reinterpret_cast<const double*>(st + Re * Wp * 8);
           int jj = rotU;
           for (int n = 0; n < njU; ++n) {
-            const int col = p + tpr * jj;
-            if (col < W) {
-              const double u = Us[col];
+            const int cp = p + tpr * jj;
+            if (cp < NP) {
+              double2 u = U2[cp];
+              if (2 * cp + 1 >= W) u.y = 0.0;  // padding column of an odd W
+              if (NR == 1) {
+                const double2 z = reinterpret_cast<const double2*>(Zs)[cp];
+                acc[0] = fma(u.x, z.x, acc[0]);
+                acc2[0] = fma(u.y, z.y, acc2[0]);
+              } else {
 #pragma unroll
-              for (int kk = 0; kk < NR; ++kk) acc[kk] = fma(u, Zs[col * NR + kk], acc[kk]);
+                for (int kk = 0; kk < NR; ++kk) {
+                  acc[kk] = fma(u.x, Zs[(2 * cp) * NR + kk], acc[kk]);
+                  acc2[kk] = fma(u.y, Zs[(2 * cp + 1) * NR + kk], acc2[kk]);
+                }
+              }
             }
             if (++jj == njU) jj = 0;
           }
         } else {
-          const double* Ds = reinterpret_cast<const double*>(st) + ri * Dp;
+          const double2* D2 = reinterpret_cast<const double2*>(st) + ri * NPD;
           const double* xs = reinterpret_cast<const double*>(st + Re * Dp * 8);
           int xo[NR];
 #pragma unroll
           for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + leaf0) & 1);
           int jj = rotD;
           for (int n = 0; n < njD; ++n) {
-            const int col = p + tpr * jj;
-            if (col < b) {
-              const double dv = Ds[col];
+            const int cp = p + tpr * jj;
+            if (cp < NPD) {
+              const double2 dv = D2[cp];
+              const bool odd_ok = 2 * cp + 1 < b;  // padding column of an odd b
 #pragma unroll
-              for (int kk = 0; kk < NR; ++kk) acc[kk] = fma(dv, xs[xo[kk] + col], acc[kk]);
+              for (int kk = 0; kk < NR; ++kk) {
+                acc[kk] = fma(dv.x, xs[xo[kk] + 2 * cp], acc[kk]);
+                if (odd_ok) acc2[kk] = fma(dv.y, xs[xo[kk] + 2 * cp + 1], acc2[kk]);
+              }
             }
             if (++jj == njD) jj = 0;
           }
@@ -163,11 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1) expand_kernel(const __grid_consta
       }
       __syncwarp();
       if (lane == 0) dev::mbar_arrive(&empty[slot]);
-      ++it;
+      if (++slot == NS) {
+        slot = 0;
+        phase ^= 1;
+      }
     }
 #pragma unroll
-    for (int kk = 0; kk < NR; ++kk)
+    for (int kk = 0; kk < NR; ++kk) {
+      acc[kk] += acc2[kk];
       for (int off = tpr >> 1; off >= 1; off >>= 1) acc[kk] += __shfl_xor_sync(0xffffffffu, acc[kk], off);
+    }
     if (active && p == 0) {
 #pragma unroll
       for (int kk = 0; kk < NR; ++kk)

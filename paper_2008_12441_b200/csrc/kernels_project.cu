@@ -8,9 +8,10 @@
 // V_1 | V_2 | ... | V_L.
 //
 // Structure (persistent, warp-specialised):
-//   * grid = min(#SM x CTAs/SM, #stages); CTA b owns the contiguous stage range
-//     [S b / G, S (b+1) / G) of the L * N_loc / Rp stages, so every CTA streams
-//     the same number of bytes.
+//   * grid = #SM x CTAs/SM; each level's N_loc / Rp stages are split evenly
+//     over the CTAs, CTA b owning [SL b / G, SL (b+1) / G) of every level, so
+//     every CTA streams the same bytes and the same mix of coarse levels (one
+//     node flush per many stages) and fine levels (one flush per stage).
 //   * warp 0 (one elected lane) issues 1-D bulk TMA copies of each stage --
 //     Rp rows of V_l (Rp * Wp doubles, contiguous) and the matching x segment --
 //     into an nstage-deep shared-memory ring guarded by full/empty mbarriers.
@@ -32,7 +33,6 @@ namespace {
 
 constexpr int CT = kConsumerThreads;
 constexpr int NCW = CT / 32;
-constexpr int MAXCPT = 4;  // columns per consumer thread when W > CT
 
 // CTA owning stage k under the even split [S b / G, S (b+1) / G).
 __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { return ((k + 1) * G - 1) / S; }
@@ -51,18 +51,16 @@ __device__ __forceinline__ void scatter_z(const StreamArgs& a, const LevelArgs& 
   lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)(qt * a.r + aa) * NR + kk] = v;
 }
 
-template <int NR>
-__global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_constant__ StreamArgs a) {
+template <int NR, int PAIRS>
+__global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_constant__ StreamArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t G = gridDim.x, bid = blockIdx.x;
-  const int64_t S = a.stages_p;
-  const int64_t k0 = S * bid / G, k1 = S * (bid + 1) / G;
-  const int Rp = a.Rp, W = a.W, Wp = a.Wp;
-  const int64_t SL = a.N_loc / Rp;  // stages per level
+  const int Rp = a.Rp, W = a.W, Wp = a.Wp, L = a.L;
+  const int64_t SL = a.N_loc / Rp;      // stages per level
+  const int64_t GL = G < SL ? G : SL;   // CTAs active at each level
   const int NS = a.nstage_p;
-  double* red = reinterpret_cast<double*>(smem + a.red_off_p);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_p);
   uint64_t* empty = full + NS;
   volatile int* flag = reinterpret_cast<volatile int*>(empty + NS);
@@ -75,6 +73,10 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
     dev::fence_mbar_init();
   }
   __syncthreads();
+  if (bid >= GL) return;
+  // every level is split evenly over the GL CTAs, so each CTA streams the same
+  // mix of coarse and fine levels (fine levels flush a node per stage)
+  const int64_t k0 = SL * bid / GL, k1 = SL * (bid + 1) / GL;  // this CTA's stages of each level
 
   if (warp == 0) {
     // ---------------- producer: one lane streams V_l rows + x segments -------
@@ -82,42 +84,37 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
       const uint64_t pol_stream = dev::policy_evict_first();
       const uint64_t pol_keep = dev::policy_evict_last();
       const uint32_t vbytes = static_cast<uint32_t>(Rp * Wp * 8);
-      int it = 0;
-      int64_t l = k0 / SL + 1, kl = k0 - (l - 1) * SL;  // level and stage-in-level of k
-      for (int64_t k = k0; k < k1;) {
-        if (!((a.level_mask >> (l - 1)) & 1ull)) {  // masked level: skip it
-          k += SL - kl;
-          ++l;
-          kl = 0;
-          continue;
-        }
-        const int slot = it % NS;
-        if (it >= NS) dev::mbar_wait(&empty[slot], ((it / NS) & 1) ^ 1);
-        const int64_t i0 = kl * Rp;
-        unsigned char* st = smem + slot * a.stage_bytes_p;
-        uint32_t total = vbytes;
-        int64_t lo[NR];
-        uint32_t xb[NR];
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int l = 1; l <= L; ++l) {
+        if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+        const double* Vl = a.V + (l - 1) * a.panel_stride;
+        for (int64_t k = k0; k < k1; ++k) {
+          dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
+          const int64_t i0 = k * Rp;
+          unsigned char* st = smem + slot * a.stage_bytes_p;
+          uint32_t total = vbytes;
+          int64_t lo[NR];
+          uint32_t xb[NR];
 #pragma unroll
-        for (int kk = 0; kk < NR; ++kk) {
-          if (kk < a.nr) {
-            const int64_t start = kk * a.ldx + i0;
-            lo[kk] = start & ~int64_t(1);
-            xb[kk] = static_cast<uint32_t>((((start + Rp + 1) & ~int64_t(1)) - lo[kk]) * 8);
-            total += xb[kk];
+          for (int kk = 0; kk < NR; ++kk) {
+            if (kk < a.nr) {
+              const int64_t start = kk * a.ldx + i0;
+              lo[kk] = start & ~int64_t(1);
+              xb[kk] = static_cast<uint32_t>((((start + Rp + 1) & ~int64_t(1)) - lo[kk]) * 8);
+              total += xb[kk];
+            }
           }
-        }
-        dev::mbar_arrive_expect_tx(&full[slot], total);
-        dev::bulk_g2s(st, a.V + (l - 1) * a.panel_stride + i0 * Wp, vbytes, &full[slot], pol_stream);
+          dev::mbar_arrive_expect_tx(&full[slot], total);
+          dev::bulk_g2s(st, Vl + i0 * Wp, vbytes, &full[slot], pol_stream);
 #pragma unroll
-        for (int kk = 0; kk < NR; ++kk)
-          if (kk < a.nr)
-            dev::bulk_g2s(st + vbytes + kk * a.xs_p * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
-        ++it;
-        ++k;
-        if (++kl == SL) {
-          kl = 0;
-          ++l;
+          for (int kk = 0; kk < NR; ++kk)
+            if (kk < a.nr)
+              dev::bulk_g2s(st + vbytes + kk * a.xs_p * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
+          if (++slot == NS) {
+            slot = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -126,151 +123,157 @@ __global__ void __launch_bounds__(kThreads, 1) project_kernel(const __grid_const
 
   // ---------------- consumers ------------------------------------------------
   const int t = tid - 32;
-  const int RG = W <= CT ? CT / W : 1;
-  const int rho = W <= CT ? t / W : 0;
-  const int col0 = W <= CT ? t % W : t;
-  const bool active = rho < RG;
-  const int cpt = W <= CT ? 1 : (W + CT - 1) / CT;
-  double acc[MAXCPT][NR];
+  // each thread owns column pair(s) cp (columns 2cp, 2cp+1; Wp is even) and,
+  // when the pairs fit in one pass (PAIRS == 1), the rows rho, rho+RG, ...
+  const int NP = Wp >> 1;
+  const int RG = PAIRS == 1 ? CT / NP : 1;
+  const int rho = PAIRS == 1 ? t / NP : 0;
+  const int cp0 = PAIRS == 1 ? t - rho * NP : t;
+  const bool active = PAIRS == 1 ? rho < RG : true;
+  const int64_t red_elems = (int64_t)RG * Wp * NR;  // one of two alternating buffers
+  double* red_base = reinterpret_cast<double*>(smem + a.red_off_p);
+  int red_buf = 0;
+  double2 acc[PAIRS][NR];
 #pragma unroll
-  for (int j = 0; j < MAXCPT; ++j)
+  for (int j = 0; j < PAIRS; ++j)
 #pragma unroll
-    for (int kk = 0; kk < NR; ++kk) acc[j][kk] = 0.0;
+    for (int kk = 0; kk < NR; ++kk) acc[j][kk] = make_double2(0.0, 0.0);
 
-  int it = 0;
-  int64_t l = k0 / SL + 1, kl = k0 - (l - 1) * SL;
-  // node (segment) cursor of the current level: seg_stages stages per local
-  // node, sl = local node index, pos = stage index inside the node
-  int64_t seg_stages = 0, sl = 0, pos = 0, sg0 = 0;
-  int64_t cur_level = -1;
-  for (int64_t k = k0; k < k1;) {
-    if (!((a.level_mask >> (l - 1)) & 1ull)) {
-      k += SL - kl;
-      ++l;
-      kl = 0;
-      continue;
-    }
-    if (l != cur_level) {  // entering a level: one set of divisions per level
-      cur_level = l;
-      seg_stages = a.lv[l].seg_rows / Rp;
-      sl = kl / seg_stages;
-      pos = kl - sl * seg_stages;
-      sg0 = a.row0 / a.lv[l].m;
-    }
-    const int slot = it % NS;
-    dev::mbar_wait(&full[slot], (it / NS) & 1);
-    const int64_t i0 = kl * Rp;
-    const unsigned char* st = smem + slot * a.stage_bytes_p;
-    const double* Vs = reinterpret_cast<const double*>(st);
-    const double* xs = reinterpret_cast<const double*>(st + Rp * Wp * 8);
-    int xo[NR];
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int l = 1; l <= L; ++l) {
+    if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+    const LevelArgs& lv = a.lv[l];
+    // node cursor: seg stages per local node, sl = node index, pos = stage in node
+    const int64_t seg = lv.seg_rows / Rp;
+    int64_t sl = k0 / seg, pos = k0 - sl * seg;
+    const int64_t sg0 = a.row0 / lv.m;
+    for (int64_t k = k0; k < k1; ++k) {
+      dev::mbar_wait(&full[slot], phase);
+      const int64_t i0 = k * Rp;
+      const unsigned char* st = smem + slot * a.stage_bytes_p;
+      const double2* V2 = reinterpret_cast<const double2*>(st);
+      const double* xs = reinterpret_cast<const double*>(st + Rp * Wp * 8);
+      int xo[NR];
 #pragma unroll
-    for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
-    if (active) {
+      for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
+      if (active) {
 #pragma unroll 4
-      for (int row = rho; row < Rp; row += RG) {
-        double xv[NR];
+        for (int row = rho; row < Rp; row += RG) {
+          double xv[NR];
 #pragma unroll
-        for (int kk = 0; kk < NR; ++kk) xv[kk] = kk < a.nr ? xs[xo[kk] + row] : 0.0;
+          for (int kk = 0; kk < NR; ++kk) xv[kk] = xs[xo[kk] + row];
 #pragma unroll
-        for (int j = 0; j < MAXCPT; ++j) {
-          const int col = col0 + j * CT;
-          if (j < cpt && col < W) {
-            const double v = Vs[row * Wp + col];
+          for (int j = 0; j < PAIRS; ++j) {
+            const int cp = cp0 + j * CT;
+            if (PAIRS == 1 || cp < NP) {
+              const double2 v = V2[row * NP + cp];
 #pragma unroll
-            for (int kk = 0; kk < NR; ++kk) acc[j][kk] = fma(v, xv[kk], acc[j][kk]);
+              for (int kk = 0; kk < NR; ++kk) {
+                acc[j][kk].x = fma(v.x, xv[kk], acc[j][kk].x);
+                acc[j][kk].y = fma(v.y, xv[kk], acc[j][kk].y);
+              }
+            }
           }
         }
       }
-    }
-    __syncwarp();
-    if (lane == 0) dev::mbar_arrive(&empty[slot]);
-    ++it;
-    const bool node_end = (pos + 1 == seg_stages);
-    const bool range_end = (k + 1 == k1);
-    const int64_t this_l = l, this_sl = sl;
-    // advance the cursors to the next stage
-    ++k;
-    if (++pos == seg_stages) {
-      pos = 0;
-      ++sl;
-    }
-    if (++kl == SL) {
-      kl = 0;
-      ++l;
-    }
-    if (!node_end && !range_end) continue;
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      if (++slot == NS) {
+        slot = 0;
+        phase ^= 1;
+      }
+      const bool node_end = (pos + 1 == seg);
+      const int64_t this_sl = sl;
+      if (++pos == seg) {
+        pos = 0;
+        ++sl;
+      }
+      if (!node_end && k + 1 != k1) continue;
 
-    // ---- end of a (local) node at this level, or end of this CTA's range ----
-    const LevelArgs& lv = a.lv[this_l];
-    const int64_t sa = (this_l - 1) * SL + this_sl * seg_stages, sb = sa + seg_stages;
-    const bool complete = sa >= k0 && sb <= k1;
-    const int64_t sg = sg0 + this_sl;                           // global source node
-    if (active) {
+      // ---- end of a (local) node, or end of this CTA's range of the level ----
+      const int64_t sa = this_sl * seg, sb = sa + seg;  // the node's stages
+      const bool complete = sa >= k0 && sb <= k1;
+      const int64_t sg = sg0 + this_sl;                 // global source node
+      double* red = red_base + red_buf * red_elems;
+      red_buf ^= 1;  // alternate buffers: one barrier per complete node suffices
+      if (active) {
 #pragma unroll
-      for (int j = 0; j < MAXCPT; ++j) {
-        const int col = col0 + j * CT;
-        if (j < cpt && col < W) {
+        for (int j = 0; j < PAIRS; ++j) {
+          const int cp = cp0 + j * CT;
+          if (PAIRS == 1 || cp < NP) {
 #pragma unroll
-          for (int kk = 0; kk < NR; ++kk) {
-            red[((int64_t)rho * Wp + col) * NR + kk] = acc[j][kk];
-            acc[j][kk] = 0.0;
+            for (int kk = 0; kk < NR; ++kk) {
+              red[((int64_t)rho * Wp + 2 * cp) * NR + kk] = acc[j][kk].x;
+              red[((int64_t)rho * Wp + 2 * cp + 1) * NR + kk] = acc[j][kk].y;
+              acc[j][kk] = make_double2(0.0, 0.0);
+            }
           }
         }
       }
-    }
-    dev::named_bar_sync(1, CT);
-    if (complete) {
-      for (int o = t; o < W * NR; o += CT) {
-        const int col = o / NR, kk = o - col * NR;
-        double v = 0.0;
-        for (int g = 0; g < RG; ++g) v += red[((int64_t)g * Wp + col) * NR + kk];
-        if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
-      }
       dev::named_bar_sync(1, CT);
-    } else {
-      // partial node sum of this CTA: slot 0 if the node holds our first
-      // stage, slot 1 otherwise (it then holds our last stage)
-      const int myslot = sa <= k0 ? 0 : 1;
-      double* pp = a.part + (bid * 2 + myslot) * (int64_t)Wp * NR;
-      for (int o = t; o < W * NR; o += CT) {
-        const int col = o / NR, kk = o - col * NR;
-        double v = 0.0;
-        for (int g = 0; g < RG; ++g) v += red[((int64_t)g * Wp + col) * NR + kk];
-        pp[(int64_t)col * NR + kk] = v;
-      }
-      __threadfence();
-      dev::named_bar_sync(1, CT);
-      const int64_t b0 = owner_of(sa, S, G), b1 = owner_of(sb - 1, S, G);
-      if (t == 0) {
-        const int prev = atomicAdd(&a.cnt[b1], 1);
-        *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
-      }
-      dev::named_bar_sync(1, CT);
-      if (*flag) {
-        __threadfence();
-        const int64_t kb0 = S * b0 / G;
-        const int slot0 = (sa == kb0) ? 0 : 1;
+      if (complete) {
         for (int o = t; o < W * NR; o += CT) {
           const int col = o / NR, kk = o - col * NR;
           double v = 0.0;
-          for (int64_t bb = b0; bb <= b1; ++bb) {
-            const int sl_b = bb == b0 ? slot0 : 0;
-            v += dev::ld_cg(a.part + (bb * 2 + sl_b) * (int64_t)Wp * NR + (int64_t)col * NR + kk);
-          }
+          for (int g = 0; g < RG; ++g) v += red[((int64_t)g * Wp + col) * NR + kk];
           if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
         }
-        if (t == 0) a.cnt[b1] = 0;  // re-arm the ticket for the next launch
+      } else {
+        // partial node sum of this CTA: slot 0 if the node holds our first
+        // stage of the level, slot 1 otherwise (it then holds our last one)
+        const int myslot = sa <= k0 ? 0 : 1;
+        double* pp = a.part + (((int64_t)(l - 1) * G + bid) * 2 + myslot) * (int64_t)Wp * NR;
+        for (int o = t; o < W * NR; o += CT) {
+          const int col = o / NR, kk = o - col * NR;
+          double v = 0.0;
+          for (int g = 0; g < RG; ++g) v += red[((int64_t)g * Wp + col) * NR + kk];
+          pp[(int64_t)col * NR + kk] = v;
+        }
+        __threadfence();
+        dev::named_bar_sync(1, CT);
+        const int64_t b0 = owner_of(sa, SL, GL), b1 = owner_of(sb - 1, SL, GL);
+        int* ticket = a.cnt + (int64_t)(l - 1) * G + b1;
+        if (t == 0) {
+          const int prev = atomicAdd(ticket, 1);
+          *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
+        }
+        dev::named_bar_sync(1, CT);
+        if (*flag) {
+          __threadfence();
+          const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
+          for (int o = t; o < W * NR; o += CT) {
+            const int col = o / NR, kk = o - col * NR;
+            double v = 0.0;
+            for (int64_t bb = b0; bb <= b1; ++bb) {
+              const int sl_b = bb == b0 ? slot0 : 0;
+              v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NR +
+                              (int64_t)col * NR + kk);
+            }
+            if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
+          }
+          if (t == 0) *ticket = 0;  // re-arm for the next launch
+        }
+        dev::named_bar_sync(1, CT);  // *flag is rewritten by the next partial node
       }
-      dev::named_bar_sync(1, CT);
     }
   }
 }
 
 template <int NR>
 cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  project_kernel<NR><<<grid, kThreads, smem, s>>>(a);
+  if ((a.Wp >> 1) <= CT)
+    project_kernel<NR, 1><<<grid, kThreads, smem, s>>>(a);
+  else
+    project_kernel<NR, 2><<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int NR>
+cudaError_t configure_nr(int64_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(project_kernel<NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(project_kernel<NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace
@@ -286,10 +289,10 @@ cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t sm
 
 cudaError_t configure_project(int64_t smem) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(project_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-  if ((e = cudaFuncSetAttribute(project_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-  if ((e = cudaFuncSetAttribute(project_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-  return cudaFuncSetAttribute(project_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if ((e = configure_nr<1>(smem))) return e;
+  if ((e = configure_nr<2>(smem))) return e;
+  if ((e = configure_nr<4>(smem))) return e;
+  return configure_nr<8>(smem);
 }
 
 }  // namespace hmat

@@ -98,27 +98,39 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   while (p.tpr * 2 <= 32 && p.tpr * 2 * p.Re <= kConsumerThreads) p.tpr *= 2;
   p.xs_p = static_cast<int>(round_up(p.Rp + 2, 2));
   p.xs_e = static_cast<int>(round_up(leaf + 2, 2));
-  p.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + int64_t(kMaxNR) * p.xs_p * 8, 128);
-  p.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * kMaxNR * 8,
-                                      int64_t(p.Re) * p.Dp * 8 + int64_t(kMaxNR) * p.xs_e * 8),
-                             128);
-  const int rg = p.W <= kConsumerThreads ? kConsumerThreads / p.W : 1;
-  const int64_t red_bytes = round_up(int64_t(rg) * p.Wp * kMaxNR * 8, 128);
-  const int64_t bar_bytes = 256;
-  p.nstage_p = static_cast<int>(std::min<int64_t>(opt.max_stages, (opt.smem_budget - red_bytes - bar_bytes) / p.stage_bytes_p));
-  p.nstage_e = static_cast<int>(std::min<int64_t>(opt.max_stages, (opt.smem_budget - bar_bytes) / p.stage_bytes_e));
-  if (p.nstage_p < 2 || p.nstage_e < 2) return "unsupported: pipeline stages do not fit in shared memory";
-  p.red_off_p = p.nstage_p * p.stage_bytes_p;
-  p.bar_off_p = p.red_off_p + red_bytes;
-  p.bar_off_e = p.nstage_e * p.stage_bytes_e;
-  p.smem_p = p.bar_off_p + bar_bytes;
-  p.smem_e = p.bar_off_e + bar_bytes;
-
   p.stages_p = int64_t(depth) * (p.N_loc / p.Rp);
   p.items_e = p.N_loc / p.Re;
-  const int64_t slots = int64_t(opt.num_sms) * std::max(1, opt.ctas_per_sm);
-  p.grid_p = static_cast<int>(std::min<int64_t>(slots, p.stages_p));
-  p.grid_e = static_cast<int>(std::min<int64_t>(slots, p.items_e));
+  const int np = p.Wp / 2;  // column pairs owned by project's consumer threads
+  const int rg = np <= kConsumerThreads ? kConsumerThreads / np : 1;
+  const int64_t bar_bytes = 256;
+  p.grid_p_max = 0;
+  for (int li = 0; li < 4; ++li) {
+    const int64_t NR = int64_t(1) << li;
+    Plan::Layout& y = p.lay[li];
+    y.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + NR * p.xs_p * 8, 128);
+    y.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * NR * 8,
+                                        int64_t(p.Re) * p.Dp * 8 + NR * p.xs_e * 8),
+                               128);
+    const int64_t red_bytes = round_up(2 * int64_t(rg) * p.Wp * NR * 8, 128);  // two alternating buffers
+    // the requested CTAs per SM, or fewer if two pipeline stages do not fit
+    for (int ctas = std::max(1, opt.ctas_per_sm); ctas >= 1; --ctas) {
+      const int64_t budget = std::min<int64_t>(opt.smem_budget, 227 * 1024 / ctas - 1024);
+      y.nstage_p = static_cast<int>(std::min<int64_t>(opt.max_stages_p, (budget - red_bytes - bar_bytes) / y.stage_bytes_p));
+      y.nstage_e = static_cast<int>(std::min<int64_t>(opt.max_stages_e, (budget - bar_bytes) / y.stage_bytes_e));
+      y.ctas_per_sm = ctas;
+      if (y.nstage_p >= 2 && y.nstage_e >= 2) break;
+    }
+    if (y.nstage_p < 2 || y.nstage_e < 2) return "unsupported: pipeline stages do not fit in shared memory";
+    y.red_off_p = y.nstage_p * y.stage_bytes_p;
+    y.bar_off_p = y.red_off_p + red_bytes;
+    y.bar_off_e = y.nstage_e * y.stage_bytes_e;
+    y.smem_p = y.bar_off_p + bar_bytes;
+    y.smem_e = y.bar_off_e + bar_bytes;
+    const int64_t slots = int64_t(opt.num_sms) * y.ctas_per_sm;
+    y.grid_p = static_cast<int>(std::min<int64_t>(slots, depth > 0 ? p.N_loc / p.Rp : 0));
+    y.grid_e = static_cast<int>(std::min<int64_t>(slots, p.items_e));
+    p.grid_p_max = std::max(p.grid_p_max, y.grid_p);
+  }
   *out = p;
   return "";
 }

@@ -42,22 +42,31 @@ struct Plan {
   // schedule
   int Rp = 0, Re = 0;               // rows per pipeline stage: project / expand (both divide b)
   int tpr = 0;                      // expand: threads per row
-  int nstage_p = 0, nstage_e = 0;   // pipeline depth
-  int64_t stage_bytes_p = 0, stage_bytes_e = 0;
-  int64_t smem_p = 0, smem_e = 0;   // dynamic shared memory per CTA
-  int64_t red_off_p = 0, bar_off_p = 0, bar_off_e = 0;  // byte offsets in it
-  int grid_p = 0, grid_e = 0;       // persistent grid sizes
   int64_t stages_p = 0;             // L * N_loc / Rp
   int64_t items_e = 0;              // N_loc / Re
   int xs_p = 0, xs_e = 0;           // doubles reserved per rhs for x chunks in a stage
+  // shared-memory layout and grid per right-hand-side capacity NR = 1, 2, 4, 8
+  struct Layout {
+    int ctas_per_sm = 0;
+    int nstage_p = 0, nstage_e = 0;
+    int64_t stage_bytes_p = 0, stage_bytes_e = 0;
+    int64_t red_off_p = 0, bar_off_p = 0, bar_off_e = 0;  // byte offsets
+    int64_t smem_p = 0, smem_e = 0;                        // dynamic smem per CTA
+    int grid_p = 0, grid_e = 0;                            // persistent grids
+  } lay[4];
+  int grid_p_max = 0;               // partial-sum slots to allocate
 };
+
+// index into Plan::lay of a right-hand-side capacity 1, 2, 4 or 8
+inline int nr_index(int nr_cap) { return nr_cap <= 1 ? 0 : nr_cap <= 2 ? 1 : nr_cap <= 4 ? 2 : 3; }
 
 struct PlanOptions {
   int num_sms = 148;
-  int ctas_per_sm = 1;
+  int ctas_per_sm = 2;
   int stage_cap_bytes = 36 * 1024;  // upper bound on the factor bytes of one stage
   int smem_budget = 200 * 1024;     // dynamic smem per CTA for the pipeline
-  int max_stages = 6;
+  int max_stages_p = 2;             // project: measured best at 2 stages x 2 CTAs per SM
+  int max_stages_e = 3;             // expand: measured best at 3 stages x 2 CTAs per SM
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.
