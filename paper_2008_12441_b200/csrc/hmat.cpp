@@ -108,6 +108,11 @@ struct hmat_s {
   double* ybuf = nullptr;
   size_t xcap = 0, ycap = 0;  // doubles
   hmat::Comm* comm = nullptr;
+  // DMMA (many right-hand sides) buffers, allocated on first use
+  double* zloc_d = nullptr;
+  double* zex_d = nullptr;
+  double* part_d = nullptr;
+  int* cnt_d = nullptr;
   bool prof = false;
   std::vector<EventPair> ev;
   std::vector<cudaEvent_t> pool;
@@ -130,6 +135,10 @@ void release(hmat_s* H) {
   cudaFree(H->cnt);
   cudaFree(H->xbuf);
   cudaFree(H->ybuf);
+  cudaFree(H->zloc_d);
+  cudaFree(H->zex_d);
+  cudaFree(H->part_d);
+  cudaFree(H->cnt_d);
   for (auto& e : H->ev) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -213,7 +222,8 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = cudaMemsetAsync(H->U, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->V, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->D, 0, size_t(p.N_loc) * p.Dp * sizeof(double), H->stream)) ||
-      (e = configure_all(p)) || (e = cudaStreamSynchronize(H->stream)))
+      (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(p.dsmem_p, p.dsmem_e))) ||
+      (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   if (p.P > 1) {
     std::string m = hmat::comm_create(dist->nccl_unique_id, p.P, p.rank, &H->comm);
@@ -246,6 +256,25 @@ void prof_end(hmat_s* H, EventPair* ep) {
   if (!H->prof) return;
   cudaEventRecord(ep->b, H->stream);
   H->ev.push_back(*ep);
+}
+
+bool use_dmma(const hmat::Plan& p, int nrhs) {
+  if (!p.dmma_ok || env_int("HMAT_DMMA_OFF", 0)) return false;
+  return nrhs >= env_int("HMAT_DMMA_MIN", 16);
+}
+
+hmat_status ensure_dmma(hmat_s* H) {
+  if (H->cnt_d) return HMAT_OK;
+  const hmat::Plan& p = H->plan;
+  const size_t zrow = size_t(p.W) * hmat::kDmmaNB * sizeof(double);
+  const size_t tickets = size_t(p.dgrid_p) * p.L * sizeof(int) + 256;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zloc_d), std::max<size_t>(256, size_t(p.z_local_rows) * zrow)));
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zex_d), std::max<size_t>(256, size_t(p.z_exch_rows) * zrow)));
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->part_d),
+                      std::max<size_t>(256, size_t(p.dgrid_p) * p.L * 2 * p.Wp * hmat::kDmmaNB * sizeof(double))));
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->cnt_d), tickets));
+  CUDA_TRY(cudaMemsetAsync(H->cnt_d, 0, tickets, H->stream));
+  return HMAT_OK;
 }
 
 hmat_status ensure_buf(double** buf, size_t* cap, size_t n) {
@@ -382,7 +411,48 @@ hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, ui
   a.xs_p = p.xs_p;
   a.xs_e = p.xs_e;
 
-  for (int c0 = 0; c0 < nrhs; c0 += hmat::kMaxNR) {
+  if (use_dmma(p, nrhs)) {
+    hmat_status st = ensure_dmma(H);
+    if (st != HMAT_OK) return st;
+    a.vp = p.vp;
+    a.nstage_p = p.dns_p;
+    a.stage_bytes_p = p.dstage_p;
+    a.bar_off_p = p.dns_p * p.dstage_p;
+    a.nstage_e = p.dns_e;
+    a.stage_bytes_e = p.dstage_e;
+    a.bar_off_e = p.dns_e * p.dstage_e;
+    a.part = H->part_d;
+    a.cnt = H->cnt_d;
+    for (int c0 = 0; c0 < nrhs; c0 += hmat::kDmmaNB) {
+      a.nr = nrhs - c0 < hmat::kDmmaNB ? nrhs - c0 : hmat::kDmmaNB;
+      a.x = xd + c0 * ldx;
+      a.y = yd + c0 * n;
+      for (int l = 1; l <= p.L; ++l) {
+        hmat::LevelArgs& lv = a.lv[l];
+        lv.m = p.m[l];
+        lv.seg_rows = p.m[l] < n ? p.m[l] : n;
+        lv.zt = (l <= p.cross ? H->zex_d : H->zloc_d) + p.zt_off[l] * p.W * hmat::kDmmaNB;
+        lv.tbase = p.zt_tbase[l];
+      }
+      const size_t exch = size_t(p.z_exch_rows) * p.W * hmat::kDmmaNB;
+      if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(H->zex_d, 0, exch * sizeof(double), H->stream));
+      if (p.dgrid_p > 0 && level_mask) {
+        prof_begin(H, 0, &ep);
+        CUDA_TRY(hmat::launch_project_dmma(a, p.dgrid_p, p.dsmem_p, H->stream));
+        prof_end(H, &ep);
+      }
+      if (p.P > 1 && exch) {
+        prof_begin(H, 1, &ep);
+        std::string m = hmat::comm_allreduce_sum(H->comm, H->zex_d, exch, H->stream);
+        if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+        prof_end(H, &ep);
+      }
+      prof_begin(H, 2, &ep);
+      CUDA_TRY(hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream));
+      prof_end(H, &ep);
+    }
+  }
+  for (int c0 = 0; !use_dmma(p, nrhs) && c0 < nrhs; c0 += hmat::kMaxNR) {
     const int nr = nrhs - c0 < hmat::kMaxNR ? nrhs - c0 : hmat::kMaxNR;
     const int cap = nr_cap(nr);
     const hmat::Plan::Layout& ly = p.lay[hmat::nr_index(cap)];
@@ -497,7 +567,8 @@ hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches) {
 
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs) {
   if (!H || nrhs < 1) return -1;
-  const int64_t passes = (nrhs + hmat::kMaxNR - 1) / hmat::kMaxNR;
+  const int per = use_dmma(H->plan, nrhs) ? hmat::kDmmaNB : hmat::kMaxNR;
+  const int64_t passes = (nrhs + per - 1) / per;
   return passes * ((H->plan.stages_p > 0 ? 1 : 0) + 1);
 }
 

@@ -50,6 +50,7 @@ struct StreamArgs {
   int Re, tpr, nstage_e;
   int64_t stage_bytes_e, items_e;
   int xs_p, xs_e;
+  int vp;              // DMMA project: smem pitch of staged V rows
   int64_t red_off_p;   // byte offsets inside the dynamic shared memory
   int64_t bar_off_p, bar_off_e;
   LevelArgs lv[kMaxLevels + 1];
@@ -59,6 +60,10 @@ struct StreamArgs {
 cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
 // Launch one expand pass.  grid = plan.grid_e.
 cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
+// FP64 tensor-core (DMMA) passes of kDmmaNB right-hand sides (kernels_dmma.cu).
+cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
+cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
+cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e);
 // Opt the kernels into large dynamic shared memory (once per device).
 cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e);  // max over layouts
 

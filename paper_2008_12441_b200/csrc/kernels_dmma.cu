@@ -1,0 +1,379 @@
+// kernels_dmma.cu -- the many-right-hand-side H-matvec on the FP64 tensor cores
+// (BASELINE configs[4]: 64 right-hand sides).
+//
+// With NB = 64 right-hand sides the two steps become dense contractions:
+//   project (Step 1, eq:prod-vx):  Z_s (W x NB) = V_s^T (W x m) X_s (m x NB)
+//   expand  (Step 5, eq:prod-yuz, eq:prod-ydz):      Y_tile (64 x NB) = sum_l U_l[tile] (64 x W) Zt_l[t] (W x NB)
+//                                                                       + D[tile] (64 x b) X_leaf (b x NB)
+// computed with warp-level mma.sync.m8n8k4.f64 (SASS DMMA; tcgen05 has no
+// f64 kind on sm_100a).  Measured on this B200: DMMA 37.1 TFLOP/s, DFMA 36.5
+// (scripts/fp64_peak.cu), so the tensor path's gain is issue slots and
+// operand reuse, not a higher peak.
+//
+// Operands reach shared memory by 1-D bulk TMA copies into padded pitches
+// (row pitch = 4 mod 16 doubles), which makes every m8n8k4 fragment load
+// conflict-free; Zt is stored "fragment-major" (the exact order in which the
+// expand kernel's B fragments are read), so one copy per stage brings it in.
+// Pipelines, CTA splits and the deterministic ticketed reduction of node
+// partials are the same as in the single-vector kernels.
+#include "device_utils.cuh"
+#include "kernels.h"
+
+namespace hmat {
+namespace {
+
+constexpr int CT = kConsumerThreads;   // expand: 8 consumer warps
+constexpr int NCW = CT / 32;
+// project: W/16 consumer warps (<= 14), each owning a 16 x NB slab of the
+// W x NB accumulator tile (2 M-tiles x 8 N-tiles, 64 registers), + 1 producer
+// warp: <= 15 warps keeps 4 warps per SM sub-partition at <= 128 registers.
+constexpr int kMaxThreadsP = 32 + 14 * 32;
+constexpr int NB = kDmmaNB;   // right-hand sides per pass
+constexpr int KR = kDmmaKR;   // project: V rows (the GEMM's k) per stage
+constexpr int RE = kDmmaRE;   // expand: rows per item
+constexpr int KC = kDmmaKC;   // expand: k-columns per stage
+constexpr int XP = kDmmaXP;   // smem pitch of staged X columns (= 4 mod 16)
+constexpr int AP = kDmmaAP;   // smem pitch of staged U / D row chunks (= 4 mod 16)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Fragment-major position of element (w, n) of one target's Zt block (W x NB):
+// k-step kb = w/4, N-tile pair np = n/16, lane = (n%8)*4 + w%4, half = (n/8)%2.
+__device__ __forceinline__ int64_t zfrag(int w, int n) {
+  return ((((int64_t)(w >> 2) * (NB / 16) + (n >> 4)) * 32 + (n & 7) * 4 + (w & 3)) << 1) + ((n >> 3) & 1);
+}
+
+__device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { return ((k + 1) * G - 1) / S; }
+
+// z value of column w = q r + a of source node sg, rhs n -> Zt of target sib(sg, q).
+__device__ __forceinline__ void scatter_zd(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int w, int n,
+                                           double v) {
+  const int d = __ffs(a.c) - 1;
+  const int q = w / a.r, aa = w - q * a.r;
+  const int me = static_cast<int>(sg & (a.c - 1));
+  const int64_t t = ((sg >> d) << d) + (q < me ? q : q + 1);
+  const int tc = static_cast<int>(t & (a.c - 1));
+  const int qt = me < tc ? me : me - 1;
+  lv.zt[(t - lv.tbase) * (int64_t)a.W * NB + zfrag(qt * a.r + aa, n)] = v;
+}
+
+// ============================ project ========================================
+__global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __grid_constant__ StreamArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t G = gridDim.x, bid = blockIdx.x;
+  const int W = a.W, Wp = a.Wp, L = a.L;
+  const int ncw = W / 16;                  // consumer warps
+  const int ctp = ncw * 32;
+  const int VP = a.vp;                     // smem pitch of V rows (= 4 mod 16)
+  const int64_t SL = a.N_loc / KR;
+  const int64_t GL = G < SL ? G : SL;
+  const int NS = a.nstage_p;
+  const int64_t vbytes = (int64_t)KR * VP * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_p);
+  uint64_t* empty = full + NS;
+  volatile int* flag = reinterpret_cast<volatile int*>(empty + NS);
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], ncw);
+    }
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+  if (bid >= GL) return;
+  const int64_t k0 = SL * bid / GL, k1 = SL * (bid + 1) / GL;
+
+  if (warp == 0) {
+    // producer: the whole warp issues the row / column copies of a stage
+    const uint64_t pol_stream = dev::policy_evict_first();
+    const uint64_t pol_keep = dev::policy_evict_last();
+    int slot = 0;
+    uint32_t phase = 0;
+    const uint32_t total = static_cast<uint32_t>(KR * Wp * 8 + a.nr * KR * 8);
+    for (int l = 1; l <= L; ++l) {
+      if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+      const double* Vl = a.V + (l - 1) * a.panel_stride;
+      for (int64_t k = k0; k < k1; ++k) {
+        dev::mbar_wait(&empty[slot], phase ^ 1);
+        const int64_t i0 = k * KR;
+        unsigned char* st = smem + slot * a.stage_bytes_p;
+        if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
+        __syncwarp();
+        for (int rr = lane; rr < KR; rr += 32)
+          dev::bulk_g2s(st + rr * VP * 8, Vl + (i0 + rr) * Wp, Wp * 8, &full[slot], pol_stream);
+        for (int n = lane; n < a.nr; n += 32)
+          dev::bulk_g2s(st + vbytes + n * XP * 8, a.x + n * a.ldx + i0, KR * 8, &full[slot], pol_keep);
+        if (++slot == NS) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  const int cw = warp - 1;            // consumer warp: columns w in [16 cw, 16 cw + 16)
+  const int g = lane >> 2, tq = lane & 3;
+  double acc[2][8][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int l = 1; l <= L; ++l) {
+    if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+    const LevelArgs& lv = a.lv[l];
+    const int64_t seg = lv.seg_rows / KR;
+    int64_t sl = k0 / seg, pos = k0 - sl * seg;
+    const int64_t sg0 = a.row0 / lv.m;
+    for (int64_t k = k0; k < k1; ++k) {
+      dev::mbar_wait(&full[slot], phase);
+      const double* Vs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p);
+      const double* Xs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p + vbytes);
+#pragma unroll
+      for (int ks = 0; ks < KR / 4; ++ks) {
+        double av[2], bv[8];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) av[mt] = Vs[(ks * 4 + tq) * VP + cw * 16 + mt * 8 + g];  // A = V^T
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) bv[nt] = Xs[(nt * 8 + g) * XP + ks * 4 + tq];          // B = X
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+      }
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      if (++slot == NS) {
+        slot = 0;
+        phase ^= 1;
+      }
+      const bool node_end = (pos + 1 == seg);
+      const int64_t this_sl = sl;
+      if (++pos == seg) {
+        pos = 0;
+        ++sl;
+      }
+      if (!node_end && k + 1 != k1) continue;
+
+      // ---- node flush ----
+      const int64_t sa = this_sl * seg, sb = sa + seg;
+      const bool complete = sa >= k0 && sb <= k1;
+      const int64_t sg = sg0 + this_sl;
+      if (complete) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int w = cw * 16 + mt * 8 + g;
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int n = nt * 8 + tq * 2 + h;
+              if (n < a.nr) scatter_zd(a, lv, sg, w, n, acc[mt][nt][h]);
+              acc[mt][nt][h] = 0.0;
+            }
+        }
+      } else {
+        const int myslot = sa <= k0 ? 0 : 1;
+        double* pp = a.part + (((int64_t)(l - 1) * G + bid) * 2 + myslot) * (int64_t)Wp * NB;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int w = cw * 16 + mt * 8 + g;
+#pragma unroll
+          for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              pp[(int64_t)w * NB + nt * 8 + tq * 2 + h] = acc[mt][nt][h];
+              acc[mt][nt][h] = 0.0;
+            }
+        }
+        __threadfence();
+        dev::named_bar_sync(1, ctp);
+        const int64_t b0 = owner_of(sa, SL, GL), b1 = owner_of(sb - 1, SL, GL);
+        int* ticket = a.cnt + (int64_t)(l - 1) * G + b1;
+        if (cw == 0 && lane == 0) {
+          const int prev = atomicAdd(ticket, 1);
+          *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
+        }
+        dev::named_bar_sync(1, ctp);
+        if (*flag) {
+          __threadfence();
+          const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
+          for (int o = tid - 32; o < W * NB; o += ctp) {
+            const int w = o / NB, n = o - w * NB;
+            double v = 0.0;
+            for (int64_t bb = b0; bb <= b1; ++bb) {
+              const int sl_b = bb == b0 ? slot0 : 0;
+              v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NB + o);
+            }
+            if (n < a.nr) scatter_zd(a, lv, sg, w, n, v);
+          }
+          if (cw == 0 && lane == 0) *ticket = 0;
+        }
+        dev::named_bar_sync(1, ctp);
+      }
+    }
+  }
+}
+
+// ============================ expand =========================================
+// CTA item: RE = 64 rows x NB rhs; warp owns rows [wm*16, wm*16+16) (2 M-tiles)
+// and rhs [wn*32, wn*32+32) (4 N-tiles).
+__global__ void __launch_bounds__(kThreads, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t G = gridDim.x, bid = blockIdx.x;
+  const int W = a.W, Wp = a.Wp, Dp = a.Dp, b = a.b, L = a.L;
+  const int64_t items = a.N_loc / RE;
+  const int64_t j0 = items * bid / G, j1 = items * (bid + 1) / G;
+  const int NS = a.nstage_e;
+  const int kcw = W / KC, kcd = b / KC;      // k-chunks per level / for the dense block
+  const int64_t abytes = (int64_t)RE * AP * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
+  uint64_t* empty = full + NS;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], NCW);
+    }
+    dev::fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    const uint64_t pol_stream = dev::policy_evict_first();
+    const uint64_t pol_keep = dev::policy_evict_last();
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int64_t j = j0; j < j1; ++j) {
+      const int64_t i0 = j * RE;
+      const int64_t leaf0 = (i0 / b) * b;
+      for (int l = 1; l <= L + 1; ++l) {
+        const bool is_d = (l == L + 1);
+        if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+        const int nkc = is_d ? kcd : kcw;
+        const double* src = is_d ? a.D : a.U + (l - 1) * a.panel_stride;
+        const int pitch = is_d ? Dp : Wp;
+        const double* zt = nullptr;
+        if (!is_d) {
+          const LevelArgs& lv = a.lv[l];
+          zt = lv.zt + ((a.row0 + i0) / lv.m - lv.tbase) * (int64_t)W * NB;
+        }
+        for (int kc = 0; kc < nkc; ++kc) {
+          dev::mbar_wait(&empty[slot], phase ^ 1);
+          unsigned char* st = smem + slot * a.stage_bytes_e;
+          const uint32_t bbytes = is_d ? static_cast<uint32_t>(a.nr * KC * 8) : static_cast<uint32_t>(KC * NB * 8);
+          if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], RE * KC * 8 + bbytes);
+          __syncwarp();
+          for (int rr = lane; rr < RE; rr += 32)
+            dev::bulk_g2s(st + rr * AP * 8, src + (i0 + rr) * pitch + kc * KC, KC * 8, &full[slot], pol_stream);
+          if (!is_d) {
+            if (lane == 0)
+              dev::bulk_g2s(st + abytes, zt + (int64_t)kc * KC * NB, KC * NB * 8, &full[slot], pol_keep);
+          } else {
+            for (int n = lane; n < a.nr; n += 32)
+              dev::bulk_g2s(st + abytes + n * XP * 8, a.x + n * a.ldx + leaf0 + kc * KC, KC * 8, &full[slot],
+                            pol_keep);
+          }
+          if (++slot == NS) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const int cw = warp - 1;
+  const int wm = cw & 3, wn = cw >> 2;
+  const int g = lane >> 2, tq = lane & 3;
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int64_t j = j0; j < j1; ++j) {
+    const int64_t i0 = j * RE;
+    double acc[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+    for (int l = 1; l <= L + 1; ++l) {
+      const bool is_d = (l == L + 1);
+      if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+      const int nkc = is_d ? kcd : kcw;
+      for (int kc = 0; kc < nkc; ++kc) {
+        dev::mbar_wait(&full[slot], phase);
+        const double* As = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e);
+        const double* Bs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e + abytes);
+#pragma unroll
+        for (int ks = 0; ks < KC / 4; ++ks) {
+          double av[2], bv[4];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
+          if (!is_d) {
+            // fragment-major Zt chunk: k-step ks, N-tile pairs wn*2, wn*2+1
+#pragma unroll
+            for (int np = 0; np < 2; ++np) {
+              const double2 v = reinterpret_cast<const double2*>(Bs)[(ks * (NB / 16) + wn * 2 + np) * 32 + lane];
+              bv[np * 2] = v.x;
+              bv[np * 2 + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) bv[nt] = Bs[((wn * 4 + nt) * 8 + g) * XP + ks * 4 + tq];
+          }
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+        }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&empty[slot]);
+        if (++slot == NS) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t row = i0 + wm * 16 + mt * 8 + g;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = (wn * 4 + nt) * 8 + tq * 2 + h;
+          if (n < a.nr) a.y[n * a.ldy + row] = acc[mt][nt][h];
+        }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  project_dmma_kernel<<<grid, 32 + (a.W / 16) * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  expand_dmma_kernel<<<grid, kThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e) {
+  cudaError_t e = cudaFuncSetAttribute(project_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(expand_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+}
+
+}  // namespace hmat

@@ -19,6 +19,14 @@ constexpr int kMaxNR = 8;        // right-hand sides per streaming pass
 constexpr int kConsumerThreads = 256;
 constexpr int kThreads = 32 + kConsumerThreads;  // 1 producer warp + 8 consumer warps
 
+// FP64 tensor-core (DMMA) path for many right-hand sides (kernels_dmma.cu)
+constexpr int kDmmaNB = 64;   // right-hand sides per pass
+constexpr int kDmmaKR = 32;   // project: V rows per stage
+constexpr int kDmmaRE = 64;   // expand: rows per item
+constexpr int kDmmaKC = 32;   // expand: k-columns per stage
+constexpr int kDmmaXP = 36;   // smem pitch of staged x columns (= 4 mod 16 doubles)
+constexpr int kDmmaAP = kDmmaKC + 4;  // smem pitch of staged U / D row chunks
+
 struct Plan {
   // problem
   int d = 0, c = 0, L = 0, b = 0, r = 0, W = 0;
@@ -55,6 +63,12 @@ struct Plan {
     int grid_p = 0, grid_e = 0;                            // persistent grids
   } lay[4];
   int grid_p_max = 0;               // partial-sum slots to allocate
+  // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
+  bool dmma_ok = false;
+  int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
+  int dns_p = 0, dns_e = 0;
+  int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
+  int dgrid_p = 0, dgrid_e = 0;
 };
 
 // index into Plan::lay of a right-hand-side capacity 1, 2, 4 or 8

@@ -185,3 +185,51 @@ def test_full_size_sampled_rows(name):
     finally:
         hm.hmat_destroy(h)
         torch.cuda.empty_cache()
+
+
+DMMA = [HConfig("d3L2", d=3, L=2, b=64, r=32, seed=501), HConfig("d3L3", d=3, L=3, b=64, r=32, seed=502),
+        HConfig("d2L3", d=2, L=3, b=64, r=32, seed=503), HConfig("d2b128", d=2, L=3, b=128, r=64, seed=504)]
+
+
+@pytest.mark.parametrize("cfg", DMMA, ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [16, 64, 70])
+def test_dmma_many_rhs(cfg, nrhs):
+    """FP64 tensor-core path (nrhs >= 16, W % 32 == 0, 64 | b): passes of 64
+    right-hand sides, ragged last pass, vs the oracle."""
+    U, V, D, x = host_case(cfg, nrhs)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        assert hm.hmat_launches_per_matvec(h, nrhs) == 2 * ((nrhs + 63) // 64)  # the DMMA passes ran
+    finally:
+        hm.hmat_destroy(h)
+    assert_parity(gpu_matvec(cfg, U, V, D, x), ref)
+
+
+def test_c5_full_size_sampled_rows():
+    """BASELINE configs[4] (N = 2^21, 64 right-hand sides) at full size through
+    the DMMA path: sampled rows of all 64 columns vs the oracle."""
+    cfg = CONFIGS["c5"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < cfg.factor_bytes * 1.2:
+        pytest.skip("not enough device memory")
+    h = device_operator(cfg, hm)
+    try:
+        n = cfg.N
+        X = torch.empty(cfg.nrhs, n, dtype=torch.float64, device="cuda")
+        hgen.dev_fill_x(cfg, cfg.nrhs, 0, 0, n, X.data_ptr(), n)
+        Y = torch.empty_like(X)
+        hm.hmat_matvec(h, X.t(), Y.t())
+        torch.cuda.synchronize()
+        assert hm.hmat_launches_per_matvec(h, cfg.nrhs) == 2
+        xh = X.t().cpu().numpy()
+        rows = np.array([0, 63, 64, 1000, n - 1])
+        ref = oracle.rows_generated(cfg, np.asfortranarray(xh), rows)
+        yall = Y.t().cpu().numpy()
+        got = yall[rows]
+        for k in range(cfg.nrhs):
+            scale = np.abs(yall[:, k]).max()
+            assert np.abs(got[:, k] - ref[:, k]).max() <= 1e-12 * scale
+    finally:
+        hm.hmat_destroy(h)
+        torch.cuda.empty_cache()
