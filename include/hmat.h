@@ -101,6 +101,26 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
  * reduction, cross-GPU exchange when P > 1, fused expand + dense). */
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
 
+/* GEMV form y = alpha op(H) x + beta y ("do not initialize y
+ * as a zero vector and modify eq:prod-yuz, eq:prod-yz, eq:prod-ydz
+ * accordingly"), op(H) = H (trans = 0) or H^T (trans = 1).  H^T has H's block
+ * structure with U and V exchanged and every dense leaf block transposed; the
+ * first trans = 1 call builds D^T once (N_loc x leaf_size more device memory).
+ * beta == 0: y is write-only (not read).  Same vectors/streams rules as
+ * hmat_matvec. */
+hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double beta, double* y, int nrhs);
+
+/* The paper-strict reading of Def 2.4 (conditions checked in
+ * order, "leaf" first): every child pair of a leaf-parent is dense, so each
+ * leaf-parent diagonal block (2^dim leaf_size square) is dense and low-rank
+ * sibling blocks exist at levels 1..depth-1 only.  U, V: depth-1
+ * canonical panels (levels 1..depth-1); Dc: N_loc x (2^dim leaf_size), row i
+ * of leaf-parent p = i / (2^dim leaf_size) holds row i - p 2^dim leaf_size of
+ * p's dense diagonal block.  This is the structure of hmat_create(depth - 1,
+ * dim, 2^dim leaf_size, ...) and is built as such.  depth >= 1. */
+hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                               const double* const* V, const double* Dc, const hmat_dist_t* dist, hmat_t* out);
+
 /* Diagnostic form: only the low-rank levels l with bit (l-1) of level_mask set
  * and, if dense != 0, the dense leaf blocks: y = y_D + sum_{l in mask} y_l. */
 hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, uint64_t level_mask,

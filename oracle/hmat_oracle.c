@@ -83,6 +83,27 @@ static void visit_root(int c, int L, block_fn fn, void* ctx) {
   else visit(c, L, 0, 0, fn, ctx);
 }
 
+/* The paper-strict reading of Def 2.4 (R1): the three
+ * conditions checked in the paper's order -- (1) a child pair whose domains are
+ * leaves is dense, (2) else an admissible pair is low rank, (3) else recurse.
+ * So every child pair of a leaf-parent is a dense b x b block. */
+static void visit_strict(int c, int L, int level, int64_t node, block_fn fn, void* ctx) {
+  for (int a = 0; a < c; ++a) {
+    for (int bb = 0; bb < c; ++bb) {
+      int64_t t = node * c + a, s = node * c + bb;
+      if (level + 1 == L) fn(ctx, 0, level + 1, t, s);   /* leaves: dense */
+      else if (t != s) fn(ctx, 1, level + 1, t, s);      /* admissible: low rank */
+      else visit_strict(c, L, level + 1, t, fn, ctx);    /* hierarchical */
+    }
+  }
+}
+
+static void visit_root_v(int strict, int c, int L, block_fn fn, void* ctx) {
+  if (L == 0) fn(ctx, 0, 0, 0, 0);
+  else if (strict) visit_strict(c, L, 0, 0, fn, ctx);
+  else visit(c, L, 0, 0, fn, ctx);
+}
+
 typedef struct { int64_t lowrank, dense, lowrank_level1; } census_t;
 
 static void census_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
@@ -110,11 +131,19 @@ static void cover_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
 }
 
 /* count[i*N + j] = number of blocks covering entry (i, j) (must be 1). */
-void oracle_cover_count(int d, int L, int b, int32_t* count) {
+void oracle_cover_count_v(int strict, int d, int L, int b, int32_t* count) {
   cover_t cv;
   cv.c = 1 << d; cv.L = L; cv.b = b; cv.N = (int64_t)b * ipow(cv.c, L); cv.count = count;
   memset(count, 0, sizeof(int32_t) * (size_t)(cv.N * cv.N));
-  visit_root(cv.c, L, cover_cb, &cv);
+  visit_root_v(strict, cv.c, L, cover_cb, &cv);
+}
+
+void oracle_cover_count(int d, int L, int b, int32_t* count) { oracle_cover_count_v(0, d, L, b, count); }
+
+void oracle_block_census_strict(int d, int L, int64_t* n_lowrank, int64_t* n_dense, int64_t* n_lowrank_level1) {
+  census_t cs = {0, 0, 0};
+  visit_root_v(1, 1 << d, L, census_cb, &cs);
+  *n_lowrank = cs.lowrank; *n_dense = cs.dense; *n_lowrank_level1 = cs.lowrank_level1;
 }
 
 /* ---- the matvec, eq:hmat-vec-add ----------------------------------------
@@ -167,20 +196,107 @@ void oracle_matvec(int d, int L, int b, int r, const double* const* U, const dou
   oracle_matvec_masked(d, L, b, r, U, V, D, x, y, nrhs, ~0ull, 1);
 }
 
+/* ---- the transposed product H^T x (GEMV "T", PAPER.md:961-969 remark) ------
+ * Every block contributes its transpose: for a dense D_k, y_k += D_k^T x_k; for
+ * a low-rank block (t, s): w = U_ts^T x_t, y_s += V_ts w. */
+void oracle_matvec_t(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                     const double* D, const double* x, double* y, int nrhs) {
+  const int c = 1 << d;
+  const int64_t N = (int64_t)b * ipow(c, L);
+  const int W = (c - 1) * r;
+  double* w = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  for (int k = 0; k < nrhs; ++k) {
+    const double* xk = x + (int64_t)k * N;
+    double* yk = y + (int64_t)k * N;
+    for (int64_t i = 0; i < N; ++i) yk[i] = 0.0;
+    for (int64_t leaf = 0; leaf < N / b; ++leaf)
+      for (int i = 0; i < b; ++i)
+        for (int j = 0; j < b; ++j)
+          yk[leaf * b + j] += D[(leaf * b + i) * b + j] * xk[leaf * b + i];
+    for (int l = 1; l <= L; ++l) {
+      const int64_t m = N / ipow(c, l);
+      const double* Ul = U[l - 1];
+      const double* Vl = V[l - 1];
+      for (int64_t t = 0; t < ipow(c, l); ++t) {
+        for (int q = 0; q < c - 1; ++q) {
+          int64_t s = oracle_sibling(c, t, q);
+          int qs = oracle_slot(c, s, t);
+          for (int a = 0; a < r; ++a) w[a] = 0.0;
+          for (int64_t i = 0; i < m; ++i)       /* w = U_ts^T x_t */
+            for (int a = 0; a < r; ++a)
+              w[a] += Ul[(t * m + i) * W + q * r + a] * xk[t * m + i];
+          for (int64_t j = 0; j < m; ++j)       /* y_s += V_ts w */
+            for (int a = 0; a < r; ++a)
+              yk[s * m + j] += Vl[(s * m + j) * W + qs * r + a] * w[a];
+        }
+      }
+    }
+  }
+  free(w);
+}
+
+/* ---- paper-strict structure (f2): dense leaf-parent blocks ------------------
+ * U, V hold levels 1..L-1 (canonical layout); Dc is N x (c b): row i of
+ * leaf-parent p = i / (c b) holds row i - p c b of the dense (c b) x (c b)
+ * diagonal block of p, i.e. the c dense leaf blocks D_{t,s} of t's row. */
+void oracle_matvec_strict(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                          const double* Dc, const double* x, double* y, int nrhs) {
+  const int c = 1 << d;
+  const int64_t N = (int64_t)b * ipow(c, L);
+  const int W = (c - 1) * r;
+  const int cb = (L >= 1 ? c : 1) * b;  /* L = 0: the root is a leaf (b x b) */
+  double* z = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  for (int k = 0; k < nrhs; ++k) {
+    const double* xk = x + (int64_t)k * N;
+    double* yk = y + (int64_t)k * N;
+    for (int64_t i = 0; i < N; ++i) yk[i] = 0.0;
+    /* dense blocks: every child pair (t, s) of each leaf-parent */
+    for (int64_t p = 0; p < N / cb; ++p)
+      for (int64_t i = 0; i < cb; ++i)
+        for (int64_t j = 0; j < cb; ++j)
+          yk[p * cb + i] += Dc[(p * cb + i) * cb + j] * xk[p * cb + j];
+    for (int l = 1; l <= L - 1; ++l) {
+      const int64_t m = N / ipow(c, l);
+      const double* Ul = U[l - 1];
+      const double* Vl = V[l - 1];
+      for (int64_t t = 0; t < ipow(c, l); ++t) {
+        for (int q = 0; q < c - 1; ++q) {
+          int64_t s = oracle_sibling(c, t, q);
+          int qs = oracle_slot(c, s, t);
+          for (int a = 0; a < r; ++a) z[a] = 0.0;
+          for (int64_t j = 0; j < m; ++j)
+            for (int a = 0; a < r; ++a) z[a] += Vl[(s * m + j) * W + qs * r + a] * xk[s * m + j];
+          for (int64_t i = 0; i < m; ++i)
+            for (int a = 0; a < r; ++a) yk[t * m + i] += Ul[(t * m + i) * W + q * r + a] * z[a];
+        }
+      }
+    }
+  }
+  free(z);
+}
+
 /* ---- dense assembly + brute-force matvec (small N) --------------------- */
 
 typedef struct {
-  int c, L, b, r, W; int64_t N;
+  int c, L, b, r, W, strict; int64_t N;
   const double* const* U; const double* const* V; const double* D; double* A;
 } assemble_t;
 
 static void assemble_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
   assemble_t* as = (assemble_t*)ctx;
   const int64_t N = as->N;
-  if (kind == 0) { /* dense leaf block D_t, t == s */
+  if (kind == 0 && !as->strict) { /* dense leaf block D_t, t == s */
     for (int i = 0; i < as->b; ++i)
       for (int j = 0; j < as->b; ++j)
         as->A[(t * as->b + i) * N + (s * as->b + j)] = as->D[(t * as->b + i) * as->b + j];
+    return;
+  }
+  if (kind == 0) { /* strict: dense leaf-pair block D_ts from the leaf-parent panel */
+    const int cb = (as->L >= 1 ? as->c : 1) * as->b;
+    const int64_t p0 = (t * as->b) / cb * cb; /* first row of the leaf-parent */
+    for (int i = 0; i < as->b; ++i)
+      for (int j = 0; j < as->b; ++j)
+        as->A[(t * as->b + i) * N + (s * as->b + j)] = as->D[(t * as->b + i) * cb + (s * as->b - p0) + j];
     return;
   }
   const int64_t m = N / ipow(as->c, level);
@@ -197,14 +313,19 @@ static void assemble_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
 }
 
 /* A (N x N row-major) = the matrix the blocks define. */
-void oracle_assemble(int d, int L, int b, int r, const double* const* U, const double* const* V,
-                     const double* D, double* A) {
+void oracle_assemble_v(int strict, int d, int L, int b, int r, const double* const* U, const double* const* V,
+                       const double* D, double* A) {
   assemble_t as;
-  as.c = 1 << d; as.L = L; as.b = b; as.r = r; as.W = (as.c - 1) * r;
+  as.c = 1 << d; as.L = L; as.b = b; as.r = r; as.W = (as.c - 1) * r; as.strict = strict;
   as.N = (int64_t)b * ipow(as.c, L);
   as.U = U; as.V = V; as.D = D; as.A = A;
   memset(A, 0, sizeof(double) * (size_t)(as.N * as.N));
-  visit_root(as.c, L, assemble_cb, &as);
+  visit_root_v(strict, as.c, L, assemble_cb, &as);
+}
+
+void oracle_assemble(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                     const double* D, double* A) {
+  oracle_assemble_v(0, d, L, b, r, U, V, D, A);
 }
 
 /* y = A x by the definition of a matrix-vector product (brute force). */

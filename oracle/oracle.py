@@ -43,6 +43,18 @@ def _load():
                                                                  ctypes.c_int]
         lib.oracle_assemble.restype = None
         lib.oracle_assemble.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_block_census_strict.restype = None
+        lib.oracle_block_census_strict.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int64)] * 3
+        lib.oracle_cover_count_v.restype = None
+        lib.oracle_cover_count_v.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p]
+        lib.oracle_assemble_v.restype = None
+        lib.oracle_assemble_v.argtypes = [ctypes.c_int] * 5 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_matvec_t.restype = None
+        lib.oracle_matvec_t.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p,
+                                                             ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_matvec_strict.restype = None
+        lib.oracle_matvec_strict.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p,
+                                                                  ctypes.c_void_p, ctypes.c_int]
         lib.oracle_dense_matvec.restype = None
         lib.oracle_dense_matvec.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_int]
@@ -139,3 +151,49 @@ def rows_generated(cfg, x, rows) -> np.ndarray:
     _load().oracle_rows_generated(cfg.d, cfg.L, cfg.b, cfg.r, cfg.seed, xc.ctypes.data, nrhs, len(rows),
                                   rows.ctypes.data, out.ctypes.data)
     return out[:, 0] if np.ndim(x) == 1 else out
+
+
+def block_census_strict(d: int, L: int):
+    """Block counts of the paper-strict reading of Def 2.4 (leaves checked first)."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _load().oracle_block_census_strict(d, L, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+    return a.value, b.value, c.value
+
+
+def cover_count_strict(d: int, L: int, b: int) -> np.ndarray:
+    N = b * (1 << d) ** L
+    out = np.zeros((N, N), dtype=np.int32)
+    _load().oracle_cover_count_v(1, d, L, b, out.ctypes.data)
+    return out
+
+
+def assemble_strict(d: int, L: int, b: int, r: int, U, V, Dc) -> np.ndarray:
+    """Strict structure: U, V = levels 1..L-1, Dc = N x (2^d b) leaf-parent dense panel."""
+    N = b * (1 << d) ** L
+    A = np.zeros((N, N), dtype=np.float64)
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dc = _c(Dc)
+    _load().oracle_assemble_v(1, d, L, b, r, up, vp, Dc.ctypes.data, A.ctypes.data)
+    return A
+
+
+def _mv(fn, d, L, b, r, U, V, D, x):
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    y = np.zeros((N, nrhs), dtype=np.float64, order="F")
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dc = _c(D)
+    fn(d, L, b, r, up, vp, Dc.ctypes.data, xc.ctypes.data, y.ctypes.data, nrhs)
+    return y[:, 0] if np.ndim(x) == 1 else y
+
+
+def matvec_t(d: int, L: int, b: int, r: int, U, V, D, x) -> np.ndarray:
+    """y = H^T x by the transposed block loop."""
+    return _mv(_load().oracle_matvec_t, d, L, b, r, U, V, D, x)
+
+
+def matvec_strict(d: int, L: int, b: int, r: int, U, V, Dc, x) -> np.ndarray:
+    """y = H x for the paper-strict structure (U, V levels 1..L-1, leaf-parent dense panel)."""
+    return _mv(_load().oracle_matvec_strict, d, L, b, r, U, V, Dc, x)

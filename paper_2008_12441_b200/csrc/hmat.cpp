@@ -113,6 +113,7 @@ struct hmat_s {
   double* zex_d = nullptr;
   double* part_d = nullptr;
   int* cnt_d = nullptr;
+  double* Dt = nullptr;  // D^T, built on the first transposed product
   bool prof = false;
   std::vector<EventPair> ev;
   std::vector<cudaEvent_t> pool;
@@ -139,6 +140,7 @@ void release(hmat_s* H) {
   cudaFree(H->zex_d);
   cudaFree(H->part_d);
   cudaFree(H->cnt_d);
+  cudaFree(H->Dt);
   for (auto& e : H->ev) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -222,6 +224,9 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = cudaMemsetAsync(H->U, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->V, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->D, 0, size_t(p.N_loc) * p.Dp * sizeof(double), H->stream)) ||
+      // z rows: padding columns (odd W) are multiplied by zero padding of U, so keep them finite
+      (e = cudaMemsetAsync(H->zloc, 0, std::max<size_t>(256, size_t(p.z_local_rows) * zrow), H->stream)) ||
+      (e = cudaMemsetAsync(H->zex, 0, std::max<size_t>(256, size_t(p.z_exch_rows) * zrow), H->stream)) ||
       (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(p.dsmem_p, p.dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
@@ -347,13 +352,35 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
   return HMAT_OK;
 }
 
-hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, uint64_t level_mask, int dense) {
+}  // extern "C"
+
+namespace {
+
+// D^T panel for the transposed product, built on first use (one-time kernel).
+hmat_status ensure_dt(hmat_s* H) {
+  if (H->Dt) return HMAT_OK;
+  const hmat::Plan& p = H->plan;
+  const size_t bytes = size_t(p.N_loc) * p.Dp * sizeof(double);
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->Dt), bytes));
+  CUDA_TRY(cudaMemsetAsync(H->Dt, 0, bytes, H->stream));
+  CUDA_TRY(hmat::launch_transpose_leaf_blocks(H->D, H->Dt, p.N_loc / p.b, p.b, p.Dp, H->stream));
+  return HMAT_OK;
+}
+
+// y = alpha op(H) x + beta y restricted to the selected parts (the whole path).
+hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta, double* y, int nrhs,
+                uint64_t level_mask, int dense) {
   if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
   if (!x || !y) return fail(HMAT_ERR_INVALID, "x or y is NULL");
   if (nrhs < 1) return fail(HMAT_ERR_INVALID, "nrhs must be >= 1");
+  if (trans != 0 && trans != 1) return fail(HMAT_ERR_INVALID, "trans must be 0 (H) or 1 (H^T)");
   if (static_cast<const void*>(x) == static_cast<const void*>(y)) return fail(HMAT_ERR_INVALID, "x and y alias");
   const hmat::Plan& p = H->plan;
   CUDA_TRY(cudaSetDevice(H->device));
+  if (trans) {
+    hmat_status st = ensure_dt(H);
+    if (st != HMAT_OK) return st;
+  }
   const int64_t n = p.N_loc;
   const bool x_dev = is_device_ptr(x), y_dev = is_device_ptr(y);
   const bool host_io = !x_dev || !y_dev;
@@ -380,13 +407,22 @@ hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, ui
     hmat_status st = ensure_buf(&H->ybuf, &H->ycap, size_t(n) * nrhs);
     if (st != HMAT_OK) return st;
     yd = H->ybuf;
+    if (beta != 0.0) {  // y is an input too
+      prof_begin(H, 3, &ep);
+      CUDA_TRY(cudaMemcpyAsync(yd, y, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
+      prof_end(H, &ep);
+    }
   }
 
   hmat::StreamArgs a;
   memset(&a, 0, sizeof a);
-  a.U = H->U;
-  a.V = H->V;
-  a.D = H->D;
+  // H^T has H's block structure with U and V exchanged and D_k -> D_k^T
+  // (the source-major V panel is the target-major panel of H^T and vice versa)
+  a.U = trans ? H->V : H->U;
+  a.V = trans ? H->U : H->V;
+  a.D = trans ? H->Dt : H->D;
+  a.alpha = alpha;
+  a.beta = beta;
   a.panel_stride = p.panel_stride;
   a.ldx = ldx;
   a.ldy = n;
@@ -500,8 +536,32 @@ hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, ui
   return HMAT_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, uint64_t level_mask, int dense) {
+  return run(H, 0, 1.0, x, 0.0, y, nrhs, level_mask, dense);
+}
+
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs) {
-  return hmat_matvec_parts(H, x, y, nrhs, ~0ull, 1);
+  return run(H, 0, 1.0, x, 0.0, y, nrhs, ~0ull, 1);
+}
+
+hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double beta, double* y, int nrhs) {
+  return run(H, trans, alpha, x, beta, y, nrhs, ~0ull, 1);
+}
+
+hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                               const double* const* V, const double* Dc, const hmat_dist_t* dist, hmat_t* out) {
+  // Def 2.4 read literally (leaves checked first): the leaf-parent diagonal
+  // blocks (2^dim leaf_size square) are dense and low-rank blocks exist at
+  // levels 1..depth-1 -- exactly the structure of depth-1 with leaf 2^dim leaf_size.
+  if (out) *out = nullptr;
+  if (depth < 1) return fail(HMAT_ERR_INVALID, "strict structure needs depth >= 1");
+  if (dim < 1 || dim > 3) return fail(HMAT_ERR_INVALID, "dim must be 1, 2 or 3 (ideal domains, PAPER.md:243-246)");
+  if (leaf_size < 1 || leaf_size > (1 << 28)) return fail(HMAT_ERR_INVALID, "leaf_size must be >= 1");
+  return hmat_create(depth - 1, dim, leaf_size << dim, rank, U, V, Dc, dist, out);
 }
 
 hmat_status hmat_destroy(hmat_t H) {

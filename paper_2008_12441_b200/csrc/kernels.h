@@ -36,6 +36,7 @@ struct StreamArgs {
   double* y;
   int64_t ldy;
   int nr;            // active right-hand sides in this pass (<= NR template)
+  double alpha, beta;  // y = alpha op(H) x + beta y (beta == 0: y is not read)
   // shape
   int L, c, r, W, Wp, Dp, b;
   int64_t N_loc, row0;
@@ -64,6 +65,8 @@ cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t sme
 cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
 cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
 cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e);
+// D^T of every dense leaf block (for H^T x); one-time helper.
+cudaError_t launch_transpose_leaf_blocks(const double* D, double* Dt, int64_t n_leaves, int b, int Dp, cudaStream_t s);
 // Opt the kernels into large dynamic shared memory (once per device).
 cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e);  // max over layouts
 

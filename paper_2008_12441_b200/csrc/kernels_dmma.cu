@@ -352,7 +352,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_dmma_kernel(const __grid_c
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int n = (wn * 4 + nt) * 8 + tq * 2 + h;
-          if (n < a.nr) a.y[n * a.ldy + row] = acc[mt][nt][h];
+          if (n < a.nr) {
+            double* yp = a.y + n * a.ldy + row;
+            *yp = a.beta == 0.0 ? a.alpha * acc[mt][nt][h] : a.alpha * acc[mt][nt][h] + a.beta * *yp;
+          }
         }
     }
   }

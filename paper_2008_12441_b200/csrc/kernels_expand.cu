@@ -146,16 +146,11 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             if (cp < NP) {
               double2 u = U2[cp];
               if (2 * cp + 1 >= W) u.y = 0.0;  // padding column of an odd W
-              if (NR == 1) {
-                const double2 z = reinterpret_cast<const double2*>(Zs)[cp];
-                acc[0] = fma(u.x, z.x, acc[0]);
-                acc2[0] = fma(u.y, z.y, acc2[0]);
-              } else {
 #pragma unroll
-                for (int kk = 0; kk < NR; ++kk) {
-                  acc[kk] = fma(u.x, Zs[(2 * cp) * NR + kk], acc[kk]);
-                  acc2[kk] = fma(u.y, Zs[(2 * cp + 1) * NR + kk], acc2[kk]);
-                }
+              for (int kk = 0; kk < NR; ++kk) {  // Zt row layout [rhs][col]
+                const double2 z = reinterpret_cast<const double2*>(Zs + kk * Wp)[cp];
+                acc[kk] = fma(u.x, z.x, acc[kk]);
+                acc2[kk] = fma(u.y, z.y, acc2[kk]);
               }
             }
             if (++jj == njU) jj = 0;
@@ -197,7 +192,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     if (active && p == 0) {
 #pragma unroll
       for (int kk = 0; kk < NR; ++kk)
-        if (kk < a.nr) a.y[kk * a.ldy + i0 + ri] = acc[kk];
+        if (kk < a.nr) {
+          double* yp = a.y + kk * a.ldy + i0 + ri;  // y = alpha (H x) + beta y (GEMV)
+          *yp = a.beta == 0.0 ? a.alpha * acc[kk] : a.alpha * acc[kk] + a.beta * *yp;
+        }
     }
     if (++in_leaf == ipl) {
       in_leaf = 0;

@@ -48,7 +48,7 @@ __device__ __forceinline__ void scatter_z(const StreamArgs& a, const LevelArgs& 
   const int64_t t = ((sg >> d) << d) + (q < me ? q : q + 1);
   const int tc = static_cast<int>(t & (a.c - 1));
   const int qt = me < tc ? me : me - 1;
-  lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)(qt * a.r + aa) * NR + kk] = v;
+  lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)kk * a.Wp + qt * a.r + aa] = v;  // [t][rhs][col]
 }
 
 template <int NR, int PAIRS>
@@ -204,8 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           if (PAIRS == 1 || cp < NP) {
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk) {
-              red[((int64_t)rho * Wp + 2 * cp) * NR + kk] = acc[j][kk].x;
-              red[((int64_t)rho * Wp + 2 * cp + 1) * NR + kk] = acc[j][kk].y;
+              reinterpret_cast<double2*>(red + ((int64_t)rho * NR + kk) * Wp)[cp] = acc[j][kk];
               acc[j][kk] = make_double2(0.0, 0.0);
             }
           }
@@ -214,9 +213,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       dev::named_bar_sync(1, CT);
       if (complete) {
         for (int o = t; o < W * NR; o += CT) {
-          const int col = o / NR, kk = o - col * NR;
+          const int kk = o / W, col = o - kk * W;
           double v = 0.0;
-          for (int g = 0; g < RG; ++g) v += red[((int64_t)g * Wp + col) * NR + kk];
+          for (int g = 0; g < RG; ++g) v += red[((int64_t)g * NR + kk) * Wp + col];
           if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
         }
       } else {
@@ -225,10 +224,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         const int myslot = sa <= k0 ? 0 : 1;
         double* pp = a.part + (((int64_t)(l - 1) * G + bid) * 2 + myslot) * (int64_t)Wp * NR;
         for (int o = t; o < W * NR; o += CT) {
-          const int col = o / NR, kk = o - col * NR;
+          const int kk = o / W, col = o - kk * W;
           double v = 0.0;
-          for (int g = 0; g < RG; ++g) v += red[((int64_t)g * Wp + col) * NR + kk];
-          pp[(int64_t)col * NR + kk] = v;
+          for (int g = 0; g < RG; ++g) v += red[((int64_t)g * NR + kk) * Wp + col];
+          pp[(int64_t)kk * Wp + col] = v;
         }
         __threadfence();
         dev::named_bar_sync(1, CT);
@@ -243,12 +242,12 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           __threadfence();
           const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
           for (int o = t; o < W * NR; o += CT) {
-            const int col = o / NR, kk = o - col * NR;
+            const int kk = o / W, col = o - kk * W;
             double v = 0.0;
             for (int64_t bb = b0; bb <= b1; ++bb) {
               const int sl_b = bb == b0 ? slot0 : 0;
               v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NR +
-                              (int64_t)col * NR + kk);
+                              (int64_t)kk * Wp + col);
             }
             if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
           }

@@ -38,7 +38,7 @@ struct Plan {
   // device layout (doubles)
   int Wp = 0, Dp = 0;               // row pitches of U/V panels and D (even => 16-B rows)
   int64_t panel_stride = 0;         // doubles between consecutive level panels (128-B multiple)
-  // z storage per level l (target-major, per rhs-pass): Zt_l[t][col][k], pitch Wp*kMaxNR
+  // z storage per level l (target-major, per rhs-pass): Zt_l[t][rhs][col], Wp*NR per target
   // levels 1..cross live in the exchange buffer (all c^l targets), others in the
   // local buffer (this shard's targets only).
   int cross = 0;                    // levels 1..cross need the cross-GPU exchange (c^{l-1} < P)

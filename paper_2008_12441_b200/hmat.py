@@ -26,7 +26,8 @@ HMAT_NUM_PHASES = 4
 PHASES = ("project", "exchange", "expand", "copies")
 
 # Every symbol include/hmat.h declares (checked by tests/test_abi.py).
-EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_panel", "hmat_matvec", "hmat_matvec_parts", "hmat_destroy",
+EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_panel", "hmat_matvec", "hmat_gemv",
+           "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query")
 
@@ -60,6 +61,8 @@ _sigs = {
     "hmat_panel": (_i, [_H, _i, _i, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                         ctypes.POINTER(_i64)]),
     "hmat_matvec": (_i, [_H, _P, _P, _i]),
+    "hmat_gemv": (_i, [_H, _i, ctypes.c_double, _P, ctypes.c_double, _P, _i]),
+    "hmat_create_strict": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
     "hmat_matvec_parts": (_i, [_H, _P, _P, _i, _u64, _i]),
     "hmat_destroy": (_i, [_H]),
     "hmat_last_error": (ctypes.c_char_p, []),
@@ -155,6 +158,17 @@ def hmat_create(depth, dim, leaf_size, rank, U, V, D, dist: hmat_dist_t | None =
     return h
 
 
+def hmat_create_strict(depth, dim, leaf_size, rank, U, V, Dc, dist: hmat_dist_t | None = None):
+    """Paper-strict Def 2.4 structure: U, V = depth-1 panels, Dc = N x (2^dim leaf) dense panel."""
+    Up = (ctypes.c_void_p * max(1, len(U)))(*[_ptr(u) for u in U])
+    Vp = (ctypes.c_void_p * max(1, len(V)))(*[_ptr(v) for v in V])
+    h = _H()
+    _check(_lib.hmat_create_strict(depth, dim, leaf_size, rank, ctypes.cast(Up, _P), ctypes.cast(Vp, _P), _ptr(Dc),
+                                   ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)),
+           "hmat_create_strict")
+    return h
+
+
 def hmat_create_uninit(depth, dim, leaf_size, rank, dist: hmat_dist_t | None = None):
     h = _H()
     _check(_lib.hmat_create_uninit(depth, dim, leaf_size, rank, ctypes.byref(dist) if dist is not None else None,
@@ -178,6 +192,17 @@ def hmat_matvec(h, x, y, nrhs: int | None = None):
     nrhs = kx if nrhs is None else nrhs
     assert kx >= nrhs and ky >= nrhs
     _check(_lib.hmat_matvec(h, xp, yp, nrhs), "hmat_matvec")
+
+
+def hmat_gemv(h, trans: int, alpha: float, x, beta: float, y, nrhs: int | None = None):
+    """y = alpha op(H) x + beta y, op = H (trans=0) or H^T (trans=1)."""
+    n = hmat_local_rows(h)
+    n = n[1] - n[0]
+    xp, kx = _vec(x, n)
+    yp, ky = _vec(y, n)
+    nrhs = kx if nrhs is None else nrhs
+    assert kx >= nrhs and ky >= nrhs
+    _check(_lib.hmat_gemv(h, int(trans), float(alpha), xp, float(beta), yp, nrhs), "hmat_gemv")
 
 
 def hmat_matvec_parts(h, x, y, level_mask: int, dense: bool, nrhs: int | None = None):

@@ -18,9 +18,13 @@ from paper_2008_12441_b200 import hmat as hm  # noqa: E402
 
 
 def run(cfg, setting, reps=10):
+    import dataclasses
     keys = []
     for kv in filter(None, setting.split(",")):
         k, v = kv.split("=")
+        if k == "NRHS":  # override the config's right-hand-side count
+            cfg = dataclasses.replace(cfg, nrhs=int(v))
+            continue
         os.environ[k] = v
         keys.append(k)
     try:
@@ -44,19 +48,28 @@ def run(cfg, setting, reps=10):
         W, L, b, N = cfg.W, cfg.L, cfg.b, cfg.N
         pb = 8 * N * W * L + 8 * N * cfg.nrhs
         eb = 8 * N * (W * L + b) + 16 * N * cfg.nrhs
-        pm = prof["project"][0] / max(1, prof["project"][1])
-        em = prof["expand"][0] / max(1, prof["expand"][1])
+        pm = prof["project"][0] / reps  # per matvec (all passes)
+        em = prof["expand"][0] / reps
         print(f"{cfg.name} [{setting or 'default'}] Rp={info.Rp} Re={info.Re} tpr={info.tpr} "
               f"ns_p={info.nstage_p} ns_e={info.nstage_e} grid={info.grid_p}/{info.grid_e} | "
               f"project {pm:.3f} ms {pb / pm / 1e6:.0f} GB/s | expand {em:.3f} ms {eb / em / 1e6:.0f} GB/s | "
-              f"total {pm + em:.3f} ms", flush=True)
+              f"total {pm + em:.3f} ms ({2 * cfg.N * (2 * W * L + b) * cfg.nrhs / (pm + em) / 1e9:.2f} TFLOP/s) "
+              f"launches/matvec={prof['project'][1] // reps}+{prof['expand'][1] // reps}", flush=True)
     finally:
         for k in keys:
             os.environ.pop(k, None)
         torch.cuda.empty_cache()
 
 
+def parse_cfg(spec):
+    """a BASELINE config name (c1..c5) or an ad-hoc shape 'd=3,L=4,b=64,r=32,nrhs=64'"""
+    if spec in hgen.CONFIGS:
+        return hgen.CONFIGS[spec]
+    kv = dict(item.split("=") for item in spec.split(","))
+    return hgen.HConfig(spec, **{k: int(v) for k, v in kv.items()}, seed=hgen.SEED_BASE + 99)
+
+
 if __name__ == "__main__":
-    cfg = hgen.CONFIGS[sys.argv[1]]
+    cfg = parse_cfg(sys.argv[1])
     for setting in (sys.argv[2:] or [""]):
         run(cfg, setting)

@@ -233,3 +233,84 @@ def test_c5_full_size_sampled_rows():
     finally:
         hm.hmat_destroy(h)
         torch.cuda.empty_cache()
+
+
+def _dev_cols(x):
+    """host (N,) / (N, k) array -> device tensor with the same column-major layout."""
+    if x.ndim == 1:
+        return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+
+
+@pytest.mark.parametrize("cfg", [HConfig("g1", d=2, L=3, b=16, r=4, seed=81), HConfig("g2", d=3, L=2, b=7, r=3, seed=82),
+                                 HConfig("g3", d=1, L=5, b=4, r=2, seed=83)], ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_gemv_alpha_beta_and_transpose(cfg, nrhs):
+    """hmat_gemv: y = alpha op(H) x + beta y (PAPER.md:961-969) for op = H, H^T;
+    beta = 0 must not read y (NaN in y stays out of the result)."""
+    U, V, D, x = host_case(cfg, nrhs)
+    Hx = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    HTx = oracle.matvec_t(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    rng = np.random.default_rng(5)
+    y0 = rng.standard_normal(x.shape)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        for trans, ref in ((0, Hx), (1, HTx)):
+            yd = _dev_cols(y0)
+            hm.hmat_gemv(h, trans, -1.5, _dev_cols(x), 0.25, yd)
+            assert_parity(yd.cpu().numpy(), -1.5 * ref + 0.25 * y0)
+            yn = _dev_cols(np.full(x.shape, np.nan))
+            hm.hmat_gemv(h, trans, 2.0, _dev_cols(x), 0.0, yn)
+            assert_parity(yn.cpu().numpy(), 2.0 * ref)
+        # host y with beta != 0 is read and written
+        yh = np.asfortranarray(y0.copy()) if y0.ndim > 1 else y0.copy()
+        hm.hmat_gemv(h, 1, 1.0, np.asfortranarray(x) if x.ndim > 1 else x, 1.0, yh)
+        assert_parity(yh, HTx + y0)
+    finally:
+        hm.hmat_destroy(h)
+
+
+def test_adjoint_identity_c2_and_dmma():
+    """<y', H x> = <H^T y', x> at C2 size (SIMT path) and on a DMMA-eligible
+    shape with 64 right-hand sides (tensor-core path)."""
+    for cfg, nrhs in ((CONFIGS["c2"], 1), (HConfig("adj", d=3, L=3, b=64, r=32, seed=85), 64)):
+        h = device_operator(cfg, hm)
+        try:
+            n = cfg.N
+            X = torch.empty(nrhs, n, dtype=torch.float64, device="cuda")
+            Yp = torch.empty_like(X)
+            hgen.dev_fill_x(cfg, nrhs, 0, 0, n, X.data_ptr(), n)
+            hgen.dev_fill_x(cfg, nrhs, 1, 0, n, Yp.data_ptr(), n)
+            HX = torch.empty_like(X)
+            HTY = torch.empty_like(X)
+            hm.hmat_gemv(h, 0, 1.0, X.t(), 0.0, HX.t())
+            hm.hmat_gemv(h, 1, 1.0, Yp.t(), 0.0, HTY.t())
+            lhs = (Yp * HX).sum(dim=1)
+            rhs = (HTY * X).sum(dim=1)
+            scale = (Yp.abs() * HX.abs()).sum(dim=1)
+            assert torch.all((lhs - rhs).abs() <= 1e-12 * scale)
+        finally:
+            hm.hmat_destroy(h)
+            torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("d,L,b,r", [(2, 3, 16, 4), (3, 2, 8, 2), (1, 4, 2, 3), (2, 1, 5, 2)])
+def test_strict_structure(d, L, b, r):
+    """hmat_create_strict (Def 2.4 read literally: leaf-parent diagonal blocks
+    dense) vs the oracle's strict block loop."""
+    c = 1 << d
+    N = b * c ** L
+    W = (c - 1) * r
+    rng = np.random.default_rng(90 + L)
+    U = [rng.standard_normal((N, W)) / 8 for _ in range(L - 1)]
+    V = [rng.standard_normal((N, W)) / 8 for _ in range(L - 1)]
+    Dc = rng.standard_normal((N, c * b)) / 8
+    x = rng.uniform(-1, 1, (N, 2))
+    ref = oracle.matvec_strict(d, L, b, r, U, V, Dc, x)
+    h = hm.hmat_create_strict(L, d, b, r, U, V, Dc)
+    try:
+        y = _dev_cols(np.zeros((N, 2)))
+        hm.hmat_matvec(h, _dev_cols(x), y)
+        assert_parity(y.cpu().numpy(), ref)
+    finally:
+        hm.hmat_destroy(h)

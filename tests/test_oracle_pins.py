@@ -259,3 +259,63 @@ def test_rows_generated_equals_block_loop(cfg):
     rows = np.array(sorted(set([0, 1, cfg.b - 1, cfg.b, cfg.N // 2, cfg.N - 1] + list(range(0, cfg.N, 37)))))
     yr = oracle.rows_generated(cfg, x, rows)
     assert rel(yr, y[rows]) < 1e-13
+
+
+# -- transposed product (GEMV "T") -------------------------------
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 3, 2, 2), (2, 2, 4, 3), (3, 1, 8, 2), (2, 3, 3, 1), (1, 0, 5, 2)])
+def test_transpose_block_loop_equals_brute_force(d, L, b, r):
+    """oracle.matvec_t = A^T x with A the assembled matrix (brute force)."""
+    U, V, D = rand_panels(d, L, b, r, 60 + d + L)
+    A = oracle.assemble(d, L, b, r, U, V, D)
+    x = np.random.default_rng(61).standard_normal((len(D), 2))
+    assert rel(oracle.matvec_t(d, L, b, r, U, V, D, x), A.T @ x) < 1e-13
+
+
+# -- the paper-strict reading of Def 2.4 (SURVEY §8 f2, DESIGN.md R1) -----------------
+
+@pytest.mark.parametrize("d,L", [(1, 1), (1, 4), (2, 1), (2, 2), (2, 3), (3, 2)])
+def test_strict_census(d, L):
+    """Leaves checked first: every child pair of a leaf-parent is dense, so
+    low-rank blocks live at levels 1..L-1 (c^L - c of them) and c^{L+1} dense
+    b x b blocks tile the leaf-parent diagonal."""
+    c = 1 << d
+    lr, dense, lr1 = oracle.block_census_strict(d, L)
+    assert lr == c ** L - c
+    assert dense == c ** (L + 1)
+    if d == 2 and L >= 2:
+        assert lr1 == 12  # the paper's walkthrough: 12 of 16 (PAPER.md:350-351)
+    if L == 1:
+        assert lr1 == 0   # the root's children are leaves: all pairs dense
+
+
+@pytest.mark.parametrize("d,L,b", [(1, 3, 2), (2, 2, 2), (3, 2, 1), (2, 1, 3)])
+def test_strict_tiles_exactly_once(d, L, b):
+    cnt = oracle.cover_count_strict(d, L, b)
+    assert cnt.min() == 1 and cnt.max() == 1
+
+
+def test_strict_storage_matches_survey():
+    """8 [2(c-1) r N (L-1) + N c b] bytes: 137.44 GB for configs[3]'s shape, vs
+    124.55 GB for the BASELINE reading (the survey's byte check of R1)."""
+    c, r, N, L, b = 4, 16, 2 ** 24, 9, 64
+    assert 8 * (2 * (c - 1) * r * N * (L - 1) + N * c * b) == 137_438_953_472
+
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 3, 2, 2), (2, 2, 2, 3), (3, 2, 1, 2), (2, 3, 4, 1)])
+def test_strict_block_loop_brute_force_and_equivalence(d, L, b, r):
+    """Strict block loop = brute force of the strict assembled matrix, and the
+    strict H-matrix of depth L, leaf b is the BASELINE-reading H-matrix of
+    depth L-1, leaf 2^d b on the same panels (what hmat_create_strict uses)."""
+    c = 1 << d
+    N = b * c ** L
+    W = (c - 1) * r
+    rng = np.random.default_rng(70 + d * 10 + L)
+    U = [rng.standard_normal((N, W)) for _ in range(L - 1)]
+    V = [rng.standard_normal((N, W)) for _ in range(L - 1)]
+    Dc = rng.standard_normal((N, c * b))
+    x = rng.standard_normal((N, 2))
+    A = oracle.assemble_strict(d, L, b, r, U, V, Dc)
+    y = oracle.matvec_strict(d, L, b, r, U, V, Dc, x)
+    assert rel(y, A @ x) < 1e-13
+    assert rel(oracle.matvec(d, L - 1, c * b, r, U, V, Dc, x), y) < 1e-14
