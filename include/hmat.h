@@ -75,6 +75,9 @@ typedef struct {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId (same on all ranks); P > 1 only */
   void* cuda_stream;          /* cudaStream_t to enqueue on; NULL => library-owned    */
   int device;                 /* CUDA ordinal of this rank's GPU                     */
+  int external_exchange;      /* P > 1: 0 = NCCL inside hmat_matvec (needs the id);  */
+                              /* 1 = the caller sums the exchange buffer between     */
+                              /*     hmat_project and hmat_expand (MPI, torch, ...)  */
 } hmat_dist_t;
 
 /* Build H from canonical panels (see above).  U and V are arrays of `depth`
@@ -120,6 +123,23 @@ hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double
  * dim, 2^dim leaf_size, ...) and is built as such.  depth >= 1. */
 hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
                                const double* const* V, const double* Dc, const hmat_dist_t* dist, hmat_t* out);
+
+/* Split-phase form (one pass: nrhs <= 8, or <= 64 on the tensor-core path), for
+ * a caller-provided exchange (hmat_dist_t.external_exchange = 1: MPI,
+ * torch.distributed, ...) or to overlap other work.  x, y, exchange are device
+ * pointers on H's device; work is enqueued on H's stream.
+ *   hmat_exchange_size: doubles of this pass's packed exchange buffer (level-
+ *     major, target-major z of the levels whose parent spans > 1 rank; 0 when
+ *     P = 1), per hmat_plan_query's layout.
+ *   hmat_project: Step 1 + on-chip Step 2; writes this rank's
+ *     contributions (partial node sums, zeros elsewhere) to exchange[0..count).
+ *   the caller sums exchange over all ranks (Steps 2-4);
+ *   hmat_expand: reads the summed exchange, Step 5: y = H x.
+ * With NCCL (external_exchange = 0) hmat_matvec does exactly this with an
+ * in-place ncclAllReduce. */
+hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count);
+hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange);
+hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, double* y, int nrhs);
 
 /* Diagnostic form: only the low-rank levels l with bit (l-1) of level_mask set
  * and, if dense != 0, the dense leaf blocks: y = y_D + sum_{l in mask} y_l. */

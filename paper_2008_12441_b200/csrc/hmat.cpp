@@ -114,6 +114,7 @@ struct hmat_s {
   double* part_d = nullptr;
   int* cnt_d = nullptr;
   double* Dt = nullptr;  // D^T, built on the first transposed product
+  bool external = false;  // P > 1 with a caller-provided exchange (split-phase API)
   bool prof = false;
   std::vector<EventPair> ev;
   std::vector<cudaEvent_t> pool;
@@ -157,7 +158,8 @@ hmat_status validate_dist(const hmat_dist_t* dist, int* P, int* rank) {
   if (!dist) return HMAT_OK;
   *P = dist->nranks;
   *rank = dist->rank;
-  if (dist->nranks > 1 && !dist->nccl_unique_id) return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1");
+  if (dist->nranks > 1 && !dist->nccl_unique_id && !dist->external_exchange)
+    return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1 (and no external exchange)");
   if (dist->device < 0) return fail(HMAT_ERR_INVALID, "device ordinal must be >= 0");
   return HMAT_OK;
 }
@@ -230,7 +232,8 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(p.dsmem_p, p.dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
-  if (p.P > 1) {
+  H->external = p.P > 1 && dist->external_exchange;
+  if (p.P > 1 && !H->external) {
     std::string m = hmat::comm_create(dist->nccl_unique_id, p.P, p.rank, &H->comm);
     if (!m.empty()) return bail(fail(HMAT_ERR_NCCL, m));
   }
@@ -367,14 +370,19 @@ hmat_status ensure_dt(hmat_s* H) {
   return HMAT_OK;
 }
 
+enum { kPhaseProject = 1, kPhaseExchange = 2, kPhaseExpand = 4, kPhaseAll = 7 };
+
 // y = alpha op(H) x + beta y restricted to the selected parts (the whole path).
+// `phases` selects project / exchange / expand (split-phase API: one pass only).
 hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta, double* y, int nrhs,
-                uint64_t level_mask, int dense) {
+                uint64_t level_mask, int dense, int phases = kPhaseAll, double* exch_out = nullptr,
+                const double* exch_in = nullptr) {
   if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
-  if (!x || !y) return fail(HMAT_ERR_INVALID, "x or y is NULL");
+  if (!x || (!y && (phases & kPhaseExpand))) return fail(HMAT_ERR_INVALID, "x or y is NULL");
   if (nrhs < 1) return fail(HMAT_ERR_INVALID, "nrhs must be >= 1");
   if (trans != 0 && trans != 1) return fail(HMAT_ERR_INVALID, "trans must be 0 (H) or 1 (H^T)");
-  if (static_cast<const void*>(x) == static_cast<const void*>(y)) return fail(HMAT_ERR_INVALID, "x and y alias");
+  if (y && static_cast<const void*>(x) == static_cast<const void*>(y))
+    return fail(HMAT_ERR_INVALID, "x and y alias");
   const hmat::Plan& p = H->plan;
   CUDA_TRY(cudaSetDevice(H->device));
   if (trans) {
@@ -382,7 +390,14 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     if (st != HMAT_OK) return st;
   }
   const int64_t n = p.N_loc;
-  const bool x_dev = is_device_ptr(x), y_dev = is_device_ptr(y);
+  const bool x_dev = is_device_ptr(x), y_dev = y ? is_device_ptr(y) : true;
+  if (phases != kPhaseAll) {
+    const int width = use_dmma(p, nrhs) ? hmat::kDmmaNB : hmat::kMaxNR;
+    if (nrhs > width) return fail(HMAT_ERR_INVALID, "split-phase calls take at most one pass of right-hand sides");
+    if (!x_dev || !y_dev) return fail(HMAT_ERR_INVALID, "split-phase calls need device x and y");
+  } else if (p.P > 1 && H->external) {
+    return fail(HMAT_ERR_UNSUPPORTED, "external exchange: use hmat_project / hmat_expand");
+  }
   const bool host_io = !x_dev || !y_dev;
   if (p.L < 64) level_mask &= (p.L == 0 ? 0ull : (~0ull >> (64 - p.L)));
 
@@ -447,6 +462,34 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.xs_p = p.xs_p;
   a.xs_e = p.xs_e;
 
+  // One pass of right-hand sides: [zero the exchange levels] project
+  // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
+  auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project) -> hmat_status {
+    const size_t bytes = exch * sizeof(double);
+    if (phases & kPhaseProject) {
+      if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(zex, 0, bytes, H->stream));
+      if (has_project && level_mask) {
+        prof_begin(H, 0, &ep);
+        CUDA_TRY(project());
+        prof_end(H, &ep);
+      }
+      if (exch_out && exch) CUDA_TRY(cudaMemcpyAsync(exch_out, zex, bytes, cudaMemcpyDeviceToDevice, H->stream));
+    }
+    if ((phases & kPhaseExchange) && !H->external && p.P > 1 && exch) {
+      prof_begin(H, 1, &ep);
+      std::string m = hmat::comm_allreduce_sum(H->comm, zex, exch, H->stream);
+      if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+      prof_end(H, &ep);
+    }
+    if (phases & kPhaseExpand) {
+      if (exch_in && exch) CUDA_TRY(cudaMemcpyAsync(zex, exch_in, bytes, cudaMemcpyDeviceToDevice, H->stream));
+      prof_begin(H, 2, &ep);
+      CUDA_TRY(expand());
+      prof_end(H, &ep);
+    }
+    return HMAT_OK;
+  };
+
   if (use_dmma(p, nrhs)) {
     hmat_status st = ensure_dmma(H);
     if (st != HMAT_OK) return st;
@@ -471,21 +514,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         lv.tbase = p.zt_tbase[l];
       }
       const size_t exch = size_t(p.z_exch_rows) * p.W * hmat::kDmmaNB;
-      if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(H->zex_d, 0, exch * sizeof(double), H->stream));
-      if (p.dgrid_p > 0 && level_mask) {
-        prof_begin(H, 0, &ep);
-        CUDA_TRY(hmat::launch_project_dmma(a, p.dgrid_p, p.dsmem_p, H->stream));
-        prof_end(H, &ep);
-      }
-      if (p.P > 1 && exch) {
-        prof_begin(H, 1, &ep);
-        std::string m = hmat::comm_allreduce_sum(H->comm, H->zex_d, exch, H->stream);
-        if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
-        prof_end(H, &ep);
-      }
-      prof_begin(H, 2, &ep);
-      CUDA_TRY(hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream));
-      prof_end(H, &ep);
+      hmat_status st2 = pass(
+          H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, p.dgrid_p, p.dsmem_p, H->stream); },
+          [&] { return hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream); }, p.dgrid_p > 0);
+      if (st2 != HMAT_OK) return st2;
     }
   }
   for (int c0 = 0; !use_dmma(p, nrhs) && c0 < nrhs; c0 += hmat::kMaxNR) {
@@ -510,23 +542,12 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       lv.tbase = p.zt_tbase[l];
     }
     const size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
-    if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(H->zex, 0, exch * sizeof(double), H->stream));
-    if (ly.grid_p > 0 && level_mask) {
-      prof_begin(H, 0, &ep);
-      CUDA_TRY(hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream));
-      prof_end(H, &ep);
-    }
-    if (p.P > 1 && exch) {
-      prof_begin(H, 1, &ep);
-      std::string m = hmat::comm_allreduce_sum(H->comm, H->zex, exch, H->stream);
-      if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
-      prof_end(H, &ep);
-    }
-    prof_begin(H, 2, &ep);
-    CUDA_TRY(hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream));
-    prof_end(H, &ep);
+    hmat_status st2 = pass(
+        H->zex, exch, [&] { return hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream); },
+        [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0);
+    if (st2 != HMAT_OK) return st2;
   }
-  if (!y_dev) {
+  if (!y_dev && (phases & kPhaseExpand)) {
     prof_begin(H, 3, &ep);
     CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
     prof_end(H, &ep);
@@ -550,6 +571,35 @@ hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs) {
 
 hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double beta, double* y, int nrhs) {
   return run(H, trans, alpha, x, beta, y, nrhs, ~0ull, 1);
+}
+
+hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count) {
+  if (!H || !count || nrhs < 1) return fail(HMAT_ERR_INVALID, "NULL argument or nrhs < 1");
+  const hmat::Plan& p = H->plan;
+  if (use_dmma(p, nrhs)) {
+    if (nrhs > hmat::kDmmaNB) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
+    *count = p.P > 1 ? p.z_exch_rows * p.W * hmat::kDmmaNB : 0;
+  } else {
+    if (nrhs > hmat::kMaxNR) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
+    *count = p.P > 1 ? p.z_exch_rows * p.Wp * nr_cap(nrhs) : 0;
+  }
+  return HMAT_OK;
+}
+
+hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange) {
+  int64_t count = 0;
+  hmat_status st = hmat_exchange_size(H, nrhs, &count);
+  if (st != HMAT_OK) return st;
+  if (count && !exchange) return fail(HMAT_ERR_INVALID, "exchange is NULL");
+  return run(H, 0, 1.0, x, 0.0, nullptr, nrhs, ~0ull, 1, kPhaseProject, exchange, nullptr);
+}
+
+hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, double* y, int nrhs) {
+  int64_t count = 0;
+  hmat_status st = hmat_exchange_size(H, nrhs, &count);
+  if (st != HMAT_OK) return st;
+  if (count && !exchange) return fail(HMAT_ERR_INVALID, "exchange is NULL");
+  return run(H, 0, 1.0, x, 0.0, y, nrhs, ~0ull, 1, kPhaseExpand, nullptr, exchange);
 }
 
 hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,

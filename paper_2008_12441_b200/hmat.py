@@ -27,7 +27,7 @@ PHASES = ("project", "exchange", "expand", "copies")
 
 # Every symbol include/hmat.h declares (checked by tests/test_abi.py).
 EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_panel", "hmat_matvec", "hmat_gemv",
-           "hmat_matvec_parts", "hmat_destroy",
+           "hmat_exchange_size", "hmat_project", "hmat_expand", "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query")
 
@@ -40,7 +40,7 @@ class HMatError(RuntimeError):
 
 class hmat_dist_t(ctypes.Structure):
     _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int)]
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int), ("external_exchange", ctypes.c_int)]
 
 
 class hmat_plan_info_t(ctypes.Structure):
@@ -63,6 +63,9 @@ _sigs = {
     "hmat_matvec": (_i, [_H, _P, _P, _i]),
     "hmat_gemv": (_i, [_H, _i, ctypes.c_double, _P, ctypes.c_double, _P, _i]),
     "hmat_create_strict": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
+    "hmat_exchange_size": (_i, [_H, _i, ctypes.POINTER(_i64)]),
+    "hmat_project": (_i, [_H, _P, _i, _P]),
+    "hmat_expand": (_i, [_H, _P, _P, _P, _i]),
     "hmat_matvec_parts": (_i, [_H, _P, _P, _i, _u64, _i]),
     "hmat_destroy": (_i, [_H]),
     "hmat_last_error": (ctypes.c_char_p, []),
@@ -132,9 +135,10 @@ def _vec(a, n: int):
     return a.data_ptr(), a.shape[1]
 
 
-def _dist(nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, device=None):
+def _dist(nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, device=None, external_exchange=False):
     d = hmat_dist_t()
     d.nranks, d.rank = nranks, rank
+    d.external_exchange = int(bool(external_exchange))
     d._id_buf = None
     if nccl_unique_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
@@ -203,6 +207,32 @@ def hmat_gemv(h, trans: int, alpha: float, x, beta: float, y, nrhs: int | None =
     nrhs = kx if nrhs is None else nrhs
     assert kx >= nrhs and ky >= nrhs
     _check(_lib.hmat_gemv(h, int(trans), float(alpha), xp, float(beta), yp, nrhs), "hmat_gemv")
+
+
+def hmat_exchange_size(h, nrhs: int) -> int:
+    """doubles of one pass's packed exchange buffer (0 when P = 1)."""
+    cnt = _i64()
+    _check(_lib.hmat_exchange_size(h, nrhs, ctypes.byref(cnt)), "hmat_exchange_size")
+    return cnt.value
+
+
+def hmat_project(h, x, exchange, nrhs: int | None = None):
+    """Split phase 1: this rank's contributions -> exchange (device, >= exchange_size doubles)."""
+    n = hmat_local_rows(h)
+    n = n[1] - n[0]
+    xp, kx = _vec(x, n)
+    nrhs = kx if nrhs is None else nrhs
+    _check(_lib.hmat_project(h, xp, nrhs, _ptr(exchange)), "hmat_project")
+
+
+def hmat_expand(h, x, exchange, y, nrhs: int | None = None):
+    """Split phase 3: y = H x from the exchange buffer summed over all ranks."""
+    n = hmat_local_rows(h)
+    n = n[1] - n[0]
+    xp, kx = _vec(x, n)
+    yp, ky = _vec(y, n)
+    nrhs = kx if nrhs is None else nrhs
+    _check(_lib.hmat_expand(h, xp, _ptr(exchange), yp, nrhs), "hmat_expand")
 
 
 def hmat_matvec_parts(h, x, y, level_mask: int, dense: bool, nrhs: int | None = None):

@@ -1,0 +1,105 @@
+"""The P > 1 data path on one GPU, rank after rank.
+
+P shards (hmat_dist_t.nranks = P, external_exchange = 1), each built from ITS
+rows of the panels, run the split-phase API: hmat_project for every rank, the
+exchange buffers summed over ranks here (what ncclAllReduce does inside
+hmat_matvec), then hmat_expand for every rank.  No kernel waits on another
+rank's kernel (the ranks run one after the other), so this is safe on one GPU
+and exercises every multi-GPU code path of the kernels: exchanged levels in
+the packed buffer, nodes split across shards, per-shard target bases.  Only
+the NCCL call itself is not covered (tests/test_multigpu_cpu.py covers the
+layout with real multi-process gloo communication).
+"""
+import numpy as np
+import pytest
+
+from gen import hgen
+from gen.hgen import HConfig
+from oracle import oracle
+from tests.helpers import assert_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2008_12441_b200 import hmat as hm
+
+
+def sharded_matvec(cfg, P, nrhs):
+    hs, xs = [], []
+    for g in range(P):
+        r0, r1 = g * cfg.N // P, (g + 1) * cfg.N // P
+        U, V, D = hgen.inputs(cfg, r0, r1)
+        d = hm._dist(nranks=P, rank=g, device=0, external_exchange=True)
+        hs.append(hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D, d))
+        x = hgen.xblock(cfg, nrhs=nrhs, row_begin=r0, row_end=r1)
+        xs.append(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())  # (nrhs, n) = column-major (n, nrhs)
+    try:
+        cnt = hm.hmat_exchange_size(hs[0], nrhs)
+        assert all(hm.hmat_exchange_size(h, nrhs) == cnt for h in hs)
+        ex = [torch.zeros(max(cnt, 1), dtype=torch.float64, device="cuda") for _ in range(P)]
+        for g in range(P):                       # Step 1 + on-chip Step 2 on every rank
+            hm.hmat_project(hs[g], xs[g].t(), ex[g], nrhs)
+        torch.cuda.synchronize()
+        total = torch.stack(ex).sum(dim=0)       # Steps 2-4 across ranks
+        ys = []
+        for g in range(P):                       # Step 5 on every rank
+            y = torch.empty_like(xs[g])
+            hm.hmat_expand(hs[g], xs[g].t(), total, y.t(), nrhs)
+            ys.append(y)
+        torch.cuda.synchronize()
+        return torch.cat(ys, dim=1).t().cpu().numpy(), cnt
+    finally:
+        for h in hs:
+            hm.hmat_destroy(h)
+
+
+CASES = [
+    (HConfig("p2d", d=2, L=4, b=16, r=4, seed=301), 2, 1),
+    (HConfig("p2d", d=2, L=4, b=16, r=4, seed=301), 4, 3),
+    (HConfig("p2d", d=2, L=4, b=16, r=4, seed=301), 8, 2),
+    (HConfig("p2d", d=2, L=4, b=16, r=4, seed=301), 16, 1),
+    (HConfig("p3d", d=3, L=3, b=8, r=3, seed=302), 8, 1),
+    (HConfig("p3d", d=3, L=3, b=8, r=3, seed=302), 2, 5),
+    (HConfig("p1d", d=1, L=7, b=4, r=2, seed=303), 8, 2),
+    (HConfig("podd", d=2, L=3, b=7, r=3, seed=304), 4, 1),
+    (HConfig("pdmma", d=3, L=3, b=64, r=32, seed=305), 8, 64),   # tensor-core path
+    (HConfig("pdmma2", d=2, L=4, b=64, r=32, seed=306), 4, 20),  # tensor-core path, ragged rhs
+]
+
+
+@pytest.mark.parametrize("cfg,P,nrhs", CASES, ids=lambda v: getattr(v, "name", str(v)))
+def test_sharded_split_phase_matches_oracle(cfg, P, nrhs):
+    y, cnt = sharded_matvec(cfg, P, nrhs)
+    U, V, D = hgen.inputs(cfg)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, hgen.xblock(cfg, nrhs=nrhs))
+    assert_parity(y, ref)
+    assert cnt > 0
+
+
+def test_sharded_equals_single_gpu_c2_shape():
+    """P = 4 shards of a C2-sized operator agree with the P = 1 operator."""
+    cfg = HConfig("c2s", d=2, L=6, b=64, r=16, seed=307)
+    y4, _ = sharded_matvec(cfg, 4, 1)
+    U, V, D = hgen.inputs(cfg)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        x = torch.from_numpy(np.ascontiguousarray(hgen.xblock(cfg, nrhs=1)[:, 0])).cuda()
+        y1 = torch.empty_like(x)
+        hm.hmat_matvec(h, x, y1)
+        assert_parity(y4[:, 0], y1.cpu().numpy())
+    finally:
+        hm.hmat_destroy(h)
+
+
+def test_external_exchange_requires_split_api():
+    cfg = HConfig("p", d=2, L=2, b=4, r=2, seed=308)
+    U, V, D = hgen.inputs(cfg, 0, cfg.N // 2)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D, hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
+    try:
+        x = torch.zeros(cfg.N // 2, dtype=torch.float64, device="cuda")
+        with pytest.raises(hm.HMatError) as ei:
+            hm.hmat_matvec(h, x, torch.empty_like(x))
+        assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
+    finally:
+        hm.hmat_destroy(h)
