@@ -34,6 +34,7 @@ class HConfig:
     r: int
     nrhs: int = 1
     seed: int = SEED_BASE
+    adm: int = 0  # 0 = weak admissibility, 1 = standard admissibility
 
     @property
     def c(self) -> int:
@@ -44,8 +45,18 @@ class HConfig:
         return self.b * self.c ** self.L
 
     @property
+    def slots(self) -> int:
+        """low-rank slots per node: 2^d - 1 siblings (weak) or 6^d - 3^d (standard)."""
+        return self.c - 1 if self.adm == 0 else 6 ** self.d - 3 ** self.d
+
+    @property
     def W(self) -> int:
-        return (self.c - 1) * self.r
+        return self.slots * self.r
+
+    @property
+    def dcols(self) -> int:
+        """columns of the dense panel: b (leaf diagonal) or 3^d b (near field)."""
+        return self.b if self.adm == 0 else 3 ** self.d * self.b
 
     def m(self, level: int) -> int:
         """Rows of a level-`level` node, m_l = N / c^l."""
@@ -58,7 +69,7 @@ class HConfig:
     @property
     def factor_scalars(self) -> int:
         """N (2 (c-1) r L + b): the exact O(rN log N) storage."""
-        return self.N * (2 * self.W * self.L + self.b)
+        return self.N * (2 * self.W * self.L + self.dcols)
 
     @property
     def factor_bytes(self) -> int:
@@ -142,7 +153,7 @@ def _ptr(a: np.ndarray) -> int:
 def panel(cfg: HConfig, tag: int, level: int, row_begin: int = 0, row_end: int | None = None) -> np.ndarray:
     """Rows [row_begin, row_end) of U_level (TAG_U), V_level (TAG_V) or D (TAG_D)."""
     row_end = cfg.N if row_end is None else row_end
-    ncols = cfg.b if tag == TAG_D else cfg.W
+    ncols = cfg.dcols if tag == TAG_D else cfg.W
     scale = 0.125 if tag == TAG_D else cfg.lowrank_scale(level)
     lvl = 0 if tag == TAG_D else level
     out = np.empty((row_end - row_begin, ncols), dtype=np.float64)
@@ -176,7 +187,7 @@ def dev_fill_panel(cfg: HConfig, tag: int, level: int, row_begin: int, row_end: 
                    out_ptr: int, ld: int, stream: int = 0) -> None:
     """Device twin of panel(): writes rows [row_begin,row_end) to device memory
     at out_ptr with leading dimension ld (doubles)."""
-    ncols = cfg.b if tag == TAG_D else cfg.W
+    ncols = cfg.dcols if tag == TAG_D else cfg.W
     scale = 0.125 if tag == TAG_D else cfg.lowrank_scale(level)
     lvl = 0 if tag == TAG_D else level
     rc = _load_dev().hgen_dev_fill_rowmajor(cfg.seed, tag, lvl, 0, row_begin, row_end, ncols, scale,

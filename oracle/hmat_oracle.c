@@ -400,3 +400,234 @@ void oracle_rows_generated(int d, int L, int b, int r, uint64_t seed, const doub
   free(zc);
   free(last_t);
 }
+
+/* ===========================================================================
+ * STANDARD admissibility: Def 2.4 with the standard admissibility
+ * condition eq:standard-ad-cond, rho = sqrt(d), on the ideal
+ * domain [0,1]^d with a non-periodic boundary (the paper's load-balance case,
+ * PAPER.md:606-629; R17).
+ *
+ * A level-l node k is the box of side h = 2^-l with integer coordinates
+ * (k decoded from Morton bits: bit j of coordinate i is bit j d + i of k).
+ * Two level-l boxes with coordinate differences D_i have
+ *   diam = sqrt(d) h,  dist = h sqrt(sum_i g_i^2),  g_i = max(0, |D_i| - 1),
+ * so min(diam, diam) <= rho dist  <=>  d h^2 <= d h^2 sum_i g_i^2
+ *                                 <=>  sum_i g_i^2 >= 1   (exact integers).
+ *
+ * Canonical panels (the input format of hmat_create_standard):
+ *   M = 6^d - 3^d slots per node: for target t (child position tau of its
+ *   parent) the candidate sources s are the children sigma of the parent's
+ *   3^d neighbours eps in {-1,0,1}^d; slots enumerate the pairs (eps, sigma)
+ *   in increasing order of (sum_i (eps_i+1) 3^i) 2^d + sum_i sigma_i 2^i,
+ *   skipping those where s is a neighbour of t; pairs outside the domain keep
+ *   their slot (zero factors).
+ *   U_l row i, columns [q r, (q+1) r): row i - t m_l of U_{t,s}, s = slot q of t.
+ *   V_l row j, columns [q r, (q+1) r): row j - s m_l of V_{t,s}, t = slot q of s.
+ *   Dn row i (leaf t), columns [e b, (e+1) b): row i - t b of D_{t,s},
+ *   s = t + eps, e = sum_i (eps_i + 1) 3^i (neighbours incl. t; zero if absent).
+ * =========================================================================*/
+
+static void morton_decode(int d, int64_t k, int level, int64_t* x) {
+  for (int i = 0; i < d; ++i) x[i] = 0;
+  for (int j = 0; j < level; ++j)
+    for (int i = 0; i < d; ++i) x[i] |= ((k >> (j * d + i)) & 1) << j;
+}
+
+/* standard admissibility of two level-l boxes (eq:standard-ad-cond, rho = sqrt(d)) */
+static int std_admissible(int d, const int64_t* xt, const int64_t* xs) {
+  int64_t sum_g2 = 0;
+  for (int i = 0; i < d; ++i) {
+    int64_t D = xt[i] - xs[i];
+    if (D < 0) D = -D;
+    int64_t g = D - 1 > 0 ? D - 1 : 0;
+    sum_g2 += g * g;
+  }
+  return d * 1 <= d * sum_g2; /* diam^2 <= rho^2 dist^2, both divided by h^2 */
+}
+
+static int std_neighbour(int d, const int64_t* xt, const int64_t* xs) {
+  for (int i = 0; i < d; ++i) {
+    int64_t D = xt[i] - xs[i];
+    if (D < -1 || D > 1) return 0;
+  }
+  return 1;
+}
+
+int oracle_std_slots(int d) {
+  int p6 = 1, p3 = 1;
+  for (int i = 0; i < d; ++i) { p6 *= 6; p3 *= 3; }
+  return p6 - p3;
+}
+
+/* slot of source s in target t's list (both at `level`), -1 if s is not a
+ * candidate (its parent is not a neighbour of t's parent, or s neighbours t). */
+int oracle_std_slot(int d, int level, int64_t t, int64_t s) {
+  int64_t xt[3], xs[3];
+  morton_decode(d, t, level, xt);
+  morton_decode(d, s, level, xs);
+  int64_t eps_t[3], sig_t[3];
+  for (int i = 0; i < d; ++i) {
+    eps_t[i] = (xs[i] >> 1) - (xt[i] >> 1);
+    sig_t[i] = xs[i] & 1;
+    if (eps_t[i] < -1 || eps_t[i] > 1) return -1;
+  }
+  if (std_neighbour(d, xt, xs)) return -1;
+  int c = 1 << d, p3 = 1;
+  for (int i = 0; i < d; ++i) p3 *= 3;
+  int target_code = 0, mul = 1, sc = 0;
+  for (int i = 0; i < d; ++i) { target_code += (int)(eps_t[i] + 1) * mul; mul *= 3; }
+  for (int i = 0; i < d; ++i) sc |= (int)sig_t[i] << i;
+  target_code = target_code * c + sc;
+  /* count valid (eps, sigma) pairs before target_code, for t's child position */
+  int q = 0;
+  for (int code = 0; code < target_code; ++code) {
+    int e = code / c, sg = code % c, rem = e;
+    int64_t xc[3];
+    for (int i = 0; i < d; ++i) {
+      int ei = rem % 3 - 1;
+      rem /= 3;
+      xc[i] = 2 * ((xt[i] >> 1) + ei) + ((sg >> i) & 1);
+    }
+    if (!std_neighbour(d, xt, xc)) ++q;
+  }
+  (void)p3;
+  return q;
+}
+
+/* Def 2.4 recursion with standard admissibility over hierarchical pairs (P_t, P_s). */
+static void visit_std(int d, int L, int level, int64_t pt, int64_t ps, block_fn fn, void* ctx) {
+  const int c = 1 << d;
+  for (int a = 0; a < c; ++a)
+    for (int bb = 0; bb < c; ++bb) {
+      int64_t t = pt * c + a, s = ps * c + bb;
+      int64_t xt[3], xs[3];
+      morton_decode(d, t, level + 1, xt);
+      morton_decode(d, s, level + 1, xs);
+      if (std_admissible(d, xt, xs)) fn(ctx, 1, level + 1, t, s);
+      else if (level + 1 == L) fn(ctx, 0, level + 1, t, s);
+      else visit_std(d, L, level + 1, t, s, fn, ctx);
+    }
+}
+
+static void visit_root_std(int d, int L, block_fn fn, void* ctx) {
+  if (L == 0) fn(ctx, 0, 0, 0, 0);
+  else visit_std(d, L, 0, 0, 0, fn, ctx);
+}
+
+typedef struct { int64_t lowrank, dense; int level; int64_t target; int64_t target_lowrank; } std_census_t;
+
+static void std_census_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_census_t* cs = (std_census_t*)ctx;
+  (void)s;
+  if (kind == 1) {
+    cs->lowrank++;
+    if (level == cs->level && t == cs->target) cs->target_lowrank++;
+  } else {
+    cs->dense++;
+  }
+}
+
+/* totals, and the number of low-rank blocks of target `target` at `level` */
+void oracle_std_census(int d, int L, int level, int64_t target, int64_t* n_lowrank, int64_t* n_dense,
+                       int64_t* n_target) {
+  std_census_t cs = {0, 0, level, target, 0};
+  visit_root_std(d, L, std_census_cb, &cs);
+  *n_lowrank = cs.lowrank; *n_dense = cs.dense; *n_target = cs.target_lowrank;
+}
+
+void oracle_std_cover_count(int d, int L, int b, int32_t* count) {
+  cover_t cv;
+  cv.c = 1 << d; cv.L = L; cv.b = b; cv.N = (int64_t)b * ipow(cv.c, L); cv.count = count;
+  memset(count, 0, sizeof(int32_t) * (size_t)(cv.N * cv.N));
+  visit_root_std(d, L, cover_cb, &cv);
+}
+
+static int std_neighbour_index(int d, int64_t t, int64_t s, int level) {
+  int64_t xt[3], xs[3];
+  morton_decode(d, t, level, xt);
+  morton_decode(d, s, level, xs);
+  int e = 0, mul = 1;
+  for (int i = 0; i < d; ++i) { e += (int)(xs[i] - xt[i] + 1) * mul; mul *= 3; }
+  return e;
+}
+
+typedef struct {
+  int d, L, b, r, M, ND; int64_t N;
+  const double* const* U; const double* const* V; const double* Dn; double* A;
+} std_assemble_t;
+
+static void std_assemble_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_assemble_t* as = (std_assemble_t*)ctx;
+  const int64_t N = as->N;
+  if (kind == 0) {
+    const int e = std_neighbour_index(as->d, t, s, level);
+    for (int i = 0; i < as->b; ++i)
+      for (int j = 0; j < as->b; ++j)
+        as->A[(t * as->b + i) * N + (s * as->b + j)] = as->Dn[(t * as->b + i) * (as->ND * as->b) + e * as->b + j];
+    return;
+  }
+  const int64_t m = N / ipow(1 << as->d, level);
+  const int qt = oracle_std_slot(as->d, level, t, s), qs = oracle_std_slot(as->d, level, s, t);
+  const int W = as->M * as->r;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      double acc = 0.0;
+      for (int a = 0; a < as->r; ++a)
+        acc += as->U[level - 1][(t * m + i) * W + qt * as->r + a] * as->V[level - 1][(s * m + j) * W + qs * as->r + a];
+      as->A[(t * m + i) * N + (s * m + j)] = acc;
+    }
+}
+
+void oracle_std_assemble(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                         const double* Dn, double* A) {
+  std_assemble_t as;
+  as.d = d; as.L = L; as.b = b; as.r = r; as.M = oracle_std_slots(d);
+  as.ND = (int)ipow(3, d); as.N = (int64_t)b * ipow(1 << d, L);
+  as.U = U; as.V = V; as.Dn = Dn; as.A = A;
+  memset(A, 0, sizeof(double) * (size_t)(as.N * as.N));
+  visit_root_std(d, L, std_assemble_cb, &as);
+}
+
+/* y = H x, eq:hmat-vec-add over the standard-admissibility blocks */
+typedef struct {
+  int d, b, r, M, ND, nrhs; int64_t N;
+  const double* const* U; const double* const* V; const double* Dn; const double* x; double* y; double* z;
+} std_mv_t;
+
+static void std_mv_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_mv_t* mv = (std_mv_t*)ctx;
+  const int64_t N = mv->N;
+  for (int k = 0; k < mv->nrhs; ++k) {
+    const double* xk = mv->x + (int64_t)k * N;
+    double* yk = mv->y + (int64_t)k * N;
+    if (kind == 0) { /* y_t += D_ts x_s */
+      const int e = std_neighbour_index(mv->d, t, s, level);
+      for (int i = 0; i < mv->b; ++i)
+        for (int j = 0; j < mv->b; ++j)
+          yk[t * mv->b + i] += mv->Dn[(t * mv->b + i) * (mv->ND * mv->b) + e * mv->b + j] * xk[s * mv->b + j];
+      continue;
+    }
+    const int64_t m = N / ipow(1 << mv->d, level);
+    const int qt = oracle_std_slot(mv->d, level, t, s), qs = oracle_std_slot(mv->d, level, s, t);
+    const int W = mv->M * mv->r;
+    const double* Ul = mv->U[level - 1];
+    const double* Vl = mv->V[level - 1];
+    for (int a = 0; a < mv->r; ++a) mv->z[a] = 0.0;
+    for (int64_t j = 0; j < m; ++j)   /* z = V_ts^T x_s */
+      for (int a = 0; a < mv->r; ++a) mv->z[a] += Vl[(s * m + j) * W + qs * mv->r + a] * xk[s * m + j];
+    for (int64_t i = 0; i < m; ++i)   /* y_t += U_ts z */
+      for (int a = 0; a < mv->r; ++a) yk[t * m + i] += Ul[(t * m + i) * W + qt * mv->r + a] * mv->z[a];
+  }
+}
+
+void oracle_std_matvec(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                       const double* Dn, const double* x, double* y, int nrhs) {
+  std_mv_t mv;
+  mv.d = d; mv.b = b; mv.r = r; mv.M = oracle_std_slots(d); mv.ND = (int)ipow(3, d); mv.nrhs = nrhs;
+  mv.N = (int64_t)b * ipow(1 << d, L);
+  mv.U = U; mv.V = V; mv.Dn = Dn; mv.x = x; mv.y = y;
+  mv.z = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  for (int64_t i = 0; i < mv.N * nrhs; ++i) y[i] = 0.0;
+  visit_root_std(d, L, std_mv_cb, &mv);
+  free(mv.z);
+}

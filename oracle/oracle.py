@@ -197,3 +197,66 @@ def matvec_t(d: int, L: int, b: int, r: int, U, V, D, x) -> np.ndarray:
 def matvec_strict(d: int, L: int, b: int, r: int, U, V, Dc, x) -> np.ndarray:
     """y = H x for the paper-strict structure (U, V levels 1..L-1, leaf-parent dense panel)."""
     return _mv(_load().oracle_matvec_strict, d, L, b, r, U, V, Dc, x)
+
+
+# -- standard admissibility (SURVEY §8 f3) ------------------------------------------
+
+def _std_lib():
+    lib = _load()
+    if not getattr(lib, "_std_ready", False):
+        pp = ctypes.POINTER(_dp)
+        lib.oracle_std_slots.restype = ctypes.c_int
+        lib.oracle_std_slots.argtypes = [ctypes.c_int]
+        lib.oracle_std_slot.restype = ctypes.c_int
+        lib.oracle_std_slot.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64]
+        lib.oracle_std_census.restype = None
+        lib.oracle_std_census.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64] + \
+            [ctypes.POINTER(ctypes.c_int64)] * 3
+        lib.oracle_std_cover_count.restype = None
+        lib.oracle_std_cover_count.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p]
+        lib.oracle_std_assemble.restype = None
+        lib.oracle_std_assemble.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_std_matvec.restype = None
+        lib.oracle_std_matvec.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p,
+                                                               ctypes.c_void_p, ctypes.c_int]
+        lib._std_ready = True
+    return lib
+
+
+def std_slots(d: int) -> int:
+    """M = 6^d - 3^d interaction slots per node."""
+    return _std_lib().oracle_std_slots(d)
+
+
+def std_slot(d: int, level: int, t: int, s: int) -> int:
+    return _std_lib().oracle_std_slot(d, level, t, s)
+
+
+def std_census(d: int, L: int, level: int = 0, target: int = -1):
+    """(#low-rank, #dense, #low-rank blocks of `target` at `level`) by walking
+    Def 2.4 with standard admissibility."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _std_lib().oracle_std_census(d, L, level, target, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+    return a.value, b.value, c.value
+
+
+def std_cover_count(d: int, L: int, b: int) -> np.ndarray:
+    N = b * (1 << d) ** L
+    out = np.zeros((N, N), dtype=np.int32)
+    _std_lib().oracle_std_cover_count(d, L, b, out.ctypes.data)
+    return out
+
+
+def std_assemble(d: int, L: int, b: int, r: int, U, V, Dn) -> np.ndarray:
+    N = b * (1 << d) ** L
+    A = np.zeros((N, N), dtype=np.float64)
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dn = _c(Dn)
+    _std_lib().oracle_std_assemble(d, L, b, r, up, vp, Dn.ctypes.data, A.ctypes.data)
+    return A
+
+
+def std_matvec(d: int, L: int, b: int, r: int, U, V, Dn, x) -> np.ndarray:
+    _std_lib()
+    return _mv(_load().oracle_std_matvec, d, L, b, r, U, V, Dn, x)

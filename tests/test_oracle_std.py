@@ -1,0 +1,141 @@
+"""Pins of the standard-admissibility oracle (R17):
+the paper's interaction counts and load-balance factor, exact tiling, closed
+forms and brute force on tiny inputs."""
+import numpy as np
+import pytest
+
+from gen import hgen
+from gen.hgen import HConfig
+from oracle import oracle
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def std_panels(d, L, b, r, seed):
+    rng = np.random.default_rng(seed)
+    c = 1 << d
+    N = b * c ** L
+    M = 6 ** d - 3 ** d
+    U = [rng.standard_normal((N, M * r)) for _ in range(L)]
+    V = [rng.standard_normal((N, M * r)) for _ in range(L)]
+    Dn = rng.standard_normal((N, 3 ** d * b))
+    return U, V, Dn
+
+
+def morton(d, coords, level):
+    k = 0
+    for j in range(level):
+        for i in range(d):
+            k |= ((coords[i] >> j) & 1) << (j * d + i)
+    return k
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_interaction_counts_and_load_balance(d):
+    """an interior level-l box has 3^d 2^d - 3^d admissible
+    boxes, a corner box 2^d 2^d - 2^d; the ratio is the load-balance factor
+    (3/2)^d."""
+    L = {1: 6, 2: 4, 3: 4}[d]
+    level = L - 1
+    n = 1 << level
+    centre = morton(d, [n // 2 - 1] * d, level)   # parent is interior (level >= 3 in 1D/2D)
+    corner = morton(d, [0] * d, level)
+    _, _, nc = oracle.std_census(d, L, level, centre)
+    _, _, nk = oracle.std_census(d, L, level, corner)
+    assert nc == 3 ** d * 2 ** d - 3 ** d
+    assert nk == 2 ** d * 2 ** d - 2 ** d
+    assert nc / nk == pytest.approx((3 / 2) ** d)  # the paper's bound (3/2)^d, attained
+    assert oracle.std_slots(d) == 6 ** d - 3 ** d
+    # no admissible pair at level 1 (all 2^d children of the root touch)
+    assert all(oracle.std_census(d, L, 1, t)[2] == 0 for t in range(1 << d))
+
+
+@pytest.mark.parametrize("d,L,b", [(1, 4, 2), (2, 3, 1), (2, 3, 2), (3, 2, 1)])
+def test_std_tiles_exactly_once(d, L, b):
+    cnt = oracle.std_cover_count(d, L, b)
+    assert cnt.min() == 1 and cnt.max() == 1
+
+
+def test_dense_count_is_neighbour_count():
+    """Dense blocks = pairs of touching leaves (incl. the diagonal): in 2D with
+    n x n leaves, n^2 + 2 n (n-1) * 2 + 2 (n-1)^2 * 2."""
+    d, L = 2, 3
+    n = 1 << L
+    _, dense, _ = oracle.std_census(d, L)
+    assert dense == n * n + 4 * n * (n - 1) + 4 * (n - 1) ** 2
+
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 4, 2, 2), (2, 3, 1, 2), (2, 3, 2, 1), (3, 2, 1, 2), (2, 2, 3, 1)])
+def test_std_block_loop_equals_brute_force(d, L, b, r):
+    U, V, Dn = std_panels(d, L, b, r, 10 * d + L)
+    A = oracle.std_assemble(d, L, b, r, U, V, Dn)
+    x = np.random.default_rng(3).standard_normal((len(Dn), 2))
+    assert rel(oracle.std_matvec(d, L, b, r, U, V, Dn, x), A @ x) < 1e-13
+
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 5, 2, 3), (2, 3, 2, 2), (3, 2, 2, 1)])
+def test_std_all_ones_closed_form(d, L, b, r):
+    """All U, V = 1: every far-field entry equals r, so
+    y_i = sum_{j near leaf(i)} D_ij x_j + r sum_{j not near leaf(i)} x_j.
+    Catches a missing / extra interaction or a wrong near field."""
+    c = 1 << d
+    N = b * c ** L
+    M = 6 ** d - 3 ** d
+    U = [np.ones((N, M * r)) for _ in range(L)]
+    V = [np.ones((N, M * r)) for _ in range(L)]
+    Dn = np.zeros((N, 3 ** d * b))
+    x = np.random.default_rng(4).integers(-8, 9, N).astype(np.float64)
+    n = 1 << L
+    # leaf coordinates by brute force
+    coords = {}
+    for k in range(c ** L):
+        xc = [0] * d
+        for j in range(L):
+            for i in range(d):
+                xc[i] |= ((k >> (j * d + i)) & 1) << j
+        coords[k] = xc
+    y = oracle.std_matvec(d, L, b, r, U, V, Dn, x)
+    for i in range(0, N, max(1, N // 50)):
+        t = i // b
+        near = [s for s in range(c ** L) if all(abs(coords[s][q] - coords[t][q]) <= 1 for q in range(d))]
+        near_sum = sum(x[s * b:(s + 1) * b].sum() for s in near)
+        assert y[i] == pytest.approx(r * (x.sum() - near_sum), abs=1e-12)
+
+
+def test_std_delta_factor_single_entry():
+    """One admissible block (t, s) at level 3 in 2D with U_ts = e_a e_k^T,
+    V_ts = e_bb e_k^T gives H = e_{t m + a} e_{s m + bb}^T.  Panel columns use
+    slot(t -> s) for U and slot(s -> t) for V (the canonical layout)."""
+    d, L, b, r = 2, 3, 2, 2
+    N = b * 4 ** L
+    M = 27
+    level, m = 3, 2
+    t = morton(d, [2, 3], level)
+    s = morton(d, [5, 4], level)      # parents (1,1) and (2,2): neighbours; boxes 3 apart: admissible
+    qt, qs = oracle.std_slot(d, level, t, s), oracle.std_slot(d, level, s, t)
+    assert qt >= 0 and qs >= 0
+    U = [np.zeros((N, M * r)) for _ in range(L)]
+    V = [np.zeros((N, M * r)) for _ in range(L)]
+    U[level - 1][t * m + 1, qt * r + 1] = 1.0
+    V[level - 1][s * m + 0, qs * r + 1] = 1.0
+    A = oracle.std_assemble(d, L, b, r, U, V, np.zeros((N, 9 * b)))
+    expect = np.zeros((N, N))
+    expect[t * m + 1, s * m + 0] = 1.0
+    assert np.array_equal(A, expect)
+
+
+def test_std_slot_enumeration_is_a_bijection():
+    """For every box, slots 0..M-1 are each used exactly once by the in-domain
+    and out-of-domain candidates together; in-domain ones are symmetric."""
+    d, level = 2, 3
+    n = 1 << level
+    for t in range(n * n):
+        used = []
+        for s in range(n * n):
+            q = oracle.std_slot(d, level, t, s)
+            if q >= 0:
+                used.append(q)
+                assert oracle.std_slot(d, level, s, t) >= 0
+        assert len(set(used)) == len(used) and max(used) < 27
