@@ -113,6 +113,30 @@ hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
  * hmat_matvec. */
 hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double beta, double* y, int nrhs);
 
+/* STANDARD admissibility: Def 2.4 with eq:standard-ad-cond
+ * (PAPER.md:279-297), rho = sqrt(d), on [0,1]^dim with a non-periodic boundary:
+ * two same-level boxes are admissible iff they do not touch.  Every node t at
+ * levels 2..depth has a rank-`rank` block against each box of its interaction
+ * list (children of the parent's 3^dim neighbours that do not touch t; at most
+ * M = 6^dim - 3^dim); dense blocks D_{t,s} join every pair of
+ * touching leaves (3^dim per leaf, incl. t).  Box coordinates: Morton, bit j of
+ * coordinate i = bit j dim + i of the node index.
+ * Canonical panels:
+ *   M slots per node: for a box with child position tau, the candidates are the
+ *   children sigma of the parent's neighbours eps in {-1,0,1}^dim, enumerated in
+ *   increasing (sum_i (eps_i+1) 3^i) 2^dim + sum_i sigma_i 2^i, skipping those
+ *   that touch the box; candidates outside the domain keep their slot (unused).
+ *   U[l-1], V[l-1]: N x (M rank), like the weak panels with "sibling q" replaced
+ *   by "slot q" (U target-major, V source-major).
+ *   Dn: N x (3^dim leaf_size): row i of leaf t, columns [e b, (e+1) b) = row
+ *   i - t b of D_{t, t+eps}, e = sum_i (eps_i + 1) 3^i (ignored if outside).
+ * One GPU only (HMAT_ERR_UNSUPPORTED for nranks > 1), no transposed product;
+ * M rank <= 1024.  hmat_panel(kind 2, level e) returns dense panel e. */
+hmat_status hmat_create_standard(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                                 const double* const* V, const double* Dn, const hmat_dist_t* dist, hmat_t* out);
+hmat_status hmat_create_standard_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist,
+                                        hmat_t* out);
+
 /* The paper-strict reading of Def 2.4 (conditions checked in
  * order, "leaf" first): every child pair of a leaf-parent is dense, so each
  * leaf-parent diagonal block (2^dim leaf_size square) is dense and low-rank

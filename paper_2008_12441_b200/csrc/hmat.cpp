@@ -164,14 +164,17 @@ hmat_status validate_dist(const hmat_dist_t* dist, int* P, int* rank) {
   return HMAT_OK;
 }
 
-hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dist_t* dist, hmat_t* out) {
+hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dist_t* dist, hmat_t* out,
+                          int adm = 0) {
   if (!out) return fail(HMAT_ERR_INVALID, "out is NULL");
   *out = nullptr;
   int P, shard;
   hmat_status st = validate_dist(dist, &P, &shard);
   if (st != HMAT_OK) return st;
   hmat::Plan plan;
-  std::string msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, options_from_env(148), &plan);
+  hmat::PlanOptions opt0 = options_from_env(148);
+  opt0.adm = adm;
+  std::string msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, opt0, &plan);
   if (!msg.empty()) return plan_status(msg);
 
   // ---- device work starts here ----
@@ -184,7 +187,9 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   }
   int sms = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, options_from_env(sms), &plan);
+  hmat::PlanOptions opt = options_from_env(sms);
+  opt.adm = adm;
+  msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, opt, &plan);
   if (!msg.empty()) return plan_status(msg);
 
   hmat_s* H = new hmat_s;
@@ -214,7 +219,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   const size_t zrow = size_t(p.Wp) * hmat::kMaxNR * sizeof(double);
   if ((e = alloc(reinterpret_cast<void**>(&H->U), panels, "U")) ||
       (e = alloc(reinterpret_cast<void**>(&H->V), panels, "V")) ||
-      (e = alloc(reinterpret_cast<void**>(&H->D), size_t(p.N_loc) * p.Dp * sizeof(double), "D")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->D), size_t(p.nd) * p.d_stride * sizeof(double), "D")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zloc), size_t(p.z_local_rows) * zrow, "z")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zex), size_t(p.z_exch_rows) * zrow, "exchange")) ||
       (e = alloc(reinterpret_cast<void**>(&H->part), size_t(p.grid_p_max) * p.L * 2 * zrow, "partials")) ||
@@ -225,7 +230,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   if ((e = cudaMemsetAsync(H->cnt, 0, size_t(p.grid_p_max) * p.L * sizeof(int) + 256, H->stream)) ||
       (e = cudaMemsetAsync(H->U, 0, panels ? panels : 256, H->stream)) ||
       (e = cudaMemsetAsync(H->V, 0, panels ? panels : 256, H->stream)) ||
-      (e = cudaMemsetAsync(H->D, 0, size_t(p.N_loc) * p.Dp * sizeof(double), H->stream)) ||
+      (e = cudaMemsetAsync(H->D, 0, size_t(p.nd) * p.d_stride * sizeof(double), H->stream)) ||
       // z rows: padding columns (odd W) are multiplied by zero padding of U, so keep them finite
       (e = cudaMemsetAsync(H->zloc, 0, std::max<size_t>(256, size_t(p.z_local_rows) * zrow), H->stream)) ||
       (e = cudaMemsetAsync(H->zex, 0, std::max<size_t>(256, size_t(p.z_exch_rows) * zrow), H->stream)) ||
@@ -233,6 +238,12 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   H->external = p.P > 1 && dist->external_exchange;
+  if (p.adm) {  // interaction-list slot tables for the project kernel's scatter
+    static int16_t code[3][8][hmat::kStdMaxSlots], slot[3][8][hmat::kStdMaxCodes];
+    hmat::std_slot_tables(code, slot);
+    if ((e = hmat::init_std_tables(&code[0][0][0], &slot[0][0][0])) != cudaSuccess)
+      return bail(cuda_fail(e, "init_std_tables"));
+  }
   if (p.P > 1 && !H->external) {
     std::string m = hmat::comm_create(dist->nccl_unique_id, p.P, p.rank, &H->comm);
     if (!m.empty()) return bail(fail(HMAT_ERR_NCCL, m));
@@ -299,12 +310,22 @@ hmat_status ensure_buf(double** buf, size_t* cap, size_t n) {
 
 extern "C" {
 
+hmat_status hmat_create_standard_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist,
+                                       hmat_t* out) {
+  return create_common(depth, dim, leaf_size, rank, dist, out, 1);
+}
+
 hmat_status hmat_create_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist, hmat_t* out) {
   return create_common(depth, dim, leaf_size, rank, dist, out);
 }
 
-hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const double* const* U, const double* const* V,
-                        const double* D, const hmat_dist_t* dist, hmat_t* out) {
+}  // extern "C"
+
+namespace {
+
+hmat_status create_from_panels(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                               const double* const* V, const double* D, const hmat_dist_t* dist, hmat_t* out,
+                               int adm) {
   if (!out) return fail(HMAT_ERR_INVALID, "out is NULL");
   *out = nullptr;
   if (depth > 0 && (!U || !V)) return fail(HMAT_ERR_INVALID, "U or V is NULL");
@@ -312,7 +333,7 @@ hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const doubl
   for (int l = 0; depth > 0 && l < depth && l < hmat::kMaxLevels; ++l)
     if (!U[l] || !V[l]) return fail(HMAT_ERR_INVALID, "a U or V panel pointer is NULL");
   hmat_t H = nullptr;
-  hmat_status st = create_common(depth, dim, leaf_size, rank, dist, &H);
+  hmat_status st = create_common(depth, dim, leaf_size, rank, dist, &H, adm);
   if (st != HMAT_OK) return st;
   const hmat::Plan& p = H->plan;
   cudaError_t e = cudaSuccess;
@@ -324,8 +345,10 @@ hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const doubl
                             p.W * sizeof(double), p.N_loc, cudaMemcpyDefault, H->stream);
   }
   if (e == cudaSuccess)
-    e = cudaMemcpy2DAsync(H->D, p.Dp * sizeof(double), D, p.b * sizeof(double), p.b * sizeof(double), p.N_loc,
-                          cudaMemcpyDefault, H->stream);
+    for (int k = 0; k < p.nd && e == cudaSuccess; ++k)  // canonical N_loc x (nd b) -> nd panels
+      e = cudaMemcpy2DAsync(H->D + k * p.d_stride, p.Dp * sizeof(double), D + k * p.b,
+                            size_t(p.nd) * p.b * sizeof(double), p.b * sizeof(double), p.N_loc, cudaMemcpyDefault,
+                            H->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(H->stream);
   if (e != cudaSuccess) {
     hmat_status s = cuda_fail(e, "copying panels");
@@ -334,6 +357,20 @@ hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const doubl
   }
   *out = H;
   return HMAT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const double* const* U, const double* const* V,
+                        const double* D, const hmat_dist_t* dist, hmat_t* out) {
+  return create_from_panels(depth, dim, leaf_size, rank, U, V, D, dist, out, 0);
+}
+
+hmat_status hmat_create_standard(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                                 const double* const* V, const double* Dn, const hmat_dist_t* dist, hmat_t* out) {
+  return create_from_panels(depth, dim, leaf_size, rank, U, V, Dn, dist, out, 1);
 }
 
 hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* rows, int64_t* cols, int64_t* ld) {
@@ -345,7 +382,8 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
     if (cols) *cols = p.W;
     if (ld) *ld = p.Wp;
   } else if (kind == 2) {
-    *ptr = H->D;
+    if (level < 0 || level >= p.nd) return fail(HMAT_ERR_INVALID, "dense panel index out of range");
+    *ptr = H->D + level * p.d_stride;
     if (cols) *cols = p.b;
     if (ld) *ld = p.Dp;
   } else {
@@ -385,6 +423,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     return fail(HMAT_ERR_INVALID, "x and y alias");
   const hmat::Plan& p = H->plan;
   CUDA_TRY(cudaSetDevice(H->device));
+  if (trans && p.adm) return fail(HMAT_ERR_UNSUPPORTED, "transposed product with standard admissibility");
   if (trans) {
     hmat_status st = ensure_dt(H);
     if (st != HMAT_OK) return st;
@@ -400,6 +439,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   }
   const bool host_io = !x_dev || !y_dev;
   if (p.L < 64) level_mask &= (p.L == 0 ? 0ull : (~0ull >> (64 - p.L)));
+  if (p.adm) level_mask &= ~1ull;  // standard admissibility: no admissible pair at level 1
 
   EventPair ep{};
   // ---- x: stage when it is host memory, misaligned, or its last column would
@@ -442,6 +482,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.ldx = ldx;
   a.ldy = n;
   a.L = p.L;
+  a.d = p.d;
+  a.adm = p.adm;
+  a.nd = p.nd;
+  a.d_stride = p.d_stride;
   a.c = p.c;
   a.r = p.r;
   a.W = p.W;

@@ -39,6 +39,8 @@ struct StreamArgs {
   double alpha, beta;  // y = alpha op(H) x + beta y (beta == 0: y is not read)
   // shape
   int L, c, r, W, Wp, Dp, b;
+  int d, adm, nd;        // dim; admissibility (0 weak, 1 standard); dense panels
+  int64_t d_stride;      // doubles between dense panels (standard: one per neighbour offset)
   int64_t N_loc, row0;
   uint64_t level_mask;
   int dense;
@@ -65,6 +67,9 @@ cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t sme
 cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
 cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
 cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e);
+// Standard admissibility: upload the interaction-list slot tables (plan.h
+// std_slot_tables) to the project kernel's constant memory (per device).
+cudaError_t init_std_tables(const int16_t* code, const int16_t* slot);
 // D^T of every dense leaf block (for H^T x); one-time helper.
 cudaError_t launch_transpose_leaf_blocks(const double* D, double* Dt, int64_t n_leaves, int b, int Dp, cudaStream_t s);
 // Opt the kernels into large dynamic shared memory (once per device).

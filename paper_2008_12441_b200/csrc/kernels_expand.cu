@@ -19,6 +19,7 @@
 // pitches used here), fp64 FMAs into registers, a shuffle reduction across
 // the tpr lanes, one store of y per row and rhs.
 #include "device_utils.cuh"
+#include "geometry.cuh"
 #include "kernels.h"
 
 namespace hmat {
@@ -60,11 +61,20 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       uint32_t phase = 0;
       const int64_t ipl = b / Re;                        // items per leaf
       int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
+      // standard admissibility: dense near field = the 3^d neighbour leaves
+      int64_t leaf_idx = (a.row0 + leaf0) / b;
+      int lx[3] = {0, 0, 0};
+      uint32_t nmask = 1u;
+      if (a.adm) {
+        geo::morton_decode(a.d, leaf_idx, L, lx);
+        nmask = geo::near_mask(a.d, lx, 1 << L);
+      }
       for (int64_t j = j0; j < j1; ++j) {
         const int64_t i0 = j * Re;
-        for (int l = 1; l <= L + 1; ++l) {
-          const bool is_d = (l == L + 1);
-          if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+        for (int l = 1; l <= L + a.nd; ++l) {
+          const bool is_d = (l > L);
+          const int e = l - L - 1;  // dense panel / near-field offset index
+          if (is_d ? (!a.dense || !((nmask >> e) & 1u)) : !((a.level_mask >> (l - 1)) & 1ull)) continue;
           dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
           unsigned char* st = smem + slot * a.stage_bytes_e;
           if (!is_d) {
@@ -77,20 +87,22 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             dev::bulk_g2s(st + ub, lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR, zb, &full[slot], pol_keep);
           } else {
             const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
+            // source leaf of this dense block: the leaf itself (weak) or its neighbour e
+            const int64_t src0 = a.adm ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
             uint32_t total = db;
             int64_t lo[NR];
             uint32_t xb[NR];
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk) {
               if (kk < a.nr) {
-                const int64_t start = kk * a.ldx + leaf0;
+                const int64_t start = kk * a.ldx + src0;
                 lo[kk] = start & ~int64_t(1);
                 xb[kk] = static_cast<uint32_t>((((start + b + 1) & ~int64_t(1)) - lo[kk]) * 8);
                 total += xb[kk];
               }
             }
             dev::mbar_arrive_expect_tx(&full[slot], total);
-            dev::bulk_g2s(st, a.D + i0 * Dp, db, &full[slot], pol_stream);
+            dev::bulk_g2s(st, a.D + e * a.d_stride + i0 * Dp, db, &full[slot], pol_stream);
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk)
               if (kk < a.nr)
@@ -104,6 +116,11 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         if (++in_leaf == ipl) {
           in_leaf = 0;
           leaf0 += b;
+          if (a.adm) {
+            ++leaf_idx;
+            geo::morton_decode(a.d, leaf_idx, L, lx);
+            nmask = geo::near_mask(a.d, lx, 1 << L);
+          }
         }
       }
     }
@@ -124,6 +141,13 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   const int rotU = ri % njU, rotD = ri % njD;
   const int64_t ipl = b / Re;
   int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
+  int64_t leaf_idx = (a.row0 + leaf0) / b;
+  int lx[3] = {0, 0, 0};
+  uint32_t nmask = 1u;
+  if (a.adm) {
+    geo::morton_decode(a.d, leaf_idx, L, lx);
+    nmask = geo::near_mask(a.d, lx, 1 << L);
+  }
   int slot = 0;
   uint32_t phase = 0;
   for (int64_t j = j0; j < j1; ++j) {
@@ -131,9 +155,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     double acc[NR], acc2[NR];  // two chains: even / odd columns
 #pragma unroll
     for (int kk = 0; kk < NR; ++kk) acc[kk] = acc2[kk] = 0.0;
-    for (int l = 1; l <= L + 1; ++l) {
-      const bool is_d = (l == L + 1);
-      if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+    for (int l = 1; l <= L + a.nd; ++l) {
+      const bool is_d = (l > L);
+      const int e = l - L - 1;
+      if (is_d ? (!a.dense || !((nmask >> e) & 1u)) : !((a.level_mask >> (l - 1)) & 1ull)) continue;
       dev::mbar_wait(&full[slot], phase);
       const unsigned char* st = smem + slot * a.stage_bytes_e;
       if (active) {
@@ -158,9 +183,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         } else {
           const double2* D2 = reinterpret_cast<const double2*>(st) + ri * NPD;
           const double* xs = reinterpret_cast<const double*>(st + Re * Dp * 8);
+          const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
           int xo[NR];
 #pragma unroll
-          for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + leaf0) & 1);
+          for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + src0) & 1);
           int jj = rotD;
           for (int n = 0; n < njD; ++n) {
             const int cp = p + tpr * jj;
@@ -200,6 +226,11 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     if (++in_leaf == ipl) {
       in_leaf = 0;
       leaf0 += b;
+      if (a.adm) {
+        ++leaf_idx;
+        geo::morton_decode(a.d, leaf_idx, L, lx);
+        nmask = geo::near_mask(a.d, lx, 1 << L);
+      }
     }
   }
 }

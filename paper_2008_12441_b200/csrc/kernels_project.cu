@@ -26,6 +26,7 @@
 //     expand kernel reads (and, for levels above the partition level, the
 //     packed exchange buffer of Steps 2-4).
 #include "device_utils.cuh"
+#include "geometry.cuh"
 #include "kernels.h"
 
 namespace hmat {
@@ -39,6 +40,45 @@ __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { r
 
 // z value (column col = q r + a of source node sg, rhs kk) -> Zt_l of target
 // t = q-th sibling of sg, at slot(t -> sg).
+// Standard admissibility: slot tables of the interaction lists,
+// written by init_std_tables() from the host enumeration (plan.cpp):
+//   c_std_code[d-1][tau][q]     = e * 2^d + sigma of slot q of a box with child
+//                                 position tau (e = near-field index of the parent's
+//                                 neighbour eps, sigma = child position of the source)
+//   c_std_slot[d-1][tau][code]  = the inverse (-1 if the code is a neighbour).
+__constant__ int16_t c_std_code[3][8][kStdMaxSlots];
+__constant__ int16_t c_std_slot[3][8][kStdMaxCodes];
+
+// z value of column col = q r + a of source node sg at `level` -> Zt of target
+// t = slot q of sg, at slot(t -> sg).  nbr[e] = Morton index of sg's parent's
+// neighbour e (-1 outside the domain), computed once per node.
+template <int NR>
+__device__ __forceinline__ void scatter_z_std(const StreamArgs& a, const LevelArgs& lv, int64_t sg,
+                                              const int64_t* nbr, int col, int kk, double v) {
+  const int d = a.d, c = a.c;
+  const int q = col / a.r, aa = col - q * a.r;
+  const int tau = static_cast<int>(sg & (c - 1));
+  const int code = c_std_code[d - 1][tau][q];
+  const int e = code >> d, sigma = code & (c - 1);
+  const int64_t pt = nbr[e];
+  if (pt < 0) return;  // the interaction partner lies outside the domain
+  const int64_t t = pt * c + sigma;
+  const int nd = d == 1 ? 3 : d == 2 ? 9 : 27;
+  const int qt = c_std_slot[d - 1][sigma][(nd - 1 - e) * c + tau];  // eps -> -eps, sigma <-> tau
+  lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)kk * a.Wp + qt * a.r + aa] = v;
+}
+
+// nbr[e] for the parent of source node sg at `level` (threads 0..nd-1).
+__device__ __forceinline__ void std_parent_neighbours(const StreamArgs& a, int64_t sg, int level, int t,
+                                                      int64_t* nbr) {
+  if (t < a.nd) {
+    int x[3];
+    geo::morton_decode(a.d, sg >> a.d, level - 1, x);
+    const uint32_t m = geo::near_mask(a.d, x, 1 << (level - 1));
+    nbr[t] = ((m >> t) & 1u) ? geo::neighbour(a.d, x, t, level - 1) : -1;
+  }
+}
+
 template <int NR>
 __device__ __forceinline__ void scatter_z(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int col, int kk,
                                           double v) {
@@ -132,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   const bool active = PAIRS == 1 ? rho < RG : true;
   const int64_t red_elems = (int64_t)RG * Wp * NR;  // one of two alternating buffers
   double* red_base = reinterpret_cast<double*>(smem + a.red_off_p);
+  int64_t* nbr_base = reinterpret_cast<int64_t*>(smem + a.bar_off_p + 256);  // 2 x 32 entries
   int red_buf = 0;
   double2 acc[PAIRS][NR];
 #pragma unroll
@@ -196,7 +237,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       const bool complete = sa >= k0 && sb <= k1;
       const int64_t sg = sg0 + this_sl;                 // global source node
       double* red = red_base + red_buf * red_elems;
+      int64_t* nbr = nbr_base + red_buf * 32;  // standard admissibility: parent's neighbours
       red_buf ^= 1;  // alternate buffers: one barrier per complete node suffices
+      if (a.adm) std_parent_neighbours(a, sg, l, t, nbr);
       if (active) {
 #pragma unroll
         for (int j = 0; j < PAIRS; ++j) {
@@ -216,7 +259,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           const int kk = o / W, col = o - kk * W;
           double v = 0.0;
           for (int g = 0; g < RG; ++g) v += red[((int64_t)g * NR + kk) * Wp + col];
-          if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
+          if (kk < a.nr) {
+            if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);
+            else scatter_z<NR>(a, lv, sg, col, kk, v);
+          }
         }
       } else {
         // partial node sum of this CTA: slot 0 if the node holds our first
@@ -249,7 +295,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
               v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NR +
                               (int64_t)kk * Wp + col);
             }
-            if (kk < a.nr) scatter_z<NR>(a, lv, sg, col, kk, v);
+            if (kk < a.nr) {
+              if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);
+              else scatter_z<NR>(a, lv, sg, col, kk, v);
+            }
           }
           if (t == 0) *ticket = 0;  // re-arm for the next launch
         }
@@ -284,6 +333,12 @@ cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t sm
     case 4: return launch_nr<4>(a, grid, smem, s);
     default: return launch_nr<8>(a, grid, smem, s);
   }
+}
+
+cudaError_t init_std_tables(const int16_t* code, const int16_t* slot) {
+  cudaError_t e = cudaMemcpyToSymbol(c_std_code, code, sizeof(int16_t) * 3 * 8 * kStdMaxSlots);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_std_slot, slot, sizeof(int16_t) * 3 * 8 * kStdMaxCodes);
 }
 
 cudaError_t configure_project(int64_t smem) {

@@ -20,6 +20,38 @@ int pick_rows(int b, int rmax, int64_t width_doubles, int64_t cap) {
 
 }  // namespace
 
+void std_slot_tables(int16_t code[3][8][kStdMaxSlots], int16_t slot[3][8][kStdMaxCodes]) {
+  for (int d = 1; d <= 3; ++d) {
+    const int c = 1 << d;
+    int nd = 1;
+    for (int i = 0; i < d; ++i) nd *= 3;
+    for (int tau = 0; tau < 8; ++tau) {
+      for (int q = 0; q < kStdMaxSlots; ++q) code[d - 1][tau][q] = -1;
+      for (int k = 0; k < kStdMaxCodes; ++k) slot[d - 1][tau][k] = -1;
+      if (tau >= c) continue;
+      int q = 0;
+      // candidates: child sigma of the parent's neighbour eps, in increasing
+      // code = e 2^d + sigma; a candidate is in the list unless it touches the
+      // box (offset 2 eps + sigma - tau in {-1,0,1}^d)
+      for (int cd = 0; cd < nd * c; ++cd) {
+        const int e = cd / c, sigma = cd % c;
+        int rem = e;
+        bool touches = true;
+        for (int i = 0; i < d; ++i) {
+          const int eps = rem % 3 - 1;
+          rem /= 3;
+          const int off = 2 * eps + ((sigma >> i) & 1) - ((tau >> i) & 1);
+          touches = touches && off >= -1 && off <= 1;
+        }
+        if (touches) continue;
+        code[d - 1][tau][q] = static_cast<int16_t>(cd);
+        slot[d - 1][tau][cd] = static_cast<int16_t>(q);
+        ++q;
+      }
+    }
+  }
+}
+
 std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard, const PlanOptions& opt,
                        Plan* out) {
   char msg[256];
@@ -36,7 +68,20 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.L = depth;
   p.b = leaf;
   p.r = rank;
-  p.W = (p.c - 1) * rank;
+  p.adm = opt.adm;
+  if (p.adm == 0) {
+    p.M = p.c - 1;  // siblings (weak admissibility)
+    p.nd = 1;
+  } else {
+    int p6 = 1, p3 = 1;
+    for (int i = 0; i < dim; ++i) {
+      p6 *= 6;
+      p3 *= 3;
+    }
+    p.M = p6 - p3;  // interaction list (standard admissibility)
+    p.nd = p3;      // near-field neighbours incl. self
+  }
+  p.W = p.M * rank;
   // N = b c^L must stay below 2^62
   int64_t N = leaf;
   for (int l = 0; l < depth; ++l) {
@@ -53,7 +98,8 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   if (P < 1 || (P & (P - 1)) != 0) return "nranks must be a power of two";
   if (P > leaves) return "nranks must not exceed the number of leaves 2^(dim*depth)";
   if (shard < 0 || shard >= P) return "rank id out of range [0, nranks)";
-  if (p.W > 4 * kConsumerThreads) return "unsupported: (2^dim - 1) * rank must be <= 1024";
+  if (p.W > 4 * kConsumerThreads) return "unsupported: slots * rank must be <= 1024";
+  if (p.adm != 0 && P > 1) return "unsupported: standard admissibility with nranks > 1";
   p.P = P;
   p.rank = shard;
   p.N_loc = N / P;
@@ -61,6 +107,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.Wp = p.W + (p.W & 1);
   p.Dp = leaf + (leaf & 1);
   p.panel_stride = round_up(p.N_loc * p.Wp, 16);
+  p.d_stride = round_up(p.N_loc * p.Dp, 16);
 
   // Levels whose parent spans more than one shard need the exchange
   // (Steps 2-4): c^{l-1} < P.
@@ -102,7 +149,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.items_e = p.N_loc / p.Re;
   const int np = p.Wp / 2;  // column pairs owned by project's consumer threads
   const int rg = np <= kConsumerThreads ? kConsumerThreads / np : 1;
-  const int64_t bar_bytes = 256;
+  const int64_t bar_bytes = 1024;  // mbarriers + flag (256 B) + 2 x 32 neighbour entries
   p.grid_p_max = 0;
   for (int li = 0; li < 4; ++li) {
     const int64_t NR = int64_t(1) << li;
@@ -132,7 +179,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     p.grid_p_max = std::max(p.grid_p_max, y.grid_p);
   }
   // DMMA layouts (1 project CTA per SM: 2 stages of ~77 KB; 2 expand CTAs per SM)
-  p.dmma_ok = p.W % 32 == 0 && p.W <= 224 && leaf % kDmmaRE == 0 && leaf % kDmmaKR == 0 && p.N_loc % kDmmaRE == 0;
+  p.dmma_ok = p.adm == 0 && p.W % 32 == 0 && p.W <= 224 && leaf % kDmmaRE == 0 && leaf % kDmmaKR == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
     p.dstage_p = round_up(int64_t(kDmmaKR) * p.vp * 8 + int64_t(kDmmaNB) * kDmmaXP * 8, 128);

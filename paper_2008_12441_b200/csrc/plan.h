@@ -19,6 +19,14 @@ constexpr int kMaxNR = 8;        // right-hand sides per streaming pass
 constexpr int kConsumerThreads = 256;
 constexpr int kThreads = 32 + kConsumerThreads;  // 1 producer warp + 8 consumer warps
 
+// standard admissibility: interaction-list slot tables (6^d - 3^d <= 189 slots,
+// 3^d 2^d <= 216 (neighbour, child) codes)
+constexpr int kStdMaxSlots = 192;
+constexpr int kStdMaxCodes = 216;
+// Host enumeration of the canonical slot order (include/hmat.h, standard panels):
+// code[d-1][tau][q] = e 2^d + sigma of slot q, slot[d-1][tau][code] = q or -1.
+void std_slot_tables(int16_t code[3][8][kStdMaxSlots], int16_t slot[3][8][kStdMaxCodes]);
+
 // FP64 tensor-core (DMMA) path for many right-hand sides (kernels_dmma.cu)
 constexpr int kDmmaNB = 64;   // right-hand sides per pass
 constexpr int kDmmaKR = 32;   // project: V rows per stage
@@ -30,6 +38,11 @@ constexpr int kDmmaAP = kDmmaKC + 4;  // smem pitch of staged U / D row chunks
 struct Plan {
   // problem
   int d = 0, c = 0, L = 0, b = 0, r = 0, W = 0;
+  // admissibility: 0 = weak (M = c-1 sibling slots, one dense leaf-diagonal
+  // panel), 1 = standard (M = 6^d - 3^d interaction slots, nd = 3^d dense
+  // near-field panels, one per neighbour offset); W = M r
+  int adm = 0, M = 0, nd = 1;
+  int64_t d_stride = 0;             // doubles between consecutive dense panels
   int64_t N = 0;
   int64_t m[kMaxLevels + 1] = {};   // m[l] = N / c^l
   // shard
@@ -81,6 +94,7 @@ struct PlanOptions {
   int smem_budget = 200 * 1024;     // dynamic smem per CTA for the pipeline
   int max_stages_p = 2;             // project: measured best at 2 stages x 2 CTAs per SM
   int max_stages_e = 3;             // expand: measured best at 3 stages x 2 CTAs per SM
+  int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.

@@ -26,7 +26,8 @@ HMAT_NUM_PHASES = 4
 PHASES = ("project", "exchange", "expand", "copies")
 
 # Every symbol include/hmat.h declares (checked by tests/test_abi.py).
-EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_panel", "hmat_matvec", "hmat_gemv",
+EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_create_standard",
+           "hmat_create_standard_uninit", "hmat_panel", "hmat_matvec", "hmat_gemv",
            "hmat_exchange_size", "hmat_project", "hmat_expand", "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query")
@@ -63,6 +64,8 @@ _sigs = {
     "hmat_matvec": (_i, [_H, _P, _P, _i]),
     "hmat_gemv": (_i, [_H, _i, ctypes.c_double, _P, ctypes.c_double, _P, _i]),
     "hmat_create_strict": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
+    "hmat_create_standard": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
+    "hmat_create_standard_uninit": (_i, [_i, _i, _i, _i, _P, ctypes.POINTER(_H)]),
     "hmat_exchange_size": (_i, [_H, _i, ctypes.POINTER(_i64)]),
     "hmat_project": (_i, [_H, _P, _i, _P]),
     "hmat_expand": (_i, [_H, _P, _P, _P, _i]),
@@ -170,6 +173,25 @@ def hmat_create_strict(depth, dim, leaf_size, rank, U, V, Dc, dist: hmat_dist_t 
     _check(_lib.hmat_create_strict(depth, dim, leaf_size, rank, ctypes.cast(Up, _P), ctypes.cast(Vp, _P), _ptr(Dc),
                                    ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)),
            "hmat_create_strict")
+    return h
+
+
+def hmat_create_standard(depth, dim, leaf_size, rank, U, V, Dn, dist: hmat_dist_t | None = None):
+    """Standard admissibility (interaction lists + near field); canonical standard panels."""
+    Up = (ctypes.c_void_p * max(1, len(U)))(*[_ptr(u) for u in U])
+    Vp = (ctypes.c_void_p * max(1, len(V)))(*[_ptr(v) for v in V])
+    h = _H()
+    _check(_lib.hmat_create_standard(depth, dim, leaf_size, rank, ctypes.cast(Up, _P), ctypes.cast(Vp, _P),
+                                     _ptr(Dn), ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)),
+           "hmat_create_standard")
+    return h
+
+
+def hmat_create_standard_uninit(depth, dim, leaf_size, rank, dist: hmat_dist_t | None = None):
+    h = _H()
+    _check(_lib.hmat_create_standard_uninit(depth, dim, leaf_size, rank,
+                                            ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)),
+           "hmat_create_standard_uninit")
     return h
 
 

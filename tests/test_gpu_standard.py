@@ -1,0 +1,74 @@
+"""GPU parity of the standard-admissibility path against the
+oracle's block loop (tests/test_oracle_std.py pins that oracle)."""
+import numpy as np
+import pytest
+
+from gen import hgen
+from gen.hgen import HConfig
+from oracle import oracle
+from tests.helpers import assert_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2008_12441_b200 import hmat as hm
+
+
+def run_std(cfg, nrhs, **parts):
+    U, V, Dn = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
+    try:
+        xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        yd = torch.empty_like(xd)
+        if parts:
+            hm.hmat_matvec_parts(h, xd.t(), yd.t(), **parts)
+        else:
+            hm.hmat_matvec(h, xd.t(), yd.t())
+        torch.cuda.synchronize()
+        return yd.t().cpu().numpy(), (U, V, Dn, x)
+    finally:
+        hm.hmat_destroy(h)
+
+
+STD = [HConfig(f"std{d}{L}{b}{r}", d=d, L=L, b=b, r=r, adm=1, seed=700 + 31 * d + 7 * L + b + r)
+       for d, L, b, r in [(1, 5, 4, 2), (1, 8, 2, 3), (2, 2, 4, 2), (2, 3, 8, 2), (2, 4, 16, 4), (2, 3, 7, 3),
+                          (3, 2, 4, 1), (3, 3, 8, 1), (2, 5, 64, 8)]]
+
+
+@pytest.mark.parametrize("cfg", STD, ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_standard_admissibility_parity(cfg, nrhs):
+    y, (U, V, Dn, x) = run_std(cfg, nrhs)
+    ref = oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x)
+    assert_parity(y, ref)
+
+
+def test_standard_near_field_only_and_far_field_only():
+    """level parts: the dense near field alone and the far field alone."""
+    cfg = HConfig("stdp", d=2, L=4, b=8, r=3, adm=1, seed=777)
+    U, V, Dn = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=1)
+    Z = [np.zeros_like(u) for u in U]
+    y, _ = run_std(cfg, 1, level_mask=0, dense=True)
+    assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, Z, Z, Dn, x))
+    y, _ = run_std(cfg, 1, level_mask=(1 << cfg.L) - 1, dense=False)
+    assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, np.zeros_like(Dn), x))
+
+
+def test_standard_unsupported_cases():
+    cfg = HConfig("stdu", d=2, L=3, b=4, r=2, adm=1, seed=778)
+    U, V, Dn = hgen.inputs(cfg)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
+    try:
+        x = torch.zeros(cfg.N, dtype=torch.float64, device="cuda")
+        with pytest.raises(hm.HMatError) as ei:
+            hm.hmat_gemv(h, 1, 1.0, x, 0.0, torch.empty_like(x))
+        assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
+    finally:
+        hm.hmat_destroy(h)
+    with pytest.raises(hm.HMatError) as ei:
+        hm.hmat_create_standard_uninit(cfg.L, cfg.d, cfg.b, cfg.r,
+                                       hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
+    assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
