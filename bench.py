@@ -33,7 +33,9 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 from gen import hgen  # noqa: E402
-from gen.hgen import CONFIGS  # noqa: E402
+from gen.hgen import CONFIGS, EXTRA_CONFIGS  # noqa: E402
+
+ALL_CONFIGS = {**CONFIGS, **EXTRA_CONFIGS}
 
 METRIC = "H-matvec GB/s of factor data & matvecs/s vs HBM roofline, 1/2/4/8 B200"
 
@@ -43,7 +45,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(ALL_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -51,6 +53,11 @@ def parse():
 
 
 def workload_desc(cfg):
+    if cfg.adm:
+        return (f"{cfg.name}: {cfg.d}D H-matrix fp64, STANDARD admissibility (rho=sqrt(d)), N={cfg.N} (Morton), "
+                f"depth L={cfg.L}, leaf b={cfg.b}, rank r={cfg.r} blocks vs up to {cfg.slots} interaction-list "
+                f"boxes per node, dense {cfg.b}x{cfg.b} near-field blocks (3^d per leaf), nrhs={cfg.nrhs}, seeded "
+                f"synthetic (U,V~N(0,1)/sqrt(m_l), D~N(0,1)/8, x~U[-1,1]); not a BASELINE config")
     return (f"{cfg.name}: {cfg.d}D H-matrix fp64, weak admissibility, N={cfg.N} (Morton), depth L={cfg.L}, "
             f"leaf b={cfg.b}, rank r={cfg.r} blocks vs each of {cfg.c - 1} siblings at every level, "
             f"dense {cfg.b}x{cfg.b} leaf-diagonal blocks, nrhs={cfg.nrhs}, seeded synthetic "
@@ -60,7 +67,8 @@ def workload_desc(cfg):
 def alg_bytes(cfg, n_rows, nrhs):
     """Algorithmic bytes of one matvec over n_rows rows:
     factor panels once + x in + y out.  Split per kernel."""
-    W, L, b = cfg.W, cfg.L, cfg.b
+    W, b = cfg.W, cfg.dcols
+    L = cfg.L - (1 if cfg.adm else 0)  # standard admissibility: level 1 holds no blocks and is skipped
     project = 8 * n_rows * (W * L) + 8 * n_rows * nrhs
     expand = 8 * n_rows * (W * L + b) + 16 * n_rows * nrhs
     factor = 8 * n_rows * (2 * W * L + b)
@@ -72,7 +80,7 @@ FP64_PEAK_TFLOPS = 37.07  # scripts/fp64_peak.cu, DMMA m8n8k4, this pool (profil
 
 def alg_flops(cfg, n_rows, nrhs):
     """Algorithmic flops of one matvec over n_rows rows: 2 per multiply-add."""
-    W, L, b = cfg.W, cfg.L, cfg.b
+    W, L, b = cfg.W, cfg.L, cfg.dcols
     return {"project": 2 * n_rows * W * L * nrhs, "expand": 2 * n_rows * (W * L + b) * nrhs}
 
 
@@ -163,7 +171,7 @@ def oracle_sample(cfg, budget_bytes):
     for q in range(0, cfg.L + 1):
         n = cfg.N // cfg.c ** q
         depth = cfg.L - q
-        fb = 8 * n * (2 * cfg.W * depth + cfg.b)
+        fb = 8 * n * (2 * cfg.W * depth + cfg.dcols)
         if fb <= budget_bytes:
             return q, n, depth, fb
     return cfg.L, cfg.b, 0, 8 * cfg.b * cfg.b
@@ -171,6 +179,19 @@ def oracle_sample(cfg, budget_bytes):
 
 def run_oracle_sample(cfg, q, n, depth, reps, nrhs):
     from oracle import oracle
+    if cfg.adm:
+        # standard admissibility: a standalone operator of depth L-q with the same
+        # b, r, d (a sub-block is not an H-matrix of the same kind at the boundary)
+        import dataclasses
+        sub = dataclasses.replace(cfg, L=depth)
+        U, V, D = hgen.inputs(sub)
+        x = hgen.xblock(sub, nrhs=nrhs)
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            oracle.std_matvec(sub.d, sub.L, sub.b, sub.r, U, V, D, x)
+            times.append(time.perf_counter() - t0)
+        return times
     # panels of levels q+1..L restricted to rows [0, n): generated from the full
     # operator's streams (same values as the GPU operator)
     U = [hgen.panel(cfg, hgen.TAG_U, q + l, 0, n) for l in range(1, depth + 1)]
@@ -210,7 +231,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
+    cfg = ALL_CONFIGS[args.config]
     steps, warm = args.steps, args.warmup
     # size each step so the whole run stays within ~2-3 minutes at ~1.5 GB/s
     budget = max(64e6, min(6.5e9, 150e9 / (steps + warm)))
@@ -248,7 +269,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = CONFIGS[args.config]
+    cfg = ALL_CONFIGS[args.config]
     nrhs = cfg.nrhs
     stream = torch.cuda.Stream()   # one stream for fills, matvecs and the timing events
     torch.cuda.set_stream(stream)
@@ -262,7 +283,8 @@ def run_ours(args):
     dd = hm._dist(nranks=world, rank=rank, nccl_unique_id=nid, cuda_stream=sptr, device=local)
 
     t_setup = time.perf_counter()
-    h = hm.hmat_create_uninit(cfg.L, cfg.d, cfg.b, cfg.r, dd)
+    create = hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit
+    h = create(cfg.L, cfg.d, cfg.b, cfg.r, dd)
     r0, r1 = hm.hmat_local_rows(h)
     n = r1 - r0
     hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, sptr)
@@ -367,7 +389,7 @@ def run_ours(args):
                 "per_kernel": per_kernel, "frac_of_8TBps_nominal": achieved / 8000.0}
 
     value = 1e3 / ms_step  # matvecs/s of the whole job (one operator across all ranks)
-    factor_gbps = cfg.factor_bytes / (ms_step * 1e-3) / 1e9
+    factor_gbps = alg_bytes(cfg, cfg.N, nrhs)["factor"] / (ms_step * 1e-3) / 1e9
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:

@@ -84,6 +84,12 @@ CONFIGS = {
     "c4": HConfig("c4", d=2, L=9, b=64, r=16, nrhs=1, seed=SEED_BASE + 4),
     "c5": HConfig("c5", d=3, L=5, b=64, r=32, nrhs=64, seed=SEED_BASE + 5),
 }
+# Not a BASELINE config: the standard-admissibility path at C2's
+# size (2D, N = 2^20, L = 7, b = 64, r = 16; 27 interaction slots, 9 near-field
+# blocks per row) -- the paper's "Standard" columns use the same 1024^2 domain.
+EXTRA_CONFIGS = {
+    "s2": HConfig("s2", d=2, L=7, b=64, r=16, nrhs=1, seed=SEED_BASE + 12, adm=1),
+}
 
 _lib = None
 _dev = None
@@ -125,6 +131,11 @@ def _load_dev():
         lib.hgen_dev_fill_rowmajor.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
                                                ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
                                                ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        lib.hgen_dev_fill_cols.restype = ctypes.c_int
+        lib.hgen_dev_fill_cols.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_uint64,
+                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
+                                           ctypes.c_void_p]
         lib.hgen_dev_fill_x.restype = ctypes.c_int
         lib.hgen_dev_fill_x.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
                                         ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
@@ -212,6 +223,11 @@ def dev_fill_operator(cfg: HConfig, panel_fn, row_begin: int, row_end: int, stre
             ptr, rows, cols, ld = panel_fn(kind, level)
             assert rows == row_end - row_begin and cols == cfg.W
             dev_fill_panel(cfg, tag, level, row_begin, row_end, ptr, ld, stream)
-    ptr, rows, cols, ld = panel_fn(2, 0)
-    assert rows == row_end - row_begin and cols == cfg.b
-    dev_fill_panel(cfg, TAG_D, 0, row_begin, row_end, ptr, ld, stream)
+    nd = cfg.dcols // cfg.b  # 1 (leaf diagonal) or 3^d near-field panels (standard)
+    for e in range(nd):
+        ptr, rows, cols, ld = panel_fn(2, e)
+        assert rows == row_end - row_begin and cols == cfg.b
+        rc = _load_dev().hgen_dev_fill_cols(cfg.seed, TAG_D, 0, 0, row_begin, row_end, cfg.dcols, e * cfg.b,
+                                            cfg.b, 0.125, ptr, ld, stream)
+        if rc != 0:
+            raise RuntimeError(f"hgen_dev_fill_cols: cuda error {rc}")

@@ -77,9 +77,9 @@ int nr_cap(int nr) { return nr <= 1 ? 1 : nr <= 2 ? 2 : nr <= 4 ? 4 : 8; }
 
 cudaError_t configure_all(const hmat::Plan& p) {
   int64_t sp = 0, se = 0;
-  for (const auto& y : p.lay) {
-    sp = std::max(sp, y.smem_p);
-    se = std::max(se, y.smem_e);
+  for (int li = 0; li < 4 && (1 << li) <= p.max_nr; ++li) {  // layouts that fit
+    sp = std::max(sp, p.lay[li].smem_p);
+    se = std::max(se, p.lay[li].smem_e);
   }
   return hmat::configure_kernels(sp, se);
 }
@@ -115,6 +115,7 @@ struct hmat_s {
   int* cnt_d = nullptr;
   double* Dt = nullptr;  // D^T, built on the first transposed product
   bool external = false;  // P > 1 with a caller-provided exchange (split-phase API)
+  int zt_cap = 1;         // rhs width of the z-buffer layout last written (zeroed at create)
   bool prof = false;
   std::vector<EventPair> ev;
   std::vector<cudaEvent_t> pool;
@@ -431,7 +432,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   const int64_t n = p.N_loc;
   const bool x_dev = is_device_ptr(x), y_dev = y ? is_device_ptr(y) : true;
   if (phases != kPhaseAll) {
-    const int width = use_dmma(p, nrhs) ? hmat::kDmmaNB : hmat::kMaxNR;
+    const int width = use_dmma(p, nrhs) ? hmat::kDmmaNB : p.max_nr;
     if (nrhs > width) return fail(HMAT_ERR_INVALID, "split-phase calls take at most one pass of right-hand sides");
     if (!x_dev || !y_dev) return fail(HMAT_ERR_INVALID, "split-phase calls need device x and y");
   } else if (p.P > 1 && H->external) {
@@ -564,8 +565,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       if (st2 != HMAT_OK) return st2;
     }
   }
-  for (int c0 = 0; !use_dmma(p, nrhs) && c0 < nrhs; c0 += hmat::kMaxNR) {
-    const int nr = nrhs - c0 < hmat::kMaxNR ? nrhs - c0 : hmat::kMaxNR;
+  for (int c0 = 0; !use_dmma(p, nrhs) && c0 < nrhs; c0 += p.max_nr) {
+    const int nr = nrhs - c0 < p.max_nr ? nrhs - c0 : p.max_nr;
     const int cap = nr_cap(nr);
     const hmat::Plan::Layout& ly = p.lay[hmat::nr_index(cap)];
     a.nstage_p = ly.nstage_p;
@@ -586,6 +587,14 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       lv.tbase = p.zt_tbase[l];
     }
     const size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
+    // Standard admissibility: slots whose partner lies outside the domain are
+    // never written and must read as zero; after a pass with another rhs width
+    // the buffer holds values at other positions, so clear it on a layout change.
+    if (p.adm && H->zt_cap != cap && (phases & kPhaseProject)) {
+      CUDA_TRY(cudaMemsetAsync(H->zloc, 0, std::max<size_t>(256, size_t(p.z_local_rows) * p.Wp * cap * 8),
+                               H->stream));
+      H->zt_cap = cap;
+    }
     hmat_status st2 = pass(
         H->zex, exch, [&] { return hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream); },
         [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0);
@@ -624,7 +633,7 @@ hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count) {
     if (nrhs > hmat::kDmmaNB) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
     *count = p.P > 1 ? p.z_exch_rows * p.W * hmat::kDmmaNB : 0;
   } else {
-    if (nrhs > hmat::kMaxNR) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
+    if (nrhs > p.max_nr) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
     *count = p.P > 1 ? p.z_exch_rows * p.Wp * nr_cap(nrhs) : 0;
   }
   return HMAT_OK;
@@ -721,7 +730,7 @@ hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches) {
 
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs) {
   if (!H || nrhs < 1) return -1;
-  const int per = use_dmma(H->plan, nrhs) ? hmat::kDmmaNB : hmat::kMaxNR;
+  const int per = use_dmma(H->plan, nrhs) ? hmat::kDmmaNB : H->plan.max_nr;
   const int64_t passes = (nrhs + per - 1) / per;
   return passes * ((H->plan.stages_p > 0 ? 1 : 0) + 1);
 }

@@ -53,31 +53,36 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   __syncthreads();
 
   if (warp == 0) {
-    // ---------------- producer ------------------------------------------------
-    if (lane == 0) {
-      const uint64_t pol_stream = dev::policy_evict_first();
-      const uint64_t pol_keep = dev::policy_evict_last();
-      int slot = 0;
-      uint32_t phase = 0;
-      const int64_t ipl = b / Re;                        // items per leaf
-      int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
-      // standard admissibility: dense near field = the 3^d neighbour leaves
-      int64_t leaf_idx = (a.row0 + leaf0) / b;
-      int lx[3] = {0, 0, 0};
-      uint32_t nmask = 1u;
-      if (a.adm) {
-        geo::morton_decode(a.d, leaf_idx, L, lx);
-        nmask = geo::near_mask(a.d, lx, 1 << L);
-      }
-      for (int64_t j = j0; j < j1; ++j) {
-        const int64_t i0 = j * Re;
-        for (int l = 1; l <= L + a.nd; ++l) {
-          const bool is_d = (l > L);
-          const int e = l - L - 1;  // dense panel / near-field offset index
-          if (is_d ? (!a.dense || !((nmask >> e) & 1u)) : !((a.level_mask >> (l - 1)) & 1ull)) continue;
-          dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
-          unsigned char* st = smem + slot * a.stage_bytes_e;
-          if (!is_d) {
+    // ---------------- producer (the whole warp: lane e owns dense block e) ----
+    const uint64_t pol_stream = dev::policy_evict_first();
+    const uint64_t pol_keep = dev::policy_evict_last();
+    int slot = 0;
+    uint32_t phase = 0;
+    const int64_t ipl = b / Re;                        // items per leaf
+    int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
+    // dense source of lane e: the leaf itself (weak) or its near-field
+    // neighbour e (standard; -1 when it lies outside the domain)
+    int64_t leaf_idx = (a.row0 + leaf0) / b;
+    auto dense_source = [&]() -> int64_t {
+      if (!a.adm) return lane == 0 ? leaf0 : -1;
+      if (lane >= a.nd) return -1;
+      int lx[3];
+      geo::morton_decode(a.d, leaf_idx, L, lx);
+      if (!((geo::near_mask(a.d, lx, 1 << L) >> lane) & 1u)) return -1;
+      return geo::neighbour(a.d, lx, lane, L) * b - a.row0;
+    };
+    int64_t src = dense_source();
+    const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
+    const int64_t dblk = db + int64_t(NR) * a.xs_e * 8;
+    for (int64_t j = j0; j < j1; ++j) {
+      const int64_t i0 = j * Re;
+      for (int l = 1; l <= L + 1; ++l) {
+        const bool is_d = (l == L + 1);
+        if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+        dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
+        unsigned char* st = smem + slot * a.stage_bytes_e;
+        if (!is_d) {
+          if (lane == 0) {
             const LevelArgs& lv = a.lv[l];
             const uint32_t ub = static_cast<uint32_t>(Re * Wp * 8);
             const uint32_t zb = static_cast<uint32_t>(Wp * NR * 8);
@@ -85,43 +90,47 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             dev::mbar_arrive_expect_tx(&full[slot], ub + zb);
             dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
             dev::bulk_g2s(st + ub, lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR, zb, &full[slot], pol_keep);
-          } else {
-            const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
-            // source leaf of this dense block: the leaf itself (weak) or its neighbour e
-            const int64_t src0 = a.adm ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
-            uint32_t total = db;
-            int64_t lo[NR];
-            uint32_t xb[NR];
+          }
+        } else {
+          // one stage holds every dense block of the tile's rows, block e at
+          // byte offset e * dblk followed by its source x segment (16-byte
+          // aligned superset per rhs); lanes issue their own blocks
+          uint32_t mine = 0;
+          int64_t lo[NR];
+          uint32_t xb[NR];
+          if (src >= 0) {
+            mine = db;
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk) {
               if (kk < a.nr) {
-                const int64_t start = kk * a.ldx + src0;
+                const int64_t start = kk * a.ldx + src;
                 lo[kk] = start & ~int64_t(1);
                 xb[kk] = static_cast<uint32_t>((((start + b + 1) & ~int64_t(1)) - lo[kk]) * 8);
-                total += xb[kk];
+                mine += xb[kk];
               }
             }
-            dev::mbar_arrive_expect_tx(&full[slot], total);
-            dev::bulk_g2s(st, a.D + e * a.d_stride + i0 * Dp, db, &full[slot], pol_stream);
+          }
+          const uint32_t total = __reduce_add_sync(0xffffffffu, mine);
+          if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
+          __syncwarp();
+          if (src >= 0) {
+            unsigned char* se = st + lane * dblk;
+            dev::bulk_g2s(se, a.D + lane * a.d_stride + i0 * Dp, db, &full[slot], pol_stream);
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk)
-              if (kk < a.nr)
-                dev::bulk_g2s(st + db + kk * a.xs_e * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
-          }
-          if (++slot == NS) {
-            slot = 0;
-            phase ^= 1;
+              if (kk < a.nr) dev::bulk_g2s(se + db + kk * a.xs_e * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
           }
         }
-        if (++in_leaf == ipl) {
-          in_leaf = 0;
-          leaf0 += b;
-          if (a.adm) {
-            ++leaf_idx;
-            geo::morton_decode(a.d, leaf_idx, L, lx);
-            nmask = geo::near_mask(a.d, lx, 1 << L);
-          }
+        if (++slot == NS) {
+          slot = 0;
+          phase ^= 1;
         }
+      }
+      if (++in_leaf == ipl) {
+        in_leaf = 0;
+        leaf0 += b;
+        ++leaf_idx;
+        src = dense_source();
       }
     }
     return;
@@ -155,10 +164,9 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     double acc[NR], acc2[NR];  // two chains: even / odd columns
 #pragma unroll
     for (int kk = 0; kk < NR; ++kk) acc[kk] = acc2[kk] = 0.0;
-    for (int l = 1; l <= L + a.nd; ++l) {
-      const bool is_d = (l > L);
-      const int e = l - L - 1;
-      if (is_d ? (!a.dense || !((nmask >> e) & 1u)) : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+    for (int l = 1; l <= L + 1; ++l) {
+      const bool is_d = (l == L + 1);
+      if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
       dev::mbar_wait(&full[slot], phase);
       const unsigned char* st = smem + slot * a.stage_bytes_e;
       if (active) {
@@ -181,25 +189,30 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             if (++jj == njU) jj = 0;
           }
         } else {
-          const double2* D2 = reinterpret_cast<const double2*>(st) + ri * NPD;
-          const double* xs = reinterpret_cast<const double*>(st + Re * Dp * 8);
-          const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
-          int xo[NR];
+          const int64_t dblk = int64_t(Re) * Dp * 8 + int64_t(NR) * a.xs_e * 8;
+          for (int e = 0; e < a.nd; ++e) {  // dense blocks present in this stage
+            if (!((nmask >> e) & 1u)) continue;
+            const unsigned char* se = st + e * dblk;
+            const double2* D2 = reinterpret_cast<const double2*>(se) + ri * NPD;
+            const double* xs = reinterpret_cast<const double*>(se + Re * Dp * 8);
+            const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
+            int xo[NR];
 #pragma unroll
-          for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + src0) & 1);
-          int jj = rotD;
-          for (int n = 0; n < njD; ++n) {
-            const int cp = p + tpr * jj;
-            if (cp < NPD) {
-              const double2 dv = D2[cp];
-              const bool odd_ok = 2 * cp + 1 < b;  // padding column of an odd b
+            for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + src0) & 1);
+            int jj = rotD;
+            for (int n = 0; n < njD; ++n) {
+              const int cp = p + tpr * jj;
+              if (cp < NPD) {
+                const double2 dv = D2[cp];
+                const bool odd_ok = 2 * cp + 1 < b;  // padding column of an odd b
 #pragma unroll
-              for (int kk = 0; kk < NR; ++kk) {
-                acc[kk] = fma(dv.x, xs[xo[kk] + 2 * cp], acc[kk]);
-                if (odd_ok) acc2[kk] = fma(dv.y, xs[xo[kk] + 2 * cp + 1], acc2[kk]);
+                for (int kk = 0; kk < NR; ++kk) {
+                  acc[kk] = fma(dv.x, xs[xo[kk] + 2 * cp], acc[kk]);
+                  if (odd_ok) acc2[kk] = fma(dv.y, xs[xo[kk] + 2 * cp + 1], acc2[kk]);
+                }
               }
+              if (++jj == njD) jj = 0;
             }
-            if (++jj == njD) jj = 0;
           }
         }
       }

@@ -140,7 +140,10 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   // node at every level (m_l = b c^{L-l}).
   const int64_t cap = opt.stage_cap_bytes;
   p.Rp = pick_rows(leaf, kConsumerThreads, p.Wp, cap);
-  p.Re = pick_rows(leaf, kConsumerThreads, std::max(p.Wp, p.Dp), cap);
+  // expand: one stage holds U_l rows, or all nd dense blocks of the tile's rows
+  // (standard admissibility: 3^d near-field blocks; a larger cap keeps Re >= 8)
+  p.Re = pick_rows(leaf, kConsumerThreads, std::max<int64_t>(p.Wp, int64_t(p.nd) * p.Dp),
+                   p.adm ? std::max<int64_t>(cap, 48 * 1024) : cap);
   p.tpr = 1;
   while (p.tpr * 2 <= 32 && p.tpr * 2 * p.Re <= kConsumerThreads) p.tpr *= 2;
   p.xs_p = static_cast<int>(round_up(p.Rp + 2, 2));
@@ -156,7 +159,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     Plan::Layout& y = p.lay[li];
     y.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + NR * p.xs_p * 8, 128);
     y.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * NR * 8,
-                                        int64_t(p.Re) * p.Dp * 8 + NR * p.xs_e * 8),
+                                        int64_t(p.nd) * (int64_t(p.Re) * p.Dp * 8 + NR * p.xs_e * 8)),
                                128);
     const int64_t red_bytes = round_up(2 * int64_t(rg) * p.Wp * NR * 8, 128);  // two alternating buffers
     // the requested CTAs per SM, or fewer if two pipeline stages do not fit
@@ -167,7 +170,11 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       y.ctas_per_sm = ctas;
       if (y.nstage_p >= 2 && y.nstage_e >= 2) break;
     }
-    if (y.nstage_p < 2 || y.nstage_e < 2) return "unsupported: pipeline stages do not fit in shared memory";
+    if (y.nstage_p < 2 || y.nstage_e < 2) {
+      if (li == 0) return "unsupported: pipeline stages do not fit in shared memory";
+      break;  // wider right-hand-side passes do not fit: cap the pass width
+    }
+    p.max_nr = static_cast<int>(NR);
     y.red_off_p = y.nstage_p * y.stage_bytes_p;
     y.bar_off_p = y.red_off_p + red_bytes;
     y.bar_off_e = y.nstage_e * y.stage_bytes_e;

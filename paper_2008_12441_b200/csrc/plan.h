@@ -76,6 +76,7 @@ struct Plan {
     int grid_p = 0, grid_e = 0;                            // persistent grids
   } lay[4];
   int grid_p_max = 0;               // partial-sum slots to allocate
+  int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)

@@ -28,7 +28,7 @@ def run(cfg, setting, reps=10):
         os.environ[k] = v
         keys.append(k)
     try:
-        h = hm.hmat_create_uninit(cfg.L, cfg.d, cfg.b, cfg.r)
+        h = (hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit)(cfg.L, cfg.d, cfg.b, cfg.r)
         info = hm.hmat_plan_query(cfg.L, cfg.d, cfg.b, cfg.r)
         r0, r1 = hm.hmat_local_rows(h)
         hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, 0)
@@ -45,7 +45,7 @@ def run(cfg, setting, reps=10):
             hm.hmat_matvec(h, x.t(), y.t(), cfg.nrhs)
         prof = hm.hmat_profile_read(h)
         hm.hmat_destroy(h)
-        W, L, b, N = cfg.W, cfg.L, cfg.b, cfg.N
+        W, L, b, N = cfg.W, cfg.L - (1 if cfg.adm else 0), cfg.dcols, cfg.N
         pb = 8 * N * W * L + 8 * N * cfg.nrhs
         eb = 8 * N * (W * L + b) + 16 * N * cfg.nrhs
         pm = prof["project"][0] / reps  # per matvec (all passes)
@@ -65,6 +65,8 @@ def parse_cfg(spec):
     """a BASELINE config name (c1..c5) or an ad-hoc shape 'd=3,L=4,b=64,r=32,nrhs=64'"""
     if spec in hgen.CONFIGS:
         return hgen.CONFIGS[spec]
+    if spec in hgen.EXTRA_CONFIGS:
+        return hgen.EXTRA_CONFIGS[spec]
     kv = dict(item.split("=") for item in spec.split(","))
     return hgen.HConfig(spec, **{k: int(v) for k, v in kv.items()}, seed=hgen.SEED_BASE + 99)
 

@@ -11,9 +11,9 @@ import torch  # noqa: E402
 from gen import hgen  # noqa: E402
 from paper_2008_12441_b200 import hmat as hm  # noqa: E402
 
-cfg = hgen.CONFIGS[sys.argv[1]]
+cfg = {**hgen.CONFIGS, **hgen.EXTRA_CONFIGS}[sys.argv[1]]
 reps = 10
-h = hm.hmat_create_uninit(cfg.L, cfg.d, cfg.b, cfg.r)
+h = (hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit)(cfg.L, cfg.d, cfg.b, cfg.r)
 r0, r1 = hm.hmat_local_rows(h)
 hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, 0)
 n = r1 - r0
@@ -33,7 +33,7 @@ for name, mask, dense in cases:
     hm.hmat_profile(h, False)
     nl = bin(mask).count("1")
     pb = 8 * n * cfg.W * nl
-    eb = 8 * n * (cfg.W * nl + (cfg.b if dense else 0))
+    eb = 8 * n * (cfg.W * nl + (cfg.dcols if dense else 0))
     pm = prof["project"][0] / max(1, prof["project"][1])
     em = prof["expand"][0] / max(1, prof["expand"][1])
     print(f"{cfg.name} {name:9s} project {pm:8.3f} ms {pb / max(pm, 1e-9) / 1e6:6.0f} GB/s | "

@@ -34,7 +34,8 @@ def rel_err(y, ref):
 def device_operator(cfg, hm, dist=None, stream=0):
     """hmat_create_uninit + in-place device generation of the seeded panels."""
     from gen import hgen
-    h = hm.hmat_create_uninit(cfg.L, cfg.d, cfg.b, cfg.r, dist)
+    create = hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit
+    h = create(cfg.L, cfg.d, cfg.b, cfg.r, dist)
     r0, r1 = hm.hmat_local_rows(h)
     hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, stream)
     return h

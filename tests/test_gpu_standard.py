@@ -72,3 +72,30 @@ def test_standard_unsupported_cases():
         hm.hmat_create_standard_uninit(cfg.L, cfg.d, cfg.b, cfg.r,
                                        hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
     assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
+
+
+def test_standard_device_generated_operator():
+    """In-place device generation of the standard panels (as bench.py --config s2
+    does) gives the operator the oracle sees from host-generated panels."""
+    from tests.helpers import device_operator
+    cfg = HConfig("stdg", d=2, L=5, b=64, r=8, adm=1, seed=779)
+    h = device_operator(cfg, hm)
+    try:
+        x = torch.empty(cfg.N, dtype=torch.float64, device="cuda")
+        hgen.dev_fill_x(cfg, 1, 0, 0, cfg.N, x.data_ptr(), cfg.N)
+        y = torch.empty_like(x)
+        hm.hmat_matvec(h, x, y)
+        torch.cuda.synchronize()
+        U, V, Dn = hgen.inputs(cfg)
+        ref = oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x.cpu().numpy())
+        assert_parity(y.cpu().numpy(), ref)
+    finally:
+        hm.hmat_destroy(h)
+
+
+def test_standard_3d_leaf64_caps_pass_width():
+    """3D, b = 64: 27 near-field blocks per row make wide rhs passes too big for
+    shared memory; the plan caps the pass width and multi-rhs still matches."""
+    cfg = HConfig("std3w", d=3, L=2, b=64, r=1, adm=1, seed=780)
+    y, (U, V, Dn, x) = run_std(cfg, 5)
+    assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
