@@ -75,10 +75,25 @@ typedef struct {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId (same on all ranks); P > 1 only */
   void* cuda_stream;          /* cudaStream_t to enqueue on; NULL => library-owned    */
   int device;                 /* CUDA ordinal of this rank's GPU                     */
-  int external_exchange;      /* P > 1: 0 = NCCL inside hmat_matvec (needs the id);  */
-                              /* 1 = the caller sums the exchange buffer between     */
-                              /*     hmat_project and hmat_expand (MPI, torch, ...)  */
+  int exchange;               /* P > 1: one of HMAT_EXCHANGE_*                       */
 } hmat_dist_t;
+
+/* How ranks exchange the projected vectors of the levels whose parent spans
+ * more than one GPU (Steps 2-4):
+ *   NCCL     ncclAllReduce(sum) of the packed buffer inside hmat_matvec
+ *            (needs nccl_unique_id);
+ *   EXTERNAL the caller sums the buffer between hmat_project and hmat_expand;
+ *   PEER     in-kernel over NVLink peer memory: the project
+ *            kernel's last CTA writes this rank's contributions into slot
+ *            `rank` of every rank's mailbox and raises a flag there; the expand
+ *            kernel waits for the P flags and sums the P slots in rank order.
+ *            Mailboxes are connected once with hmat_peer_export/_import (CUDA
+ *            IPC, one process per GPU) or hmat_peer_connect_local (one process).
+ *            No host or NCCL call per matvec; the many-rhs tensor-core path is
+ *            not used in this mode. */
+#define HMAT_EXCHANGE_NCCL 0
+#define HMAT_EXCHANGE_EXTERNAL 1
+#define HMAT_EXCHANGE_PEER 2
 
 /* Build H from canonical panels (see above).  U and V are arrays of `depth`
  * pointers (ignored when depth == 0); each panel and D may be host (pageable or
@@ -149,7 +164,7 @@ hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, cons
                                const double* const* V, const double* Dc, const hmat_dist_t* dist, hmat_t* out);
 
 /* Split-phase form (one pass: nrhs <= 8, or <= 64 on the tensor-core path), for
- * a caller-provided exchange (hmat_dist_t.external_exchange = 1: MPI,
+ * a caller-provided exchange (hmat_dist_t.exchange = HMAT_EXCHANGE_EXTERNAL: MPI,
  * torch.distributed, ...) or to overlap other work.  x, y, exchange are device
  * pointers on H's device; work is enqueued on H's stream.
  *   hmat_exchange_size: doubles of this pass's packed exchange buffer (level-
@@ -159,11 +174,23 @@ hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, cons
  *     contributions (partial node sums, zeros elsewhere) to exchange[0..count).
  *   the caller sums exchange over all ranks (Steps 2-4);
  *   hmat_expand: reads the summed exchange, Step 5: y = H x.
- * With NCCL (external_exchange = 0) hmat_matvec does exactly this with an
- * in-place ncclAllReduce. */
+ * With HMAT_EXCHANGE_NCCL hmat_matvec does exactly this with an
+ * in-place ncclAllReduce.  With HMAT_EXCHANGE_PEER `exchange` is ignored (may
+ * be NULL): the kernels exchange through the connected mailboxes. */
 hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count);
 hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange);
 hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, double* y, int nrhs);
+
+/* PEER exchange set-up (collective in spirit: every rank must connect before
+ * the first product).  hmat_peer_export writes the 64-byte CUDA IPC handle of
+ * H's mailbox; after gathering all ranks' handles (rank order), each rank calls
+ * hmat_peer_import with them.  hmat_peer_connect_local connects the P handles of
+ * ONE process directly (e.g. P shards on one GPU; only the split-phase calls
+ * may then be used, projects of all ranks before any expand, since an expand
+ * waits for every rank's project). */
+hmat_status hmat_peer_export(hmat_t H, void* handle64);
+hmat_status hmat_peer_import(hmat_t H, const void* handles);
+hmat_status hmat_peer_connect_local(hmat_t H, const hmat_t* ranks);
 
 /* Diagnostic form: only the low-rank levels l with bit (l-1) of level_mask set
  * and, if dense != 0, the dense leaf blocks: y = y_D + sum_{l in mask} y_l. */

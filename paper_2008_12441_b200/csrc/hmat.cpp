@@ -115,6 +115,16 @@ struct hmat_s {
   int* cnt_d = nullptr;
   double* Dt = nullptr;  // D^T, built on the first transposed product
   bool external = false;  // P > 1 with a caller-provided exchange (split-phase API)
+  // in-kernel peer exchange (HMAT_EXCHANGE_PEER): this rank's mailbox
+  // [2 parities][P slots][mb] doubles + [2][P] uint64 flags, and the device
+  // table of every rank's mailbox address (peer memory)
+  bool peer = false, connected = false;
+  double* mbox = nullptr;
+  double** mbox_dev = nullptr;
+  unsigned int* done = nullptr;
+  int64_t mb = 0;
+  uint64_t epoch = 0;
+  std::vector<void*> opened;  // IPC mappings to close
   int zt_cap = 1;         // rhs width of the z-buffer layout last written (zeroed at create)
   bool prof = false;
   std::vector<EventPair> ev;
@@ -143,6 +153,10 @@ void release(hmat_s* H) {
   cudaFree(H->part_d);
   cudaFree(H->cnt_d);
   cudaFree(H->Dt);
+  for (void* q : H->opened) cudaIpcCloseMemHandle(q);
+  cudaFree(H->mbox);
+  cudaFree(H->mbox_dev);
+  cudaFree(H->done);
   for (auto& e : H->ev) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -159,8 +173,10 @@ hmat_status validate_dist(const hmat_dist_t* dist, int* P, int* rank) {
   if (!dist) return HMAT_OK;
   *P = dist->nranks;
   *rank = dist->rank;
-  if (dist->nranks > 1 && !dist->nccl_unique_id && !dist->external_exchange)
-    return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1 (and no external exchange)");
+  if (dist->exchange < HMAT_EXCHANGE_NCCL || dist->exchange > HMAT_EXCHANGE_PEER)
+    return fail(HMAT_ERR_INVALID, "exchange must be HMAT_EXCHANGE_NCCL, _EXTERNAL or _PEER");
+  if (dist->nranks > 1 && dist->exchange == HMAT_EXCHANGE_NCCL && !dist->nccl_unique_id)
+    return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1 and the NCCL exchange");
   if (dist->device < 0) return fail(HMAT_ERR_INVALID, "device ordinal must be >= 0");
   return HMAT_OK;
 }
@@ -173,8 +189,10 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   hmat_status st = validate_dist(dist, &P, &shard);
   if (st != HMAT_OK) return st;
   hmat::Plan plan;
+  const bool peer = dist && dist->nranks > 1 && dist->exchange == HMAT_EXCHANGE_PEER;
   hmat::PlanOptions opt0 = options_from_env(148);
   opt0.adm = adm;
+  opt0.peer = peer;
   std::string msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, opt0, &plan);
   if (!msg.empty()) return plan_status(msg);
 
@@ -190,6 +208,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   hmat::PlanOptions opt = options_from_env(sms);
   opt.adm = adm;
+  opt.peer = peer;
   msg = hmat::plan_build(depth, dim, leaf, rank, P, shard, opt, &plan);
   if (!msg.empty()) return plan_status(msg);
 
@@ -238,14 +257,25 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(p.dsmem_p, p.dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
-  H->external = p.P > 1 && dist->external_exchange;
+  H->external = p.P > 1 && dist->exchange == HMAT_EXCHANGE_EXTERNAL;
+  H->peer = peer;
+  if (peer) {
+    H->mb = (p.z_exch_rows * p.Wp * hmat::kMaxNR + 15) / 16 * 16;
+    const size_t mbytes = (size_t(2) * p.P * H->mb + size_t(2) * p.P) * sizeof(double);
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&H->mbox), mbytes)) ||
+        (e = cudaMalloc(reinterpret_cast<void**>(&H->mbox_dev), size_t(p.P) * sizeof(double*))) ||
+        (e = cudaMalloc(reinterpret_cast<void**>(&H->done), 256)) ||
+        (e = cudaMemset(H->mbox, 0, mbytes)) || (e = cudaMemset(H->mbox_dev, 0, size_t(p.P) * sizeof(double*))) ||
+        (e = cudaMemset(H->done, 0, 256)))
+      return bail(cuda_fail(e, "allocating the peer mailbox"));
+  }
   if (p.adm) {  // interaction-list slot tables for the project kernel's scatter
     static int16_t code[3][8][hmat::kStdMaxSlots], slot[3][8][hmat::kStdMaxCodes];
     hmat::std_slot_tables(code, slot);
     if ((e = hmat::init_std_tables(&code[0][0][0], &slot[0][0][0])) != cudaSuccess)
       return bail(cuda_fail(e, "init_std_tables"));
   }
-  if (p.P > 1 && !H->external) {
+  if (p.P > 1 && !H->external && !peer) {
     std::string m = hmat::comm_create(dist->nccl_unique_id, p.P, p.rank, &H->comm);
     if (!m.empty()) return bail(fail(HMAT_ERR_NCCL, m));
   }
@@ -438,6 +468,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   } else if (p.P > 1 && H->external) {
     return fail(HMAT_ERR_UNSUPPORTED, "external exchange: use hmat_project / hmat_expand");
   }
+  if (H->peer && !H->connected) return fail(HMAT_ERR_INVALID, "peer exchange: mailboxes not connected");
   const bool host_io = !x_dev || !y_dev;
   if (p.L < 64) level_mask &= (p.L == 0 ? 0ull : (~0ull >> (64 - p.L)));
   if (p.adm) level_mask &= ~1ull;  // standard admissibility: no admissible pair at level 1
@@ -506,11 +537,22 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.items_e = p.items_e;
   a.xs_p = p.xs_p;
   a.xs_e = p.xs_e;
+  a.cross = p.cross;
+  a.P = p.P;
+  a.rank = p.rank;
+  a.peer = H->peer ? 1 : 0;
+  a.mbox = H->mbox_dev;
+  a.mb = H->mb;
+  a.done = H->done;
+  a.zex_base = H->zex;
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
   auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project) -> hmat_status {
     const size_t bytes = exch * sizeof(double);
+    a.exch = int64_t(exch);
+    if (phases & kPhaseProject) ++H->epoch;  // peer exchange: a new pass (same count on every rank)
+    a.epoch = H->epoch;
     if (phases & kPhaseProject) {
       if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(zex, 0, bytes, H->stream));
       if (has_project && level_mask) {
@@ -520,7 +562,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       }
       if (exch_out && exch) CUDA_TRY(cudaMemcpyAsync(exch_out, zex, bytes, cudaMemcpyDeviceToDevice, H->stream));
     }
-    if ((phases & kPhaseExchange) && !H->external && p.P > 1 && exch) {
+    if ((phases & kPhaseExchange) && !H->external && !H->peer && p.P > 1 && exch) {
       prof_begin(H, 1, &ep);
       std::string m = hmat::comm_allreduce_sum(H->comm, zex, exch, H->stream);
       if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
@@ -643,7 +685,7 @@ hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange) 
   int64_t count = 0;
   hmat_status st = hmat_exchange_size(H, nrhs, &count);
   if (st != HMAT_OK) return st;
-  if (count && !exchange) return fail(HMAT_ERR_INVALID, "exchange is NULL");
+  if (count && !exchange && !H->peer) return fail(HMAT_ERR_INVALID, "exchange is NULL");
   return run(H, 0, 1.0, x, 0.0, nullptr, nrhs, ~0ull, 1, kPhaseProject, exchange, nullptr);
 }
 
@@ -651,7 +693,7 @@ hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, doubl
   int64_t count = 0;
   hmat_status st = hmat_exchange_size(H, nrhs, &count);
   if (st != HMAT_OK) return st;
-  if (count && !exchange) return fail(HMAT_ERR_INVALID, "exchange is NULL");
+  if (count && !exchange && !H->peer) return fail(HMAT_ERR_INVALID, "exchange is NULL");
   return run(H, 0, 1.0, x, 0.0, y, nrhs, ~0ull, 1, kPhaseExpand, nullptr, exchange);
 }
 
@@ -697,6 +739,56 @@ hmat_status hmat_nccl_unique_id(void* out128) {
   if (!out128) return fail(HMAT_ERR_INVALID, "out is NULL");
   std::string m = hmat::comm_unique_id(out128);
   if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  return HMAT_OK;
+}
+
+hmat_status hmat_peer_export(hmat_t H, void* handle64) {
+  if (!H || !handle64) return fail(HMAT_ERR_INVALID, "NULL argument");
+  if (!H->peer) return fail(HMAT_ERR_INVALID, "H does not use the peer exchange");
+  CUDA_TRY(cudaSetDevice(H->device));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  CUDA_TRY(cudaIpcGetMemHandle(&h, H->mbox));
+  memcpy(handle64, &h, sizeof h);
+  return HMAT_OK;
+}
+
+hmat_status hmat_peer_import(hmat_t H, const void* handles) {
+  if (!H || !handles) return fail(HMAT_ERR_INVALID, "NULL argument");
+  if (!H->peer) return fail(HMAT_ERR_INVALID, "H does not use the peer exchange");
+  CUDA_TRY(cudaSetDevice(H->device));
+  const int P = H->plan.P;
+  std::vector<double*> ptrs(P);
+  for (int g = 0; g < P; ++g) {
+    if (g == H->plan.rank) {
+      ptrs[g] = H->mbox;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + 64 * g, sizeof h);
+    void* q = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+    H->opened.push_back(q);
+    ptrs[g] = static_cast<double*>(q);
+  }
+  CUDA_TRY(cudaMemcpy(H->mbox_dev, ptrs.data(), P * sizeof(double*), cudaMemcpyHostToDevice));
+  H->connected = true;
+  return HMAT_OK;
+}
+
+hmat_status hmat_peer_connect_local(hmat_t H, const hmat_t* ranks) {
+  if (!H || !ranks) return fail(HMAT_ERR_INVALID, "NULL argument");
+  if (!H->peer) return fail(HMAT_ERR_INVALID, "H does not use the peer exchange");
+  const int P = H->plan.P;
+  std::vector<double*> ptrs(P);
+  for (int g = 0; g < P; ++g) {
+    if (!ranks[g] || !ranks[g]->peer || ranks[g]->plan.P != P || ranks[g]->plan.rank != g)
+      return fail(HMAT_ERR_INVALID, "ranks[g] must be rank g's handle of the same peer-exchange operator");
+    ptrs[g] = ranks[g]->mbox;
+  }
+  CUDA_TRY(cudaSetDevice(H->device));
+  CUDA_TRY(cudaMemcpy(H->mbox_dev, ptrs.data(), P * sizeof(double*), cudaMemcpyHostToDevice));
+  H->connected = true;
   return HMAT_OK;
 }
 

@@ -54,6 +54,17 @@ struct StreamArgs {
   int64_t stage_bytes_e, items_e;
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows
+  // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
+  // CTA pushes this rank's exchange levels into slot `rank` of every rank's
+  // mailbox and raises its flag there; expand sums the P slots in rank order
+  int peer, P, rank;
+  double* const* mbox;       // [P] device pointers: each rank's mailbox base (peer memory)
+  int64_t mb;                // doubles per slot (this pass's exchange levels, padded)
+  uint64_t epoch;            // pass counter (identical on all ranks)
+  unsigned int* done;        // project CTAs finished (last one pushes)
+  const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
+  int64_t exch;              // doubles of this pass's exchange levels
+  int cross;                 // levels 1..cross are exchange levels
   int64_t red_off_p;   // byte offsets inside the dynamic shared memory
   int64_t bar_off_p, bar_off_e;
   LevelArgs lv[kMaxLevels + 1];

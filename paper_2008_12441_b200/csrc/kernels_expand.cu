@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       return geo::neighbour(a.d, lx, lane, L) * b - a.row0;
     };
     int64_t src = dense_source();
+    bool peers_ready = false;
     const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
     const int64_t dblk = db + int64_t(NR) * a.xs_e * 8;
     for (int64_t j = j0; j < j1; ++j) {
@@ -87,9 +88,33 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             const uint32_t ub = static_cast<uint32_t>(Re * Wp * 8);
             const uint32_t zb = static_cast<uint32_t>(Wp * NR * 8);
             const int64_t tg = (a.row0 + i0) / lv.m;
-            dev::mbar_arrive_expect_tx(&full[slot], ub + zb);
-            dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
-            dev::bulk_g2s(st + ub, lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR, zb, &full[slot], pol_keep);
+            const double* zrow = lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR;
+            if (a.peer && l <= a.cross) {
+              // peer exchange: the P ranks' contributions sit in this rank's
+              // mailbox slots; wait once for every rank's flag of this pass
+              const int par = static_cast<int>(a.epoch & 1);
+              const double* mb = a.mbox[a.rank] + (int64_t)par * a.P * a.mb;
+              if (!peers_ready) {
+                const uint64_t* fl = reinterpret_cast<const uint64_t*>(a.mbox[a.rank] + 2 * a.P * a.mb) + par * a.P;
+                const long long t0 = clock64();
+                for (int g = 0; g < a.P; ++g)
+                  while (dev::ld_acquire_sys(fl + g) != a.epoch) {
+                    __nanosleep(256);
+                    if (clock64() - t0 > (1ll << 35)) __trap();  // ~17 s: never hang the GPU
+                  }
+                dev::fence_proxy_async_global();
+                peers_ready = true;
+              }
+              const int64_t off = zrow - a.zex_base;
+              dev::mbar_arrive_expect_tx(&full[slot], ub + a.P * zb);
+              dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
+              for (int g = 0; g < a.P; ++g)
+                dev::bulk_g2s(st + ub + g * zb, mb + g * a.mb + off, zb, &full[slot], pol_keep);
+            } else {
+              dev::mbar_arrive_expect_tx(&full[slot], ub + zb);
+              dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
+              dev::bulk_g2s(st + ub, zrow, zb, &full[slot], pol_keep);
+            }
           }
         } else {
           // one stage holds every dense block of the tile's rows, block e at
@@ -173,6 +198,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         if (!is_d) {
           const double2* U2 = reinterpret_cast<const double2*>(st) + ri * NP;
           const double* Zs = reinterpret_cast<const double*>(st + Re * Wp * 8);
+          // peer exchange levels: the stage holds the P ranks' rows, summed here in rank order
+          const int nz = (a.peer && l <= a.cross) ? a.P : 1;
           int jj = rotU;
           for (int n = 0; n < njU; ++n) {
             const int cp = p + tpr * jj;
@@ -181,7 +208,12 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
               if (2 * cp + 1 >= W) u.y = 0.0;  // padding column of an odd W
 #pragma unroll
               for (int kk = 0; kk < NR; ++kk) {  // Zt row layout [rhs][col]
-                const double2 z = reinterpret_cast<const double2*>(Zs + kk * Wp)[cp];
+                double2 z = reinterpret_cast<const double2*>(Zs + kk * Wp)[cp];
+                for (int g = 1; g < nz; ++g) {
+                  const double2 zg = reinterpret_cast<const double2*>(Zs + (int64_t)g * Wp * NR + kk * Wp)[cp];
+                  z.x += zg.x;
+                  z.y += zg.y;
+                }
                 acc[kk] = fma(u.x, z.x, acc[kk]);
                 acc2[kk] = fma(u.y, z.y, acc2[kk]);
               }

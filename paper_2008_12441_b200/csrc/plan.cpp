@@ -158,7 +158,8 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     const int64_t NR = int64_t(1) << li;
     Plan::Layout& y = p.lay[li];
     y.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + NR * p.xs_p * 8, 128);
-    y.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * NR * 8,
+    const int64_t zrows = opt.peer ? P : 1;  // peer exchange: one z row per rank on exchange levels
+    y.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * NR * 8 * zrows,
                                         int64_t(p.nd) * (int64_t(p.Re) * p.Dp * 8 + NR * p.xs_e * 8)),
                                128);
     const int64_t red_bytes = round_up(2 * int64_t(rg) * p.Wp * NR * 8, 128);  // two alternating buffers
@@ -186,7 +187,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     p.grid_p_max = std::max(p.grid_p_max, y.grid_p);
   }
   // DMMA layouts (1 project CTA per SM: 2 stages of ~77 KB; 2 expand CTAs per SM)
-  p.dmma_ok = p.adm == 0 && p.W % 32 == 0 && p.W <= 224 && leaf % kDmmaRE == 0 && leaf % kDmmaKR == 0 && p.N_loc % kDmmaRE == 0;
+  p.dmma_ok = p.adm == 0 && !opt.peer && p.W % 32 == 0 && p.W <= 224 && leaf % kDmmaRE == 0 && leaf % kDmmaKR == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
     p.dstage_p = round_up(int64_t(kDmmaKR) * p.vp * 8 + int64_t(kDmmaNB) * kDmmaXP * 8, 128);

@@ -96,6 +96,7 @@ struct PlanOptions {
   int max_stages_p = 2;             // project: measured best at 2 stages x 2 CTAs per SM
   int max_stages_e = 3;             // expand: measured best at 3 stages x 2 CTAs per SM
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
+  int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.

@@ -23,6 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 HMAT_OK, HMAT_ERR_INVALID, HMAT_ERR_NOMEM, HMAT_ERR_CUDA, HMAT_ERR_NCCL, HMAT_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 HMAT_NUM_PHASES = 4
+HMAT_EXCHANGE_NCCL, HMAT_EXCHANGE_EXTERNAL, HMAT_EXCHANGE_PEER = 0, 1, 2
 PHASES = ("project", "exchange", "expand", "copies")
 
 # Every symbol include/hmat.h declares (checked by tests/test_abi.py).
@@ -30,7 +31,8 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_create_standard_uninit", "hmat_panel", "hmat_matvec", "hmat_gemv",
            "hmat_exchange_size", "hmat_project", "hmat_expand", "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
-           "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query")
+           "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
+           "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local")
 
 
 class HMatError(RuntimeError):
@@ -41,7 +43,7 @@ class HMatError(RuntimeError):
 
 class hmat_dist_t(ctypes.Structure):
     _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int), ("external_exchange", ctypes.c_int)]
+                ("cuda_stream", ctypes.c_void_p), ("device", ctypes.c_int), ("exchange", ctypes.c_int)]
 
 
 class hmat_plan_info_t(ctypes.Structure):
@@ -80,6 +82,9 @@ _sigs = {
     "hmat_profile_read": (_i, [_H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
     "hmat_launches_per_matvec": (_i64, [_H, _i]),
     "hmat_plan_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_plan_info_t)]),
+    "hmat_peer_export": (_i, [_H, _P]),
+    "hmat_peer_import": (_i, [_H, _P]),
+    "hmat_peer_connect_local": (_i, [_H, _P]),
 }
 for _name, (_res, _args) in _sigs.items():
     _f = getattr(_lib, _name)
@@ -138,10 +143,12 @@ def _vec(a, n: int):
     return a.data_ptr(), a.shape[1]
 
 
-def _dist(nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, device=None, external_exchange=False):
+def _dist(nranks=1, rank=0, nccl_unique_id=None, cuda_stream=None, device=None, external_exchange=False,
+          exchange=None):
     d = hmat_dist_t()
     d.nranks, d.rank = nranks, rank
-    d.external_exchange = int(bool(external_exchange))
+    d.exchange = exchange if exchange is not None else (HMAT_EXCHANGE_EXTERNAL if external_exchange
+                                                        else HMAT_EXCHANGE_NCCL)
     d._id_buf = None
     if nccl_unique_id is not None:
         buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
@@ -347,3 +354,22 @@ class HMatrix:
             self.close()
         except Exception:
             pass
+
+
+def hmat_peer_export(h) -> bytes:
+    """64-byte CUDA IPC handle of this rank's peer-exchange mailbox."""
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.hmat_peer_export(h, ctypes.cast(buf, _P)), "hmat_peer_export")
+    return buf.raw
+
+
+def hmat_peer_import(h, handles):
+    """handles: the P ranks' 64-byte handles in rank order."""
+    blob = ctypes.create_string_buffer(b"".join(bytes(x) for x in handles), 64 * len(handles))
+    _check(_lib.hmat_peer_import(h, ctypes.cast(blob, _P)), "hmat_peer_import")
+
+
+def hmat_peer_connect_local(h, ranks):
+    """connect the mailboxes of P handles of this process (rank order)."""
+    arr = (ctypes.c_void_p * len(ranks))(*[r.value for r in ranks])
+    _check(_lib.hmat_peer_connect_local(h, ctypes.cast(arr, _P)), "hmat_peer_connect_local")

@@ -103,3 +103,67 @@ def test_external_exchange_requires_split_api():
         assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
     finally:
         hm.hmat_destroy(h)
+
+
+def peer_split_matvec(cfg, P, nrhs, reps=2):
+    """HMAT_EXCHANGE_PEER on one GPU: every rank's project kernel pushes its
+    exchange levels into all mailboxes and raises its flags; then every rank's
+    expand kernel consumes them (projects of all ranks first, so no kernel ever
+    waits for another one on this single GPU)."""
+    hs, xs = [], []
+    for g in range(P):
+        r0, r1 = g * cfg.N // P, (g + 1) * cfg.N // P
+        U, V, D = hgen.inputs(cfg, r0, r1)
+        d = hm._dist(nranks=P, rank=g, device=0, exchange=hm.HMAT_EXCHANGE_PEER)
+        hs.append(hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D, d))
+        xs.append(torch.from_numpy(np.ascontiguousarray(hgen.xblock(cfg, nrhs=nrhs, row_begin=r0,
+                                                                    row_end=r1).T)).cuda())
+    try:
+        for h in hs:
+            hm.hmat_peer_connect_local(h, hs)
+        out = []
+        for rep in range(reps):  # several passes: mailbox parities alternate
+            for g in range(P):
+                hm.hmat_project(hs[g], xs[g].t(), None, nrhs)
+            ys = []
+            for g in range(P):
+                y = torch.empty_like(xs[g])
+                hm.hmat_expand(hs[g], xs[g].t(), None, y.t(), nrhs)
+                ys.append(y)
+            torch.cuda.synchronize()
+            out.append(torch.cat(ys, dim=1).t().cpu().numpy())
+        return out
+    finally:
+        for h in hs:
+            hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("cfg,P,nrhs", [
+    (HConfig("q2d", d=2, L=4, b=16, r=4, seed=401), 2, 1),
+    (HConfig("q2d", d=2, L=4, b=16, r=4, seed=401), 8, 3),
+    (HConfig("q3d", d=3, L=3, b=8, r=3, seed=402), 4, 2),
+    (HConfig("q3d", d=3, L=3, b=64, r=32, seed=403), 8, 1),
+    (HConfig("q1d", d=1, L=7, b=4, r=2, seed=404), 16, 8),
+], ids=lambda v: getattr(v, "name", str(v)))
+def test_peer_exchange_matches_oracle(cfg, P, nrhs):
+    outs = peer_split_matvec(cfg, P, nrhs)
+    U, V, D = hgen.inputs(cfg)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, hgen.xblock(cfg, nrhs=nrhs))
+    for y in outs:
+        assert_parity(y, ref)
+    assert np.array_equal(outs[0], outs[1])  # deterministic (rank-order sums)
+
+
+def test_peer_exchange_needs_connection():
+    cfg = HConfig("qc", d=2, L=2, b=4, r=2, seed=405)
+    U, V, D = hgen.inputs(cfg, 0, cfg.N // 2)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D,
+                       hm._dist(nranks=2, rank=0, device=0, exchange=hm.HMAT_EXCHANGE_PEER))
+    try:
+        x = torch.zeros(cfg.N // 2, dtype=torch.float64, device="cuda")
+        with pytest.raises(hm.HMatError) as ei:
+            hm.hmat_project(h, x, None)
+        assert ei.value.status == hm.HMAT_ERR_INVALID
+        assert len(hm.hmat_peer_export(h)) == 64
+    finally:
+        hm.hmat_destroy(h)
