@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: in-kernel exchange over NVLink peer memory (default) or ncclAllReduce")
     return ap.parse_args()
 
 
@@ -280,11 +282,33 @@ def run_ours(args):
         obj = [hm.hmat_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    dd = hm._dist(nranks=world, rank=rank, nccl_unique_id=nid, cuda_stream=sptr, device=local)
-
-    t_setup = time.perf_counter()
     create = hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit
-    h = create(cfg.L, cfg.d, cfg.b, cfg.r, dd)
+    t_setup = time.perf_counter()
+    exchange = args.exchange if world > 1 else "none"
+    h = None
+    if exchange == "peer":
+        # mailboxes connected once through CUDA IPC handles (hmat_peer_export/_import)
+        err = ""
+        try:
+            h = create(cfg.L, cfg.d, cfg.b, cfg.r,
+                       hm._dist(nranks=world, rank=rank, cuda_stream=sptr, device=local,
+                                exchange=hm.HMAT_EXCHANGE_PEER))
+            handles = [None] * world
+            dist.all_gather_object(handles, hm.hmat_peer_export(h))
+            hm.hmat_peer_import(h, handles)
+        except Exception as e:  # reported in the JSON line, never silent
+            err = f"{type(e).__name__}: {e}"
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if any(errs):
+            print(f"warning: peer exchange unavailable ({[e for e in errs if e][0]}); using NCCL", file=sys.stderr)
+            if h is not None:
+                hm.hmat_destroy(h)
+            h = None
+            exchange = "nccl (peer unavailable: " + [e for e in errs if e][0][:120] + ")"
+    if h is None:
+        dd = hm._dist(nranks=world, rank=rank, nccl_unique_id=nid, cuda_stream=sptr, device=local)
+        h = create(cfg.L, cfg.d, cfg.b, cfg.r, dd)
     r0, r1 = hm.hmat_local_rows(h)
     n = r1 - r0
     hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, sptr)
@@ -400,7 +424,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "N": cfg.N, "nrhs": nrhs,
                        "factor_bytes": cfg.factor_bytes, "parallelism": f"subtree shards x{world} (Morton rows)",
-                       "l2": "working set 1000x L2; no flush needed", "distinct_x": nvec},
+                       "l2": "working set 1000x L2; no flush needed", "distinct_x": nvec,
+                       "exchange": exchange},
             "factor_GBps": factor_gbps,
             "alg_GBps": ab["total"] * world / (ms_step * 1e-3) / 1e9,
             "roofline": roof,
@@ -412,6 +437,7 @@ def run_ours(args):
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
+    barrier()  # peer mailboxes are mapped by every rank: free them together
     hm.hmat_destroy(h)
     if world > 1:
         dist.destroy_process_group()
