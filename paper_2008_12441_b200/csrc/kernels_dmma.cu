@@ -49,16 +49,17 @@ __device__ __forceinline__ int64_t zfrag(int w, int n) {
 
 __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { return ((k + 1) * G - 1) / S; }
 
-// z value of column w = q r + a of source node sg, rhs n -> Zt of target sib(sg, q).
-__device__ __forceinline__ void scatter_zd(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int w, int n,
-                                           double v) {
+// Column w = q r + aa of source node sg's z goes to target t = sib(sg, q), into
+// t's column qt r + aa (qt = slot of sg in t's list).  Returns the Zt block of t
+// with the column's fragment-major base folded in: element (w, n) then sits at
+// + zfrag(0, n) (zfrag is additive in its w and n parts).
+__device__ __forceinline__ double* zt_column(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int q, int aa) {
   const int d = __ffs(a.c) - 1;
-  const int q = w / a.r, aa = w - q * a.r;
   const int me = static_cast<int>(sg & (a.c - 1));
   const int64_t t = ((sg >> d) << d) + (q < me ? q : q + 1);
   const int tc = static_cast<int>(t & (a.c - 1));
   const int qt = me < tc ? me : me - 1;
-  lv.zt[(t - lv.tbase) * (int64_t)a.W * NB + zfrag(qt * a.r + aa, n)] = v;
+  return lv.zt + (t - lv.tbase) * (int64_t)a.W * NB + zfrag(qt * a.r + aa, 0);
 }
 
 // ============================ project ========================================
@@ -120,6 +121,13 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
 
   const int cw = warp - 1;            // consumer warp: columns w in [16 cw, 16 cw + 16)
   const int g = lane >> 2, tq = lane & 3;
+  int wq[2], wa[2];                   // the thread's two accumulator columns w = q r + aa
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int w = cw * 16 + mt * 8 + g;
+    wq[mt] = w / a.r;
+    wa[mt] = w - wq[mt] * a.r;
+  }
   double acc[2][8][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -171,13 +179,13 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
       if (complete) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-          const int w = cw * 16 + mt * 8 + g;
+          // n = nt 8 + tq 2 + h  ->  zfrag(0, n) = (nt/2) 64 + tq 16 + h 8 + nt%2
+          double* zc = zt_column(a, lv, sg, wq[mt], wa[mt]) + tq * 16;
 #pragma unroll
           for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int n = nt * 8 + tq * 2 + h;
-              if (n < a.nr) scatter_zd(a, lv, sg, w, n, acc[mt][nt][h]);
+              if (nt * 8 + tq * 2 + h < a.nr) zc[(nt >> 1) * 64 + h * 8 + (nt & 1)] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -207,14 +215,19 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
         if (*flag) {
           __threadfence();
           const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
-          for (int o = tid - 32; o < W * NB; o += ctp) {
-            const int w = o / NB, n = o - w * NB;
+          // thread: rhs n = tt % NB, columns w = tt / NB, + ctp / NB, ... (ctp is a multiple of NB)
+          const int tt = tid - 32, n = tt % NB, wstep = ctp / NB;
+          const int64_t zn = zfrag(0, n);
+          int w = tt / NB, q = w / a.r, aa = w - q * a.r;
+          for (; w < W; w += wstep) {
             double v = 0.0;
             for (int64_t bb = b0; bb <= b1; ++bb) {
               const int sl_b = bb == b0 ? slot0 : 0;
-              v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NB + o);
+              v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NB +
+                              (int64_t)w * NB + n);
             }
-            if (n < a.nr) scatter_zd(a, lv, sg, w, n, v);
+            if (n < a.nr) zt_column(a, lv, sg, q, aa)[zn] = v;
+            for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
           }
           if (cw == 0 && lane == 0) *ticket = 0;
         }
