@@ -31,6 +31,15 @@ namespace {
 constexpr int CT = kConsumerThreads;
 constexpr int NCW = CT / 32;
 
+// Order of an item's stages: levels 1..L, then the dense block (L + 1).  With
+// the peer exchange the levels 1..cross wait for other ranks' flags, so they go
+// last: local levels and the dense block first (overlap).
+__device__ __forceinline__ int level_order(const StreamArgs& a, int li) {
+  if (!a.peer) return li;
+  const int nloc = a.L + 1 - a.cross;
+  return li <= nloc ? li + a.cross : li - nloc;
+}
+
 template <int NR>
 __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_constant__ StreamArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -77,7 +86,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     const int64_t dblk = db + int64_t(NR) * a.xs_e * 8;
     for (int64_t j = j0; j < j1; ++j) {
       const int64_t i0 = j * Re;
-      for (int l = 1; l <= L + 1; ++l) {
+      for (int li = 1; li <= L + 1; ++li) {
+        const int l = level_order(a, li);
         const bool is_d = (l == L + 1);
         if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
         dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
@@ -189,7 +199,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     double acc[NR], acc2[NR];  // two chains: even / odd columns
 #pragma unroll
     for (int kk = 0; kk < NR; ++kk) acc[kk] = acc2[kk] = 0.0;
-    for (int l = 1; l <= L + 1; ++l) {
+    for (int li = 1; li <= L + 1; ++li) {
+      const int l = level_order(a, li);
       const bool is_d = (l == L + 1);
       if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
       dev::mbar_wait(&full[slot], phase);
