@@ -225,6 +225,16 @@ hmat_status hmat_nccl_unique_id(void* out128);
 hmat_status hmat_profile(hmat_t H, int enable);
 hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches);
 
+/* Per-CTA trace (load-balance diagnostics).  hmat_cta_trace(H, 1) allocates a
+ * device buffer; every later project / expand launch on H then records, per CTA
+ * b, [start ns, end ns, SM id] (%globaltimer at the CTA's start and at its last
+ * warp's exit; end is 0 for a CTA that did not run).  hmat_cta_trace(H, 0) frees
+ * it.  hmat_cta_trace_read synchronises H's stream and copies the records of the
+ * LAST launch of `kernel` (0 = project, 1 = expand) into out[3 * b + 0..2] for
+ * b < min(grid, max_ctas, 8192); *n_ctas = that count. */
+hmat_status hmat_cta_trace(hmat_t H, int enable);
+hmat_status hmat_cta_trace_read(hmat_t H, int kernel, int64_t* out, int max_ctas, int* n_ctas);
+
 /* Kernel launches one hmat_matvec(nrhs) performs on this rank. */
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs);
 

@@ -103,5 +103,45 @@ __device__ __forceinline__ double ld_cg(const double* p) {
   return v;
 }
 
+// Per-CTA trace (hmat_cta_trace): [start ns, end ns, SM id] of CTA bid.  The
+// constructor runs after the kernel's __syncthreads(); the destructor runs at
+// every exit of every warp and keeps the latest exit time (buffer zeroed by the
+// host before the launch).
+struct CtaTrace {
+  unsigned long long* tr;
+  __device__ __forceinline__ CtaTrace(unsigned long long* t, int64_t bid) : tr(t ? t + bid * 3 : nullptr) {
+    if (tr && threadIdx.x == 0) {
+      unsigned long long ns;
+      unsigned int sm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      tr[0] = ns;
+      tr[2] = sm;
+    }
+  }
+  __device__ __forceinline__ ~CtaTrace() {
+    if (tr && (threadIdx.x & 31) == 0) {
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      atomicMax(tr + 1, ns);
+    }
+  }
+};
+
+// v + p[0] + p[stride] + ... + p[(n-1) stride], added in index order (so the
+// result is the same every run), with the L2 loads issued 8 at a time: an
+// in-order warp would otherwise wait one full L2 latency per term.
+__device__ __forceinline__ double sum_cg(double v, const double* p, int64_t stride, int64_t n) {
+  for (int64_t i = 0; i < n; i += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = (i + u < n) ? ld_cg(p + (i + u) * stride) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i + u < n) v += t[u];
+  }
+  return v;
+}
+
 }  // namespace dev
 }  // namespace hmat

@@ -127,6 +127,9 @@ struct hmat_s {
   std::vector<void*> opened;  // IPC mappings to close
   int zt_cap = 1;         // rhs width of the z-buffer layout last written (zeroed at create)
   bool prof = false;
+  // per-CTA trace of the last project / expand launch (hmat_cta_trace)
+  unsigned long long* trace = nullptr;
+  int trace_n[2] = {0, 0};
   std::vector<EventPair> ev;
   std::vector<cudaEvent_t> pool;
   double ms[HMAT_NUM_PHASES] = {};
@@ -139,6 +142,7 @@ void release(hmat_s* H) {
   if (!H) return;
   cudaSetDevice(H->device);
   if (H->stream) cudaStreamSynchronize(H->stream);
+  cudaFree(H->trace);
   cudaFree(H->U);
   cudaFree(H->V);
   cudaFree(H->D);
@@ -439,6 +443,8 @@ hmat_status ensure_dt(hmat_s* H) {
   return HMAT_OK;
 }
 
+constexpr int kTraceCap = 8192;  // CTAs recorded per kernel
+
 enum { kPhaseProject = 1, kPhaseExchange = 2, kPhaseExpand = 4, kPhaseAll = 7 };
 
 // y = alpha op(H) x + beta y restricted to the selected parts (the whole path).
@@ -548,14 +554,23 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
-  auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project) -> hmat_status {
+  auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project, int gp,
+                  int ge) -> hmat_status {
     const size_t bytes = exch * sizeof(double);
+    // optional per-CTA trace: zeroed slots, filled by the kernels
+    auto trace = [&](int ph, int grid) -> cudaError_t {
+      if (!H->trace) return cudaSuccess;
+      a.trace = H->trace + (int64_t)ph * kTraceCap * 3;
+      H->trace_n[ph] = grid < kTraceCap ? grid : kTraceCap;
+      return grid <= kTraceCap ? cudaMemsetAsync(a.trace, 0, size_t(grid) * 3 * 8, H->stream) : cudaSuccess;
+    };
     a.exch = int64_t(exch);
     if (phases & kPhaseProject) ++H->epoch;  // peer exchange: a new pass (same count on every rank)
     a.epoch = H->epoch;
     if (phases & kPhaseProject) {
       if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(zex, 0, bytes, H->stream));
       if (has_project && level_mask) {
+        CUDA_TRY(trace(0, gp));
         prof_begin(H, 0, &ep);
         CUDA_TRY(project());
         prof_end(H, &ep);
@@ -570,6 +585,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     if (phases & kPhaseExpand) {
       if (exch_in && exch) CUDA_TRY(cudaMemcpyAsync(zex, exch_in, bytes, cudaMemcpyDeviceToDevice, H->stream));
+      CUDA_TRY(trace(1, ge));
       prof_begin(H, 2, &ep);
       CUDA_TRY(expand());
       prof_end(H, &ep);
@@ -603,7 +619,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       const size_t exch = size_t(p.z_exch_rows) * p.W * hmat::kDmmaNB;
       hmat_status st2 = pass(
           H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, p.dgrid_p, p.dsmem_p, H->stream); },
-          [&] { return hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream); }, p.dgrid_p > 0);
+          [&] { return hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream); }, p.dgrid_p > 0, p.dgrid_p,
+          p.dgrid_e);
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -639,7 +656,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     hmat_status st2 = pass(
         H->zex, exch, [&] { return hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream); },
-        [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0);
+        [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0, ly.grid_p,
+        ly.grid_e);
     if (st2 != HMAT_OK) return st2;
   }
   if (!y_dev && (phases & kPhaseExpand)) {
@@ -795,6 +813,32 @@ hmat_status hmat_peer_connect_local(hmat_t H, const hmat_t* ranks) {
 hmat_status hmat_profile(hmat_t H, int enable) {
   if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
   H->prof = enable != 0;
+  return HMAT_OK;
+}
+
+hmat_status hmat_cta_trace(hmat_t H, int enable) {
+  if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
+  CUDA_TRY(cudaSetDevice(H->device));
+  CUDA_TRY(cudaStreamSynchronize(H->stream));
+  if (enable && !H->trace) {
+    CUDA_TRY(cudaMalloc(&H->trace, size_t(2) * kTraceCap * 3 * sizeof(unsigned long long)));
+  } else if (!enable && H->trace) {
+    cudaFree(H->trace);
+    H->trace = nullptr;
+  }
+  H->trace_n[0] = H->trace_n[1] = 0;
+  return HMAT_OK;
+}
+
+hmat_status hmat_cta_trace_read(hmat_t H, int kernel, int64_t* out, int max_ctas, int* n_ctas) {
+  if (!H || !out || !n_ctas || (kernel != 0 && kernel != 1)) return fail(HMAT_ERR_INVALID, "bad argument");
+  if (!H->trace) return fail(HMAT_ERR_INVALID, "tracing is not enabled (hmat_cta_trace)");
+  CUDA_TRY(cudaSetDevice(H->device));
+  CUDA_TRY(cudaStreamSynchronize(H->stream));
+  const int n = H->trace_n[kernel] < max_ctas ? H->trace_n[kernel] : max_ctas;
+  if (n > 0)
+    CUDA_TRY(cudaMemcpy(out, H->trace + (int64_t)kernel * kTraceCap * 3, size_t(n) * 3 * 8, cudaMemcpyDeviceToHost));
+  *n_ctas = n;
   return HMAT_OK;
 }
 

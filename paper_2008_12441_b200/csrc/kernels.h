@@ -65,6 +65,7 @@ struct StreamArgs {
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
   int64_t exch;              // doubles of this pass's exchange levels
   int cross;                 // levels 1..cross are exchange levels
+  unsigned long long* trace; // optional per-CTA [start ns, end ns, SM id] (hmat_cta_trace)
   int64_t red_off_p;   // byte offsets inside the dynamic shared memory
   int64_t bar_off_p, bar_off_e;
   LevelArgs lv[kMaxLevels + 1];

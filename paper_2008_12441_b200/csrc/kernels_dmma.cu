@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
     dev::fence_mbar_init();
   }
   __syncthreads();
+  const dev::CtaTrace trace_scope(a.trace, bid);
   if (bid >= GL) return;
   const int64_t k0 = SL * bid / GL, k1 = SL * (bid + 1) / GL;
 
@@ -219,13 +220,12 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
           const int tt = tid - 32, n = tt % NB, wstep = ctp / NB;
           const int64_t zn = zfrag(0, n);
           int w = tt / NB, q = w / a.r, aa = w - q * a.r;
+          const int64_t ps = (int64_t)Wp * NB;
+          const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
+          const double* p1 = a.part + (((int64_t)(l - 1) * G + b0 + 1) * 2) * ps;
           for (; w < W; w += wstep) {
-            double v = 0.0;
-            for (int64_t bb = b0; bb <= b1; ++bb) {
-              const int sl_b = bb == b0 ? slot0 : 0;
-              v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NB +
-                              (int64_t)w * NB + n);
-            }
+            const int64_t off = (int64_t)w * NB + n;
+            const double v = dev::sum_cg(dev::ld_cg(p0 + off), p1 + off, 2 * ps, b1 - b0);
             if (n < a.nr) zt_column(a, lv, sg, q, aa)[zn] = v;
             for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
           }
@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_dmma_kernel(const __grid_c
     dev::fence_mbar_init();
   }
   __syncthreads();
+  const dev::CtaTrace trace_scope(a.trace, bid);
 
   if (warp == 0) {
     const uint64_t pol_stream = dev::policy_evict_first();

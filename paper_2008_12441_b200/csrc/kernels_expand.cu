@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     dev::fence_mbar_init();
   }
   __syncthreads();
+  const dev::CtaTrace trace_scope(a.trace, bid);
 
   if (warp == 0) {
     // ---------------- producer (the whole warp: lane e owns dense block e) ----

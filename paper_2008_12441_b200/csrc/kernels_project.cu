@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     dev::fence_mbar_init();
   }
   __syncthreads();
+  const dev::CtaTrace trace_scope(a.trace, bid);
   if (bid >= GL) return;
   // every level is split evenly over the GL CTAs, so each CTA streams the same
   // mix of coarse and fine levels (fine levels flush a node per stage)
@@ -318,14 +319,40 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         dev::named_bar_sync(1, CT);
         if (*flag) {
           __threadfence();
+          // partial i = 0..nb: CTA b0 + i's slot (slot0 for i = 0, slot 0 after);
+          // consecutive CTAs' slot-0 partials are 2 ps doubles apart
           const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
-          for (int o = t; o < W * NR; o += CT) {
+          const int64_t ps = (int64_t)Wp * NR, nb = b1 - b0;
+          const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
+          const double* p1 = a.part + (((int64_t)(l - 1) * G + b0 + 1) * 2) * ps;
+          const int WN = W * NR;
+          // few outputs (W NR < CT): spl threads per output, thread s summing the
+          // partials i = s mod spl in order, then the spl sums in order (smem)
+          const int spl = WN < CT ? CT / WN : 1;
+          if (spl > 1) {
+            if (t < spl * WN) {
+              const int o = t % WN, s = t / WN;
+              const int kk = o / W, col = o - kk * W;
+              const int64_t off = (int64_t)kk * Wp + col;
+              double v = 0.0;
+              if (s == 0) {
+                v = dev::ld_cg(p0 + off);
+                v = dev::sum_cg(v, p1 + (spl - 1) * 2 * ps + off, spl * 2 * ps, nb / spl);
+              } else if (s <= nb) {
+                v = dev::sum_cg(v, p1 + (s - 1) * 2 * ps + off, spl * 2 * ps, (nb - s) / spl + 1);
+              }
+              red[t] = v;
+            }
+            dev::named_bar_sync(1, CT);
+          }
+          for (int o = t; o < WN; o += CT) {
             const int kk = o / W, col = o - kk * W;
             double v = 0.0;
-            for (int64_t bb = b0; bb <= b1; ++bb) {
-              const int sl_b = bb == b0 ? slot0 : 0;
-              v += dev::ld_cg(a.part + (((int64_t)(l - 1) * G + bb) * 2 + sl_b) * (int64_t)Wp * NR +
-                              (int64_t)kk * Wp + col);
+            if (spl > 1) {
+              for (int s = 0; s < spl; ++s) v += red[s * WN + o];
+            } else {
+              const int64_t off = (int64_t)kk * Wp + col;
+              v = dev::sum_cg(dev::ld_cg(p0 + off), p1 + off, 2 * ps, nb);
             }
             if (kk < a.nr) {
               if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);

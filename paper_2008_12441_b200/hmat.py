@@ -32,7 +32,8 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_exchange_size", "hmat_project", "hmat_expand", "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
-           "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local")
+           "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local", "hmat_cta_trace",
+           "hmat_cta_trace_read")
 
 
 class HMatError(RuntimeError):
@@ -83,6 +84,8 @@ _sigs = {
     "hmat_launches_per_matvec": (_i64, [_H, _i]),
     "hmat_plan_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_plan_info_t)]),
     "hmat_peer_export": (_i, [_H, _P]),
+    "hmat_cta_trace": (_i, [_H, _i]),
+    "hmat_cta_trace_read": (_i, [_H, _i, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(ctypes.c_int)]),
     "hmat_peer_import": (_i, [_H, _P]),
     "hmat_peer_connect_local": (_i, [_H, _P]),
 }
@@ -373,3 +376,15 @@ def hmat_peer_connect_local(h, ranks):
     """connect the mailboxes of P handles of this process (rank order)."""
     arr = (ctypes.c_void_p * len(ranks))(*[r.value for r in ranks])
     _check(_lib.hmat_peer_connect_local(h, ctypes.cast(arr, _P)), "hmat_peer_connect_local")
+
+
+def hmat_cta_trace(h, enable=True):
+    _check(_lib.hmat_cta_trace(h, int(bool(enable))), "hmat_cta_trace")
+
+
+def hmat_cta_trace_read(h, kernel, max_ctas=8192):
+    """[(start_ns, end_ns, sm_id)] per CTA of the last project (0) / expand (1) launch."""
+    buf = (ctypes.c_int64 * (3 * max_ctas))()
+    n = ctypes.c_int(0)
+    _check(_lib.hmat_cta_trace_read(h, kernel, buf, max_ctas, ctypes.byref(n)), "hmat_cta_trace_read")
+    return [(buf[3 * b], buf[3 * b + 1], buf[3 * b + 2]) for b in range(n.value)]
