@@ -10,6 +10,7 @@
 #include "hmat.h"
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 
 #include <algorithm>
 #include <cstdint>
@@ -56,6 +57,8 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.smem_budget = env_int("HMAT_SMEM_KB", 200) * 1024;
   o.max_stages_p = env_int("HMAT_MAX_STAGES_P", env_int("HMAT_MAX_STAGES", o.max_stages_p));
   o.max_stages_e = env_int("HMAT_MAX_STAGES_E", env_int("HMAT_MAX_STAGES", o.max_stages_e));
+  o.dmma_kr = env_int("HMAT_DMMA_KR", o.dmma_kr);
+  o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
   return o;
 }
 
@@ -310,6 +313,34 @@ void prof_end(hmat_s* H, EventPair* ep) {
   if (!H->prof) return;
   cudaEventRecord(ep->b, H->stream);
   H->ev.push_back(*ep);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+// A tiled fp64 map of `rank` dims (innermost first), strides in bytes for
+// dims 1..rank-1, zero fill out of bounds, no swizzle.
+hmat_status encode_map(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                       const uint32_t* box) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return fail(HMAT_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bx[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    if (i + 1 < rank) gs[i] = strides[i];
+  }
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), gd, gs, bx, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HMAT_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string(r) + ")");
+  return HMAT_OK;
 }
 
 bool use_dmma(const hmat::Plan& p, int nrhs) {
@@ -597,6 +628,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     hmat_status st = ensure_dmma(H);
     if (st != HMAT_OK) return st;
     a.vp = p.vp;
+    a.dkr = p.dkr;
     a.nstage_p = p.dns_p;
     a.stage_bytes_p = p.dstage_p;
     a.bar_off_p = p.dns_p * p.dstage_p;
@@ -605,10 +637,24 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     a.bar_off_e = p.dns_e * p.dstage_e;
     a.part = H->part_d;
     a.cnt = H->cnt_d;
+    if (p.L > 0) {  // V-role panels [L][N_loc][Wp], box [1][dkr][vp]
+      const uint64_t dims[3] = {uint64_t(p.Wp), uint64_t(n), uint64_t(p.L)};
+      const uint64_t strides[2] = {uint64_t(p.Wp) * 8, uint64_t(p.panel_stride) * 8};
+      const uint32_t box[3] = {uint32_t(p.vp), uint32_t(p.dkr), 1};
+      hmat_status st3 = encode_map(&a.tm_v, 3, a.V, dims, strides, box);
+      if (st3 != HMAT_OK) return st3;
+    }
     for (int c0 = 0; c0 < nrhs; c0 += hmat::kDmmaNB) {
       a.nr = nrhs - c0 < hmat::kDmmaNB ? nrhs - c0 : hmat::kDmmaNB;
       a.x = xd + c0 * ldx;
       a.y = yd + c0 * n;
+      {  // this pass's x columns [nr][N_loc] (ld = ldx), box [64][dkr + 4]
+        const uint64_t dims[2] = {uint64_t(n), uint64_t(a.nr)};
+        const uint64_t strides[1] = {uint64_t(ldx) * 8};
+        const uint32_t box[2] = {uint32_t(p.dkr + 4), uint32_t(hmat::kDmmaNB)};
+        hmat_status st3 = encode_map(&a.tm_x, 2, a.x, dims, strides, box);
+        if (st3 != HMAT_OK) return st3;
+      }
       for (int l = 1; l <= p.L; ++l) {
         hmat::LevelArgs& lv = a.lv[l];
         lv.m = p.m[l];

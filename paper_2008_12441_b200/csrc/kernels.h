@@ -9,6 +9,7 @@
 //            D_k[i,:] . x_k (eq:prod-yuz, eq:prod-ydz), fused over siblings,
 //            levels and the dense leaf blocks so y is written once.
 #pragma once
+#include <cuda.h>  // CUtensorMap (type only; maps are encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -54,6 +55,7 @@ struct StreamArgs {
   int64_t stage_bytes_e, items_e;
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows
+  int dkr;             // DMMA project: V rows per stage (16 or 32)
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
   // CTA pushes this rank's exchange levels into slot `rank` of every rank's
   // mailbox and raises its flag there; expand sums the P slots in rank order
@@ -69,6 +71,13 @@ struct StreamArgs {
   int64_t red_off_p;   // byte offsets inside the dynamic shared memory
   int64_t bar_off_p, bar_off_e;
   LevelArgs lv[kMaxLevels + 1];
+  // DMMA project (tensor TMA, one copy per operand per stage):
+  //   tm_v  3-D map over the V-role panels [L][N_loc][Wp], box [1][dkr][vp]
+  //         (the vp - Wp padding columns are out of bounds: zero-filled);
+  //   tm_x  2-D map over this pass's x columns [nr][N_loc] (ld = ldx), box
+  //         [64][dkr + 4]: the staged x block with the conflict-free pitch.
+  alignas(64) CUtensorMap tm_v;
+  alignas(64) CUtensorMap tm_x;
 };
 
 // Launch one project pass (template NR chosen from args.nr).  grid = plan.grid_p.

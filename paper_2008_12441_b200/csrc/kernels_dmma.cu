@@ -24,12 +24,10 @@ namespace {
 
 constexpr int CT = kConsumerThreads;   // expand: 8 consumer warps
 constexpr int NCW = CT / 32;
-// project: W/16 consumer warps (<= 14), each owning a 16 x NB slab of the
-// W x NB accumulator tile (2 M-tiles x 8 N-tiles, 64 registers), + 1 producer
-// warp: <= 15 warps keeps 4 warps per SM sub-partition at <= 128 registers.
-constexpr int kMaxThreadsP = 32 + 14 * 32;
+// project: 16 warps (4 per SM sub-partition), no producer warp
+constexpr int kDmmaProjWarps = 16;
+constexpr int kMaxThreadsP = kDmmaProjWarps * 32;
 constexpr int NB = kDmmaNB;   // right-hand sides per pass
-constexpr int KR = kDmmaKR;   // project: V rows (the GEMM's k) per stage
 constexpr int RE = kDmmaRE;   // expand: rows per item
 constexpr int KC = kDmmaKC;   // expand: k-columns per stage
 constexpr int XP = kDmmaXP;   // smem pitch of staged X columns (= 4 mod 16)
@@ -63,77 +61,77 @@ __device__ __forceinline__ double* zt_column(const StreamArgs& a, const LevelArg
 }
 
 // ============================ project ========================================
+// KR: V rows (the GEMM's k) per stage; the staged x columns have pitch KR + 4
+// (= 4 mod 16 doubles: conflict-free B-fragment loads).
+// MT = W / 32: the W x NB accumulator tile is split over 16 warps as 4 column
+// groups (MT M-tiles of 8 columns) x 4 rhs groups (2 N-tiles of 8 rhs), so each
+// of the SM's 4 sub-partitions runs exactly 4 warps (a W/16-warp split leaves 3
+// or 4 warps per sub-partition: with W = 224 the tensor pipe then idles 1/8).
+// No producer warp: a stage is two tensor-TMA copies (the KR x VP block of V
+// rows, padding columns out of bounds = zero-filled, and the NB x (KR+4) block
+// of x), issued by the LAST warp to finish reading the slot (smem counter), so
+// all 16 warps compute and each gets 128 registers.
+template <int KR, int MT>
 __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __grid_constant__ StreamArgs a) {
+  constexpr int XPP = KR + 4;
+  constexpr int NCW = kDmmaProjWarps;
+  constexpr int CTP = NCW * 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t G = gridDim.x, bid = blockIdx.x;
   const int W = a.W, Wp = a.Wp, L = a.L;
-  const int ncw = W / 16;                  // consumer warps
-  const int ctp = ncw * 32;
   const int VP = a.vp;                     // smem pitch of V rows (= 4 mod 16)
   const int64_t SL = a.N_loc / KR;
   const int64_t GL = G < SL ? G : SL;
   const int NS = a.nstage_p;
   const int64_t vbytes = (int64_t)KR * VP * 8;
+  const uint32_t stage_tx = static_cast<uint32_t>(vbytes + NB * XPP * 8);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_p);
-  uint64_t* empty = full + NS;
-  volatile int* flag = reinterpret_cast<volatile int*>(empty + NS);
+  int* done = reinterpret_cast<int*>(full + NS);           // readers finished, per slot
+  volatile int* flag = reinterpret_cast<volatile int*>(done + NS);
+  const int64_t k0 = SL * bid / (GL > 0 ? GL : 1), k1 = SL * (bid + 1) / (GL > 0 ? GL : 1);
+  const uint64_t pol_stream = dev::policy_evict_first();
+  const uint64_t pol_keep = dev::policy_evict_last();
+  // the refill cursor (level lr, stage kr): identical in every warp
+  int lr = 0;
+  int64_t kr = k1;
+  auto advance = [&]() {
+    if (++kr < k1) return;
+    for (++lr; lr <= L && !((a.level_mask >> (lr - 1)) & 1ull); ++lr) {
+    }
+    kr = k0;
+  };
+  auto issue = [&](int sl) {  // one thread: the next stage into slot sl
+    dev::mbar_arrive_expect_tx(&full[sl], stage_tx);
+    dev::tma_load_3d(smem + sl * a.stage_bytes_p, &a.tm_v, 0, static_cast<int>(kr * KR), lr - 1, &full[sl],
+                     pol_stream);
+    dev::tma_load_2d(smem + sl * a.stage_bytes_p + vbytes, &a.tm_x, static_cast<int>(kr * KR), 0, &full[sl],
+                     pol_keep);
+  };
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       dev::mbar_init(&full[i], 1);
-      dev::mbar_init(&empty[i], ncw);
+      done[i] = 0;
     }
     dev::fence_mbar_init();
   }
   __syncthreads();
   const dev::CtaTrace trace_scope(a.trace, bid);
   if (bid >= GL) return;
-  const int64_t k0 = SL * bid / GL, k1 = SL * (bid + 1) / GL;
-
-  if (warp == 0) {
-    // producer: the whole warp issues the row / column copies of a stage
-    const uint64_t pol_stream = dev::policy_evict_first();
-    const uint64_t pol_keep = dev::policy_evict_last();
-    int slot = 0;
-    uint32_t phase = 0;
-    const uint32_t total = static_cast<uint32_t>(KR * Wp * 8 + a.nr * KR * 8);
-    for (int l = 1; l <= L; ++l) {
-      if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
-      const double* Vl = a.V + (l - 1) * a.panel_stride;
-      for (int64_t k = k0; k < k1; ++k) {
-        dev::mbar_wait(&empty[slot], phase ^ 1);
-        const int64_t i0 = k * KR;
-        unsigned char* st = smem + slot * a.stage_bytes_p;
-        if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
-        __syncwarp();
-        for (int rr = lane; rr < KR; rr += 32)
-          dev::bulk_g2s(st + rr * VP * 8, Vl + (i0 + rr) * Wp, Wp * 8, &full[slot], pol_stream);
-        for (int n = lane; n < a.nr; n += 32)
-          dev::bulk_g2s(st + vbytes + n * XP * 8, a.x + n * a.ldx + i0, KR * 8, &full[slot], pol_keep);
-        if (++slot == NS) {
-          slot = 0;
-          phase ^= 1;
-        }
-      }
-    }
-    return;
+  advance();  // first stage
+  for (int i = 0; i < NS && lr <= L; ++i) {
+    if (tid == 0) issue(i);
+    advance();
   }
 
-  const int cw = warp - 1;            // consumer warp: columns w in [16 cw, 16 cw + 16)
+  const int mg = warp & 3, ng = warp >> 2;  // columns [mg 8 MT, (mg+1) 8 MT), rhs [16 ng, 16 ng + 16)
   const int g = lane >> 2, tq = lane & 3;
-  int wq[2], wa[2];                   // the thread's two accumulator columns w = q r + aa
+  double acc[MT][2][2];
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
-    const int w = cw * 16 + mt * 8 + g;
-    wq[mt] = w / a.r;
-    wa[mt] = w - wq[mt] * a.r;
-  }
-  double acc[2][8][2];
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   int slot = 0;
   uint32_t phase = 0;
@@ -145,22 +143,35 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
     const int64_t sg0 = a.row0 / lv.m;
     for (int64_t k = k0; k < k1; ++k) {
       dev::mbar_wait(&full[slot], phase);
-      const double* Vs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p);
-      const double* Xs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p + vbytes);
+      const double* Vs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p) + mg * 8 * MT + g;
+      const double* Xs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p + vbytes) +
+                         (ng * 16 + g) * XPP + tq;
 #pragma unroll
       for (int ks = 0; ks < KR / 4; ++ks) {
-        double av[2], bv[8];
+        double av[MT], bv[2];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) av[mt] = Vs[(ks * 4 + tq) * VP + cw * 16 + mt * 8 + g];  // A = V^T
+        for (int mt = 0; mt < MT; ++mt) av[mt] = Vs[(ks * 4 + tq) * VP + mt * 8];  // A = V^T
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) bv[nt] = Xs[(nt * 8 + g) * XP + ks * 4 + tq];          // B = X
+        for (int nt = 0; nt < 2; ++nt) bv[nt] = Xs[nt * 8 * XPP + ks * 4];          // B = X
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 8; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+          for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
       }
+      // release the slot: the last of the 16 warps refills it with the stage
+      // NS ahead (its smem reads are complete: their values fed the DMMAs)
       __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      if (lane == 0) {
+        const int prev = atomicAdd(&done[slot], 1);
+        if (prev == NCW - 1) {
+          done[slot] = 0;
+          if (lr <= L) {
+            dev::fence_proxy_async_smem();
+            issue(slot);
+          }
+        }
+      }
+      if (lr <= L) advance();
       if (++slot == NS) {
         slot = 0;
         phase ^= 1;
@@ -179,14 +190,17 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
       const int64_t sg = sg0 + this_sl;
       if (complete) {
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          // n = nt 8 + tq 2 + h  ->  zfrag(0, n) = (nt/2) 64 + tq 16 + h 8 + nt%2
-          double* zc = zt_column(a, lv, sg, wq[mt], wa[mt]) + tq * 16;
+        for (int mt = 0; mt < MT; ++mt) {
+          // column w = q r + aa; rhs n = 16 ng + 8 nt + 2 tq + h  ->
+          // zfrag(0, n) = 64 ng + 16 tq + 8 h + nt
+          const int w = (mg * MT + mt) * 8 + g;
+          const int q = w / a.r;
+          double* zc = zt_column(a, lv, sg, q, w - q * a.r) + ng * 64 + tq * 16;
 #pragma unroll
-          for (int nt = 0; nt < 8; ++nt)
+          for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (nt * 8 + tq * 2 + h < a.nr) zc[(nt >> 1) * 64 + h * 8 + (nt & 1)] = acc[mt][nt][h];
+              if (ng * 16 + nt * 8 + tq * 2 + h < a.nr) zc[h * 8 + nt] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -194,32 +208,32 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
         const int myslot = sa <= k0 ? 0 : 1;
         double* pp = a.part + (((int64_t)(l - 1) * G + bid) * 2 + myslot) * (int64_t)Wp * NB;
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int w = cw * 16 + mt * 8 + g;
+        for (int mt = 0; mt < MT; ++mt) {
+          const int w = (mg * MT + mt) * 8 + g;
 #pragma unroll
-          for (int nt = 0; nt < 8; ++nt)
+          for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              pp[(int64_t)w * NB + nt * 8 + tq * 2 + h] = acc[mt][nt][h];
+              pp[(int64_t)w * NB + ng * 16 + nt * 8 + tq * 2 + h] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
         __threadfence();
-        dev::named_bar_sync(1, ctp);
+        dev::named_bar_sync(1, CTP);
         const int64_t b0 = owner_of(sa, SL, GL), b1 = owner_of(sb - 1, SL, GL);
         int* ticket = a.cnt + (int64_t)(l - 1) * G + b1;
-        if (cw == 0 && lane == 0) {
+        if (tid == 0) {
           const int prev = atomicAdd(ticket, 1);
           *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
         }
-        dev::named_bar_sync(1, ctp);
+        dev::named_bar_sync(1, CTP);
         if (*flag) {
           __threadfence();
           const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
-          // thread: rhs n = tt % NB, columns w = tt / NB, + ctp / NB, ... (ctp is a multiple of NB)
-          const int tt = tid - 32, n = tt % NB, wstep = ctp / NB;
+          // thread: rhs n = tid % NB, columns w = tid / NB, + CTP / NB, ... (CTP is a multiple of NB)
+          const int n = tid % NB, wstep = CTP / NB;
           const int64_t zn = zfrag(0, n);
-          int w = tt / NB, q = w / a.r, aa = w - q * a.r;
+          int w = tid / NB, q = w / a.r, aa = w - q * a.r;
           const int64_t ps = (int64_t)Wp * NB;
           const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
           const double* p1 = a.part + (((int64_t)(l - 1) * G + b0 + 1) * 2) * ps;
@@ -229,9 +243,9 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
             if (n < a.nr) zt_column(a, lv, sg, q, aa)[zn] = v;
             for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
           }
-          if (cw == 0 && lane == 0) *ticket = 0;
+          if (tid == 0) *ticket = 0;
         }
-        dev::named_bar_sync(1, ctp);
+        dev::named_bar_sync(1, CTP);
       }
     }
   }
@@ -375,11 +389,40 @@ __global__ void __launch_bounds__(kThreads, 2) expand_dmma_kernel(const __grid_c
   }
 }
 
+template <int KR>
+cudaError_t launch_project_kr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  switch (a.W / 32) {
+    case 1: project_dmma_kernel<KR, 1><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+    case 2: project_dmma_kernel<KR, 2><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+    case 3: project_dmma_kernel<KR, 3><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+    case 4: project_dmma_kernel<KR, 4><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+    case 5: project_dmma_kernel<KR, 5><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+    case 6: project_dmma_kernel<KR, 6><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+    default: project_dmma_kernel<KR, 7><<<grid, kMaxThreadsP, smem, s>>>(a); break;
+  }
+  return cudaGetLastError();
+}
+
+template <int KR>
+cudaError_t configure_project_kr(int64_t smem) {
+  cudaError_t e = cudaSuccess;
+  auto set = [&](auto kern) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  };
+  set(project_dmma_kernel<KR, 1>);
+  set(project_dmma_kernel<KR, 2>);
+  set(project_dmma_kernel<KR, 3>);
+  set(project_dmma_kernel<KR, 4>);
+  set(project_dmma_kernel<KR, 5>);
+  set(project_dmma_kernel<KR, 6>);
+  set(project_dmma_kernel<KR, 7>);
+  return e;
+}
+
 }  // namespace
 
 cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  project_dmma_kernel<<<grid, 32 + (a.W / 16) * 32, smem, s>>>(a);
-  return cudaGetLastError();
+  return a.dkr == 16 ? launch_project_kr<16>(a, grid, smem, s) : launch_project_kr<32>(a, grid, smem, s);
 }
 
 cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
@@ -388,8 +431,9 @@ cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cuda
 }
 
 cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e) {
-  cudaError_t e = cudaFuncSetAttribute(project_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+  cudaError_t e = configure_project_kr<16>(smem_p);
   if (e != cudaSuccess) return e;
+  if ((e = configure_project_kr<32>(smem_p)) != cudaSuccess) return e;
   return cudaFuncSetAttribute(expand_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
 }
 
