@@ -643,6 +643,15 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       const uint32_t box[3] = {uint32_t(p.vp), uint32_t(p.dkr), 1};
       hmat_status st3 = encode_map(&a.tm_v, 3, a.V, dims, strides, box);
       if (st3 != HMAT_OK) return st3;
+      const uint32_t ubox[3] = {uint32_t(hmat::kDmmaKC + 4), uint32_t(hmat::kDmmaRE), 1};
+      if ((st3 = encode_map(&a.tm_u, 3, a.U, dims, strides, ubox)) != HMAT_OK) return st3;
+    }
+    {  // D-role panel [N_loc][Dp], box [64][KC+4]
+      const uint64_t dims[2] = {uint64_t(p.Dp), uint64_t(n)};
+      const uint64_t strides[1] = {uint64_t(p.Dp) * 8};
+      const uint32_t box[2] = {uint32_t(hmat::kDmmaKC + 4), uint32_t(hmat::kDmmaRE)};
+      hmat_status st3 = encode_map(&a.tm_d, 2, a.D, dims, strides, box);
+      if (st3 != HMAT_OK) return st3;
     }
     for (int c0 = 0; c0 < nrhs; c0 += hmat::kDmmaNB) {
       a.nr = nrhs - c0 < hmat::kDmmaNB ? nrhs - c0 : hmat::kDmmaNB;
@@ -654,6 +663,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         const uint32_t box[2] = {uint32_t(p.dkr + 4), uint32_t(hmat::kDmmaNB)};
         hmat_status st3 = encode_map(&a.tm_x, 2, a.x, dims, strides, box);
         if (st3 != HMAT_OK) return st3;
+        const uint32_t xbox[2] = {uint32_t(hmat::kDmmaKC + 4), uint32_t(hmat::kDmmaNB)};
+        if ((st3 = encode_map(&a.tm_xe, 2, a.x, dims, strides, xbox)) != HMAT_OK) return st3;
       }
       for (int l = 1; l <= p.L; ++l) {
         hmat::LevelArgs& lv = a.lv[l];

@@ -78,6 +78,12 @@ struct StreamArgs {
   //         [64][dkr + 4]: the staged x block with the conflict-free pitch.
   alignas(64) CUtensorMap tm_v;
   alignas(64) CUtensorMap tm_x;
+  // DMMA expand: tm_u 3-D over the U-role panels, box [1][64][KC+4]; tm_d 2-D
+  // over the D-role panel [N_loc][Dp], box [64][KC+4]; tm_xe like tm_x with box
+  // [64][KC+4]
+  alignas(64) CUtensorMap tm_u;
+  alignas(64) CUtensorMap tm_d;
+  alignas(64) CUtensorMap tm_xe;
 };
 
 // Launch one project pass (template NR chosen from args.nr).  grid = plan.grid_p.

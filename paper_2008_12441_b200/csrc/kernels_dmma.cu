@@ -28,6 +28,7 @@ constexpr int NCW = CT / 32;
 constexpr int kDmmaProjWarps = 16;
 constexpr int kMaxThreadsP = kDmmaProjWarps * 32;
 constexpr int NB = kDmmaNB;   // right-hand sides per pass
+constexpr int kThreadsE = 256;  // expand: 8 warps, no producer warp
 constexpr int RE = kDmmaRE;   // expand: rows per item
 constexpr int KC = kDmmaKC;   // expand: k-columns per stage
 constexpr int XP = kDmmaXP;   // smem pitch of staged X columns (= 4 mod 16)
@@ -253,77 +254,78 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
 
 // ============================ expand =========================================
 // CTA item: RE = 64 rows x NB rhs; warp owns rows [wm*16, wm*16+16) (2 M-tiles)
-// and rhs [wn*32, wn*32+32) (4 N-tiles).
-__global__ void __launch_bounds__(kThreads, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
+// and rhs [wn*32, wn*32+32) (4 N-tiles).  A stage is one k-chunk of KC
+// columns: the RE x (KC+4) box of U_l (tm_u) + the chunk of the target's
+// fragment-major Zt (one bulk copy), or of D (tm_d) + the (KC+4) x NB box of
+// the leaf's x (tm_xe); the extra 4 columns / rows give the conflict-free
+// pitch AP = XP = KC + 4 and are never read.  As in project, no producer warp:
+// the last of the 8 warps to finish a slot refills it.
+__global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
+  constexpr int NCW = kThreadsE / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t G = gridDim.x, bid = blockIdx.x;
-  const int W = a.W, Wp = a.Wp, Dp = a.Dp, b = a.b, L = a.L;
+  const int W = a.W, b = a.b, L = a.L;
   const int64_t items = a.N_loc / RE;
   const int64_t j0 = items * bid / G, j1 = items * (bid + 1) / G;
   const int NS = a.nstage_e;
   const int kcw = W / KC, kcd = b / KC;      // k-chunks per level / for the dense block
   const int64_t abytes = (int64_t)RE * AP * 8;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
-  uint64_t* empty = full + NS;
+  int* done = reinterpret_cast<int*>(full + NS);
+  const uint64_t pol_stream = dev::policy_evict_first();
+  const uint64_t pol_keep = dev::policy_evict_last();
+  auto level_on = [&](int l) -> bool {
+    return l == L + 1 ? a.dense != 0 : ((a.level_mask >> (l - 1)) & 1ull) != 0;
+  };
+  // refill cursor (item jr, level lr in 1..L+1 (L+1 = dense), chunk kcr): identical in every warp
+  int64_t jr = j0;
+  int lr = 1, kcr = 0;
+  bool any = false;
+  for (int l = 1; l <= L + 1; ++l) any = any || level_on(l);
+  if (!any) jr = j1;
+  while (jr < j1 && !level_on(lr)) ++lr;
+  auto advance = [&]() {
+    if (++kcr < (lr == L + 1 ? kcd : kcw)) return;
+    kcr = 0;
+    do {
+      if (++lr > L + 1) {
+        lr = 1;
+        ++jr;
+      }
+    } while (!level_on(lr));
+  };
+  auto issue = [&](int sl) {  // one thread: stage (jr, lr, kcr) into slot sl
+    unsigned char* st = smem + sl * a.stage_bytes_e;
+    const int i0 = static_cast<int>(jr * RE);
+    if (lr == L + 1) {
+      dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes + NB * XP * 8));
+      dev::tma_load_2d(st, &a.tm_d, kcr * KC, i0, &full[sl], pol_stream);
+      dev::tma_load_2d(st + abytes, &a.tm_xe, (i0 / b) * b + kcr * KC, 0, &full[sl], pol_keep);
+    } else {
+      const LevelArgs& lv = a.lv[lr];
+      const double* zt = lv.zt + ((a.row0 + i0) / lv.m - lv.tbase) * (int64_t)W * NB;
+      dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes + KC * NB * 8));
+      dev::tma_load_3d(st, &a.tm_u, kcr * KC, i0, lr - 1, &full[sl], pol_stream);
+      dev::bulk_g2s(st + abytes, zt + (int64_t)kcr * KC * NB, KC * NB * 8, &full[sl], pol_keep);
+    }
+  };
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       dev::mbar_init(&full[i], 1);
-      dev::mbar_init(&empty[i], NCW);
+      done[i] = 0;
     }
     dev::fence_mbar_init();
   }
   __syncthreads();
   const dev::CtaTrace trace_scope(a.trace, bid);
-
-  if (warp == 0) {
-    const uint64_t pol_stream = dev::policy_evict_first();
-    const uint64_t pol_keep = dev::policy_evict_last();
-    int slot = 0;
-    uint32_t phase = 0;
-    for (int64_t j = j0; j < j1; ++j) {
-      const int64_t i0 = j * RE;
-      const int64_t leaf0 = (i0 / b) * b;
-      for (int l = 1; l <= L + 1; ++l) {
-        const bool is_d = (l == L + 1);
-        if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
-        const int nkc = is_d ? kcd : kcw;
-        const double* src = is_d ? a.D : a.U + (l - 1) * a.panel_stride;
-        const int pitch = is_d ? Dp : Wp;
-        const double* zt = nullptr;
-        if (!is_d) {
-          const LevelArgs& lv = a.lv[l];
-          zt = lv.zt + ((a.row0 + i0) / lv.m - lv.tbase) * (int64_t)W * NB;
-        }
-        for (int kc = 0; kc < nkc; ++kc) {
-          dev::mbar_wait(&empty[slot], phase ^ 1);
-          unsigned char* st = smem + slot * a.stage_bytes_e;
-          const uint32_t bbytes = is_d ? static_cast<uint32_t>(a.nr * KC * 8) : static_cast<uint32_t>(KC * NB * 8);
-          if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], RE * KC * 8 + bbytes);
-          __syncwarp();
-          for (int rr = lane; rr < RE; rr += 32)
-            dev::bulk_g2s(st + rr * AP * 8, src + (i0 + rr) * pitch + kc * KC, KC * 8, &full[slot], pol_stream);
-          if (!is_d) {
-            if (lane == 0)
-              dev::bulk_g2s(st + abytes, zt + (int64_t)kc * KC * NB, KC * NB * 8, &full[slot], pol_keep);
-          } else {
-            for (int n = lane; n < a.nr; n += 32)
-              dev::bulk_g2s(st + abytes + n * XP * 8, a.x + n * a.ldx + leaf0 + kc * KC, KC * 8, &full[slot],
-                            pol_keep);
-          }
-          if (++slot == NS) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-    return;
+  for (int i = 0; i < NS && jr < j1; ++i) {
+    if (tid == 0) issue(i);
+    advance();
   }
 
-  const int cw = warp - 1;
-  const int wm = cw & 3, wn = cw >> 2;
+  const int wm = warp & 3, wn = warp >> 2;
   const int g = lane >> 2, tq = lane & 3;
   int slot = 0;
   uint32_t phase = 0;
@@ -364,8 +366,19 @@ __global__ void __launch_bounds__(kThreads, 2) expand_dmma_kernel(const __grid_c
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
         }
+        // release: the last of the NCW warps refills the slot NS stages ahead
         __syncwarp();
-        if (lane == 0) dev::mbar_arrive(&empty[slot]);
+        if (lane == 0) {
+          const int prev = atomicAdd(&done[slot], 1);
+          if (prev == NCW - 1) {
+            done[slot] = 0;
+            if (jr < j1) {
+              dev::fence_proxy_async_smem();
+              issue(slot);
+            }
+          }
+        }
+        if (jr < j1) advance();
         if (++slot == NS) {
           slot = 0;
           phase ^= 1;
@@ -426,7 +439,7 @@ cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cud
 }
 
 cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  expand_dmma_kernel<<<grid, kThreads, smem, s>>>(a);
+  expand_dmma_kernel<<<grid, kThreadsE, smem, s>>>(a);
   return cudaGetLastError();
 }
 
