@@ -582,6 +582,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.mb = H->mb;
   a.done = H->done;
   a.zex_base = H->zex;
+  a.dbg = env_int("HMAT_DEBUG_SKIP", 0);
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
       dev::mbar_wait(&full[slot], phase);
       const unsigned char* st = smem + slot * a.stage_bytes_e;
-      if (active) {
+      if (active && !(a.dbg & 2)) {
         if (!is_d) {
           const double2* U2 = reinterpret_cast<const double2*>(st) + ri * NP;
           const double* Zs = reinterpret_cast<const double*>(st + Re * Wp * 8);

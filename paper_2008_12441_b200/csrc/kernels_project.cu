@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       int xo[NR];
 #pragma unroll
       for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
-      if (active) {
+      if (active && !(a.dbg & 1)) {
 #pragma unroll 4
         for (int row = rho; row < Rp; row += RG) {
           double xv[NR];
