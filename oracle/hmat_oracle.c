@@ -631,3 +631,45 @@ void oracle_std_matvec(int d, int L, int b, int r, const double* const* U, const
   visit_root_std(d, L, std_mv_cb, &mv);
   free(mv.z);
 }
+
+/* y = H^T x over the standard-admissibility blocks (GEMV "T"):
+ * H^T = sum over the blocks (t, s) of Def 2.4 of (H_ts)^T placed at (s, t), so
+ * every block contributes its transpose: dense y_s += D_ts^T x_t; low rank
+ * w = U_ts^T x_t, y_s += V_ts w. */
+static void std_mv_t_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_mv_t* mv = (std_mv_t*)ctx;
+  const int64_t N = mv->N;
+  for (int k = 0; k < mv->nrhs; ++k) {
+    const double* xk = mv->x + (int64_t)k * N;
+    double* yk = mv->y + (int64_t)k * N;
+    if (kind == 0) { /* y_s += D_ts^T x_t */
+      const int e = std_neighbour_index(mv->d, t, s, level);
+      for (int i = 0; i < mv->b; ++i)
+        for (int j = 0; j < mv->b; ++j)
+          yk[s * mv->b + j] += mv->Dn[(t * mv->b + i) * (mv->ND * mv->b) + e * mv->b + j] * xk[t * mv->b + i];
+      continue;
+    }
+    const int64_t m = N / ipow(1 << mv->d, level);
+    const int qt = oracle_std_slot(mv->d, level, t, s), qs = oracle_std_slot(mv->d, level, s, t);
+    const int W = mv->M * mv->r;
+    const double* Ul = mv->U[level - 1];
+    const double* Vl = mv->V[level - 1];
+    for (int a = 0; a < mv->r; ++a) mv->z[a] = 0.0;
+    for (int64_t i = 0; i < m; ++i)   /* w = U_ts^T x_t */
+      for (int a = 0; a < mv->r; ++a) mv->z[a] += Ul[(t * m + i) * W + qt * mv->r + a] * xk[t * m + i];
+    for (int64_t j = 0; j < m; ++j)   /* y_s += V_ts w */
+      for (int a = 0; a < mv->r; ++a) yk[s * m + j] += Vl[(s * m + j) * W + qs * mv->r + a] * mv->z[a];
+  }
+}
+
+void oracle_std_matvec_t(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                         const double* Dn, const double* x, double* y, int nrhs) {
+  std_mv_t mv;
+  mv.d = d; mv.b = b; mv.r = r; mv.M = oracle_std_slots(d); mv.ND = (int)ipow(3, d); mv.nrhs = nrhs;
+  mv.N = (int64_t)b * ipow(1 << d, L);
+  mv.U = U; mv.V = V; mv.Dn = Dn; mv.x = x; mv.y = y;
+  mv.z = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  for (int64_t i = 0; i < mv.N * nrhs; ++i) y[i] = 0.0;
+  visit_root_std(d, L, std_mv_t_cb, &mv);
+  free(mv.z);
+}

@@ -219,6 +219,8 @@ def _std_lib():
         lib.oracle_std_matvec.restype = None
         lib.oracle_std_matvec.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_void_p,
                                                                ctypes.c_void_p, ctypes.c_int]
+        lib.oracle_std_matvec_t.restype = None
+        lib.oracle_std_matvec_t.argtypes = lib.oracle_std_matvec.argtypes
         lib._std_ready = True
     return lib
 
@@ -260,3 +262,9 @@ def std_assemble(d: int, L: int, b: int, r: int, U, V, Dn) -> np.ndarray:
 def std_matvec(d: int, L: int, b: int, r: int, U, V, Dn, x) -> np.ndarray:
     _std_lib()
     return _mv(_load().oracle_std_matvec, d, L, b, r, U, V, Dn, x)
+
+
+def std_matvec_t(d: int, L: int, b: int, r: int, U, V, Dn, x) -> np.ndarray:
+    """y = H^T x by the transposed standard-admissibility block loop."""
+    _std_lib()
+    return _mv(_load().oracle_std_matvec_t, d, L, b, r, U, V, Dn, x)

@@ -139,3 +139,27 @@ def test_std_slot_enumeration_is_a_bijection():
                 used.append(q)
                 assert oracle.std_slot(d, level, s, t) >= 0
         assert len(set(used)) == len(used) and max(used) < 27
+
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 4, 2, 2), (2, 3, 1, 2), (2, 3, 2, 1), (3, 2, 1, 2), (2, 2, 3, 1)])
+def test_std_transposed_loop_equals_brute_force(d, L, b, r):
+    """H^T x by the transposed block loop = A^T x of the assembled matrix (the
+    GEMV "T" of PAPER.md:961-969 written out); near-field blocks are not
+    symmetric (D_ts != D_st^T), so a loop that forgot to transpose them fails."""
+    U, V, Dn = std_panels(d, L, b, r, 20 * d + L)
+    A = oracle.std_assemble(d, L, b, r, U, V, Dn)
+    x = np.random.default_rng(5).standard_normal((len(Dn), 2))
+    assert rel(oracle.std_matvec_t(d, L, b, r, U, V, Dn, x), A.T @ x) < 1e-13
+    assert rel(A.T, A) > 1e-3  # the fixture is not symmetric
+
+
+def test_std_adjoint_identity():
+    """<y', H x> = <H^T y', x> between the forward and the transposed loops."""
+    d, L, b, r = 2, 4, 4, 3
+    U, V, Dn = std_panels(d, L, b, r, 91)
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal(len(Dn))
+    yp = rng.standard_normal(len(Dn))
+    lhs = yp @ oracle.std_matvec(d, L, b, r, U, V, Dn, x)
+    rhs = oracle.std_matvec_t(d, L, b, r, U, V, Dn, yp) @ x
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
