@@ -145,8 +145,11 @@ hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double
  *   by "slot q" (U target-major, V source-major).
  *   Dn: N x (3^dim leaf_size): row i of leaf t, columns [e b, (e+1) b) = row
  *   i - t b of D_{t, t+eps}, e = sum_i (eps_i + 1) 3^i (ignored if outside).
- * One GPU only (HMAT_ERR_UNSUPPORTED for nranks > 1), no transposed product;
- * M rank <= 1024.  hmat_panel(kind 2, level e) returns dense panel e. */
+ * hmat_gemv(trans = 1) applies H^T (the interaction relation is symmetric, so
+ * U and V swap roles; the near-field panels of H^T, (D_{t+eps,t})^T, are built
+ * once on the first transposed call: 3^dim N leaf_size more doubles).
+ * One GPU only (HMAT_ERR_UNSUPPORTED for nranks > 1); M rank <= 1024.
+ * hmat_panel(kind 2, level e) returns dense panel e. */
 hmat_status hmat_create_standard(int depth, int dim, int leaf_size, int rank, const double* const* U,
                                  const double* const* V, const double* Dn, const hmat_dist_t* dist, hmat_t* out);
 hmat_status hmat_create_standard_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist,

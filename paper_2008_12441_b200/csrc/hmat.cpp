@@ -467,10 +467,14 @@ namespace {
 hmat_status ensure_dt(hmat_s* H) {
   if (H->Dt) return HMAT_OK;
   const hmat::Plan& p = H->plan;
-  const size_t bytes = size_t(p.N_loc) * p.Dp * sizeof(double);
+  const size_t bytes = size_t(p.nd) * p.d_stride * sizeof(double);
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->Dt), bytes));
   CUDA_TRY(cudaMemsetAsync(H->Dt, 0, bytes, H->stream));
-  CUDA_TRY(hmat::launch_transpose_leaf_blocks(H->D, H->Dt, p.N_loc / p.b, p.b, p.Dp, H->stream));
+  if (p.adm)  // standard admissibility: nd near-field panels (one GPU: N_loc = N)
+    CUDA_TRY(hmat::launch_transpose_near_field(H->D, H->Dt, p.N_loc / p.b, p.d, p.L, p.b, p.Dp, p.d_stride, p.nd,
+                                               H->stream));
+  else
+    CUDA_TRY(hmat::launch_transpose_leaf_blocks(H->D, H->Dt, p.N_loc / p.b, p.b, p.Dp, H->stream));
   return HMAT_OK;
 }
 
@@ -491,7 +495,6 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     return fail(HMAT_ERR_INVALID, "x and y alias");
   const hmat::Plan& p = H->plan;
   CUDA_TRY(cudaSetDevice(H->device));
-  if (trans && p.adm) return fail(HMAT_ERR_UNSUPPORTED, "transposed product with standard admissibility");
   if (trans) {
     hmat_status st = ensure_dt(H);
     if (st != HMAT_OK) return st;

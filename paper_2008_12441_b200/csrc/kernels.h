@@ -98,6 +98,9 @@ cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e);
 // Standard admissibility: upload the interaction-list slot tables (plan.h
 // std_slot_tables) to the project kernel's constant memory (per device).
 cudaError_t init_std_tables(const int16_t* code, const int16_t* slot);
+// Standard admissibility: the transposed near-field panels of H^T (one-time helper).
+cudaError_t launch_transpose_near_field(const double* D, double* Dt, int64_t n_leaves, int d, int L, int b, int Dp,
+                                        int64_t d_stride, int nd, cudaStream_t s);
 // D^T of every dense leaf block (for H^T x); one-time helper.
 cudaError_t launch_transpose_leaf_blocks(const double* D, double* Dt, int64_t n_leaves, int b, int Dp, cudaStream_t s);
 // Opt the kernels into large dynamic shared memory (once per device).

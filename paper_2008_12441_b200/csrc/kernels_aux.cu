@@ -4,6 +4,7 @@
 // PAPER.md:961-969): H^T has the same block structure with U and V exchanged
 // and every dense leaf block transposed, so the expand kernel runs unchanged on
 // (V, U, D^T).
+#include "geometry.cuh"
 #include "kernels.h"
 
 namespace hmat {
@@ -20,7 +21,40 @@ __global__ void transpose_leaf_blocks_kernel(const double* __restrict__ D, doubl
   }
 }
 
+// Standard admissibility: H^T's near-field block (t, t + eps) is
+// (H_{t+eps, t})^T, and H_{t+eps, t} sits in the rows of leaf t + eps, panel
+// e' = nd - 1 - e (the offset -eps).  So panel e of D^T, row i of leaf t,
+// column j = panel e' of D, row j of leaf t + eps, column i (zero when t + eps
+// lies outside the domain).
+__global__ void transpose_near_field_kernel(const double* __restrict__ D, double* __restrict__ Dt,
+                                            int64_t n_leaves, int d, int L, int b, int Dp, int64_t d_stride,
+                                            int nd) {
+  const int64_t total = n_leaves * nd * b * b;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = o / ((int64_t)nd * b * b);
+    int rem = static_cast<int>(o - t * nd * b * b);
+    const int e = rem / (b * b);
+    rem -= e * b * b;
+    const int i = rem / b, j = rem - i * b;
+    int x[3];
+    geo::morton_decode(d, t, L, x);
+    if (!((geo::near_mask(d, x, 1 << L) >> e) & 1u)) continue;
+    const int64_t s = geo::neighbour(d, x, e, L);
+    Dt[e * d_stride + (t * b + i) * Dp + j] = D[(nd - 1 - e) * d_stride + (s * b + j) * Dp + i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_transpose_near_field(const double* D, double* Dt, int64_t n_leaves, int d, int L, int b, int Dp,
+                                        int64_t d_stride, int nd, cudaStream_t s) {
+  const int64_t total = n_leaves * nd * b * b;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 32) grid = 148 * 32;
+  if (grid < 1) grid = 1;
+  transpose_near_field_kernel<<<static_cast<int>(grid), 256, 0, s>>>(D, Dt, n_leaves, d, L, b, Dp, d_stride, nd);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_transpose_leaf_blocks(const double* D, double* Dt, int64_t n_leaves, int b, int Dp,
                                          cudaStream_t s) {

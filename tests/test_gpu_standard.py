@@ -57,17 +57,58 @@ def test_standard_near_field_only_and_far_field_only():
     assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, np.zeros_like(Dn), x))
 
 
-def test_standard_unsupported_cases():
-    cfg = HConfig("stdu", d=2, L=3, b=4, r=2, adm=1, seed=778)
+def run_std_gemv(cfg, nrhs, trans, alpha, beta, y0=None):
+    U, V, Dn = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
+    try:
+        xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        yd = torch.from_numpy(np.ascontiguousarray(y0.T)).cuda() if y0 is not None else torch.full_like(xd, float("nan"))
+        hm.hmat_gemv(h, trans, alpha, xd.t(), beta, yd.t())
+        torch.cuda.synchronize()
+        return yd.t().cpu().numpy(), (U, V, Dn, x)
+    finally:
+        hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("cfg", STD, ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_standard_transposed_parity(cfg, nrhs):
+    """H^T x (GEMV "T", PAPER.md:961-969) against the oracle's transposed loop;
+    beta = 0 must not read the NaN-filled y."""
+    y, (U, V, Dn, x) = run_std_gemv(cfg, nrhs, 1, 1.0, 0.0)
+    assert_parity(y, oracle.std_matvec_t(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
+
+
+def test_standard_gemv_alpha_beta_both_ops():
+    cfg = HConfig("stdab", d=2, L=4, b=8, r=3, adm=1, seed=781)
+    y0 = np.random.default_rng(8).standard_normal((cfg.N, 2))
+    for trans, fn in ((0, oracle.std_matvec), (1, oracle.std_matvec_t)):
+        y, (U, V, Dn, x) = run_std_gemv(cfg, 2, trans, -0.75, 1.5, y0)
+        assert_parity(y, -0.75 * fn(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x) + 1.5 * y0)
+
+
+def test_standard_adjoint_identity_gpu():
+    """<y', H x> = <H^T y', x> with both products on the GPU (3D, b = 64)."""
+    cfg = HConfig("stdadj", d=3, L=2, b=64, r=2, adm=1, seed=782)
     U, V, Dn = hgen.inputs(cfg)
     h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
     try:
-        x = torch.zeros(cfg.N, dtype=torch.float64, device="cuda")
-        with pytest.raises(hm.HMatError) as ei:
-            hm.hmat_gemv(h, 1, 1.0, x, 0.0, torch.empty_like(x))
-        assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
+        g = torch.Generator(device="cpu").manual_seed(9)
+        x = torch.randn(cfg.N, dtype=torch.float64, generator=g).cuda()
+        yp = torch.randn(cfg.N, dtype=torch.float64, generator=g).cuda()
+        hx, hty = torch.empty_like(x), torch.empty_like(x)
+        hm.hmat_gemv(h, 0, 1.0, x, 0.0, hx)
+        hm.hmat_gemv(h, 1, 1.0, yp, 0.0, hty)
+        torch.cuda.synchronize()
+        lhs, rhs = float(yp @ hx), float(hty @ x)
+        assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
     finally:
         hm.hmat_destroy(h)
+
+
+def test_standard_unsupported_cases():
+    cfg = HConfig("stdu", d=2, L=3, b=4, r=2, adm=1, seed=778)
     with pytest.raises(hm.HMatError) as ei:
         hm.hmat_create_standard_uninit(cfg.L, cfg.d, cfg.b, cfg.r,
                                        hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
