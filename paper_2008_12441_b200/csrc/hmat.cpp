@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "std_exchange.h"
 #include "kernels.h"
 #include "plan.h"
 
@@ -117,6 +118,12 @@ struct hmat_s {
   double* part_d = nullptr;
   int* cnt_d = nullptr;
   double* Dt = nullptr;  // D^T, built on the first transposed product
+  // standard admissibility with P > 1: the packed cross-rank exchange (std_exchange.h)
+  hmat::StdExchange* sx = nullptr;
+  int32_t* xent_d = nullptr;
+  int64_t* unpack_d = nullptr;
+  int64_t* pack_d = nullptr;
+  int32_t* halo_of_d = nullptr;
   bool external = false;  // P > 1 with a caller-provided exchange (split-phase API)
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): this rank's mailbox
   // [2 parities][P slots][mb] doubles + [2][P] uint64 flags, and the device
@@ -160,6 +167,11 @@ void release(hmat_s* H) {
   cudaFree(H->part_d);
   cudaFree(H->cnt_d);
   cudaFree(H->Dt);
+  cudaFree(H->xent_d);
+  cudaFree(H->unpack_d);
+  cudaFree(H->pack_d);
+  cudaFree(H->halo_of_d);
+  delete H->sx;
   for (void* q : H->opened) cudaIpcCloseMemHandle(q);
   cudaFree(H->mbox);
   cudaFree(H->mbox_dev);
@@ -235,6 +247,11 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
     H->own_stream = true;
   }
   const hmat::Plan& p = H->plan;
+  if (p.adm && p.P > 1) {  // the standard-admissibility exchange plan (host enumeration)
+    H->sx = new hmat::StdExchange;
+    std::string m = hmat::std_exchange_build(p, H->sx);
+    if (!m.empty()) return bail(plan_status(m));
+  }
   auto alloc = [&](void** ptr, size_t bytes, const char* what) -> cudaError_t {
     if (bytes == 0) bytes = 256;
     cudaError_t e = cudaMalloc(ptr, bytes);
@@ -248,7 +265,9 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = alloc(reinterpret_cast<void**>(&H->V), panels, "V")) ||
       (e = alloc(reinterpret_cast<void**>(&H->D), size_t(p.nd) * p.d_stride * sizeof(double), "D")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zloc), size_t(p.z_local_rows) * zrow, "z")) ||
-      (e = alloc(reinterpret_cast<void**>(&H->zex), size_t(p.z_exch_rows) * zrow, "exchange")) ||
+      (e = alloc(reinterpret_cast<void**>(&H->zex),
+                 H->sx ? size_t(H->sx->doubles(hmat::kMaxNR, p.r)) * sizeof(double) : size_t(p.z_exch_rows) * zrow,
+                 "exchange")) ||
       (e = alloc(reinterpret_cast<void**>(&H->part), size_t(p.grid_p_max) * p.L * 2 * zrow, "partials")) ||
       (e = alloc(reinterpret_cast<void**>(&H->cnt), size_t(p.grid_p_max) * p.L * sizeof(int) + 256, "tickets"))) {
     std::string what = g_err;
@@ -275,6 +294,19 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
         (e = cudaMemset(H->mbox, 0, mbytes)) || (e = cudaMemset(H->mbox_dev, 0, size_t(p.P) * sizeof(double*))) ||
         (e = cudaMemset(H->done, 0, 256)))
       return bail(cuda_fail(e, "allocating the peer mailbox"));
+  }
+  if (H->sx) {  // device copies of the exchange tables
+    const hmat::StdExchange& X = *H->sx;
+    auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+      cudaError_t e2 = cudaMalloc(dst, bytes ? bytes : 256);
+      if (e2 == cudaSuccess && bytes) e2 = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+      return e2;
+    };
+    if ((e = up(reinterpret_cast<void**>(&H->xent_d), X.src_entry.data(), X.src_entry.size() * sizeof(int32_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->unpack_d), X.unpack.data(), X.unpack.size() * sizeof(int64_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->pack_d), X.pack.data(), X.pack.size() * sizeof(int64_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->halo_of_d), X.halo_of.data(), X.halo_of.size() * sizeof(int32_t))))
+      return bail(cuda_fail(e, "uploading the standard-admissibility exchange tables"));
   }
   if (p.adm) {  // interaction-list slot tables for the project kernel's scatter
     static int16_t code[3][8][hmat::kStdMaxSlots], slot[3][8][hmat::kStdMaxCodes];
@@ -495,6 +527,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     return fail(HMAT_ERR_INVALID, "x and y alias");
   const hmat::Plan& p = H->plan;
   CUDA_TRY(cudaSetDevice(H->device));
+  if (trans && p.adm && p.P > 1)
+    return fail(HMAT_ERR_UNSUPPORTED, "transposed product with standard admissibility and nranks > 1");
   if (trans) {
     hmat_status st = ensure_dt(H);
     if (st != HMAT_OK) return st;
@@ -589,8 +623,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
-  auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project, int gp,
-                  int ge) -> hmat_status {
+  auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project, int gp, int ge,
+                  auto&& before_project, auto&& before_expand) -> hmat_status {
     const size_t bytes = exch * sizeof(double);
     // optional per-CTA trace: zeroed slots, filled by the kernels
     auto trace = [&](int ph, int grid) -> cudaError_t {
@@ -604,6 +638,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     a.epoch = H->epoch;
     if (phases & kPhaseProject) {
       if (p.P > 1 && exch) CUDA_TRY(cudaMemsetAsync(zex, 0, bytes, H->stream));
+      CUDA_TRY(before_project());
       if (has_project && level_mask) {
         CUDA_TRY(trace(0, gp));
         prof_begin(H, 0, &ep);
@@ -620,6 +655,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     if (phases & kPhaseExpand) {
       if (exch_in && exch) CUDA_TRY(cudaMemcpyAsync(zex, exch_in, bytes, cudaMemcpyDeviceToDevice, H->stream));
+      CUDA_TRY(before_expand());
       CUDA_TRY(trace(1, ge));
       prof_begin(H, 2, &ep);
       CUDA_TRY(expand());
@@ -681,7 +717,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       hmat_status st2 = pass(
           H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, p.dgrid_p, p.dsmem_p, H->stream); },
           [&] { return hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream); }, p.dgrid_p > 0, p.dgrid_p,
-          p.dgrid_e);
+          p.dgrid_e, [] { return cudaSuccess; }, [] { return cudaSuccess; });
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -706,7 +742,26 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       lv.zt = (l <= p.cross ? H->zex : H->zloc) + p.zt_off[l] * p.Wp * cap;
       lv.tbase = p.zt_tbase[l];
     }
-    const size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
+    size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
+    if (H->sx) {  // standard admissibility, P > 1: the packed cross-rank buffer
+      const hmat::StdExchange& X = *H->sx;
+      exch = size_t(X.doubles(cap, p.r));
+      a.xchg = H->zex;
+      a.halo_of = H->halo_of_d;
+      a.halo_base = X.halo_base(cap, p.r);
+      a.bpad = X.bpad;
+      for (int l = 2; l <= p.L; ++l) a.lv[l].xent = H->xent_d + X.src_off[l];
+    }
+    auto pack_x = [&]() -> cudaError_t {
+      if (!H->sx) return cudaSuccess;
+      return hmat::launch_std_pack_x(H->zex + a.halo_base, a.x, ldx, H->pack_d, int64_t(H->sx->pack.size() / 2), cap,
+                                     nr, p.b, a.bpad, H->stream);
+    };
+    auto unpack_z = [&]() -> cudaError_t {
+      if (!H->sx) return cudaSuccess;
+      return hmat::launch_std_unpack_z(H->zloc, H->zex, H->unpack_d, int64_t(H->sx->unpack.size() / 2), cap, nr,
+                                       p.Wp, p.r, H->stream);
+    };
     // Standard admissibility: slots whose partner lies outside the domain are
     // never written and must read as zero; after a pass with another rhs width
     // the buffer holds values at other positions, so clear it on a layout change.
@@ -718,7 +773,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     hmat_status st2 = pass(
         H->zex, exch, [&] { return hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream); },
         [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0, ly.grid_p,
-        ly.grid_e);
+        ly.grid_e, pack_x, unpack_z);
     if (st2 != HMAT_OK) return st2;
   }
   if (!y_dev && (phases & kPhaseExpand)) {
@@ -755,7 +810,7 @@ hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count) {
     *count = p.P > 1 ? p.z_exch_rows * p.W * hmat::kDmmaNB : 0;
   } else {
     if (nrhs > p.max_nr) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
-    *count = p.P > 1 ? p.z_exch_rows * p.Wp * nr_cap(nrhs) : 0;
+    *count = p.P > 1 ? (H->sx ? H->sx->doubles(nr_cap(nrhs), p.r) : p.z_exch_rows * p.Wp * nr_cap(nrhs)) : 0;
   }
   return HMAT_OK;
 }

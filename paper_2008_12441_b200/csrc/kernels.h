@@ -22,7 +22,10 @@ struct LevelArgs {
   int64_t m;         // rows per node at this level (global)
   int64_t seg_rows;  // rows of one local segment = min(m, N_loc)
   double* zt;        // Zt_l (target-major, pitch Wp*NR), already offset for this pass
-  int64_t tbase;     // global index of zt's first target
+  int64_t tbase;     // global index of zt's first target (= first local source node)
+  // standard admissibility, P > 1 (std_exchange.h): [source node - tbase][M] ->
+  // entry of the packed cross-rank buffer, or -1 for a pair inside this rank
+  const int32_t* xent;
 };
 
 struct StreamArgs {
@@ -68,6 +71,13 @@ struct StreamArgs {
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
   int64_t exch;              // doubles of this pass's exchange levels
   int cross;                 // levels 1..cross are exchange levels
+  // standard admissibility, P > 1 (std_exchange.h): the packed cross-rank buffer
+  // [E][NR][r] z entries then [Hn][NR][bpad] halo x; halo_of[local leaf][nd] =
+  // halo index of near-field neighbour e (-1: local or outside the domain)
+  double* xchg;
+  const int32_t* halo_of;
+  int64_t halo_base;         // doubles before the halo x region (E r NR)
+  int bpad;
   unsigned long long* trace; // optional per-CTA [start ns, end ns, SM id] (hmat_cta_trace)
   int64_t red_off_p;   // byte offsets inside the dynamic shared memory
   int64_t bar_off_p, bar_off_e;
@@ -98,6 +108,13 @@ cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e);
 // Standard admissibility: upload the interaction-list slot tables (plan.h
 // std_slot_tables) to the project kernel's constant memory (per device).
 cudaError_t init_std_tables(const int16_t* code, const int16_t* slot);
+// Standard admissibility, P > 1 (std_exchange.h): copy this rank's boundary-leaf
+// x into the packed buffer (before project) / the received z entries of its
+// targets into its Zt rows (after the exchange, before expand).
+cudaError_t launch_std_pack_x(double* xchg_halo, const double* x, int64_t ldx, const int64_t* pack, int64_t n_pack,
+                              int cap, int nr, int b, int bpad, cudaStream_t s);
+cudaError_t launch_std_unpack_z(double* zt, const double* xchg, const int64_t* unpack, int64_t n_unpack, int cap,
+                                int nr, int Wp, int r, cudaStream_t s);
 // Standard admissibility: the transposed near-field panels of H^T (one-time helper).
 cudaError_t launch_transpose_near_field(const double* D, double* Dt, int64_t n_leaves, int d, int L, int b, int Dp,
                                         int64_t d_stride, int nd, cudaStream_t s);

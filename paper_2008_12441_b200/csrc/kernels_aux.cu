@@ -44,7 +44,56 @@ __global__ void transpose_near_field_kernel(const double* __restrict__ D, double
   }
 }
 
+// x of this rank's boundary leaves -> halo entries [h][kk][bpad] of the packed buffer
+__global__ void std_pack_x_kernel(double* __restrict__ halo, const double* __restrict__ x, int64_t ldx,
+                                  const int64_t* __restrict__ pack, int64_t n_pack, int cap, int nr, int b,
+                                  int bpad) {
+  const int64_t total = n_pack * nr * b;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = o / ((int64_t)nr * b);
+    const int rem = static_cast<int>(o - it * nr * b);
+    const int kk = rem / b, j = rem - kk * b;
+    const int64_t h = pack[2 * it], leaf = pack[2 * it + 1];
+    halo[(h * cap + kk) * bpad + j] = x[kk * ldx + leaf * b + j];
+  }
+}
+
+// received z entries [e][kk][r] -> Zt rows [row][kk][Wp] at columns q r .. q r + r - 1
+__global__ void std_unpack_z_kernel(double* __restrict__ zt, const double* __restrict__ xchg,
+                                    const int64_t* __restrict__ unpack, int64_t n_unpack, int cap, int nr, int Wp,
+                                    int r) {
+  const int64_t total = n_unpack * nr * r;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = o / ((int64_t)nr * r);
+    const int rem = static_cast<int>(o - it * nr * r);
+    const int kk = rem / r, aa = rem - kk * r;
+    const int64_t e = unpack[2 * it], rq = unpack[2 * it + 1];
+    const int64_t row = rq >> 8;
+    const int q = static_cast<int>(rq & 255);
+    zt[(row * cap + kk) * Wp + q * r + aa] = xchg[(e * cap + kk) * r + aa];
+  }
+}
+
+int grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  return static_cast<int>(g < 1 ? 1 : g > 148 * 16 ? 148 * 16 : g);
+}
+
 }  // namespace
+
+cudaError_t launch_std_pack_x(double* halo, const double* x, int64_t ldx, const int64_t* pack, int64_t n_pack, int cap,
+                              int nr, int b, int bpad, cudaStream_t s) {
+  if (n_pack == 0) return cudaSuccess;
+  std_pack_x_kernel<<<grid_for(n_pack * nr * b), 256, 0, s>>>(halo, x, ldx, pack, n_pack, cap, nr, b, bpad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_std_unpack_z(double* zt, const double* xchg, const int64_t* unpack, int64_t n_unpack, int cap,
+                                int nr, int Wp, int r, cudaStream_t s) {
+  if (n_unpack == 0) return cudaSuccess;
+  std_unpack_z_kernel<<<grid_for(n_unpack * nr * r), 256, 0, s>>>(zt, xchg, unpack, n_unpack, cap, nr, Wp, r);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_transpose_near_field(const double* D, double* Dt, int64_t n_leaves, int d, int L, int b, int Dp,
                                         int64_t d_stride, int nd, cudaStream_t s) {

@@ -73,12 +73,19 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     // dense source of lane e: the leaf itself (weak) or its near-field
     // neighbour e (standard; -1 when it lies outside the domain)
     int64_t leaf_idx = (a.row0 + leaf0) / b;
+    // (P > 1, standard: a neighbour on another rank -- local row offset < 0 or
+    // >= N_loc -- is read from the packed buffer's halo entry, whose rhs
+    // columns are bpad apart).  kNone: this lane has no dense block.
+    constexpr int64_t kNone = INT64_MIN;
+    int hsrc = -1;
     auto dense_source = [&]() -> int64_t {
-      if (!a.adm) return lane == 0 ? leaf0 : -1;
-      if (lane >= a.nd) return -1;
+      hsrc = -1;
+      if (!a.adm) return lane == 0 ? leaf0 : kNone;
+      if (lane >= a.nd) return kNone;
       int lx[3];
       geo::morton_decode(a.d, leaf_idx, L, lx);
-      if (!((geo::near_mask(a.d, lx, 1 << L) >> lane) & 1u)) return -1;
+      if (!((geo::near_mask(a.d, lx, 1 << L) >> lane) & 1u)) return kNone;
+      if (a.halo_of) hsrc = a.halo_of[(leaf_idx - a.row0 / b) * a.nd + lane];
       return geo::neighbour(a.d, lx, lane, L) * b - a.row0;
     };
     int64_t src = dense_source();
@@ -134,12 +141,12 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           uint32_t mine = 0;
           int64_t lo[NR];
           uint32_t xb[NR];
-          if (src >= 0) {
+          if (src != kNone) {
             mine = db;
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk) {
               if (kk < a.nr) {
-                const int64_t start = kk * a.ldx + src;
+                const int64_t start = hsrc >= 0 ? ((int64_t)hsrc * NR + kk) * a.bpad : kk * a.ldx + src;
                 lo[kk] = start & ~int64_t(1);
                 xb[kk] = static_cast<uint32_t>((((start + b + 1) & ~int64_t(1)) - lo[kk]) * 8);
                 mine += xb[kk];
@@ -149,12 +156,14 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           const uint32_t total = __reduce_add_sync(0xffffffffu, mine);
           if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
           __syncwarp();
-          if (src >= 0) {
+          if (src != kNone) {
             unsigned char* se = st + lane * dblk;
             dev::bulk_g2s(se, a.D + lane * a.d_stride + i0 * Dp, db, &full[slot], pol_stream);
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk)
-              if (kk < a.nr) dev::bulk_g2s(se + db + kk * a.xs_e * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
+              if (kk < a.nr)
+                dev::bulk_g2s(se + db + kk * a.xs_e * 8, (hsrc >= 0 ? a.xchg + a.halo_base : a.x) + lo[kk], xb[kk],
+                              &full[slot], pol_keep);
           }
         }
         if (++slot == NS) {
@@ -240,9 +249,12 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             const double2* D2 = reinterpret_cast<const double2*>(se) + ri * NPD;
             const double* xs = reinterpret_cast<const double*>(se + Re * Dp * 8);
             const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
+            // halo segments start 16-byte aligned (bpad even): no parity offset
+            const bool halo = a.halo_of && a.halo_of[(leaf_idx - a.row0 / b) * a.nd + e] >= 0;
             int xo[NR];
 #pragma unroll
-            for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + src0) & 1);
+            for (int kk = 0; kk < NR; ++kk)
+              xo[kk] = kk * a.xs_e + (halo ? 0 : static_cast<int>((kk * a.ldx + src0) & 1));
             int jj = rotD;
             for (int n = 0; n < njD; ++n) {
               const int cp = p + tpr * jj;

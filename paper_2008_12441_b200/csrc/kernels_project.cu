@@ -62,6 +62,13 @@ __device__ __forceinline__ void scatter_z_std(const StreamArgs& a, const LevelAr
   const int e = code >> d, sigma = code & (c - 1);
   const int64_t pt = nbr[e];
   if (pt < 0) return;  // the interaction partner lies outside the domain
+  if (lv.xent) {       // P > 1: a cross-rank pair goes to the packed buffer
+    const int32_t ent = lv.xent[(sg - lv.tbase) * (a.W / a.r) + q];
+    if (ent >= 0) {
+      a.xchg[((int64_t)ent * NR + kk) * a.r + aa] = v;
+      return;
+    }
+  }
   const int64_t t = pt * c + sigma;
   const int nd = d == 1 ? 3 : d == 2 ? 9 : 27;
   const int qt = c_std_slot[d - 1][sigma][(nd - 1 - e) * c + tau];  // eps -> -eps, sigma <-> tau

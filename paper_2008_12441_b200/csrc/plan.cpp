@@ -99,7 +99,8 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   if (P > leaves) return "nranks must not exceed the number of leaves 2^(dim*depth)";
   if (shard < 0 || shard >= P) return "rank id out of range [0, nranks)";
   if (p.W > 4 * kConsumerThreads) return "unsupported: slots * rank must be <= 1024";
-  if (p.adm != 0 && P > 1) return "unsupported: standard admissibility with nranks > 1";
+  if (p.adm != 0 && P > 1 && opt.peer)
+    return "unsupported: standard admissibility with the in-kernel peer exchange (use NCCL or the split-phase API)";
   p.P = P;
   p.rank = shard;
   p.N_loc = N / P;
@@ -111,9 +112,12 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
 
   // Levels whose parent spans more than one shard need the exchange
   // (Steps 2-4): c^{l-1} < P.
+  // (Standard admissibility: no exchange levels; its cross-rank pairs travel in
+  // the packed buffer of std_exchange.h and every level keeps local Zt rows,
+  // one row for a node that spans ranks.)
   p.cross = 0;
   int64_t cpow = 1;  // c^{l-1}
-  for (int l = 1; l <= depth; ++l) {
+  for (int l = 1; l <= depth && p.adm == 0; ++l) {
     if (cpow < P) p.cross = l;
     cpow *= p.c;
   }
@@ -128,7 +132,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     } else {
       p.zt_off[l] = off_loc;
       p.zt_tbase[l] = p.row0 / p.m[l];
-      p.zt_count[l] = p.N_loc / p.m[l];
+      p.zt_count[l] = std::max<int64_t>(1, p.N_loc / p.m[l]);
       off_loc += p.zt_count[l];
     }
     if (l < depth) cpow *= p.c;

@@ -167,3 +167,76 @@ def test_peer_exchange_needs_connection():
         assert len(hm.hmat_peer_export(h)) == 64
     finally:
         hm.hmat_destroy(h)
+
+
+# ---- standard admissibility with P > 1 -------------------------------
+# Cross-rank interaction pairs exist at every level along the slice boundaries and
+# the near field of a boundary leaf reaches other ranks' x: both travel in the
+# packed buffer of csrc/std_exchange.h (summed over ranks here).
+
+def sharded_std_matvec(cfg, P, nrhs):
+    hs, xs = [], []
+    for g in range(P):
+        r0, r1 = g * cfg.N // P, (g + 1) * cfg.N // P
+        U, V, Dn = hgen.inputs(cfg, r0, r1)
+        d = hm._dist(nranks=P, rank=g, device=0, external_exchange=True)
+        hs.append(hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn, d))
+        x = hgen.xblock(cfg, nrhs=nrhs, row_begin=r0, row_end=r1)
+        xs.append(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())
+    try:
+        cnt = hm.hmat_exchange_size(hs[0], nrhs)
+        assert all(hm.hmat_exchange_size(h, nrhs) == cnt for h in hs)
+        ex = [torch.zeros(max(cnt, 1), dtype=torch.float64, device="cuda") for _ in range(P)]
+        for g in range(P):
+            hm.hmat_project(hs[g], xs[g].t(), ex[g], nrhs)
+        torch.cuda.synchronize()
+        total = torch.stack(ex).sum(dim=0)
+        ys = []
+        for rep in range(2):  # twice: the buffers are re-zeroed / re-packed per pass
+            ys = []
+            for g in range(P):
+                y = torch.full_like(xs[g], float("nan"))
+                hm.hmat_expand(hs[g], xs[g].t(), total, y.t(), nrhs)
+                ys.append(y)
+        torch.cuda.synchronize()
+        return torch.cat(ys, dim=1).t().cpu().numpy(), cnt
+    finally:
+        for h in hs:
+            hm.hmat_destroy(h)
+
+
+STD_CASES = [
+    (HConfig("s2d", d=2, L=4, b=8, r=3, adm=1, seed=311), 2, 1),
+    (HConfig("s2d", d=2, L=4, b=8, r=3, adm=1, seed=311), 4, 2),
+    (HConfig("s2d", d=2, L=4, b=8, r=3, adm=1, seed=311), 8, 1),
+    (HConfig("s2d", d=2, L=4, b=8, r=3, adm=1, seed=311), 16, 3),
+    (HConfig("s1d", d=1, L=6, b=4, r=2, adm=1, seed=312), 8, 1),    # 1D: nodes spanning ranks at levels 2, 3
+    (HConfig("s1d", d=1, L=6, b=4, r=2, adm=1, seed=312), 32, 2),
+    (HConfig("s3d", d=3, L=3, b=4, r=1, adm=1, seed=313), 8, 1),
+    (HConfig("s3d", d=3, L=3, b=4, r=1, adm=1, seed=313), 64, 1),   # one level-2 node per rank
+    (HConfig("sodd", d=2, L=3, b=7, r=2, adm=1, seed=314), 4, 1),   # odd leaf: halo x parity
+    (HConfig("s64", d=2, L=5, b=64, r=8, adm=1, seed=315), 8, 1),
+]
+
+
+@pytest.mark.parametrize("cfg,P,nrhs", STD_CASES, ids=lambda v: getattr(v, "name", str(v)))
+def test_standard_sharded_split_phase_matches_oracle(cfg, P, nrhs):
+    y, cnt = sharded_std_matvec(cfg, P, nrhs)
+    U, V, Dn = hgen.inputs(cfg)
+    ref = oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, hgen.xblock(cfg, nrhs=nrhs))
+    assert_parity(y, ref)
+    assert cnt > 0
+
+
+def test_standard_sharded_transpose_unsupported():
+    cfg = HConfig("s2t", d=2, L=3, b=4, r=2, adm=1, seed=316)
+    U, V, Dn = hgen.inputs(cfg, 0, cfg.N // 2)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn,
+                                hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
+    try:
+        x = torch.zeros(cfg.N // 2, dtype=torch.float64, device="cuda")
+        with pytest.raises(hm.HMatError) as ei:
+            hm.hmat_gemv(h, 1, 1.0, x, 0.0, torch.empty_like(x))
+        assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
+    finally:
+        hm.hmat_destroy(h)

@@ -108,10 +108,11 @@ def test_standard_adjoint_identity_gpu():
 
 
 def test_standard_unsupported_cases():
+    """The in-kernel peer exchange is weak-admissibility only."""
     cfg = HConfig("stdu", d=2, L=3, b=4, r=2, adm=1, seed=778)
     with pytest.raises(hm.HMatError) as ei:
         hm.hmat_create_standard_uninit(cfg.L, cfg.d, cfg.b, cfg.r,
-                                       hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
+                                       hm._dist(nranks=2, rank=0, device=0, exchange=hm.HMAT_EXCHANGE_PEER))
     assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
 
 
