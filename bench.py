@@ -289,7 +289,9 @@ def run_ours(args):
         nid = obj[0]
     create = hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit
     t_setup = time.perf_counter()
-    exchange = args.exchange if world > 1 else "none"
+    # the in-kernel peer exchange serves the single-rhs weak path; the standard
+    # structure and the many-rhs tensor-core path exchange through NCCL
+    exchange = ("nccl" if (cfg.adm or nrhs >= 16) else args.exchange) if world > 1 else "none"
     h = None
     if exchange == "peer":
         # mailboxes connected once through CUDA IPC handles (hmat_peer_export/_import)

@@ -260,6 +260,38 @@ typedef struct {
 hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
                             hmat_plan_info_t* info);
 
+/* Standard admissibility with nranks > 1: the packed cross-rank exchange of
+ * one rank (csrc/std_exchange.h), computed on the host exactly as
+ * hmat_create_standard does, for tests without a GPU.  One pass of `cap`
+ * right-hand sides exchanges the doubles
+ *   [E entries][cap][rank]  z_{t,s} = V_{t,s}^T x_s of every interaction pair
+ *                           (levels 2..depth) whose target and source are not
+ *                           inside one rank, numbered by (level, target in
+ *                           Morton order, slot of the target's list);
+ *   [Hn halo leaves][cap][bpad]  x of every leaf whose near field reaches
+ *                           another rank, in Morton order,
+ * the second part starting at E rank cap rounded up to even; every rank writes
+ * what it owns, zeros elsewhere, and the buffer is summed over the ranks.
+ * Tables of THIS rank (filled when the caller's array is non-NULL and its
+ * capacity is large enough; the n_* fields always receive the lengths):
+ *   src_entry  [node - first local node][M] per level l at src_off[l]: entry of
+ *              (local source node, slot of its list), -1 for a pair inside the rank;
+ *   unpack     pairs {entry, Zt row * 256 + slot}: entries of this rank's targets,
+ *              Zt row = zt_row_offset[l] + target - first local node of level l;
+ *   pack       pairs {halo index, local leaf}: this rank's leaves others need;
+ *   halo_of    [local leaf][3^dim]: halo index of near-field neighbour e, or -1. */
+typedef struct {
+  int64_t E, Hn;
+  int bpad, M;
+  int64_t src_off[64], zt_row_offset[64];
+  int32_t* src_entry; int64_t src_entry_cap, n_src_entry;
+  int64_t* unpack;    int64_t unpack_cap, n_unpack;
+  int64_t* pack;      int64_t pack_cap, n_pack;
+  int32_t* halo_of;   int64_t halo_of_cap, n_halo_of;
+} hmat_std_exchange_t;
+hmat_status hmat_std_exchange_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
+                                    hmat_std_exchange_t* q);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1015,4 +1015,36 @@ hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nra
   return HMAT_OK;
 }
 
+hmat_status hmat_std_exchange_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
+                                    hmat_std_exchange_t* q) {
+  if (!q) return fail(HMAT_ERR_INVALID, "q is NULL");
+  hmat::PlanOptions opt = options_from_env(148);
+  opt.adm = 1;
+  hmat::Plan p;
+  std::string msg = hmat::plan_build(depth, dim, leaf_size, rank, nranks, rank_id, opt, &p);
+  if (!msg.empty()) return plan_status(msg);
+  hmat::StdExchange X;
+  if (nranks > 1) {
+    msg = hmat::std_exchange_build(p, &X);
+    if (!msg.empty()) return plan_status(msg);
+  }
+  auto give = [](const auto& v, auto* dst, int64_t cap, int64_t* n) {
+    *n = int64_t(v.size());
+    if (dst && cap >= *n) std::copy(v.begin(), v.end(), dst);
+  };
+  q->E = X.E;
+  q->Hn = X.Hn;
+  q->bpad = X.bpad;
+  q->M = p.M;
+  for (int l = 0; l <= depth && l < 64; ++l) {
+    q->src_off[l] = X.src_off[l];
+    q->zt_row_offset[l] = p.zt_off[l];
+  }
+  give(X.src_entry, q->src_entry, q->src_entry_cap, &q->n_src_entry);
+  give(X.unpack, q->unpack, q->unpack_cap, &q->n_unpack);
+  give(X.pack, q->pack, q->pack_cap, &q->n_pack);
+  give(X.halo_of, q->halo_of, q->halo_of_cap, &q->n_halo_of);
+  return HMAT_OK;
+}
+
 }  // extern "C"

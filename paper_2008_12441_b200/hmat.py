@@ -33,7 +33,16 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
            "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local", "hmat_cta_trace",
-           "hmat_cta_trace_read")
+           "hmat_cta_trace_read", "hmat_std_exchange_query")
+
+
+class hmat_std_exchange_t(ctypes.Structure):
+    _fields_ = [("E", ctypes.c_int64), ("Hn", ctypes.c_int64), ("bpad", ctypes.c_int), ("M", ctypes.c_int),
+                ("src_off", ctypes.c_int64 * 64), ("zt_row_offset", ctypes.c_int64 * 64),
+                ("src_entry", ctypes.c_void_p), ("src_entry_cap", ctypes.c_int64), ("n_src_entry", ctypes.c_int64),
+                ("unpack", ctypes.c_void_p), ("unpack_cap", ctypes.c_int64), ("n_unpack", ctypes.c_int64),
+                ("pack", ctypes.c_void_p), ("pack_cap", ctypes.c_int64), ("n_pack", ctypes.c_int64),
+                ("halo_of", ctypes.c_void_p), ("halo_of_cap", ctypes.c_int64), ("n_halo_of", ctypes.c_int64)]
 
 
 class HMatError(RuntimeError):
@@ -83,6 +92,7 @@ _sigs = {
     "hmat_profile_read": (_i, [_H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
     "hmat_launches_per_matvec": (_i64, [_H, _i]),
     "hmat_plan_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_plan_info_t)]),
+    "hmat_std_exchange_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_std_exchange_t)]),
     "hmat_peer_export": (_i, [_H, _P]),
     "hmat_cta_trace": (_i, [_H, _i]),
     "hmat_cta_trace_read": (_i, [_H, _i, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(ctypes.c_int)]),
@@ -322,6 +332,29 @@ def hmat_plan_query(depth, dim, leaf_size, rank, nranks=1, rank_id=0) -> hmat_pl
     _check(_lib.hmat_plan_query(depth, dim, leaf_size, rank, nranks, rank_id, ctypes.byref(info)),
            "hmat_plan_query")
     return info
+
+
+def hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id) -> dict:
+    """The packed cross-rank exchange of one rank of a standard-admissibility
+    operator (include/hmat.h): counts, offsets and this rank's tables (numpy)."""
+    import numpy as np
+    q = hmat_std_exchange_t()
+    _check(_lib.hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id, ctypes.byref(q)),
+           "hmat_std_exchange_query")
+    src = np.zeros(max(1, q.n_src_entry), dtype=np.int32)
+    unp = np.zeros(max(1, 2 * (q.n_unpack // 2)), dtype=np.int64)
+    pk = np.zeros(max(1, q.n_pack), dtype=np.int64)
+    ho = np.zeros(max(1, q.n_halo_of), dtype=np.int32)
+    q.src_entry, q.src_entry_cap = src.ctypes.data, src.size
+    q.unpack, q.unpack_cap = unp.ctypes.data, unp.size
+    q.pack, q.pack_cap = pk.ctypes.data, pk.size
+    q.halo_of, q.halo_of_cap = ho.ctypes.data, ho.size
+    _check(_lib.hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id, ctypes.byref(q)),
+           "hmat_std_exchange_query")
+    return {"E": q.E, "Hn": q.Hn, "bpad": q.bpad, "M": q.M, "src_off": list(q.src_off)[:depth + 1],
+            "zt_row_offset": list(q.zt_row_offset)[:depth + 1], "src_entry": src[:q.n_src_entry],
+            "unpack": unp[:q.n_unpack].reshape(-1, 2), "pack": pk[:q.n_pack].reshape(-1, 2),
+            "halo_of": ho[:q.n_halo_of]}
 
 
 class HMatrix:
