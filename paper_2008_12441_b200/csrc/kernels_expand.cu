@@ -76,16 +76,26 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     // (P > 1, standard: a neighbour on another rank -- local row offset < 0 or
     // >= N_loc -- is read from the packed buffer's halo entry, whose rhs
     // columns are bpad apart).  kNone: this lane has no dense block.
+    // The lane's x source: xsrc + kk xld for rhs kk.
     constexpr int64_t kNone = INT64_MIN;
-    int hsrc = -1;
+    const double* xsrc = a.x;
+    int64_t xld = a.ldx;
     auto dense_source = [&]() -> int64_t {
-      hsrc = -1;
+      xsrc = a.x;
+      xld = a.ldx;
       if (!a.adm) return lane == 0 ? leaf0 : kNone;
       if (lane >= a.nd) return kNone;
       int lx[3];
       geo::morton_decode(a.d, leaf_idx, L, lx);
       if (!((geo::near_mask(a.d, lx, 1 << L) >> lane) & 1u)) return kNone;
-      if (a.halo_of) hsrc = a.halo_of[(leaf_idx - a.row0 / b) * a.nd + lane];
+      if (a.halo_of) {
+        const int h = a.halo_of[(leaf_idx - a.row0 / b) * a.nd + lane];
+        if (h >= 0) {
+          xsrc = a.xchg + a.halo_base;
+          xld = a.bpad;
+          return (int64_t)h * NR * a.bpad;
+        }
+      }
       return geo::neighbour(a.d, lx, lane, L) * b - a.row0;
     };
     int64_t src = dense_source();
@@ -146,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk) {
               if (kk < a.nr) {
-                const int64_t start = hsrc >= 0 ? ((int64_t)hsrc * NR + kk) * a.bpad : kk * a.ldx + src;
+                const int64_t start = kk * xld + src;
                 lo[kk] = start & ~int64_t(1);
                 xb[kk] = static_cast<uint32_t>((((start + b + 1) & ~int64_t(1)) - lo[kk]) * 8);
                 mine += xb[kk];
@@ -162,8 +172,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk)
               if (kk < a.nr)
-                dev::bulk_g2s(se + db + kk * a.xs_e * 8, (hsrc >= 0 ? a.xchg + a.halo_base : a.x) + lo[kk], xb[kk],
-                              &full[slot], pol_keep);
+                dev::bulk_g2s(se + db + kk * a.xs_e * 8, xsrc + lo[kk], xb[kk], &full[slot], pol_keep);
           }
         }
         if (++slot == NS) {
@@ -197,10 +206,18 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
   int64_t leaf_idx = (a.row0 + leaf0) / b;
   int lx[3] = {0, 0, 0};
-  uint32_t nmask = 1u;
+  uint32_t nmask = 1u, hmask = 0u;  // neighbours present / read from the halo buffer (P > 1)
+  const int64_t lbase = a.row0 / b;
+  auto halo_mask = [&]() -> uint32_t {
+    uint32_t m = 0u;
+    if (a.halo_of)
+      for (int e = 0; e < a.nd; ++e) m |= (a.halo_of[(leaf_idx - lbase) * a.nd + e] >= 0 ? 1u : 0u) << e;
+    return m;
+  };
   if (a.adm) {
     geo::morton_decode(a.d, leaf_idx, L, lx);
     nmask = geo::near_mask(a.d, lx, 1 << L);
+    hmask = halo_mask();
   }
   int slot = 0;
   uint32_t phase = 0;
@@ -250,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             const double* xs = reinterpret_cast<const double*>(se + Re * Dp * 8);
             const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
             // halo segments start 16-byte aligned (bpad even): no parity offset
-            const bool halo = a.halo_of && a.halo_of[(leaf_idx - a.row0 / b) * a.nd + e] >= 0;
+            const bool halo = (hmask >> e) & 1u;
             int xo[NR];
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk)
@@ -299,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         ++leaf_idx;
         geo::morton_decode(a.d, leaf_idx, L, lx);
         nmask = geo::near_mask(a.d, lx, 1 << L);
+        hmask = halo_mask();
       }
     }
   }
