@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     // dense source of lane e: the leaf itself (weak) or its near-field
     // neighbour e (standard; -1 when it lies outside the domain)
     int64_t leaf_idx = (a.row0 + leaf0) / b;
+    const int dd = __ffs(a.c) - 1;  // c = 2^d
     // (P > 1, standard: a neighbour on another rank -- local row offset < 0 or
     // >= N_loc -- is read from the packed buffer's halo entry, whose rhs
     // columns are bpad apart).  kNone: this lane has no dense block.
@@ -115,7 +116,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             const LevelArgs& lv = a.lv[l];
             const uint32_t ub = static_cast<uint32_t>(Re * Wp * 8);
             const uint32_t zb = static_cast<uint32_t>(Wp * NR * 8);
-            const int64_t tg = (a.row0 + i0) / lv.m;
+            // target node of the item at level l: m_l = b c^{L-l}, so the leaf's
+            // index shifted right by d (L - l) bits (no 64-bit division on the
+            // producer's critical path)
+            const int64_t tg = leaf_idx >> (dd * (L - l));
             const double* zrow = lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR;
             if (a.peer && l <= a.cross) {
               // peer exchange: the P ranks' contributions sit in this rank's

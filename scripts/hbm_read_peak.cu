@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <vector>
 #include <cstdlib>
+#include <string>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e_), __LINE__); return 1; } } while (0)
 
@@ -134,6 +135,65 @@ __global__ void bulk_ring(const char* __restrict__ p, int64_t bytes, int stage_b
 }
 
 static int g_sustain = 100;
+// expand-shaped stream: per 64-row item, 9 stages of 64 rows x 384 B (9 "U
+// panels") + 1 stage of 64 rows x 512 B ("D"), `nslot` slots of `slot_bytes`.
+// dsplit = 2: the D stage is two stages of 64 rows x 256 B columns halves... (as two 16 KB copies of rows 0..31 / 32..63)
+__global__ void expand_ring(const char* __restrict__ p, int64_t rows, int nslot, int slot_bytes, int dsplit,
+                            double* out) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (int64_t)slot_bytes * nslot);
+  uint64_t* empty = full + nslot;
+  const int ncw = blockDim.x / 32 - 1;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslot; ++i) {
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(sa(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(sa(&empty[i])), "r"(ncw));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const int64_t items = rows / 64;
+  const int64_t j0 = items * blockIdx.x / gridDim.x, j1 = items * (blockIdx.x + 1) / gridDim.x;
+  const int64_t upanel = rows * 384, dbase = 9 * upanel;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nst = 9 + dsplit;
+  int slot = 0;
+  uint32_t phase = 0;
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      for (int64_t j = j0; j < j1; ++j)
+        for (int st = 0; st < nst; ++st) {
+          asm volatile("{.reg .pred P; W: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra W;}" ::"r"(sa(&empty[slot])), "r"(phase ^ 1));
+          const char* src;
+          int n;
+          if (st < 9) { src = p + st * upanel + j * 64 * 384; n = 64 * 384; }
+          else { n = 64 * 512 / dsplit; src = p + dbase + j * 64 * 512 + (st - 9) * n; }
+          asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(sa(&full[slot])), "r"(n));
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                       ::"r"(sa(smem + (int64_t)slot * slot_bytes)), "l"(src), "r"(n), "r"(sa(&full[slot])), "l"(pol) : "memory");
+          if (++slot == nslot) { slot = 0; phase ^= 1; }
+        }
+    }
+    return;
+  }
+  double acc = 0;
+  for (int64_t j = j0; j < j1; ++j)
+    for (int st = 0; st < nst; ++st) {
+      asm volatile("{.reg .pred P; W: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra W;}" ::"r"(sa(&full[slot])), "r"(phase));
+      const double2* s2 = reinterpret_cast<const double2*>(smem + (int64_t)slot * slot_bytes);
+      const int n16 = (st < 9 ? 64 * 384 : 64 * 512 / dsplit) / 16;
+      double2 a2 = make_double2(0, 0);
+      for (int i = threadIdx.x - 32; i < n16; i += blockDim.x - 32) { double2 v = s2[i]; a2.x = fma(v.x, 1.0001, a2.x); a2.y = fma(v.y, 0.9999, a2.y); }
+      acc += a2.x + a2.y;
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(sa(&empty[slot])));
+      if (++slot == nslot) { slot = 0; phase ^= 1; }
+    }
+  if (acc == 123.456) out[0] = acc;
+}
+
 int main(int argc, char** argv) {
   if (argc > 2) g_sustain = atoi(argv[2]);
   int nsm = 0;
@@ -194,6 +254,36 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&xv, bytes / 48 + 4096));  // one double per 384 B row
   CK(cudaMemset(xv, 0, bytes / 48 + 4096));
   struct Cfg { int stage_kb, nstage, cta_per_sm, xmode, nlev; };
+  if (argc > 3 && std::string(argv[3]) == "expand") {
+    CK(cudaFuncSetAttribute(expand_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    const int64_t rows = 1ll << 24;  // 9 x 6.44 GB + 8.6 GB: the c4 expand stream
+    CK(cudaFree(p));
+    const int64_t big = rows * (9 * 384 + 512);
+    CK(cudaMalloc(&p, big));
+    fill_random<<<4096, 256>>>((uint64_t*)p, big / 8);
+    CK(cudaDeviceSynchronize());
+    struct E { int nslot, slot_kb, dsplit; };
+    for (E c : std::vector<E>{{3, 33, 1}, {2, 33, 1}, {4, 25, 2}, {3, 25, 2}, {2, 32, 1}, {5, 17, 4}}) {
+      const int sb = c.slot_kb * 1024;
+      const int smem = sb * c.nslot + 16 * c.nslot;
+      if ((smem + 1024) * 2 > 228 * 1024) continue;
+      snprintf(name, sizeof name, "expand ring %d slots x %d KB, D in %d", c.nslot, c.slot_kb, c.dsplit);
+      const int64_t tot = rows * (9 * 384 + 512);
+      auto launch = [&] { expand_ring<<<nsm * 2, 288, smem>>>(p, rows, c.nslot, sb, c.dsplit, out); };
+      launch();
+      cudaDeviceSynchronize();
+      cudaEventRecord(e0);
+      for (int rep = 0; rep < 20; ++rep) launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaError_t er = cudaGetLastError();
+      printf("%-48s sustained %8.1f GB/s (%.3f ms) %s\n", name, 20.0 * tot / (ms * 1e-3) / 1e9, ms / 20,
+             er == cudaSuccess ? "" : cudaGetErrorString(er));
+    }
+    return 0;
+  }
   if (argc > 3) {
     // TLB reach: the same 16 GiB of reads, spread over a 126 GB allocation (9 "levels" 14 GB apart)
     CK(cudaFree(p));
