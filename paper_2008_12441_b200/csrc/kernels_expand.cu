@@ -109,18 +109,21 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         const int l = level_order(a, li);
         const bool is_d = (l == L + 1);
         if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
-        dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
+        // Everything about the stage is computed BEFORE waiting for its slot:
+        // the slot's refill latency (release -> copies issued) is on the
+        // critical path of the stream, the address arithmetic is not.
         unsigned char* st = smem + slot * a.stage_bytes_e;
         if (!is_d) {
+          const uint32_t ub = static_cast<uint32_t>(Re * Wp * 8);
+          const uint32_t zb = static_cast<uint32_t>(Wp * NR * 8);
+          const LevelArgs& lv = a.lv[l];
+          // target node of the item at level l: m_l = b c^{L-l}, so the leaf's
+          // index shifted right by d (L - l) bits (no 64-bit division)
+          const int64_t tg = leaf_idx >> (dd * (L - l));
+          const double* zrow = lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR;
+          const double* usrc = a.U + (l - 1) * a.panel_stride + i0 * Wp;
+          dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
           if (lane == 0) {
-            const LevelArgs& lv = a.lv[l];
-            const uint32_t ub = static_cast<uint32_t>(Re * Wp * 8);
-            const uint32_t zb = static_cast<uint32_t>(Wp * NR * 8);
-            // target node of the item at level l: m_l = b c^{L-l}, so the leaf's
-            // index shifted right by d (L - l) bits (no 64-bit division on the
-            // producer's critical path)
-            const int64_t tg = leaf_idx >> (dd * (L - l));
-            const double* zrow = lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR;
             if (a.peer && l <= a.cross) {
               // peer exchange: the P ranks' contributions sit in this rank's
               // mailbox slots; wait once for every rank's flag of this pass
@@ -139,12 +142,12 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
               }
               const int64_t off = zrow - a.zex_base;
               dev::mbar_arrive_expect_tx(&full[slot], ub + a.P * zb);
-              dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
+              dev::bulk_g2s(st, usrc, ub, &full[slot], pol_stream);
               for (int g = 0; g < a.P; ++g)
                 dev::bulk_g2s(st + ub + g * zb, mb + g * a.mb + off, zb, &full[slot], pol_keep);
             } else {
               dev::mbar_arrive_expect_tx(&full[slot], ub + zb);
-              dev::bulk_g2s(st, a.U + (l - 1) * a.panel_stride + i0 * Wp, ub, &full[slot], pol_stream);
+              dev::bulk_g2s(st, usrc, ub, &full[slot], pol_stream);
               dev::bulk_g2s(st + ub, zrow, zb, &full[slot], pol_keep);
             }
           }
@@ -168,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             }
           }
           const uint32_t total = __reduce_add_sync(0xffffffffu, mine);
+          dev::mbar_wait(&empty[slot], phase ^ 1);
           if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
           __syncwarp();
           if (src != kNone) {

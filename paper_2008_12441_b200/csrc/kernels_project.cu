@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
         const double* Vl = a.V + (l - 1) * a.panel_stride;
         for (int64_t k = k0; k < k1; ++k) {
-          dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
+          // the stage's addresses first, then wait for the slot (the refill
+          // latency is on the stream's critical path)
           const int64_t i0 = k * Rp;
           unsigned char* st = smem + slot * a.stage_bytes_p;
           uint32_t total = vbytes;
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
               total += xb[kk];
             }
           }
+          dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
           dev::mbar_arrive_expect_tx(&full[slot], total);
           dev::bulk_g2s(st, Vl + i0 * Wp, vbytes, &full[slot], pol_stream);
 #pragma unroll
