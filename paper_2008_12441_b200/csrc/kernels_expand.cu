@@ -210,6 +210,24 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   const int njU = (NP + tpr - 1) / tpr;
   const int njD = (NPD + tpr - 1) / tpr;
   const int rotU = ri % njU, rotD = ri % njD;
+  // The thread's U column pairs in visiting order, fixed for the whole kernel
+  // (kMaxJ of them at most on the fast path; -1 = none): the stage loop is then
+  // a straight run of 2 LDS.128 + 2 DFMA per pair.  The consumers' per-stage
+  // time is on the stream's critical path (a slot is refilled only after every
+  // warp has read it), so their instruction count per stage matters.
+  constexpr int kMaxJ = 8;
+  const bool fastU = NR <= 4 && njU <= kMaxJ && !(W & 1);  // (NR = 8: registers; odd W: padding column)
+  int coff[kMaxJ];
+#pragma unroll
+  for (int n = 0; n < kMaxJ; ++n) {
+    if constexpr (NR <= 4) {
+      const int jj = n < njU ? (rotU + n) % njU : 0;
+      const int cp = p + tpr * jj;
+      coff[n] = (n < njU && cp < NP) ? cp : -1;
+    } else {
+      coff[n] = -1;
+    }
+  }
   const int64_t ipl = b / Re;
   int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
   int64_t leaf_idx = (a.row0 + leaf0) / b;
@@ -246,6 +264,21 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           const double* Zs = reinterpret_cast<const double*>(st + Re * Wp * 8);
           // peer exchange levels: the stage holds the P ranks' rows, summed here in rank order
           const int nz = (a.peer && l <= a.cross) ? a.P : 1;
+          if (NR <= 4 && fastU && nz == 1) {
+            const double2* Z2 = reinterpret_cast<const double2*>(Zs);
+#pragma unroll
+            for (int n = 0; n < kMaxJ; ++n) {
+              if (coff[n] >= 0) {
+                const double2 u = U2[coff[n]];
+#pragma unroll
+                for (int kk = 0; kk < NR; ++kk) {
+                  const double2 z = Z2[kk * NP + coff[n]];
+                  acc[kk] = fma(u.x, z.x, acc[kk]);
+                  acc2[kk] = fma(u.y, z.y, acc2[kk]);
+                }
+              }
+            }
+          } else {
           int jj = rotU;
           for (int n = 0; n < njU; ++n) {
             const int cp = p + tpr * jj;
@@ -265,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
               }
             }
             if (++jj == njU) jj = 0;
+          }
           }
         } else {
           const int64_t dblk = int64_t(Re) * Dp * 8 + int64_t(NR) * a.xs_e * 8;
