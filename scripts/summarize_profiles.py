@@ -49,13 +49,15 @@ for r in rows:
     name = "project" if "project" in r["Kernel Name"] else "expand"
     d = tr.setdefault(name, {})
     d[r["Metric Name"]] = float(r["Metric Value"])
-out = {"c4": {}}
+path = os.path.join(P, "ncu_traffic.json")
+out = json.load(open(path)) if os.path.exists(path) else {}  # keep the other configs' entries
+out["c4"] = {}
 for k, d in tr.items():
     out["c4"][k] = {"dram_bytes_per_launch": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
                     "dram_bytes_read": d["dram__bytes_read.sum"], "dram_bytes_write": d["dram__bytes_write.sum"],
                     "ncu_duration_ns": d["gpu__time_duration.sum"],
                     "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum (one launch), {rnd}"}
-with open(os.path.join(P, "ncu_traffic.json"), "w") as f:
+with open(path, "w") as f:
     json.dump(out, f, indent=1)
 
 # 3. key metrics of the full capture (c2)
