@@ -60,6 +60,10 @@ def workload_desc(cfg):
                 f"depth L={cfg.L}, leaf b={cfg.b}, rank r={cfg.r} blocks vs up to {cfg.slots} interaction-list "
                 f"boxes per node, dense {cfg.b}x{cfg.b} near-field blocks (3^d per leaf), nrhs={cfg.nrhs}, seeded "
                 f"synthetic (U,V~N(0,1)/sqrt(m_l), D~N(0,1)/8, x~U[-1,1]); not a BASELINE config")
+    if cfg.name == "c2strict":
+        return (f"c2strict: c2 (2D, N={cfg.N}, r={cfg.r}) under the paper-strict reading of Def 2.4: dense "
+                f"{cfg.b}x{cfg.b} leaf-parent diagonal blocks, rank-{cfg.r} sibling blocks at levels 1..{cfg.L} "
+                f"(= weak structure of depth {cfg.L}, leaf {cfg.b}); seeded synthetic; not a BASELINE config")
     return (f"{cfg.name}: {cfg.d}D H-matrix fp64, weak admissibility, N={cfg.N} (Morton), depth L={cfg.L}, "
             f"leaf b={cfg.b}, rank r={cfg.r} blocks vs each of {cfg.c - 1} siblings at every level, "
             f"dense {cfg.b}x{cfg.b} leaf-diagonal blocks, nrhs={cfg.nrhs}, seeded synthetic "

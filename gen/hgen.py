@@ -89,6 +89,10 @@ CONFIGS = {
 # blocks per row) -- the paper's "Standard" columns use the same 1024^2 domain.
 EXTRA_CONFIGS = {
     "s2": HConfig("s2", d=2, L=7, b=64, r=16, nrhs=1, seed=SEED_BASE + 12, adm=1),
+    # c2 under the paper-strict reading of Def 2.4 (the leaf-parent
+    # diagonal blocks, 4 x 64 = 256 square, are dense; low-rank blocks at levels
+    # 1..6): exactly the weak structure of depth 6 with leaf 256
+    "c2strict": HConfig("c2strict", d=2, L=6, b=256, r=16, nrhs=1, seed=SEED_BASE + 13),
 }
 
 _lib = None
