@@ -55,6 +55,8 @@ struct StreamArgs {
   int* cnt;          // [L][grid_p] arrival tickets
   // expand schedule
   int Re, tpr, nstage_e;
+  int64_t chunk_e;   // expand: 0 = static item ranges; > 0 = dynamic chunks of chunk_e items
+  int* sched;        // expand: [next chunk, CTAs done] (re-armed by the last CTA)
   int64_t stage_bytes_e, items_e;
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows

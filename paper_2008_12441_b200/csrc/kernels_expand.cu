@@ -51,6 +51,9 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   const int NS = a.nstage_e;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
   uint64_t* empty = full + NS;
+  volatile int* chunk_q = reinterpret_cast<volatile int*>(smem + a.bar_off_e + 512);  // [NS] chunk ids
+  const bool dyn = a.chunk_e > 0;
+  const int64_t nchunks = dyn ? (a.items_e + a.chunk_e - 1) / a.chunk_e : 0;
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -69,10 +72,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     int slot = 0;
     uint32_t phase = 0;
     const int64_t ipl = b / Re;                        // items per leaf
-    int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
+    int64_t leaf0 = 0, in_leaf = 0;
     // dense source of lane e: the leaf itself (weak) or its near-field
     // neighbour e (standard; -1 when it lies outside the domain)
-    int64_t leaf_idx = (a.row0 + leaf0) / b;
+    int64_t leaf_idx = 0;
     const int dd = __ffs(a.c) - 1;  // c = 2^d
     // (P > 1, standard: a neighbour on another rank -- local row offset < 0 or
     // >= N_loc -- is read from the packed buffer's halo entry, whose rhs
@@ -99,11 +102,52 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       }
       return geo::neighbour(a.d, lx, lane, L) * b - a.row0;
     };
-    int64_t src = dense_source();
+    int64_t src = kNone;
     bool peers_ready = false;
     const uint32_t db = static_cast<uint32_t>(Re * Dp * 8);
     const int64_t dblk = db + int64_t(NR) * a.xs_e * 8;
-    for (int64_t j = j0; j < j1; ++j) {
+    // Work: the static range [j0, j1), or (a.chunk_e > 0) chunks of chunk_e items
+    // taken from a global counter -- the CTAs that stream faster take more
+    // chunks, so they all finish within one chunk of each other (no tail).  The
+    // first stage of a chunk carries its id to the consumers (chunk_q[slot]).
+    int64_t cj0 = j0, cj1 = j1;
+    int chunk = -1;
+    bool first_range = true, first_stage = false;
+    auto next_range = [&]() -> bool {
+      if (!dyn) {
+        const bool r = first_range && j0 < j1;
+        first_range = false;
+        return r;
+      }
+      int c = 0;
+      if (lane == 0) c = atomicAdd(a.sched, 1);
+      c = __shfl_sync(0xffffffffu, c, 0);
+      if (c >= nchunks) {
+        // end of work: an empty phase with chunk id -1 tells the consumers
+        dev::mbar_wait(&empty[slot], phase ^ 1);
+        if (lane == 0) {
+          chunk_q[slot] = -1;
+          dev::mbar_arrive(&full[slot]);
+          // the last CTA to run out re-arms the counters for the next launch
+          if (atomicAdd(a.sched + 1, 1) == static_cast<int>(G) - 1) {
+            a.sched[0] = 0;
+            a.sched[1] = 0;
+          }
+        }
+        return false;
+      }
+      chunk = c;
+      cj0 = int64_t(c) * a.chunk_e;
+      cj1 = cj0 + a.chunk_e < a.items_e ? cj0 + a.chunk_e : a.items_e;
+      first_stage = true;
+      return true;
+    };
+    while (next_range()) {
+    leaf0 = (cj0 * Re / b) * b;
+    in_leaf = (cj0 * Re - leaf0) / Re;
+    leaf_idx = (a.row0 + leaf0) / b;
+    src = dense_source();
+    for (int64_t j = cj0; j < cj1; ++j) {
       const int64_t i0 = j * Re;
       for (int li = 1; li <= L + 1; ++li) {
         const int l = level_order(a, li);
@@ -123,6 +167,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           const double* zrow = lv.zt + (tg - lv.tbase) * (int64_t)Wp * NR;
           const double* usrc = a.U + (l - 1) * a.panel_stride + i0 * Wp;
           dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
+          if (lane == 0 && first_stage) chunk_q[slot] = chunk;
+          first_stage = false;
           if (lane == 0) {
             if (a.peer && l <= a.cross) {
               // peer exchange: the P ranks' contributions sit in this rank's
@@ -172,6 +218,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           }
           const uint32_t total = __reduce_add_sync(0xffffffffu, mine);
           dev::mbar_wait(&empty[slot], phase ^ 1);
+          if (lane == 0 && first_stage) chunk_q[slot] = chunk;
+          first_stage = false;
           if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
           __syncwarp();
           if (src != kNone) {
@@ -194,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         ++leaf_idx;
         src = dense_source();
       }
+    }
     }
     return;
   }
@@ -229,8 +278,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     }
   }
   const int64_t ipl = b / Re;
-  int64_t leaf0 = (j0 * Re / b) * b, in_leaf = (j0 * Re - leaf0) / Re;
-  int64_t leaf_idx = (a.row0 + leaf0) / b;
+  int64_t leaf0 = 0, in_leaf = 0;
+  int64_t leaf_idx = 0;
   int lx[3] = {0, 0, 0};
   uint32_t nmask = 1u, hmask = 0u;  // neighbours present / read from the halo buffer (P > 1)
   const int64_t lbase = a.row0 / b;
@@ -240,14 +289,35 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       for (int e = 0; e < a.nd; ++e) m |= (a.halo_of[(leaf_idx - lbase) * a.nd + e] >= 0 ? 1u : 0u) << e;
     return m;
   };
+  int slot = 0;
+  uint32_t phase = 0;
+  int64_t cj0 = j0, cj1 = j1;
+  bool first_range = true, peeked = false;
+  auto next_range = [&]() -> bool {
+    if (!dyn) {
+      const bool r = first_range && j0 < j1;
+      first_range = false;
+      return r;
+    }
+    // the next stage is the first of the producer's next chunk (or the end mark)
+    dev::mbar_wait(&full[slot], phase);
+    const int c = chunk_q[slot];
+    if (c < 0) return false;
+    cj0 = int64_t(c) * a.chunk_e;
+    cj1 = cj0 + a.chunk_e < a.items_e ? cj0 + a.chunk_e : a.items_e;
+    peeked = true;
+    return true;
+  };
+  while (next_range()) {
+  leaf0 = (cj0 * Re / b) * b;
+  in_leaf = (cj0 * Re - leaf0) / Re;
+  leaf_idx = (a.row0 + leaf0) / b;
   if (a.adm) {
     geo::morton_decode(a.d, leaf_idx, L, lx);
     nmask = geo::near_mask(a.d, lx, 1 << L);
     hmask = halo_mask();
   }
-  int slot = 0;
-  uint32_t phase = 0;
-  for (int64_t j = j0; j < j1; ++j) {
+  for (int64_t j = cj0; j < cj1; ++j) {
     const int64_t i0 = j * Re;
     double acc[NR], acc2[NR];  // two chains: even / odd columns
 #pragma unroll
@@ -256,7 +326,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       const int l = level_order(a, li);
       const bool is_d = (l == L + 1);
       if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
-      dev::mbar_wait(&full[slot], phase);
+      if (!peeked) dev::mbar_wait(&full[slot], phase);
+      peeked = false;
       const unsigned char* st = smem + slot * a.stage_bytes_e;
       if (active && !(a.dbg & 2)) {
         if (!is_d) {
@@ -361,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         hmask = halo_mask();
       }
     }
+  }
   }
 }
 
