@@ -314,3 +314,25 @@ def test_strict_structure(d, L, b, r):
         assert_parity(y.cpu().numpy(), ref)
     finally:
         hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("chunk", ["0", "1", "3"])
+def test_expand_work_distribution_and_rearm(chunk, monkeypatch):
+    """expand's item distribution: static ranges (HMAT_EXPAND_CHUNK=0) and
+    dynamic chunks of 1 / 3 items from the global counter give the same y, for
+    several matvecs in a row on one handle (the counter is re-armed by the last
+    CTA of every launch) and a ragged item count."""
+    monkeypatch.setenv("HMAT_EXPAND_CHUNK", chunk)
+    cfg = HConfig("chunks", d=2, L=4, b=16, r=4, seed=1201)   # 256 leaves: grid < items
+    U, V, D = hgen.inputs(cfg)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        for v in range(3):
+            x = np.ascontiguousarray(hgen.xblock(cfg, nrhs=1, vec=v)[:, 0])
+            xd = torch.from_numpy(x).cuda()
+            yd = torch.full_like(xd, float("nan"))
+            hm.hmat_matvec(h, xd, yd)
+            torch.cuda.synchronize()
+            assert_parity(yd.cpu().numpy(), oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x))
+    finally:
+        hm.hmat_destroy(h)
