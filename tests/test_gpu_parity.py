@@ -323,7 +323,7 @@ def test_expand_work_distribution_and_rearm(chunk, monkeypatch):
     several matvecs in a row on one handle (the counter is re-armed by the last
     CTA of every launch) and a ragged item count."""
     monkeypatch.setenv("HMAT_EXPAND_CHUNK", chunk)
-    cfg = HConfig("chunks", d=2, L=4, b=16, r=4, seed=1201)   # 256 leaves: grid < items
+    cfg = HConfig("chunks", d=2, L=6, b=16, r=4, seed=1201)   # 4096 items of 16 rows: ~14 per CTA
     U, V, D = hgen.inputs(cfg)
     h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
     try:
