@@ -344,12 +344,14 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
         dev::mbar_wait(&full[slot], phase);
         const double* As = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e);
         const double* Bs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e + abytes);
+        // two copies of the k loop (U / Zt stage, D / x stage), so the compiler
+        // does not if-convert the B loads of both layouts into every k-step
+        if (!is_d) {
 #pragma unroll
-        for (int ks = 0; ks < KC / 4; ++ks) {
-          double av[2], bv[4];
+          for (int ks = 0; ks < KC / 4; ++ks) {
+            double av[2], bv[4];
 #pragma unroll
-          for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
-          if (!is_d) {
+            for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
             // fragment-major Zt chunk: k-step ks, N-tile pairs wn*2, wn*2+1
 #pragma unroll
             for (int np = 0; np < 2; ++np) {
@@ -357,14 +359,24 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
               bv[np * 2] = v.x;
               bv[np * 2 + 1] = v.y;
             }
-          } else {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+          }
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < KC / 4; ++ks) {
+            double av[2], bv[4];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) bv[nt] = Bs[((wn * 4 + nt) * 8 + g) * XP + ks * 4 + tq];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
           }
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
         }
         // release: the last of the NCW warps refills the slot NS stages ahead
         __syncwarp();
