@@ -745,6 +745,20 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     // and when an item has no stage at all, which the chunk protocol needs)
     a.chunk_e = env_int("HMAT_EXPAND_CHUNK", p.adm ? 0 : 1);
     if (!level_mask && !dense) a.chunk_e = 0;
+    // project: the last active level in dynamic chunks of whole nodes (>= 4
+    // stages), when it is local (no exchange) and has at least 2 chunks per CTA
+    a.dyn_level = 0;
+    a.sched_p = H->sched + 4;
+    if (level_mask && env_int("HMAT_PROJECT_DYN", 1)) {
+      const int ll = 64 - __builtin_clzll(level_mask);
+      const int64_t SLs = p.N_loc / p.Rp, seg = std::min<int64_t>(p.m[ll], p.N_loc) / p.Rp;
+      int64_t ch = seg;
+      while (ch < 4) ch += seg;
+      if (ll > p.cross && SLs / ch >= 2 * int64_t(ly.grid_p)) {
+        a.dyn_level = ll;
+        a.dyn_chunk = ch;
+      }
+    }
     for (int l = 1; l <= p.L; ++l) {
       hmat::LevelArgs& lv = a.lv[l];
       lv.m = p.m[l];

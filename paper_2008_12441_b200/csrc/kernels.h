@@ -57,6 +57,9 @@ struct StreamArgs {
   int Re, tpr, nstage_e;
   int64_t chunk_e;   // expand: 0 = static item ranges; > 0 = dynamic chunks of chunk_e items
   int* sched;        // expand: [next chunk, CTAs done] (re-armed by the last CTA)
+  int dyn_level;     // project: the level handed out in dynamic chunks (0 = none)
+  int64_t dyn_chunk; // project: stages per chunk (a multiple of the level's node size)
+  int* sched_p;      // project: [next chunk, CTAs done]
   int64_t stage_bytes_e, items_e;
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows

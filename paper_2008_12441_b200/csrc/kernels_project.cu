@@ -143,6 +143,12 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_p);
   uint64_t* empty = full + NS;
   volatile int* flag = reinterpret_cast<volatile int*>(empty + NS);
+  volatile int* chunk_q = reinterpret_cast<volatile int*>(smem + a.bar_off_p + 768);  // [NS] chunk ids
+  // The last active level (a.dyn_level; 0 = none) is handed out dynamically in
+  // chunks of a.dyn_chunk stages (whole nodes: no partial sums) from a global
+  // counter, so CTAs that streamed the earlier levels faster take more of it
+  // and all end together; the other levels keep the even static split.
+  const int dyn_level = a.dyn_level;
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -169,7 +175,34 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       for (int l = 1; l <= L; ++l) {
         if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
         const double* Vl = a.V + (l - 1) * a.panel_stride;
-        for (int64_t k = k0; k < k1; ++k) {
+        const bool dyn = l == dyn_level;
+        int64_t rk0 = k0, rk1 = k1;
+        int chunk = -1;
+        for (bool first_range = true;; first_range = false) {
+        if (dyn) {
+          const int c = atomicAdd(a.sched_p, 1);
+          if (int64_t(c) * a.dyn_chunk >= SL) {
+            // end of work: an empty phase with chunk id -1 tells the consumers
+            dev::mbar_wait(&empty[slot], phase ^ 1);
+            chunk_q[slot] = -1;
+            dev::mbar_arrive(&full[slot]);
+            if (++slot == NS) {
+              slot = 0;
+              phase ^= 1;
+            }
+            if (atomicAdd(a.sched_p + 1, 1) == static_cast<int>(GL) - 1) {  // re-arm for the next launch
+              a.sched_p[0] = 0;
+              a.sched_p[1] = 0;
+            }
+            break;
+          }
+          chunk = c;
+          rk0 = int64_t(c) * a.dyn_chunk;
+          rk1 = rk0 + a.dyn_chunk < SL ? rk0 + a.dyn_chunk : SL;
+        } else if (!first_range) {
+          break;
+        }
+        for (int64_t k = rk0; k < rk1; ++k) {
           // the stage's addresses first, then wait for the slot (the refill
           // latency is on the stream's critical path)
           const int64_t i0 = k * Rp;
@@ -187,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
             }
           }
           dev::mbar_wait(&empty[slot], phase ^ 1);  // fresh barrier: parity 1 passes at once
+          if (dyn && k == rk0) chunk_q[slot] = chunk;  // the chunk travels with its first stage
           dev::mbar_arrive_expect_tx(&full[slot], total);
           dev::bulk_g2s(st, Vl + i0 * Wp, vbytes, &full[slot], pol_stream);
 #pragma unroll
@@ -197,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
             slot = 0;
             phase ^= 1;
           }
+        }
         }
       }
     }
@@ -227,12 +262,33 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   for (int l = 1; l <= L; ++l) {
     if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
     const LevelArgs& lv = a.lv[l];
+    const bool dyn = l == dyn_level;
+    const int64_t sg0 = a.row0 / lv.m;
     // node cursor: seg stages per local node, sl = node index, pos = stage in node
     const int64_t seg = lv.seg_rows / Rp;
-    int64_t sl = k0 / seg, pos = k0 - sl * seg;
-    const int64_t sg0 = a.row0 / lv.m;
-    for (int64_t k = k0; k < k1; ++k) {
+    int64_t rk0 = k0, rk1 = k1;
+    for (bool first_range = true;; first_range = false) {
+    bool peeked = false;
+    if (dyn) {  // the next stage is the first of the producer's next chunk (or the end mark)
       dev::mbar_wait(&full[slot], phase);
+      const int c = chunk_q[slot];
+      if (c < 0) {
+        if (++slot == NS) {
+          slot = 0;
+          phase ^= 1;
+        }
+        break;
+      }
+      rk0 = int64_t(c) * a.dyn_chunk;
+      rk1 = rk0 + a.dyn_chunk < SL ? rk0 + a.dyn_chunk : SL;
+      peeked = true;
+    } else if (!first_range) {
+      break;
+    }
+    int64_t sl = rk0 / seg, pos = rk0 - sl * seg;
+    for (int64_t k = rk0; k < rk1; ++k) {
+      if (!peeked) dev::mbar_wait(&full[slot], phase);
+      peeked = false;
       const int64_t i0 = k * Rp;
       const unsigned char* st = smem + slot * a.stage_bytes_p;
       const double2* V2 = reinterpret_cast<const double2*>(st);
@@ -272,11 +328,11 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         pos = 0;
         ++sl;
       }
-      if (!node_end && k + 1 != k1) continue;
+      if (!node_end && k + 1 != rk1) continue;
 
       // ---- end of a (local) node, or end of this CTA's range of the level ----
       const int64_t sa = this_sl * seg, sb = sa + seg;  // the node's stages
-      const bool complete = sa >= k0 && sb <= k1;
+      const bool complete = sa >= rk0 && sb <= rk1;
       const int64_t sg = sg0 + this_sl;                 // global source node
       double* red = red_base + red_buf * red_elems;
       int64_t* nbr = nbr_base + red_buf * 32;  // standard admissibility: parent's neighbours
@@ -372,6 +428,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         }
         dev::named_bar_sync(1, CT);  // *flag is rewritten by the next partial node
       }
+    }
     }
   }
   if (a.peer) peer_push(a, t, GL, flag);
