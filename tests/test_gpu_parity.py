@@ -316,13 +316,15 @@ def test_strict_structure(d, L, b, r):
         hm.hmat_destroy(h)
 
 
-@pytest.mark.parametrize("chunk", ["0", "1", "3"])
-def test_expand_work_distribution_and_rearm(chunk, monkeypatch):
-    """expand's item distribution: static ranges (HMAT_EXPAND_CHUNK=0) and
-    dynamic chunks of 1 / 3 items from the global counter give the same y, for
-    several matvecs in a row on one handle (the counter is re-armed by the last
-    CTA of every launch) and a ragged item count."""
+@pytest.mark.parametrize("chunk,pdyn", [("0", "0"), ("1", "1"), ("3", "1"), ("1", "0")])
+def test_expand_work_distribution_and_rearm(chunk, pdyn, monkeypatch):
+    """Work distribution: expand's static item ranges (HMAT_EXPAND_CHUNK=0) or
+    dynamic chunks of 1 / 3 items, project's last level static or in dynamic
+    node chunks (HMAT_PROJECT_DYN), give the same y, for several matvecs in a
+    row on one handle (the counters are re-armed by the last CTA of every
+    launch)."""
     monkeypatch.setenv("HMAT_EXPAND_CHUNK", chunk)
+    monkeypatch.setenv("HMAT_PROJECT_DYN", pdyn)
     cfg = HConfig("chunks", d=2, L=6, b=16, r=4, seed=1201)   # 4096 items of 16 rows: ~14 per CTA
     U, V, D = hgen.inputs(cfg)
     h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
