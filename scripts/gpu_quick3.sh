@@ -1,0 +1,6 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_multirank.py -x -q -k "dmma or DMMA or c5 or adjoint" > gpurun_out/pytest_quick3.log 2>&1; echo "pytest rc=$?"
+timeout 900 python scripts/kernel_sweep.py c5 "" "" > gpurun_out/quick3_sweep.log 2>&1
+timeout 300 python scripts/cta_trace.py c5 >> gpurun_out/quick3_sweep.log 2>&1
