@@ -611,6 +611,15 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.part = H->part;
   a.cnt = H->cnt;
   a.Re = p.Re;
+  a.ndc = p.ndc;
+  a.dc = p.dc;
+  if (p.ndc > 1) {  // the dense block's column-chunk boxes [Re][dc]
+    const uint64_t dims[2] = {uint64_t(p.Dp), uint64_t(p.N_loc)};
+    const uint64_t strides[1] = {uint64_t(p.Dp) * 8};
+    const uint32_t box[2] = {uint32_t(p.dc), uint32_t(p.Re)};
+    hmat_status st3 = encode_map(&a.tm_dse, 2, a.D, dims, strides, box);
+    if (st3 != HMAT_OK) return st3;
+  }
   a.sched = H->sched;
   a.tpr = p.tpr;
   a.items_e = p.items_e;

@@ -55,6 +55,7 @@ struct StreamArgs {
   int* cnt;          // [L][grid_p] arrival tickets
   // expand schedule
   int Re, tpr, nstage_e;
+  int ndc, dc;       // expand: dense block in ndc column-chunk stages of dc columns (ndc > 1: box tm_dse)
   int64_t chunk_e;   // expand: 0 = static item ranges; > 0 = dynamic chunks of chunk_e items
   int* sched;        // expand: [next chunk, CTAs done] (re-armed by the last CTA)
   int dyn_level;     // project: the level handed out in dynamic chunks (0 = none)
@@ -100,6 +101,8 @@ struct StreamArgs {
   alignas(64) CUtensorMap tm_u;
   alignas(64) CUtensorMap tm_d;
   alignas(64) CUtensorMap tm_xe;
+  // SIMT expand with ndc > 1: 2-D map over the D-role panel [N_loc][Dp], box [Re][dc]
+  alignas(64) CUtensorMap tm_dse;
 };
 
 // Launch one project pass (template NR chosen from args.nr).  grid = plan.grid_p.

@@ -34,9 +34,10 @@ constexpr int NCW = CT / 32;
 // Order of an item's stages: levels 1..L, then the dense block (L + 1).  With
 // the peer exchange the levels 1..cross wait for other ranks' flags, so they go
 // last: local levels and the dense block first (overlap).
+// Stages L+1 .. L+ndc are the dense block's column chunks.
 __device__ __forceinline__ int level_order(const StreamArgs& a, int li) {
   if (!a.peer) return li;
-  const int nloc = a.L + 1 - a.cross;
+  const int nloc = a.L + a.ndc - a.cross;
   return li <= nloc ? li + a.cross : li - nloc;
 }
 
@@ -149,9 +150,9 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     src = dense_source();
     for (int64_t j = cj0; j < cj1; ++j) {
       const int64_t i0 = j * Re;
-      for (int li = 1; li <= L + 1; ++li) {
+      for (int li = 1; li <= L + a.ndc; ++li) {
         const int l = level_order(a, li);
-        const bool is_d = (l == L + 1);
+        const bool is_d = (l > L);
         if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
         // Everything about the stage is computed BEFORE waiting for its slot:
         // the slot's refill latency (release -> copies issued) is on the
@@ -197,6 +198,33 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
               dev::bulk_g2s(st + ub, zrow, zb, &full[slot], pol_keep);
             }
           }
+        } else if (a.ndc > 1) {
+          // column chunk h of the (weak) dense block: the Re x dc box of D
+          // (tensor TMA) + the chunk's x segment per rhs; lane 0 issues
+          const int h = l - L - 1;
+          uint32_t total = static_cast<uint32_t>(Re * a.dc * 8);
+          int64_t lo[NR];
+          uint32_t xb[NR];
+#pragma unroll
+          for (int kk = 0; kk < NR; ++kk) {
+            if (kk < a.nr) {
+              const int64_t start = kk * a.ldx + leaf0 + h * a.dc;
+              lo[kk] = start & ~int64_t(1);
+              xb[kk] = static_cast<uint32_t>((((start + a.dc + 1) & ~int64_t(1)) - lo[kk]) * 8);
+              total += xb[kk];
+            }
+          }
+          dev::mbar_wait(&empty[slot], phase ^ 1);
+          if (lane == 0) {
+            if (first_stage) chunk_q[slot] = chunk;
+            dev::mbar_arrive_expect_tx(&full[slot], total);
+            dev::tma_load_2d(st, &a.tm_dse, h * a.dc, static_cast<int>(i0), &full[slot], pol_stream);
+#pragma unroll
+            for (int kk = 0; kk < NR; ++kk)
+              if (kk < a.nr)
+                dev::bulk_g2s(st + Re * a.dc * 8 + kk * a.xs_e * 8, a.x + lo[kk], xb[kk], &full[slot], pol_keep);
+          }
+          first_stage = false;
         } else {
           // one stage holds every dense block of the tile's rows, block e at
           // byte offset e * dblk followed by its source x segment (16-byte
@@ -322,9 +350,9 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     double acc[NR], acc2[NR];  // two chains: even / odd columns
 #pragma unroll
     for (int kk = 0; kk < NR; ++kk) acc[kk] = acc2[kk] = 0.0;
-    for (int li = 1; li <= L + 1; ++li) {
+    for (int li = 1; li <= L + a.ndc; ++li) {
       const int l = level_order(a, li);
-      const bool is_d = (l == L + 1);
+      const bool is_d = (l > L);
       if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
       if (!peeked) dev::mbar_wait(&full[slot], phase);
       peeked = false;
@@ -370,6 +398,22 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             }
             if (++jj == njU) jj = 0;
           }
+          }
+        } else if (a.ndc > 1) {
+          // column chunk h: D box [Re][dc] + x[leaf0 + h dc, + dc)
+          const int NPC = a.dc >> 1;
+          const double2* D2 = reinterpret_cast<const double2*>(st) + ri * NPC;
+          const double* xs = reinterpret_cast<const double*>(st + Re * a.dc * 8);
+          int xo[NR];
+#pragma unroll
+          for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_e + static_cast<int>((kk * a.ldx + leaf0) & 1);
+          for (int cp = p; cp < NPC; cp += tpr) {
+            const double2 dv = D2[cp];
+#pragma unroll
+            for (int kk = 0; kk < NR; ++kk) {
+              acc[kk] = fma(dv.x, xs[xo[kk] + 2 * cp], acc[kk]);
+              acc2[kk] = fma(dv.y, xs[xo[kk] + 2 * cp + 1], acc2[kk]);
+            }
           }
         } else {
           const int64_t dblk = int64_t(Re) * Dp * 8 + int64_t(NR) * a.xs_e * 8;

@@ -294,7 +294,8 @@ def test_adjoint_identity_c2_and_dmma():
             torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("d,L,b,r", [(2, 3, 16, 4), (3, 2, 8, 2), (1, 4, 2, 3), (2, 1, 5, 2)])
+@pytest.mark.parametrize("d,L,b,r", [(2, 3, 16, 4), (3, 2, 8, 2), (1, 4, 2, 3), (2, 1, 5, 2),
+                                     (2, 3, 64, 4), (3, 2, 16, 2), (1, 5, 64, 3)])  # leaf 256 / 128 / 128: chunked dense
 def test_strict_structure(d, L, b, r):
     """hmat_create_strict (Def 2.4 read literally: leaf-parent diagonal blocks
     dense) vs the oracle's strict block loop."""
