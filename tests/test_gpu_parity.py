@@ -339,3 +339,28 @@ def test_expand_work_distribution_and_rearm(chunk, pdyn, monkeypatch):
             assert_parity(yd.cpu().numpy(), oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x))
     finally:
         hm.hmat_destroy(h)
+
+
+def test_strict_chunked_dense_adjoint():
+    """Paper-strict structure with leaf 256 (the dense block travels in 64-column
+    chunks): <y', H x> = <H^T y', x> with both products on the GPU."""
+    d, L, b, r = 2, 4, 64, 4
+    c = 1 << d
+    N = b * c ** L
+    W = (c - 1) * r
+    rng = np.random.default_rng(1301)
+    U = [rng.standard_normal((N, W)) / 8 for _ in range(L - 1)]
+    V = [rng.standard_normal((N, W)) / 8 for _ in range(L - 1)]
+    Dc = rng.standard_normal((N, c * b)) / 8
+    h = hm.hmat_create_strict(L, d, b, r, U, V, Dc)
+    try:
+        x = torch.from_numpy(rng.standard_normal(N)).cuda()
+        yp = torch.from_numpy(rng.standard_normal(N)).cuda()
+        hx, hty = torch.empty_like(x), torch.empty_like(x)
+        hm.hmat_gemv(h, 0, 1.0, x, 0.0, hx)
+        hm.hmat_gemv(h, 1, 1.0, yp, 0.0, hty)
+        torch.cuda.synchronize()
+        lhs, rhs = float(yp @ hx), float(hty @ x)
+        assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    finally:
+        hm.hmat_destroy(h)
