@@ -215,6 +215,20 @@ hmat_status hmat_local_rows(hmat_t H, int64_t* begin, int64_t* end);
 /* Make H enqueue on `stream` (a cudaStream_t on H's device) from now on. */
 hmat_status hmat_set_stream(hmat_t H, void* stream);
 
+/* Asynchronous host-pointer mode (enable = 1): hmat_matvec / hmat_gemv with a
+ * host x or y return as soon as the work is enqueued.  x is copied in on a
+ * copy stream, the kernels run on H's stream, y is copied out on another copy
+ * stream; the staging buffers alternate between consecutive calls, so one
+ * call's copies overlap its neighbours' kernels (a stream of matvecs runs at
+ * the kernels' rate, not kernels + PCIe).  The caller keeps x and y valid and
+ * unmodified until hmat_synchronize(H) returns (pinned host memory for real
+ * overlap; pageable memory is correct but copies synchronously).  Device
+ * pointers are unaffected.  Disabling drains the pipeline.  Default: off. */
+hmat_status hmat_set_host_async(hmat_t H, int enable);
+
+/* Wait for all work of H (copies in, kernels, copies out). */
+hmat_status hmat_synchronize(hmat_t H);
+
 /* 128 bytes of a fresh ncclUniqueId for hmat_dist_t (call on one rank and
  * broadcast).  HMAT_ERR_NCCL if NCCL cannot be loaded. */
 hmat_status hmat_nccl_unique_id(void* out128);

@@ -112,6 +112,16 @@ struct hmat_s {
   double* xbuf = nullptr;
   double* ybuf = nullptr;
   size_t xcap = 0, ycap = 0;  // doubles
+  // asynchronous host-pointer mode (hmat_set_host_async): double-buffered
+  // staging, copies in / out on their own streams, ordered by events
+  bool host_async = false;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  double* xb2[2] = {nullptr, nullptr};
+  double* yb2[2] = {nullptr, nullptr};
+  size_t xc2[2] = {0, 0}, yc2[2] = {0, 0};
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  bool comp_rec[2] = {false, false}, out_rec[2] = {false, false};
+  int apar = 0;
   hmat::Comm* comm = nullptr;
   // DMMA (many right-hand sides) buffers, allocated on first use
   double* zloc_d = nullptr;
@@ -164,6 +174,17 @@ void release(hmat_s* H) {
   cudaFree(H->sched);
   cudaFree(H->xbuf);
   cudaFree(H->ybuf);
+  for (int i = 0; i < 2; ++i) {
+    if (H->s_in) cudaStreamSynchronize(H->s_in);
+    if (H->s_out) cudaStreamSynchronize(H->s_out);
+    cudaFree(H->xb2[i]);
+    cudaFree(H->yb2[i]);
+    if (H->ev_in[i]) cudaEventDestroy(H->ev_in[i]);
+    if (H->ev_comp[i]) cudaEventDestroy(H->ev_comp[i]);
+    if (H->ev_out[i]) cudaEventDestroy(H->ev_out[i]);
+  }
+  if (H->s_in) cudaStreamDestroy(H->s_in);
+  if (H->s_out) cudaStreamDestroy(H->s_out);
   cudaFree(H->zloc_d);
   cudaFree(H->zex_d);
   cudaFree(H->part_d);
@@ -552,11 +573,39 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   if (p.adm) level_mask &= ~1ull;  // standard admissibility: no admissible pair at level 1
 
   EventPair ep{};
+  // ---- asynchronous host-pointer mode: x in on s_in, y out on s_out, the
+  //      kernels on H's stream, staging buffers alternating between calls so
+  //      call k's copies overlap calls k-1 / k+1's kernels
+  const bool async_io = host_io && H->host_async && phases == kPhaseAll;
+  const int par = H->apar;
+  if (async_io) {
+    H->apar ^= 1;
+    if (!H->s_in) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&H->s_in, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&H->s_out, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaEventCreateWithFlags(&H->ev_in[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&H->ev_comp[i], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&H->ev_out[i], cudaEventDisableTiming));
+      }
+    }
+    if (H->comp_rec[par]) CUDA_TRY(cudaStreamWaitEvent(H->s_in, H->ev_comp[par], 0));  // x / y staging free
+    if (H->out_rec[par]) CUDA_TRY(cudaStreamWaitEvent(H->s_in, H->ev_out[par], 0));
+  }
+  cudaStream_t s_copy_in = async_io ? H->s_in : H->stream;
   // ---- x: stage when it is host memory, misaligned, or its last column would
   //      be over-read by the 16-byte-granular bulk copies
   const double* xd = x;
   int64_t ldx = n;
-  if (!x_dev || (reinterpret_cast<uintptr_t>(x) & 15) || ((n * nrhs) & 1)) {
+  if (async_io && !x_dev) {
+    const int64_t lds = n + (n & 1);
+    hmat_status st = ensure_buf(&H->xb2[par], &H->xc2[par], size_t(lds) * nrhs + 2);
+    if (st != HMAT_OK) return st;
+    CUDA_TRY(cudaMemcpy2DAsync(H->xb2[par], lds * sizeof(double), x, n * sizeof(double), n * sizeof(double), nrhs,
+                               cudaMemcpyDefault, s_copy_in));
+    xd = H->xb2[par];
+    ldx = lds;
+  } else if (!x_dev || (reinterpret_cast<uintptr_t>(x) & 15) || ((n * nrhs) & 1)) {
     const int64_t lds = n + (n & 1);
     hmat_status st = ensure_buf(&H->xbuf, &H->xcap, size_t(lds) * nrhs + 2);
     if (st != HMAT_OK) return st;
@@ -569,14 +618,19 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   }
   double* yd = y;
   if (!y_dev) {
-    hmat_status st = ensure_buf(&H->ybuf, &H->ycap, size_t(n) * nrhs);
+    hmat_status st = async_io ? ensure_buf(&H->yb2[par], &H->yc2[par], size_t(n) * nrhs)
+                              : ensure_buf(&H->ybuf, &H->ycap, size_t(n) * nrhs);
     if (st != HMAT_OK) return st;
-    yd = H->ybuf;
+    yd = async_io ? H->yb2[par] : H->ybuf;
     if (beta != 0.0) {  // y is an input too
       prof_begin(H, 3, &ep);
-      CUDA_TRY(cudaMemcpyAsync(yd, y, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
+      CUDA_TRY(cudaMemcpyAsync(yd, y, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, s_copy_in));
       prof_end(H, &ep);
     }
+  }
+  if (async_io) {  // the kernels wait for this call's inputs
+    CUDA_TRY(cudaEventRecord(H->ev_in[par], H->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(H->stream, H->ev_in[par], 0));
   }
 
   hmat::StreamArgs a;
@@ -809,6 +863,18 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         ly.grid_e, pack_x, unpack_z);
     if (st2 != HMAT_OK) return st2;
   }
+  if (async_io) {  // y out on s_out once the kernels are done; no host wait
+    CUDA_TRY(cudaEventRecord(H->ev_comp[par], H->stream));
+    H->comp_rec[par] = true;
+    if (!y_dev) {
+      CUDA_TRY(cudaStreamWaitEvent(H->s_out, H->ev_comp[par], 0));
+      CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->s_out));
+      CUDA_TRY(cudaEventRecord(H->ev_out[par], H->s_out));
+      H->out_rec[par] = true;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return HMAT_OK;
+  }
   if (!y_dev && (phases & kPhaseExpand)) {
     prof_begin(H, 3, &ep);
     CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
@@ -889,6 +955,27 @@ hmat_status hmat_local_rows(hmat_t H, int64_t* begin, int64_t* end) {
   if (!H || !begin || !end) return fail(HMAT_ERR_INVALID, "NULL argument");
   *begin = H->plan.row0;
   *end = H->plan.row0 + H->plan.N_loc;
+  return HMAT_OK;
+}
+
+hmat_status hmat_set_host_async(hmat_t H, int enable) {
+  if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
+  CUDA_TRY(cudaSetDevice(H->device));
+  if (H->host_async && !enable) {  // leaving the mode: drain the pipeline
+    if (H->s_in) CUDA_TRY(cudaStreamSynchronize(H->s_in));
+    CUDA_TRY(cudaStreamSynchronize(H->stream));
+    if (H->s_out) CUDA_TRY(cudaStreamSynchronize(H->s_out));
+  }
+  H->host_async = enable != 0;
+  return HMAT_OK;
+}
+
+hmat_status hmat_synchronize(hmat_t H) {
+  if (!H) return fail(HMAT_ERR_INVALID, "H is NULL");
+  CUDA_TRY(cudaSetDevice(H->device));
+  if (H->s_in) CUDA_TRY(cudaStreamSynchronize(H->s_in));
+  CUDA_TRY(cudaStreamSynchronize(H->stream));
+  if (H->s_out) CUDA_TRY(cudaStreamSynchronize(H->s_out));
   return HMAT_OK;
 }
 

@@ -33,7 +33,7 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
            "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local", "hmat_cta_trace",
-           "hmat_cta_trace_read", "hmat_std_exchange_query")
+           "hmat_cta_trace_read", "hmat_std_exchange_query", "hmat_set_host_async", "hmat_synchronize")
 
 
 class hmat_std_exchange_t(ctypes.Structure):
@@ -93,6 +93,8 @@ _sigs = {
     "hmat_launches_per_matvec": (_i64, [_H, _i]),
     "hmat_plan_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_plan_info_t)]),
     "hmat_std_exchange_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_std_exchange_t)]),
+    "hmat_set_host_async": (_i, [_H, _i]),
+    "hmat_synchronize": (_i, [_H]),
     "hmat_peer_export": (_i, [_H, _P]),
     "hmat_cta_trace": (_i, [_H, _i]),
     "hmat_cta_trace_read": (_i, [_H, _i, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(ctypes.c_int)]),
@@ -332,6 +334,16 @@ def hmat_plan_query(depth, dim, leaf_size, rank, nranks=1, rank_id=0) -> hmat_pl
     _check(_lib.hmat_plan_query(depth, dim, leaf_size, rank, nranks, rank_id, ctypes.byref(info)),
            "hmat_plan_query")
     return info
+
+
+def hmat_set_host_async(h, enable: bool = True) -> None:
+    """Asynchronous host-pointer mode (include/hmat.h): host-pointer matvecs
+    return once enqueued; keep x / y valid until hmat_synchronize(h)."""
+    _check(_lib.hmat_set_host_async(h, 1 if enable else 0), "hmat_set_host_async")
+
+
+def hmat_synchronize(h) -> None:
+    _check(_lib.hmat_synchronize(h), "hmat_synchronize")
 
 
 def hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id) -> dict:

@@ -364,3 +364,37 @@ def test_strict_chunked_dense_adjoint():
         assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
     finally:
         hm.hmat_destroy(h)
+
+
+def test_host_async_streaming_mode():
+    """hmat_set_host_async: host-pointer matvecs return once enqueued, copies
+    overlap neighbouring calls; after hmat_synchronize every y is right (the
+    alternating staging buffers are never reused too early), also for 3 rhs
+    and GEMV with beta != 0 (y is an input)."""
+    cfg = HConfig("async", d=2, L=5, b=16, r=4, seed=1401)
+    U, V, D = hgen.inputs(cfg)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        hm.hmat_set_host_async(h, True)
+        xs = [torch.from_numpy(np.ascontiguousarray(hgen.xblock(cfg, nrhs=1, vec=v)[:, 0])).pin_memory()
+              for v in range(5)]
+        ys = [torch.full((cfg.N,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(5)]
+        for x, y in zip(xs, ys):
+            hm.hmat_matvec(h, x, y)
+        x3 = torch.from_numpy(np.ascontiguousarray(hgen.xblock(cfg, nrhs=3, vec=7).T)).pin_memory()
+        y3 = torch.full_like(x3, float("nan")).pin_memory()
+        hm.hmat_matvec(h, x3.t(), y3.t())
+        y0 = np.random.default_rng(5).standard_normal(cfg.N)
+        yb = torch.from_numpy(y0.copy()).pin_memory()
+        hm.hmat_gemv(h, 0, 2.0, xs[0], -1.0, yb)
+        hm.hmat_synchronize(h)
+        for x, y in zip(xs, ys):
+            assert_parity(y.numpy(), oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x.numpy()))
+        assert_parity(y3.t().numpy(), oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x3.t().numpy()))
+        assert_parity(yb.numpy(), 2.0 * oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, xs[0].numpy()) - y0)
+        hm.hmat_set_host_async(h, False)            # back to blocking: returns with y home
+        yy = torch.empty(cfg.N, dtype=torch.float64).pin_memory()
+        hm.hmat_matvec(h, xs[1], yy)
+        assert_parity(yy.numpy(), ys[1].numpy())
+    finally:
+        hm.hmat_destroy(h)
