@@ -59,6 +59,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.max_stages_p = env_int("HMAT_MAX_STAGES_P", env_int("HMAT_MAX_STAGES", o.max_stages_p));
   o.max_stages_e = env_int("HMAT_MAX_STAGES_E", env_int("HMAT_MAX_STAGES", o.max_stages_e));
   o.dmma_kr = env_int("HMAT_DMMA_KR", o.dmma_kr);
+  o.max_nr = env_int("HMAT_MAX_NR", o.max_nr);
   o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
   return o;
 }

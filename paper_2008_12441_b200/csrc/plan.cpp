@@ -166,6 +166,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.grid_p_max = 0;
   for (int li = 0; li < 4; ++li) {
     const int64_t NR = int64_t(1) << li;
+    if (NR > std::max(1, opt.max_nr)) break;  // widest SIMT pass allowed
     Plan::Layout& y = p.lay[li];
     y.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + NR * p.xs_p * 8, 128);
     const int64_t zrows = opt.peer ? P : 1;  // peer exchange: one z row per rank on exchange levels

@@ -100,6 +100,8 @@ struct PlanOptions {
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
   int dmma_kr = kDmmaKR;            // DMMA project: V rows per stage (16 or 32)
+  int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
+                                    // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
 };
 
