@@ -319,3 +319,44 @@ def test_strict_block_loop_brute_force_and_equivalence(d, L, b, r):
     y = oracle.matvec_strict(d, L, b, r, U, V, Dc, x)
     assert rel(y, A @ x) < 1e-13
     assert rel(oracle.matvec(d, L - 1, c * b, r, U, V, Dc, x), y) < 1e-14
+
+
+def unit_column(d, L, b, r, U, V, D, j):
+    """H e_j written straight from the block structure, in
+    O(N r) without the oracle's loops: the dense leaf block of j's leaf gives
+    column j mod b of D_leaf in that leaf's rows; at every level l the node
+    s = anc_l(j) is the SOURCE of the blocks (t, s) for each sibling t of s, whose
+    column j is U_ts V_ts[j - s m_l, :]^T in t's rows.  Panel addressing per
+    include/hmat.h: U_l row i, slot q = sibling q of t (target-major); V_l row j,
+    slot q' = sibling q' of s, i.e. the target (source-major)."""
+    c = 1 << d
+    N = b * c ** L
+    col = np.zeros(N)
+    k = j // b
+    col[k * b:(k + 1) * b] += D[k * b:(k + 1) * b, j - k * b]
+    for l in range(1, L + 1):
+        m = N // c ** l
+        s = j // m
+        me = s % c
+        for qp in range(c - 1):                     # targets t = siblings of s, V slot qp
+            t = (s // c) * c + (qp if qp < me else qp + 1)
+            q = me if me < t % c else me - 1        # slot of s in t's list (U's column block)
+            v = V[l - 1][j, qp * r:(qp + 1) * r]
+            col[t * m:(t + 1) * m] += U[l - 1][t * m:(t + 1) * m, q * r:(q + 1) * r] @ v
+    return col
+
+
+@pytest.mark.parametrize("d,L,b,r", [(2, 6, 16, 4), (3, 4, 8, 3), (1, 12, 4, 2)])
+def test_unit_columns_at_scale(d, L, b, r):
+    """Columns of H from the definition vs the oracle's block loop on unit
+    vectors, at N = 2^14..2^16 (beyond brute-force assembly): catches a slot map
+    or node range that is only wrong away from the tiny shapes."""
+    U, V, D = rand_panels(d, L, b, r, 500 + d + L)
+    N = len(D)
+    rng = np.random.default_rng(17)
+    js = rng.integers(0, N, 12)
+    X = np.zeros((N, len(js)))
+    X[js, np.arange(len(js))] = 1.0
+    Y = oracle.matvec(d, L, b, r, U, V, D, X)
+    for k, j in enumerate(js):
+        assert rel(Y[:, k], unit_column(d, L, b, r, U, V, D, int(j))) < 1e-14
