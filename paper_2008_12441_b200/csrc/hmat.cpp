@@ -61,6 +61,11 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dmma_kr = env_int("HMAT_DMMA_KR", o.dmma_kr);
   o.max_nr = env_int("HMAT_MAX_NR", o.max_nr);
   o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
+  o.dmma_off = env_int("HMAT_DMMA_OFF", 0);
+  o.dmma_min = env_int("HMAT_DMMA_MIN", 16);
+  o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
+  o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
+  o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
   return o;
 }
 
@@ -402,8 +407,8 @@ hmat_status encode_map(CUtensorMap* m, int rank, const void* base, const uint64_
 }
 
 bool use_dmma(const hmat::Plan& p, int nrhs) {
-  if (!p.dmma_ok || env_int("HMAT_DMMA_OFF", 0)) return false;
-  return nrhs >= env_int("HMAT_DMMA_MIN", 16);
+  if (!p.dmma_ok || p.dmma_off) return false;
+  return nrhs >= p.dmma_min;
 }
 
 hmat_status ensure_dmma(hmat_s* H) {
@@ -688,7 +693,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.mb = H->mb;
   a.done = H->done;
   a.zex_base = H->zex;
-  a.dbg = env_int("HMAT_DEBUG_SKIP", 0);
+  a.dbg = p.dbg;
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
@@ -807,13 +812,13 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     // expand's dynamic chunks of 1 item (0 = static ranges: for standard
     // admissibility, where the static ranges measured faster (s2: 4.0 vs 4.5 ms),
     // and when an item has no stage at all, which the chunk protocol needs)
-    a.chunk_e = env_int("HMAT_EXPAND_CHUNK", p.adm ? 0 : 1);
+    a.chunk_e = p.expand_chunk >= 0 ? p.expand_chunk : (p.adm ? 0 : 1);
     if (!level_mask && !dense) a.chunk_e = 0;
     // project: the last active level in dynamic chunks of whole nodes (>= 4
     // stages), when it is local (no exchange) and has at least 2 chunks per CTA
     a.dyn_level = 0;
     a.sched_p = H->sched + 4;
-    if (level_mask && env_int("HMAT_PROJECT_DYN", 1)) {
+    if (level_mask && p.project_dyn) {
       const int ll = 64 - __builtin_clzll(level_mask);
       const int64_t SLs = p.N_loc / p.Rp, seg = std::min<int64_t>(p.m[ll], p.N_loc) / p.Rp;
       int64_t ch = seg;

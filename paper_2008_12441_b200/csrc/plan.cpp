@@ -69,6 +69,11 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.b = leaf;
   p.r = rank;
   p.adm = opt.adm;
+  p.dmma_off = opt.dmma_off;
+  p.dmma_min = opt.dmma_min;
+  p.dbg = opt.dbg;
+  p.expand_chunk = opt.expand_chunk;
+  p.project_dyn = opt.project_dyn;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;

@@ -80,6 +80,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
+  int dmma_off = 0, dmma_min = 16, dbg = 0, expand_chunk = -1, project_dyn = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage, 16 or 32
   int dns_p = 0, dns_e = 0;
@@ -100,6 +101,11 @@ struct PlanOptions {
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
   int dmma_kr = kDmmaKR;            // DMMA project: V rows per stage (16 or 32)
+  // per-call switches, read once at hmat_create (HMAT_* environment)
+  int dmma_off = 0, dmma_min = 16;  // tensor-core path off / from this many rhs
+  int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)
+  int expand_chunk = -1;            // expand items per dynamic chunk (-1 = default, 0 = static)
+  int project_dyn = 1;              // project's last level in dynamic chunks
   int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
