@@ -58,7 +58,6 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.smem_budget = env_int("HMAT_SMEM_KB", 200) * 1024;
   o.max_stages_p = env_int("HMAT_MAX_STAGES_P", env_int("HMAT_MAX_STAGES", o.max_stages_p));
   o.max_stages_e = env_int("HMAT_MAX_STAGES_E", env_int("HMAT_MAX_STAGES", o.max_stages_e));
-  o.dmma_kr = env_int("HMAT_DMMA_KR", o.dmma_kr);
   o.max_nr = env_int("HMAT_MAX_NR", o.max_nr);
   o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
   o.dmma_off = env_int("HMAT_DMMA_OFF", 0);
@@ -743,6 +742,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     if (st != HMAT_OK) return st;
     a.vp = p.vp;
     a.dkr = p.dkr;
+    a.dkc = p.dkc;
     a.nstage_p = p.dns_p;
     a.stage_bytes_p = p.dstage_p;
     a.bar_off_p = p.dns_p * p.dstage_p;
@@ -757,13 +757,13 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       const uint32_t box[3] = {uint32_t(p.vp), uint32_t(p.dkr), 1};
       hmat_status st3 = encode_map(&a.tm_v, 3, a.V, dims, strides, box);
       if (st3 != HMAT_OK) return st3;
-      const uint32_t ubox[3] = {uint32_t(hmat::kDmmaKC + 4), uint32_t(hmat::kDmmaRE), 1};
+      const uint32_t ubox[3] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaRE), 1};
       if ((st3 = encode_map(&a.tm_u, 3, a.U, dims, strides, ubox)) != HMAT_OK) return st3;
     }
     {  // D-role panel [N_loc][Dp], box [64][KC+4]
       const uint64_t dims[2] = {uint64_t(p.Dp), uint64_t(n)};
       const uint64_t strides[1] = {uint64_t(p.Dp) * 8};
-      const uint32_t box[2] = {uint32_t(hmat::kDmmaKC + 4), uint32_t(hmat::kDmmaRE)};
+      const uint32_t box[2] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaRE)};
       hmat_status st3 = encode_map(&a.tm_d, 2, a.D, dims, strides, box);
       if (st3 != HMAT_OK) return st3;
     }
@@ -777,7 +777,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         const uint32_t box[2] = {uint32_t(p.dkr + 4), uint32_t(hmat::kDmmaNB)};
         hmat_status st3 = encode_map(&a.tm_x, 2, a.x, dims, strides, box);
         if (st3 != HMAT_OK) return st3;
-        const uint32_t xbox[2] = {uint32_t(hmat::kDmmaKC + 4), uint32_t(hmat::kDmmaNB)};
+        const uint32_t xbox[2] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaNB)};
         if ((st3 = encode_map(&a.tm_xe, 2, a.x, dims, strides, xbox)) != HMAT_OK) return st3;
       }
       for (int l = 1; l <= p.L; ++l) {

@@ -64,7 +64,8 @@ struct StreamArgs {
   int64_t stage_bytes_e, items_e;
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows
-  int dkr;             // DMMA project: V rows per stage (16 or 32)
+  int dkr;             // DMMA project: V rows per stage (32)
+  int dkc;             // DMMA expand: k-columns per stage (32, or 16 when W % 32 != 0)
   int dbg;             // diagnostics only (HMAT_DEBUG_SKIP): bit 0 skips project's math, bit 1 expand's
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
   // CTA pushes this rank's exchange levels into slot `rank` of every rank's

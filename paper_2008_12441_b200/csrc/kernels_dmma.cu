@@ -30,9 +30,6 @@ constexpr int kMaxThreadsP = kDmmaProjWarps * 32;
 constexpr int NB = kDmmaNB;   // right-hand sides per pass
 constexpr int kThreadsE = 256;  // expand: 8 warps, no producer warp
 constexpr int RE = kDmmaRE;   // expand: rows per item
-constexpr int KC = kDmmaKC;   // expand: k-columns per stage
-constexpr int XP = kDmmaXP;   // smem pitch of staged X columns (= 4 mod 16)
-constexpr int AP = kDmmaAP;   // smem pitch of staged U / D row chunks (= 4 mod 16)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -64,17 +61,20 @@ __device__ __forceinline__ double* zt_column(const StreamArgs& a, const LevelArg
 // ============================ project ========================================
 // KR: V rows (the GEMM's k) per stage; the staged x columns have pitch KR + 4
 // (= 4 mod 16 doubles: conflict-free B-fragment loads).
-// MT = W / 32: the W x NB accumulator tile is split over 16 warps as 4 column
-// groups (MT M-tiles of 8 columns) x 4 rhs groups (2 N-tiles of 8 rhs), so each
-// of the SM's 4 sub-partitions runs exactly 4 warps (a W/16-warp split leaves 3
-// or 4 warps per sub-partition: with W = 224 the tensor pipe then idles 1/8).
+// The W x NB accumulator tile is split over 16 warps as MG column groups (MT
+// M-tiles of 8 columns each) x NG = 8 / NT rhs groups (NT N-tiles of 8 rhs),
+// MG NG = 16: NT = 2 (MG = 4, MT = W/32) when W % 32 == 0, else NT = 1 (MG = 2,
+// MT = W/16).  Each of the SM's 4 sub-partitions runs exactly 4 warps (a
+// W/16-warp split leaves 3 or 4 warps per sub-partition: with W = 224 the
+// tensor pipe then idles 1/8).
 // No producer warp: a stage is two tensor-TMA copies (the KR x VP block of V
 // rows, padding columns out of bounds = zero-filled, and the NB x (KR+4) block
 // of x), issued by the LAST warp to finish reading the slot (smem counter), so
 // all 16 warps compute and each gets 128 registers.
-template <int KR, int MT>
+template <int KR, int MT, int NT>
 __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int XPP = KR + 4;
+  constexpr int NG = 8 / NT, MG = kDmmaProjWarps / NG;
   constexpr int NCW = kDmmaProjWarps;
   constexpr int CTP = NCW * 32;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -126,13 +126,13 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
     advance();
   }
 
-  const int mg = warp & 3, ng = warp >> 2;  // columns [mg 8 MT, (mg+1) 8 MT), rhs [16 ng, 16 ng + 16)
+  const int mg = warp % MG, ng = warp / MG;  // columns [mg 8 MT, (mg+1) 8 MT), rhs [8 NT ng, 8 NT (ng+1))
   const int g = lane >> 2, tq = lane & 3;
-  double acc[MT][2][2];
+  double acc[MT][NT][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   int slot = 0;
   uint32_t phase = 0;
@@ -146,18 +146,18 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
       dev::mbar_wait(&full[slot], phase);
       const double* Vs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p) + mg * 8 * MT + g;
       const double* Xs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p + vbytes) +
-                         (ng * 16 + g) * XPP + tq;
+                         (ng * 8 * NT + g) * XPP + tq;
 #pragma unroll
       for (int ks = 0; ks < KR / 4; ++ks) {
-        double av[MT], bv[2];
+        double av[MT], bv[NT];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) av[mt] = Vs[(ks * 4 + tq) * VP + mt * 8];  // A = V^T
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) bv[nt] = Xs[nt * 8 * XPP + ks * 4];          // B = X
+        for (int nt = 0; nt < NT; ++nt) bv[nt] = Xs[nt * 8 * XPP + ks * 4];         // B = X
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
       }
       // release the slot: the last of the 16 warps refills it with the stage
       // NS ahead (its smem reads are complete: their values fed the DMMAs)
@@ -192,16 +192,16 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
       if (complete) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          // column w = q r + aa; rhs n = 16 ng + 8 nt + 2 tq + h  ->
-          // zfrag(0, n) = 64 ng + 16 tq + 8 h + nt
+          // column w = q r + aa; rhs n = 8 NT ng + 8 nt + 2 tq + h
           const int w = (mg * MT + mt) * 8 + g;
           const int q = w / a.r;
-          double* zc = zt_column(a, lv, sg, q, w - q * a.r) + ng * 64 + tq * 16;
+          double* zc = zt_column(a, lv, sg, q, w - q * a.r);
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
+          for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (ng * 16 + nt * 8 + tq * 2 + h < a.nr) zc[h * 8 + nt] = acc[mt][nt][h];
+              const int n = (ng * NT + nt) * 8 + tq * 2 + h;
+              if (n < a.nr) zc[zfrag(0, n)] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -212,10 +212,10 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
         for (int mt = 0; mt < MT; ++mt) {
           const int w = (mg * MT + mt) * 8 + g;
 #pragma unroll
-          for (int nt = 0; nt < 2; ++nt)
+          for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              pp[(int64_t)w * NB + ng * 16 + nt * 8 + tq * 2 + h] = acc[mt][nt][h];
+              pp[(int64_t)w * NB + (ng * NT + nt) * 8 + tq * 2 + h] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -260,8 +260,12 @@ __global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __g
 // the leaf's x (tm_xe); the extra 4 columns / rows give the conflict-free
 // pitch AP = XP = KC + 4 and are never read.  As in project, no producer warp:
 // the last of the 8 warps to finish a slot refills it.
+// KC: k-columns per stage (32, or 16 when W % 32 != 0); the staged U / D row
+// chunks and x columns have pitch KC + 4 (= 4 mod 16 doubles).
+template <int KC>
 __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int NCW = kThreadsE / 32;
+  constexpr int AP = KC + 4, XP = KC + 4;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -414,52 +418,60 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   }
 }
 
-template <int KR>
-cudaError_t launch_project_kr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  switch (a.W / 32) {
-    case 1: project_dmma_kernel<KR, 1><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-    case 2: project_dmma_kernel<KR, 2><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-    case 3: project_dmma_kernel<KR, 3><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-    case 4: project_dmma_kernel<KR, 4><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-    case 5: project_dmma_kernel<KR, 5><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-    case 6: project_dmma_kernel<KR, 6><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-    default: project_dmma_kernel<KR, 7><<<grid, kMaxThreadsP, smem, s>>>(a); break;
-  }
-  return cudaGetLastError();
+template <int MT, int NT>
+void launch_p(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  project_dmma_kernel<kDmmaKR, MT, NT><<<grid, kMaxThreadsP, smem, s>>>(a);
 }
 
-template <int KR>
-cudaError_t configure_project_kr(int64_t smem) {
-  cudaError_t e = cudaSuccess;
-  auto set = [&](auto kern) {
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  };
-  set(project_dmma_kernel<KR, 1>);
-  set(project_dmma_kernel<KR, 2>);
-  set(project_dmma_kernel<KR, 3>);
-  set(project_dmma_kernel<KR, 4>);
-  set(project_dmma_kernel<KR, 5>);
-  set(project_dmma_kernel<KR, 6>);
-  set(project_dmma_kernel<KR, 7>);
-  return e;
+template <int MT, int NT>
+cudaError_t set_p(int64_t smem) {
+  return cudaFuncSetAttribute(project_dmma_kernel<kDmmaKR, MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem);
 }
 
 }  // namespace
 
+// W % 32 == 0: NT = 2, MT = W / 32 (1..7); else W % 16 == 0: NT = 1, MT = W / 16 (1, 3, 5, 7)
 cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  return a.dkr == 16 ? launch_project_kr<16>(a, grid, smem, s) : launch_project_kr<32>(a, grid, smem, s);
+  if (a.W % 32 == 0) {
+    switch (a.W / 32) {
+      case 1: launch_p<1, 2>(a, grid, smem, s); break;
+      case 2: launch_p<2, 2>(a, grid, smem, s); break;
+      case 3: launch_p<3, 2>(a, grid, smem, s); break;
+      case 4: launch_p<4, 2>(a, grid, smem, s); break;
+      case 5: launch_p<5, 2>(a, grid, smem, s); break;
+      case 6: launch_p<6, 2>(a, grid, smem, s); break;
+      default: launch_p<7, 2>(a, grid, smem, s); break;
+    }
+  } else {
+    switch (a.W / 16) {
+      case 1: launch_p<1, 1>(a, grid, smem, s); break;
+      case 3: launch_p<3, 1>(a, grid, smem, s); break;
+      case 5: launch_p<5, 1>(a, grid, smem, s); break;
+      default: launch_p<7, 1>(a, grid, smem, s); break;
+    }
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  expand_dmma_kernel<<<grid, kThreadsE, smem, s>>>(a);
+  if (a.dkc == 16)
+    expand_dmma_kernel<16><<<grid, kThreadsE, smem, s>>>(a);
+  else
+    expand_dmma_kernel<32><<<grid, kThreadsE, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e) {
-  cudaError_t e = configure_project_kr<16>(smem_p);
-  if (e != cudaSuccess) return e;
-  if ((e = configure_project_kr<32>(smem_p)) != cudaSuccess) return e;
-  return cudaFuncSetAttribute(expand_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+  cudaError_t e;
+  if ((e = set_p<1, 2>(smem_p)) || (e = set_p<2, 2>(smem_p)) || (e = set_p<3, 2>(smem_p)) ||
+      (e = set_p<4, 2>(smem_p)) || (e = set_p<5, 2>(smem_p)) || (e = set_p<6, 2>(smem_p)) ||
+      (e = set_p<7, 2>(smem_p)) || (e = set_p<1, 1>(smem_p)) || (e = set_p<3, 1>(smem_p)) ||
+      (e = set_p<5, 1>(smem_p)) || (e = set_p<7, 1>(smem_p)))
+    return e;
+  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
+    return e;
+  return cudaFuncSetAttribute(expand_dmma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
 }
 
 }  // namespace hmat

@@ -203,17 +203,21 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     p.grid_p_max = std::max(p.grid_p_max, y.grid_p);
   }
   // DMMA layouts (1 project CTA per SM: 2 stages of ~77 KB; 2 expand CTAs per SM)
-  p.dkr = opt.dmma_kr == 16 ? 16 : kDmmaKR;
-  p.dmma_ok = p.adm == 0 && !opt.peer && p.W % 32 == 0 && p.W <= 224 && leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
+  // W % 32 == 0: 4 column groups of W/32 M-tiles, 32-column expand chunks;
+  // W % 16 == 0: 2 column groups of W/16 M-tiles (<= 7), 16-column chunks
+  p.dkr = kDmmaKR;
+  p.dkc = p.W % 32 == 0 ? 32 : 16;
+  p.dmma_ok = p.adm == 0 && !opt.peer && p.W % 16 == 0 && (p.W % 32 == 0 ? p.W <= 224 : p.W <= 112) &&
+              leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
     // V rows + the 64 x columns (pitch dkr + 4 = 4 mod 16 doubles)
     p.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(kDmmaNB) * (p.dkr + 4) * 8, 128);
-    p.dstage_e = round_up(int64_t(kDmmaRE) * kDmmaAP * 8 +
-                              std::max(int64_t(kDmmaKC) * kDmmaNB * 8, int64_t(kDmmaNB) * kDmmaXP * 8),
+    p.dstage_e = round_up(int64_t(kDmmaRE) * (p.dkc + 4) * 8 +
+                              std::max(int64_t(p.dkc) * kDmmaNB * 8, int64_t(kDmmaNB) * (p.dkc + 4) * 8),
                           128);
     p.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (226 * 1024 - bar_bytes) / p.dstage_p));
-    p.dns_e = static_cast<int>(std::min<int64_t>(3, (112 * 1024 - bar_bytes) / p.dstage_e));
+    p.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 32 ? 3 : 5, (112 * 1024 - bar_bytes) / p.dstage_e));
     p.dsmem_p = p.dns_p * p.dstage_p + bar_bytes;
     p.dsmem_e = p.dns_e * p.dstage_e + bar_bytes;
     p.dgrid_p = static_cast<int>(std::min<int64_t>(opt.num_sms, depth > 0 ? p.N_loc / p.dkr : 0));

@@ -29,7 +29,7 @@ void std_slot_tables(int16_t code[3][8][kStdMaxSlots], int16_t slot[3][8][kStdMa
 
 // FP64 tensor-core (DMMA) path for many right-hand sides (kernels_dmma.cu)
 constexpr int kDmmaNB = 64;   // right-hand sides per pass
-constexpr int kDmmaKR = 32;   // project: V rows per stage (largest supported; Plan::dkr picks 16 or 32)
+constexpr int kDmmaKR = 32;   // project: V rows per stage
 constexpr int kDmmaRE = 64;   // expand: rows per item
 constexpr int kDmmaKC = 32;   // expand: k-columns per stage
 constexpr int kDmmaXP = 36;   // smem pitch of staged x columns (= 4 mod 16 doubles)
@@ -82,7 +82,8 @@ struct Plan {
   bool dmma_ok = false;
   int dmma_off = 0, dmma_min = 16, dbg = 0, expand_chunk = -1, project_dyn = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
-  int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage, 16 or 32
+  int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
+  int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
   int dns_p = 0, dns_e = 0;
   int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
   int dgrid_p = 0, dgrid_e = 0;
@@ -100,7 +101,6 @@ struct PlanOptions {
   int max_stages_e = 3;             // expand: measured best at 3 stages x 2 CTAs per SM
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
-  int dmma_kr = kDmmaKR;            // DMMA project: V rows per stage (16 or 32)
   // per-call switches, read once at hmat_create (HMAT_* environment)
   int dmma_off = 0, dmma_min = 16;  // tensor-core path off / from this many rhs
   int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)

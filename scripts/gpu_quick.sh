@@ -1,5 +1,7 @@
 #!/bin/bash
 set -u
 mkdir -p gpurun_out
-timeout 900 python scripts/kernel_sweep.py c3 "NRHS=4" "NRHS=8" "NRHS=8,HMAT_MAX_NR=4" "NRHS=8,HMAT_MAX_NR=2" "NRHS=6" "NRHS=6,HMAT_MAX_NR=4" "NRHS=3" "NRHS=3,HMAT_MAX_NR=2" > gpurun_out/nrhs_sweep.log 2>&1
-timeout 900 python scripts/kernel_sweep.py c2 "NRHS=4" "NRHS=8" "NRHS=8,HMAT_MAX_NR=4" "NRHS=8,HMAT_MAX_NR=2" "NRHS=16,HMAT_MAX_NR=4" "NRHS=4,HMAT_MAX_NR=2" >> gpurun_out/nrhs_sweep.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_multirank.py -x -q -k "dmma or DMMA or c5 or adjoint" > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?"
+timeout 900 python scripts/kernel_sweep.py c5 "" > gpurun_out/quick_sweep.log 2>&1
+timeout 900 python scripts/kernel_sweep.py c2 "NRHS=64" "NRHS=64,HMAT_DMMA_OFF=1" >> gpurun_out/quick_sweep.log 2>&1
+timeout 900 python scripts/kernel_sweep.py c4 "NRHS=64" >> gpurun_out/quick_sweep.log 2>&1

@@ -188,7 +188,12 @@ def test_full_size_sampled_rows(name):
 
 
 DMMA = [HConfig("d3L2", d=3, L=2, b=64, r=32, seed=501), HConfig("d3L3", d=3, L=3, b=64, r=32, seed=502),
-        HConfig("d2L3", d=2, L=3, b=64, r=32, seed=503), HConfig("d2b128", d=2, L=3, b=128, r=64, seed=504)]
+        HConfig("d2L3", d=2, L=3, b=64, r=32, seed=503), HConfig("d2b128", d=2, L=3, b=128, r=64, seed=504),
+        # W % 32 != 0: 2 column groups x 8 rhs groups, 16-column expand chunks
+        HConfig("d2r16", d=2, L=4, b=64, r=16, seed=505),    # W = 48 (the c2 / c4 shape)
+        HConfig("d3r16", d=3, L=2, b=64, r=16, seed=506),    # W = 112
+        HConfig("d1r16", d=1, L=6, b=64, r=16, seed=507),    # W = 16
+        HConfig("d1r80", d=1, L=5, b=128, r=80, seed=508)]   # W = 80
 
 
 @pytest.mark.parametrize("cfg", DMMA, ids=lambda c: c.name)
