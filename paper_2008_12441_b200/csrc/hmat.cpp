@@ -672,7 +672,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.Re = p.Re;
   a.ndc = p.ndc;
   a.dc = p.dc;
-  if (p.ndc > 1) {  // the dense block's column-chunk boxes [Re][dc]
+  a.dgs = p.dgs;
+  if (p.ndc > 1 && !p.adm) {  // the dense block's column-chunk boxes [Re][dc]
     const uint64_t dims[2] = {uint64_t(p.Dp), uint64_t(p.N_loc)};
     const uint64_t strides[1] = {uint64_t(p.Dp) * 8};
     const uint32_t box[2] = {uint32_t(p.dc), uint32_t(p.Re)};

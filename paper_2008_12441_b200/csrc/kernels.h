@@ -55,7 +55,8 @@ struct StreamArgs {
   int* cnt;          // [L][grid_p] arrival tickets
   // expand schedule
   int Re, tpr, nstage_e;
-  int ndc, dc;       // expand: dense block in ndc column-chunk stages of dc columns (ndc > 1: box tm_dse)
+  int ndc, dc;       // expand: dense stages per item (weak, ndc > 1: column chunks of dc columns, box tm_dse;
+  int dgs;           //   standard: groups of dgs near-field blocks)
   int64_t chunk_e;   // expand: 0 = static item ranges; > 0 = dynamic chunks of chunk_e items
   int* sched;        // expand: [next chunk, CTAs done] (re-armed by the last CTA)
   int dyn_level;     // project: the level handed out in dynamic chunks (0 = none)

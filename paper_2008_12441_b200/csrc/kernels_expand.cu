@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
               dev::bulk_g2s(st + ub, zrow, zb, &full[slot], pol_keep);
             }
           }
-        } else if (a.ndc > 1) {
+        } else if (a.ndc > 1 && !a.adm) {
           // column chunk h of the (weak) dense block: the Re x dc box of D
           // (tensor TMA) + the chunk's x segment per rhs; lane 0 issues
           const int h = l - L - 1;
@@ -226,13 +226,16 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           }
           first_stage = false;
         } else {
-          // one stage holds every dense block of the tile's rows, block e at
-          // byte offset e * dblk followed by its source x segment (16-byte
-          // aligned superset per rhs); lanes issue their own blocks
+          // one stage holds the dense blocks e of group h = l - L - 1 (weak: the
+          // single leaf block; standard: neighbours [h dgs, (h+1) dgs)), block e
+          // at byte offset (e - h dgs) * dblk followed by its source x segment
+          // (16-byte aligned superset per rhs); lanes issue their own blocks
+          const int e0 = (l - L - 1) * a.dgs;
+          const bool lane_on = src != kNone && lane >= e0 && lane < e0 + a.dgs;
           uint32_t mine = 0;
           int64_t lo[NR];
           uint32_t xb[NR];
-          if (src != kNone) {
+          if (lane_on) {
             mine = db;
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk) {
@@ -250,8 +253,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           first_stage = false;
           if (lane == 0) dev::mbar_arrive_expect_tx(&full[slot], total);
           __syncwarp();
-          if (src != kNone) {
-            unsigned char* se = st + lane * dblk;
+          if (lane_on) {
+            unsigned char* se = st + (lane - e0) * dblk;
             dev::bulk_g2s(se, a.D + lane * a.d_stride + i0 * Dp, db, &full[slot], pol_stream);
 #pragma unroll
             for (int kk = 0; kk < NR; ++kk)
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             if (++jj == njU) jj = 0;
           }
           }
-        } else if (a.ndc > 1) {
+        } else if (a.ndc > 1 && !a.adm) {
           // column chunk h: D box [Re][dc] + x[leaf0 + h dc, + dc)
           const int NPC = a.dc >> 1;
           const double2* D2 = reinterpret_cast<const double2*>(st) + ri * NPC;
@@ -417,9 +420,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           }
         } else {
           const int64_t dblk = int64_t(Re) * Dp * 8 + int64_t(NR) * a.xs_e * 8;
-          for (int e = 0; e < a.nd; ++e) {  // dense blocks present in this stage
+          const int e0 = (l - L - 1) * a.dgs;
+          for (int e = e0; e < e0 + a.dgs; ++e) {  // dense blocks present in this stage
             if (!((nmask >> e) & 1u)) continue;
-            const unsigned char* se = st + e * dblk;
+            const unsigned char* se = st + (e - e0) * dblk;
             const double2* D2 = reinterpret_cast<const double2*>(se) + ri * NPD;
             const double* xs = reinterpret_cast<const double*>(se + Re * Dp * 8);
             const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;

@@ -154,10 +154,13 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   // A wide dense leaf block (paper-strict structure: 2^d b columns) travels in
   // column chunks of 64 (one tensor-TMA box each), so the stages stay U-sized
   // and the item keeps 64 rows.
-  p.ndc = (p.adm == 0 && leaf > 64 && leaf % 64 == 0) ? leaf / 64 : 1;
-  p.dc = leaf / p.ndc;
+  // Standard admissibility: the 3^d near-field blocks travel in 3 stages of
+  // 3^(d-1) neighbours (d >= 2), so a dense stage is not larger than a U stage.
+  p.ndc = (p.adm == 0 && leaf > 64 && leaf % 64 == 0) ? leaf / 64 : (p.adm && p.d >= 2 ? 3 : 1);
+  p.dc = p.adm ? leaf : leaf / p.ndc;
+  p.dgs = p.adm ? p.nd / p.ndc : 1;  // dense blocks (neighbours) per dense stage
   const int64_t dcp = p.dc + (p.dc & 1);
-  p.Re = pick_rows(leaf, kConsumerThreads, std::max<int64_t>(p.Wp, int64_t(p.nd) * dcp),
+  p.Re = pick_rows(leaf, kConsumerThreads, std::max<int64_t>(p.Wp, int64_t(p.dgs) * dcp),
                    p.adm ? std::max<int64_t>(cap, 48 * 1024) : cap);
   p.tpr = 1;
   while (p.tpr * 2 <= 32 && p.tpr * 2 * p.Re <= kConsumerThreads) p.tpr *= 2;
@@ -176,7 +179,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     y.stage_bytes_p = round_up(int64_t(p.Rp) * p.Wp * 8 + NR * p.xs_p * 8, 128);
     const int64_t zrows = opt.peer ? P : 1;  // peer exchange: one z row per rank on exchange levels
     y.stage_bytes_e = round_up(std::max(int64_t(p.Re) * p.Wp * 8 + int64_t(p.Wp) * NR * 8 * zrows,
-                                        int64_t(p.nd) * (int64_t(p.Re) * (p.dc + (p.dc & 1)) * 8 + NR * p.xs_e * 8)),
+                                        int64_t(p.dgs) * (int64_t(p.Re) * (p.dc + (p.dc & 1)) * 8 + NR * p.xs_e * 8)),
                                128);
     const int64_t red_bytes = round_up(2 * int64_t(rg) * p.Wp * NR * 8, 128);  // two alternating buffers
     // the requested CTAs per SM, or fewer if two pipeline stages do not fit

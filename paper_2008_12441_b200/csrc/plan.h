@@ -63,7 +63,8 @@ struct Plan {
   // schedule
   int Rp = 0, Re = 0;               // rows per pipeline stage: project / expand (both divide b)
   int tpr = 0;
-  int ndc = 1, dc = 0;              // expand: dense block in ndc column chunks of dc columns                      // expand: threads per row
+  int ndc = 1, dc = 0;              // expand: dense stages per item: weak = column chunks of dc columns,
+  int dgs = 1;                      //   standard = groups of dgs near-field blocks                      // expand: threads per row
   int64_t stages_p = 0;             // L * N_loc / Rp
   int64_t items_e = 0;              // N_loc / Re
   int xs_p = 0, xs_e = 0;           // doubles reserved per rhs for x chunks in a stage
