@@ -34,6 +34,12 @@ def report(name, recs):
           f"end min/med/p90/max {ends[0]:.1f}/{q(ends, .5):.1f}/{q(ends, .9):.1f}/{ends[-1]:.1f} us | "
           f"dur min/med/max {durs[0]:.1f}/{q(durs, .5):.1f}/{durs[-1]:.1f} us | "
           f"idle {1 - sum(durs) / (len(durs) * ends[-1]):.1%} of CTA-slots")
+    sm_end = collections.defaultdict(float)
+    for r in recs:
+        sm_end[r[2]] = max(sm_end[r[2]], (r[1] - t0) / 1e3)
+    se = sorted(sm_end.values())
+    print(f"  {name}: per-SM last end min/med/max {se[0]:.1f}/{q(se, .5):.1f}/{se[-1]:.1f} us "
+          f"(SM-level idle {1 - sum(se) / (len(se) * se[-1]):.1%})")
     per_sm = collections.Counter(r[2] for r in recs)
     print(f"  {name}: {len(per_sm)} SMs used, CTAs per SM {sorted(collections.Counter(per_sm.values()).items())}")
     slow = sorted(enumerate(recs), key=lambda e: e[1][1] - e[1][0], reverse=True)[:6]
