@@ -65,6 +65,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
+  o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   return o;
 }
 
@@ -744,6 +745,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     a.vp = p.vp;
     a.dkr = p.dkr;
     a.dkc = p.dkc;
+    a.dnw = p.dnw;
     a.nstage_p = p.dns_p;
     a.stage_bytes_p = p.dstage_p;
     a.bar_off_p = p.dns_p * p.dstage_p;

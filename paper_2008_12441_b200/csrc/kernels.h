@@ -67,6 +67,7 @@ struct StreamArgs {
   int vp;              // DMMA project: smem pitch of staged V rows
   int dkr;             // DMMA project: V rows per stage (32)
   int dkc;             // DMMA expand: k-columns per stage (32, or 16 when W % 32 != 0)
+  int dnw;             // DMMA project: warps per CTA (16, or 8 with two CTAs per SM)
   int dbg;             // diagnostics only (HMAT_DEBUG_SKIP): bit 0 skips project's math, bit 1 expand's
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
   // CTA pushes this rank's exchange levels into slot `rank` of every rank's

@@ -71,11 +71,14 @@ __device__ __forceinline__ double* zt_column(const StreamArgs& a, const LevelArg
 // rows, padding columns out of bounds = zero-filled, and the NB x (KR+4) block
 // of x), issued by the LAST warp to finish reading the slot (smem counter), so
 // all 16 warps compute and each gets 128 registers.
-template <int KR, int MT, int NT>
-__global__ void __launch_bounds__(kMaxThreadsP, 1) project_dmma_kernel(const __grid_constant__ StreamArgs a) {
+// NW warps per CTA: 16 (one CTA per SM) or 8 (two CTAs per SM, used for
+// W % 32 != 0 so that a warp still holds 2 N-tiles: MT + 2 fragment loads per
+// 2 MT DMMAs instead of MT + 1 per MT).
+template <int KR, int MT, int NT, int NW>
+__global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int XPP = KR + 4;
-  constexpr int NG = 8 / NT, MG = kDmmaProjWarps / NG;
-  constexpr int NCW = kDmmaProjWarps;
+  constexpr int NG = 8 / NT, MG = NW / NG;
+  constexpr int NCW = NW;
   constexpr int CTP = NCW * 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -418,14 +421,14 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   }
 }
 
-template <int MT, int NT>
+template <int MT, int NT, int NW = kDmmaProjWarps>
 void launch_p(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  project_dmma_kernel<kDmmaKR, MT, NT><<<grid, kMaxThreadsP, smem, s>>>(a);
+  project_dmma_kernel<kDmmaKR, MT, NT, NW><<<grid, NW * 32, smem, s>>>(a);
 }
 
-template <int MT, int NT>
+template <int MT, int NT, int NW = kDmmaProjWarps>
 cudaError_t set_p(int64_t smem) {
-  return cudaFuncSetAttribute(project_dmma_kernel<kDmmaKR, MT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(project_dmma_kernel<kDmmaKR, MT, NT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem);
 }
 
@@ -442,6 +445,13 @@ cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cud
       case 5: launch_p<5, 2>(a, grid, smem, s); break;
       case 6: launch_p<6, 2>(a, grid, smem, s); break;
       default: launch_p<7, 2>(a, grid, smem, s); break;
+    }
+  } else if (a.dnw == 8) {  // 2 column groups (W/16 M-tiles) x 4 rhs groups (2 N-tiles), 2 CTAs per SM
+    switch (a.W / 16) {
+      case 1: launch_p<1, 2, 8>(a, grid, smem, s); break;
+      case 3: launch_p<3, 2, 8>(a, grid, smem, s); break;
+      case 5: launch_p<5, 2, 8>(a, grid, smem, s); break;
+      default: launch_p<7, 2, 8>(a, grid, smem, s); break;
     }
   } else {
     switch (a.W / 16) {
@@ -467,7 +477,8 @@ cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e) {
   if ((e = set_p<1, 2>(smem_p)) || (e = set_p<2, 2>(smem_p)) || (e = set_p<3, 2>(smem_p)) ||
       (e = set_p<4, 2>(smem_p)) || (e = set_p<5, 2>(smem_p)) || (e = set_p<6, 2>(smem_p)) ||
       (e = set_p<7, 2>(smem_p)) || (e = set_p<1, 1>(smem_p)) || (e = set_p<3, 1>(smem_p)) ||
-      (e = set_p<5, 1>(smem_p)) || (e = set_p<7, 1>(smem_p)))
+      (e = set_p<5, 1>(smem_p)) || (e = set_p<7, 1>(smem_p)) || (e = set_p<1, 2, 8>(smem_p)) ||
+      (e = set_p<3, 2, 8>(smem_p)) || (e = set_p<5, 2, 8>(smem_p)) || (e = set_p<7, 2, 8>(smem_p)))
     return e;
   if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
     return e;

@@ -219,11 +219,14 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     p.dstage_e = round_up(int64_t(kDmmaRE) * (p.dkc + 4) * 8 +
                               std::max(int64_t(p.dkc) * kDmmaNB * 8, int64_t(kDmmaNB) * (p.dkc + 4) * 8),
                           128);
-    p.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (226 * 1024 - bar_bytes) / p.dstage_p));
+    p.dnw = (p.W % 32 != 0 && opt.dmma_nw == 8) ? 8 : 16;
+    const int64_t pbudget = p.dnw == 8 ? 112 * 1024 : 226 * 1024;  // 2 CTAs per SM with 8 warps
+    p.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / p.dstage_p));
     p.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 32 ? 3 : 5, (112 * 1024 - bar_bytes) / p.dstage_e));
     p.dsmem_p = p.dns_p * p.dstage_p + bar_bytes;
     p.dsmem_e = p.dns_e * p.dstage_e + bar_bytes;
-    p.dgrid_p = static_cast<int>(std::min<int64_t>(opt.num_sms, depth > 0 ? p.N_loc / p.dkr : 0));
+    p.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * (p.dnw == 8 ? 2 : 1),
+                                                   depth > 0 ? p.N_loc / p.dkr : 0));
     p.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * 2, p.N_loc / kDmmaRE));
     if (p.dns_p < 2 || p.dns_e < 2) p.dmma_ok = false;
   }

@@ -85,6 +85,7 @@ struct Plan {
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
+  int dnw = 16;                     // project: warps per CTA (16 at 1 CTA/SM, or 8 at 2 CTAs/SM)
   int dns_p = 0, dns_e = 0;
   int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
   int dgrid_p = 0, dgrid_e = 0;
@@ -107,6 +108,7 @@ struct PlanOptions {
   int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)
   int expand_chunk = -1;            // expand items per dynamic chunk (-1 = default, 0 = static)
   int project_dyn = 1;              // project's last level in dynamic chunks
+  int dmma_nw = 8;                  // DMMA project warps per CTA when W % 32 != 0 (8 or 16)
   int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
