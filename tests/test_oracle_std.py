@@ -163,3 +163,58 @@ def test_std_adjoint_identity():
     lhs = yp @ oracle.std_matvec(d, L, b, r, U, V, Dn, x)
     rhs = oracle.std_matvec_t(d, L, b, r, U, V, Dn, yp) @ x
     assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def _std_unit_column(d, L, b, r, U, V, Dn, j):
+    """H e_j from the definitions (eq:standard-ad-cond on boxes, Def 2.4's
+    recursion): at every level l >= 2 the node s = anc_l(j) is the source of a
+    low-rank block (t, s) for every box t of the same level that does not touch
+    s but whose parent touches s's parent; the near field is the leaves touching
+    leaf(j).  Geometry by explicit coordinates; panel columns by the canonical
+    slot order (pinned by test_std_slot_enumeration_is_a_bijection)."""
+    c = 1 << d
+    N = b * c ** L
+    M = 6 ** d - 3 ** d
+    col = np.zeros(N)
+    def coords(k, level):
+        x = [0] * d
+        for jj in range(level):
+            for i in range(d):
+                x[i] |= ((k >> (jj * d + i)) & 1) << jj
+        return x
+    def touch(a, bb):
+        return all(abs(a[i] - bb[i]) <= 1 for i in range(d))
+    leaf = j // b
+    xl = coords(leaf, L)
+    for t in range(c ** L):                                  # near field
+        xt = coords(t, L)
+        if touch(xt, xl):
+            e = sum((xl[i] - xt[i] + 1) * 3 ** i for i in range(d))
+            col[t * b:(t + 1) * b] += Dn[t * b:(t + 1) * b, e * b + (j - leaf * b)]
+    for l in range(2, L + 1):
+        m = N // c ** l
+        s = j // m
+        xs, xps = coords(s, l), coords(s >> d, l - 1)
+        for t in range(c ** l):
+            xt, xpt = coords(t, l), coords(t >> d, l - 1)
+            if touch(xt, xs) or not touch(xpt, xps):
+                continue
+            qt, qs = oracle.std_slot(d, l, t, s), oracle.std_slot(d, l, s, t)
+            v = V[l - 1][j, qs * r:(qs + 1) * r]
+            col[t * m:(t + 1) * m] += U[l - 1][t * m:(t + 1) * m, qt * r:(qt + 1) * r] @ v
+    assert M * r == U[0].shape[1] if U else True
+    return col
+
+
+@pytest.mark.parametrize("d,L,b,r", [(2, 5, 2, 2), (1, 9, 2, 2), (3, 3, 2, 1)])
+def test_std_unit_columns_at_scale(d, L, b, r):
+    """Columns of the standard-admissibility H from the definitions vs the
+    oracle's block loop, beyond brute-force sizes (N = 1024..2048)."""
+    U, V, Dn = std_panels(d, L, b, r, 600 + d + L)
+    N = len(Dn)
+    js = np.random.default_rng(19).integers(0, N, 6)
+    X = np.zeros((N, len(js)))
+    X[js, np.arange(len(js))] = 1.0
+    Y = oracle.std_matvec(d, L, b, r, U, V, Dn, X)
+    for k, j in enumerate(js):
+        assert rel(Y[:, k], _std_unit_column(d, L, b, r, U, V, Dn, int(j))) < 1e-13
