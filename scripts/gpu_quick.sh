@@ -1,7 +1,6 @@
 #!/bin/bash
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_random_shapes.py -x -q -k "multi_rhs or small or random or gemv or strict or async" > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?"
-timeout 900 python scripts/kernel_sweep.py c2 "" "NRHS=2" "NRHS=2,HMAT_EXPAND_RPT=0" "NRHS=4" "NRHS=4,HMAT_EXPAND_RPT=0" "NRHS=8" > gpurun_out/quick_sweep.log 2>&1
-timeout 900 python scripts/kernel_sweep.py c3 "" "NRHS=2" "NRHS=2,HMAT_EXPAND_RPT=0" "NRHS=4" "NRHS=4,HMAT_EXPAND_RPT=0" >> gpurun_out/quick_sweep.log 2>&1
-timeout 900 python scripts/kernel_sweep.py c4 "" >> gpurun_out/quick_sweep.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?"
+timeout 600 python bench.py --config c1 --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/bench_c1_small.json 2>/dev/null; echo "bench rc=$?"
+HMAT_SMALL=0 timeout 600 python bench.py --config c1 --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/bench_c1_stream.json 2>/dev/null
