@@ -340,7 +340,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       return bail(cuda_fail(e, "uploading the standard-admissibility exchange tables"));
   }
   if (p.adm) {  // interaction-list slot tables for the project kernel's scatter
-    static int16_t code[3][8][hmat::kStdMaxSlots], slot[3][8][hmat::kStdMaxCodes];
+    int16_t code[3][8][hmat::kStdMaxSlots], slot[3][8][hmat::kStdMaxCodes];  // ~20 KB, per call
     hmat::std_slot_tables(code, slot);
     if ((e = hmat::init_std_tables(&code[0][0][0], &slot[0][0][0])) != cudaSuccess)
       return bail(cuda_fail(e, "init_std_tables"));

@@ -36,12 +36,13 @@ int64_t shifted(int d, const int64_t x[3], int e, int level) {
 
 std::string std_exchange_build(const Plan& p, StdExchange* out) {
   if (p.adm != 1) return "std_exchange_build: not a standard-admissibility plan";
-  static int16_t code[3][8][kStdMaxSlots], slot[3][8][kStdMaxCodes];
-  static bool tables = false;
-  if (!tables) {
-    std_slot_tables(code, slot);
-    tables = true;
-  }
+  struct Tables {
+    int16_t code[3][8][kStdMaxSlots], slot[3][8][kStdMaxCodes];
+    Tables() { std_slot_tables(code, slot); }
+  };
+  static const Tables tab;  // built once; thread-safe static initialisation
+  const auto& code = tab.code;
+  const auto& slot = tab.slot;
   StdExchange X;
   const int d = p.d, c = p.c, M = p.M, nd = p.nd, L = p.L;
   const int64_t Nl = p.N_loc, row0 = p.row0;

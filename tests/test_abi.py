@@ -97,3 +97,11 @@ def test_plan_query_valid():
     assert info.W == 48 and info.cross_levels == 0 and info.exchange_rows == 0
     assert 64 % info.Rp == 0 and 64 % info.Re == 0
     assert info.smem_p <= 227 * 1024 and info.smem_e <= 227 * 1024
+
+
+def test_nccl_unique_id_resolves_the_runtime():
+    """hmat_nccl_unique_id dlopens NCCL (csrc/comm.cpp) and returns the 128-byte id
+    rank 0 broadcasts for P > 1 (include/hmat.h); two calls give different ids."""
+    import torch  # noqa: F401  (loads torch's libnccl first, as bench.py does)
+    a, b = hm.hmat_nccl_unique_id(), hm.hmat_nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b and any(a)
