@@ -233,6 +233,14 @@ hmat_status hmat_synchronize(hmat_t H);
  * broadcast).  HMAT_ERR_NCCL if NCCL cannot be loaded. */
 hmat_status hmat_nccl_unique_id(void* out128);
 
+/* Diagnostic: runs the library's NCCL layer end to end on ONE GPU -- a fresh
+ * unique id, a one-rank communicator on `device`, an in-place sum of `count`
+ * doubles (the call every multi-GPU matvec makes on its packed exchange
+ * buffer), destroy -- and checks the buffer is unchanged
+ * (a one-rank sum is the identity).  HMAT_ERR_NCCL / HMAT_ERR_CUDA on failure,
+ * HMAT_ERR_INVALID for count < 1. */
+hmat_status hmat_nccl_selftest(int device, int64_t count);
+
 /* Kernel timing: when enabled, CUDA events bracket every kernel/collective of
  * each matvec on H's stream.  hmat_profile_read() synchronises, returns the
  * accumulated milliseconds and launch counts per phase since the last read

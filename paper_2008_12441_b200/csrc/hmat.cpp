@@ -1005,6 +1005,35 @@ hmat_status hmat_nccl_unique_id(void* out128) {
   return HMAT_OK;
 }
 
+hmat_status hmat_nccl_selftest(int device, int64_t count) {
+  if (count < 1) return fail(HMAT_ERR_INVALID, "count must be >= 1");
+  CUDA_TRY(cudaSetDevice(device));
+  char id[128];
+  std::string m = hmat::comm_unique_id(id);
+  if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  hmat::Comm* c = nullptr;
+  m = hmat::comm_create(id, 1, 0, &c);
+  if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  std::vector<double> h(static_cast<size_t>(count)), back(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) h[static_cast<size_t>(i)] = 0.5 * static_cast<double>(i) - 3.0;
+  double* d = nullptr;
+  cudaStream_t s = nullptr;
+  const size_t bytes = static_cast<size_t>(count) * sizeof(double);
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) m = hmat::comm_allreduce_sum(c, d, static_cast<size_t>(count), s);
+  if (e == cudaSuccess && m.empty()) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && m.empty()) e = cudaMemcpy(back.data(), d, bytes, cudaMemcpyDeviceToHost);
+  if (s) cudaStreamDestroy(s);
+  if (d) cudaFree(d);
+  hmat::comm_destroy(c);
+  if (e != cudaSuccess) return cuda_fail(e, "hmat_nccl_selftest");
+  if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  if (back != h) return fail(HMAT_ERR_NCCL, "one-rank ncclAllReduce changed the buffer");
+  return HMAT_OK;
+}
+
 hmat_status hmat_peer_export(hmat_t H, void* handle64) {
   if (!H || !handle64) return fail(HMAT_ERR_INVALID, "NULL argument");
   if (!H->peer) return fail(HMAT_ERR_INVALID, "H does not use the peer exchange");

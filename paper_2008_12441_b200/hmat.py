@@ -31,6 +31,7 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_create_standard_uninit", "hmat_panel", "hmat_matvec", "hmat_gemv",
            "hmat_exchange_size", "hmat_project", "hmat_expand", "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
+           "hmat_nccl_selftest",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
            "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local", "hmat_cta_trace",
            "hmat_cta_trace_read", "hmat_std_exchange_query", "hmat_set_host_async", "hmat_synchronize")
@@ -88,6 +89,7 @@ _sigs = {
     "hmat_local_rows": (_i, [_H, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "hmat_set_stream": (_i, [_H, _P]),
     "hmat_nccl_unique_id": (_i, [_P]),
+    "hmat_nccl_selftest": (_i, [_i, _i64]),
     "hmat_profile": (_i, [_H, _i]),
     "hmat_profile_read": (_i, [_H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
     "hmat_launches_per_matvec": (_i64, [_H, _i]),
@@ -311,6 +313,10 @@ def hmat_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.hmat_nccl_unique_id(ctypes.cast(buf, _P)), "hmat_nccl_unique_id")
     return buf.raw
+
+
+def hmat_nccl_selftest(device: int = 0, count: int = 4096):
+    _check(_lib.hmat_nccl_selftest(device, count), "hmat_nccl_selftest")
 
 
 def hmat_profile(h, enable: bool):

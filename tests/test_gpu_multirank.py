@@ -6,9 +6,11 @@ exchange buffers summed over ranks here (what ncclAllReduce does inside
 hmat_matvec), then hmat_expand for every rank.  No kernel waits on another
 rank's kernel (the ranks run one after the other), so this is safe on one GPU
 and exercises every multi-GPU code path of the kernels: exchanged levels in
-the packed buffer, nodes split across shards, per-shard target bases.  Only
-the NCCL call itself is not covered (tests/test_multigpu_cpu.py covers the
-layout with real multi-process gloo communication).
+the packed buffer, nodes split across shards, per-shard target bases.  The
+library's NCCL layer (dlopen, communicator, in-place fp64 sum on a stream) runs
+at one rank in test_nccl_layer_one_rank; a P > 1 NCCL sum needs P GPUs
+(tests/test_multigpu_cpu.py covers the layout with real multi-process gloo
+communication).
 """
 import numpy as np
 import pytest
@@ -98,6 +100,12 @@ def test_sharded_equals_single_gpu_c2_shape():
         assert_parity(y4[:, 0], y1.cpu().numpy())
     finally:
         hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("count", [1, 4097, 1 << 20])
+def test_nccl_layer_one_rank(count):
+    torch.zeros(1, device="cuda")                     # torch's NCCL / context first, as bench.py
+    hm.hmat_nccl_selftest(0, count)
 
 
 def test_external_exchange_requires_split_api():
