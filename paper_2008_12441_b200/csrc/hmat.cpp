@@ -65,6 +65,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
+  o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   return o;
 }
@@ -695,6 +696,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.done = H->done;
   a.zex_base = H->zex;
   a.dbg = p.dbg;
+  a.snake = p.snake;
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.

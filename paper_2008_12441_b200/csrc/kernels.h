@@ -69,6 +69,7 @@ struct StreamArgs {
   int dkc;             // DMMA expand: k-columns per stage (32, or 16 when W % 32 != 0)
   int dnw;             // DMMA project: warps per CTA (16, or 8 with two CTAs per SM)
   int dbg;             // diagnostics only (HMAT_DEBUG_SKIP): bit 0 skips project's math, bit 1 expand's
+  int snake;           // project: even levels stream their range backwards (x tail reused from L2)
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
   // CTA pushes this rank's exchange levels into slot `rank` of every rank's
   // mailbox and raises its flag there; expand sums the P slots in rank order

@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
         const double* Vl = a.V + (l - 1) * a.panel_stride;
         const bool dyn = l == dyn_level;
+        const bool rev = a.snake && !dyn && !(l & 1);  // even levels: the range backwards
         int64_t rk0 = k0, rk1 = k1;
         int chunk = -1;
         for (bool first_range = true;; first_range = false) {
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         } else if (!first_range) {
           break;
         }
-        for (int64_t k = rk0; k < rk1; ++k) {
+        for (int64_t n = 0; n < rk1 - rk0; ++n) {
+          const int64_t k = rev ? rk1 - 1 - n : rk0 + n;
           // the stage's addresses first, then wait for the slot (the refill
           // latency is on the stream's critical path)
           const int64_t i0 = k * Rp;
@@ -263,6 +265,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
     const LevelArgs& lv = a.lv[l];
     const bool dyn = l == dyn_level;
+    // Even levels stream the CTA's range backwards: the x segments read last at
+    // level l - 1 (still in L2, evict_last) are the first ones read at level l,
+    // instead of a cyclic sweep through more x than L2 holds (all misses).
+    const bool rev = a.snake && !dyn && !(l & 1);
     const int64_t sg0 = a.row0 / lv.m;
     // node cursor: seg stages per local node, sl = node index, pos = stage in node
     const int64_t seg = lv.seg_rows / Rp;
@@ -285,8 +291,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     } else if (!first_range) {
       break;
     }
-    int64_t sl = rk0 / seg, pos = rk0 - sl * seg;
-    for (int64_t k = rk0; k < rk1; ++k) {
+    const int64_t kf = rev ? rk1 - 1 : rk0;
+    int64_t sl = kf / seg, pos = kf - sl * seg;
+    for (int64_t n = 0; n < rk1 - rk0; ++n) {
+      const int64_t k = rev ? rk1 - 1 - n : rk0 + n;
       if (!peeked) dev::mbar_wait(&full[slot], phase);
       peeked = false;
       const int64_t i0 = k * Rp;
@@ -322,13 +330,18 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         slot = 0;
         phase ^= 1;
       }
-      const bool node_end = (pos + 1 == seg);
+      const bool node_end = rev ? pos == 0 : pos + 1 == seg;
       const int64_t this_sl = sl;
-      if (++pos == seg) {
+      if (rev) {
+        if (pos-- == 0) {
+          pos = seg - 1;
+          --sl;
+        }
+      } else if (++pos == seg) {
         pos = 0;
         ++sl;
       }
-      if (!node_end && k + 1 != rk1) continue;
+      if (!node_end && n + 1 != rk1 - rk0) continue;
 
       // ---- end of a (local) node, or end of this CTA's range of the level ----
       const int64_t sa = this_sl * seg, sb = sa + seg;  // the node's stages

@@ -81,7 +81,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 16, dbg = 0, expand_chunk = -1, project_dyn = 1;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 16, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
@@ -108,6 +108,7 @@ struct PlanOptions {
   int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)
   int expand_chunk = -1;            // expand items per dynamic chunk (-1 = default, 0 = static)
   int project_dyn = 1;              // project's last level in dynamic chunks
+  int snake = 1;                    // project: alternate the stream direction per level
   int dmma_nw = 8;                  // DMMA project warps per CTA when W % 32 != 0 (8 or 16)
   int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)

@@ -403,3 +403,18 @@ def test_host_async_streaming_mode():
         assert_parity(yy.numpy(), ys[1].numpy())
     finally:
         hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("snake", ["0", "1"])
+def test_project_stream_direction(snake, monkeypatch):
+    """Project's per-level stream direction (HMAT_PROJECT_SNAKE): backwards even
+    levels reorder each node's row sums and the CTA partials' flushes; y stays
+    within tolerance and bitwise reproducible, with nodes cut by CTA ranges."""
+    monkeypatch.setenv("HMAT_PROJECT_SNAKE", snake)
+    monkeypatch.setenv("HMAT_PROJECT_DYN", "0")
+    cfg = HConfig("sn", d=2, L=5, b=16, r=4, seed=610)   # 1024 leaves: coarse nodes span many CTAs
+    U, V, D, x = host_case(cfg, nrhs=3)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    y1 = gpu_matvec(cfg, U, V, D, x)
+    assert_parity(y1, ref)
+    assert np.array_equal(gpu_matvec(cfg, U, V, D, x), y1)
