@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         } else if (!first_range) {
           break;
         }
-        for (int64_t n = 0; n < rk1 - rk0; ++n) {
-          const int64_t k = rev ? rk1 - 1 - n : rk0 + n;
+        const int64_t dk = rev ? -1 : 1;
+        int64_t k = rev ? rk1 - 1 : rk0;
+        for (int64_t n = rk1 - rk0; n > 0; --n, k += dk) {
           // the stage's addresses first, then wait for the slot (the refill
           // latency is on the stream's critical path)
           const int64_t i0 = k * Rp;
@@ -291,10 +292,13 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     } else if (!first_range) {
       break;
     }
-    const int64_t kf = rev ? rk1 - 1 : rk0;
-    int64_t sl = kf / seg, pos = kf - sl * seg;
-    for (int64_t n = 0; n < rk1 - rk0; ++n) {
-      const int64_t k = rev ? rk1 - 1 - n : rk0 + n;
+    // (32-bit cursors: stages per level and per node fit; fewer live registers)
+    const int dk = rev ? -1 : 1;
+    const int pend = rev ? 0 : static_cast<int>(seg) - 1;  // position of a node's last stage in stream order
+    int64_t k = rev ? rk1 - 1 : rk0;
+    int64_t sl = k / seg;
+    int pos = static_cast<int>(k - sl * seg);
+    for (int n = static_cast<int>(rk1 - rk0); n > 0; --n, k += dk) {
       if (!peeked) dev::mbar_wait(&full[slot], phase);
       peeked = false;
       const int64_t i0 = k * Rp;
@@ -330,18 +334,14 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         slot = 0;
         phase ^= 1;
       }
-      const bool node_end = rev ? pos == 0 : pos + 1 == seg;
+      const bool node_end = pos == pend;
       const int64_t this_sl = sl;
-      if (rev) {
-        if (pos-- == 0) {
-          pos = seg - 1;
-          --sl;
-        }
-      } else if (++pos == seg) {
-        pos = 0;
-        ++sl;
+      pos += dk;
+      if (node_end) {
+        pos = static_cast<int>(seg) - 1 - pend;
+        sl += dk;
       }
-      if (!node_end && n + 1 != rk1 - rk0) continue;
+      if (!node_end && n != 1) continue;
 
       // ---- end of a (local) node, or end of this CTA's range of the level ----
       const int64_t sa = this_sl * seg, sb = sa + seg;  // the node's stages
