@@ -673,3 +673,81 @@ void oracle_std_matvec_t(int d, int L, int b, int r, const double* const* U, con
   visit_root_std(d, L, std_mv_t_cb, &mv);
   free(mv.z);
 }
+
+/* Sampled rows of the SEEDED standard-admissibility operator (gen/hgen.h, the
+ * canonical standard panels above, entries generated on demand), so that full
+ * bench-size operators (s2: 55.6 GB of factors) can be checked row by row:
+ * y_i = sum over the blocks (t, s) of Def 2.4 (standard admissibility,
+ * PAPER.md:279-297, 316-339) whose target t contains row i of
+ *   dense (leaf level):  D_ts[i - t b, :] x_s                (eq:prod-dx)
+ *   low rank (level l):  U_ts[i - t m_l, :] (V_ts^T x_s)      (eq:prod-uvx)
+ * The blocks are found by the same recursion as visit_std, restricted to the
+ * child that holds row i at every level. */
+typedef struct {
+  int d, L, b, r, M, ND, nrhs; int64_t N, i; uint64_t seed;
+  const double* x; double* yi;  /* yi[k] = y[i, k] */
+} std_row_t;
+
+static void std_row_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_row_t* rw = (std_row_t*)ctx;
+  const int64_t N = rw->N, i = rw->i;
+  if (kind == 0) { /* dense neighbour block D_ts, Dn row i, columns [e b, (e+1) b) */
+    const int e = std_neighbour_index(rw->d, t, s, level);
+    const uint64_t stD = hgen_stream(rw->seed, HGEN_TAG_D, 0, 0);
+    const int64_t ld = (int64_t)rw->ND * rw->b;
+    for (int k = 0; k < rw->nrhs; ++k) {
+      double acc = 0.0;
+      for (int j = 0; j < rw->b; ++j)
+        acc += hgen_normal(stD, (uint64_t)(i * ld + e * rw->b + j)) * 0.125 * rw->x[(int64_t)k * N + s * rw->b + j];
+      rw->yi[k] += acc;
+    }
+    return;
+  }
+  const int64_t m = N / ipow(1 << rw->d, level);
+  const double scale = 1.0 / sqrt((double)m);
+  const int W = rw->M * rw->r;
+  const int qt = oracle_std_slot(rw->d, level, t, s), qs = oracle_std_slot(rw->d, level, s, t);
+  const uint64_t stU = hgen_stream(rw->seed, HGEN_TAG_U, (uint64_t)level, 0);
+  const uint64_t stV = hgen_stream(rw->seed, HGEN_TAG_V, (uint64_t)level, 0);
+  for (int k = 0; k < rw->nrhs; ++k)
+    for (int a = 0; a < rw->r; ++a) {
+      double za = 0.0; /* (V_ts^T x_s)[a] */
+#pragma omp parallel for reduction(+ : za) schedule(static)
+      for (int64_t j = 0; j < m; ++j)
+        za += hgen_normal(stV, (uint64_t)((s * m + j) * W + qs * rw->r + a)) * scale * rw->x[(int64_t)k * N + s * m + j];
+      rw->yi[k] += hgen_normal(stU, (uint64_t)(i * W + qt * rw->r + a)) * scale * za;
+    }
+}
+
+static void visit_std_row(int d, int L, int level, int64_t pt, int64_t ps, int64_t i, int64_t N, block_fn fn,
+                          void* ctx) {
+  const int c = 1 << d;
+  const int64_t t = i / (N / ipow(c, level + 1)); /* the child of pt holding row i */
+  for (int bb = 0; bb < c; ++bb) {
+    const int64_t s = ps * c + bb;
+    int64_t xt[3], xs[3];
+    morton_decode(d, t, level + 1, xt);
+    morton_decode(d, s, level + 1, xs);
+    if (std_admissible(d, xt, xs)) fn(ctx, 1, level + 1, t, s);
+    else if (level + 1 == L) fn(ctx, 0, level + 1, t, s);
+    else visit_std_row(d, L, level + 1, t, s, i, N, fn, ctx);
+  }
+  (void)pt;
+}
+
+void oracle_std_rows_generated(int d, int L, int b, int r, uint64_t seed, const double* x, int nrhs,
+                               int64_t nrows, const int64_t* rows, double* yrows) {
+  std_row_t rw;
+  rw.d = d; rw.L = L; rw.b = b; rw.r = r; rw.M = oracle_std_slots(d); rw.ND = (int)ipow(3, d);
+  rw.nrhs = nrhs; rw.N = (int64_t)b * ipow(1 << d, L); rw.seed = seed; rw.x = x;
+  double* yi = (double*)malloc(sizeof(double) * (size_t)nrhs);
+  for (int64_t n = 0; n < nrows; ++n) {
+    for (int k = 0; k < nrhs; ++k) yi[k] = 0.0;
+    rw.i = rows[n];
+    rw.yi = yi;
+    if (L == 0) std_row_cb(&rw, 0, 0, 0, 0);
+    else visit_std_row(d, L, 0, 0, 0, rw.i, rw.N, std_row_cb, &rw);
+    for (int k = 0; k < nrhs; ++k) yrows[(int64_t)k * nrows + n] = yi[k];
+  }
+  free(yi);
+}

@@ -221,6 +221,8 @@ def _std_lib():
                                                                ctypes.c_void_p, ctypes.c_int]
         lib.oracle_std_matvec_t.restype = None
         lib.oracle_std_matvec_t.argtypes = lib.oracle_std_matvec.argtypes
+        lib.oracle_std_rows_generated.restype = None
+        lib.oracle_std_rows_generated.argtypes = lib.oracle_rows_generated.argtypes
         lib._std_ready = True
     return lib
 
@@ -268,3 +270,18 @@ def std_matvec_t(d: int, L: int, b: int, r: int, U, V, Dn, x) -> np.ndarray:
     """y = H^T x by the transposed standard-admissibility block loop."""
     _std_lib()
     return _mv(_load().oracle_std_matvec_t, d, L, b, r, U, V, Dn, x)
+
+
+def std_rows_generated(cfg, x, rows) -> np.ndarray:
+    """y[rows, :] of the seeded standard-admissibility operator of `cfg` (factor
+    entries generated on demand, blocks found by the Def 2.4 recursion
+    restricted to each row); x: (N,) or (N, nrhs) host array."""
+    lib = _std_lib()
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    assert N == cfg.N and cfg.adm == 1
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.zeros((len(rows), nrhs), dtype=np.float64, order="F")
+    lib.oracle_std_rows_generated(cfg.d, cfg.L, cfg.b, cfg.r, cfg.seed, xc.ctypes.data, nrhs, len(rows),
+                                  rows.ctypes.data, out.ctypes.data)
+    return out[:, 0] if np.ndim(x) == 1 else out

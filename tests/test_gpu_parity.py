@@ -157,12 +157,13 @@ def sample_rows(cfg, rng):
     return np.array(sorted(set(int(r) for r in rows)))
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c2strict"])
 def test_full_size_sampled_rows(name):
-    """BASELINE configs at full size, in the bench's launch configuration
+    """BASELINE configs (and the bench's c2strict line: leaf 256, dense blocks in
+    64-column chunks) at full size, in the bench's launch configuration
     (device-generated panels, default plan): sampled y rows vs the oracle,
     which recomputes each row from eq:hmat-vec-add with on-demand factors."""
-    cfg = CONFIGS[name]
+    cfg = {**CONFIGS, **hgen.EXTRA_CONFIGS}[name]
     free, _ = torch.cuda.mem_get_info()
     if free < cfg.factor_bytes * 1.05:
         pytest.skip(f"needs {cfg.factor_bytes / 1e9:.0f} GB of device memory")

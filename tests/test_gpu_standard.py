@@ -141,3 +141,36 @@ def test_standard_3d_leaf64_caps_pass_width():
     cfg = HConfig("std3w", d=3, L=2, b=64, r=1, adm=1, seed=780)
     y, (U, V, Dn, x) = run_std(cfg, 5)
     assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
+
+
+def test_s2_full_size_sampled_rows():
+    """The bench's s2 line at full size (N = 2^20, 27 interaction slots, 55.6 GB
+    of factors), in the bench's launch configuration (device-generated panels,
+    default plan): sampled rows vs the oracle's row-restricted Def 2.4 walk with
+    on-demand factors."""
+    from tests.helpers import device_operator
+    cfg = hgen.EXTRA_CONFIGS["s2"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < cfg.factor_bytes * 1.05:
+        pytest.skip(f"needs {cfg.factor_bytes / 1e9:.0f} GB of device memory")
+    h = device_operator(cfg, hm)
+    try:
+        x = torch.empty(cfg.N, dtype=torch.float64, device="cuda")
+        hgen.dev_fill_x(cfg, 1, 2, 0, cfg.N, x.data_ptr(), cfg.N)
+        y = torch.empty_like(x)
+        hm.hmat_matvec(h, x, y)
+        torch.cuda.synchronize()
+        xh = x.cpu().numpy()
+        n_side = 1 << cfg.L
+        corner = [0, cfg.b - 1]                                      # domain corner leaf
+        edge = [(n_side // 2) * cfg.b + 5]                           # a boundary leaf
+        rows = np.array(sorted(set(corner + edge + [cfg.N // 2 + 17, cfg.N - 1] +
+                                   list(np.random.default_rng(4).integers(0, cfg.N, 3)))))
+        ref = oracle.std_rows_generated(cfg, xh, rows)
+        yall = y.cpu().numpy()
+        got = yall[rows]
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(yall).max()
+        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    finally:
+        hm.hmat_destroy(h)
+        torch.cuda.empty_cache()

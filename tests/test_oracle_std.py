@@ -218,3 +218,20 @@ def test_std_unit_columns_at_scale(d, L, b, r):
     Y = oracle.std_matvec(d, L, b, r, U, V, Dn, X)
     for k, j in enumerate(js):
         assert rel(Y[:, k], _std_unit_column(d, L, b, r, U, V, Dn, int(j))) < 1e-13
+
+
+@pytest.mark.parametrize("cfg", [HConfig("sr2", d=2, L=3, b=4, r=3, adm=1, seed=41),
+                                 HConfig("sr3", d=3, L=2, b=2, r=2, adm=1, seed=42),
+                                 HConfig("sr1", d=1, L=5, b=3, r=2, adm=1, seed=43),
+                                 HConfig("sr0", d=2, L=1, b=5, r=1, adm=1, seed=44)], ids=lambda c: c.name)
+def test_std_rows_generated_equals_assembled_matrix(cfg):
+    """oracle_std_rows_generated (entries generated on demand, blocks found row
+    by row) equals rows of the assembled matrix (brute force) and of the block
+    loop, over the seeded panels, at every sampled row."""
+    U, V, Dn = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=2)
+    A = oracle.std_assemble(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn)
+    rows = np.array(sorted(set([0, cfg.b - 1, cfg.b, cfg.N // 2, cfg.N - 1] + list(range(0, cfg.N, 7)))))
+    yr = oracle.std_rows_generated(cfg, x, rows)
+    assert rel(yr, (A @ x)[rows]) < 1e-13
+    assert rel(yr, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x)[rows]) < 1e-13
