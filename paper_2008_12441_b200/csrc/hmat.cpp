@@ -596,8 +596,11 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         CUDA_TRY(cudaEventCreateWithFlags(&H->ev_out[i], cudaEventDisableTiming));
       }
     }
-    if (H->comp_rec[par]) CUDA_TRY(cudaStreamWaitEvent(H->s_in, H->ev_comp[par], 0));  // x / y staging free
-    if (H->out_rec[par]) CUDA_TRY(cudaStreamWaitEvent(H->s_in, H->ev_out[par], 0));
+    // x staging free once call k-2's kernels are done; y staging once its copy
+    // out is done -- the kernels wait for that (below), the copy in only when it
+    // writes y staging too (beta != 0), so x(k) streams in while y(k-2) streams out
+    if (H->comp_rec[par]) CUDA_TRY(cudaStreamWaitEvent(H->s_in, H->ev_comp[par], 0));
+    if (H->out_rec[par] && beta != 0.0 && !y_dev) CUDA_TRY(cudaStreamWaitEvent(H->s_in, H->ev_out[par], 0));
   }
   cudaStream_t s_copy_in = async_io ? H->s_in : H->stream;
   // ---- x: stage when it is host memory, misaligned, or its last column would
@@ -635,9 +638,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       prof_end(H, &ep);
     }
   }
-  if (async_io) {  // the kernels wait for this call's inputs
+  if (async_io) {  // the kernels wait for this call's inputs and for y staging to be free
     CUDA_TRY(cudaEventRecord(H->ev_in[par], H->s_in));
     CUDA_TRY(cudaStreamWaitEvent(H->stream, H->ev_in[par], 0));
+    if (H->out_rec[par] && !y_dev) CUDA_TRY(cudaStreamWaitEvent(H->stream, H->ev_out[par], 0));
   }
 
   hmat::StreamArgs a;
