@@ -91,7 +91,8 @@ HBM_READ_STREAM_GBS = 7300.0
 
 def alg_flops(cfg, n_rows, nrhs):
     """Algorithmic flops of one matvec over n_rows rows: 2 per multiply-add."""
-    W, L, b = cfg.W, cfg.L, cfg.dcols
+    W, b = cfg.W, cfg.dcols
+    L = cfg.L - (1 if cfg.adm else 0)  # as alg_bytes
     return {"project": 2 * n_rows * W * L * nrhs, "expand": 2 * n_rows * (W * L + b) * nrhs}
 
 
