@@ -189,8 +189,13 @@ def oracle_sample(cfg, budget_bytes):
     return cfg.L, cfg.b, 0, 8 * cfg.b * cfg.b
 
 
-def run_oracle_sample(cfg, q, n, depth, reps, nrhs):
+def run_oracle_sample(cfg, q, n, depth, reps, nrhs, min_seconds=0.0):
+    """Times `reps` oracle passes over the sample, more (up to 50) until they add
+    up to min_seconds."""
     from oracle import oracle
+
+    def more(times):
+        return len(times) < reps or (sum(times) < min_seconds and len(times) < 50)
     if cfg.adm:
         # standard admissibility: a standalone operator of depth L-q with the same
         # b, r, d (a sub-block is not an H-matrix of the same kind at the boundary)
@@ -199,7 +204,7 @@ def run_oracle_sample(cfg, q, n, depth, reps, nrhs):
         U, V, D = hgen.inputs(sub)
         x = hgen.xblock(sub, nrhs=nrhs)
         times = []
-        for _ in range(reps):
+        while more(times):
             t0 = time.perf_counter()
             oracle.std_matvec(sub.d, sub.L, sub.b, sub.r, U, V, D, x)
             times.append(time.perf_counter() - t0)
@@ -211,16 +216,17 @@ def run_oracle_sample(cfg, q, n, depth, reps, nrhs):
     D = hgen.panel(cfg, hgen.TAG_D, 0, 0, n)
     x = hgen.xblock(cfg, nrhs=nrhs, vec=0, row_begin=0, row_end=n)
     times = []
-    for _ in range(reps):
+    while more(times):
         t0 = time.perf_counter()
         oracle.matvec(cfg.d, depth, cfg.b, cfg.r, U, V, D, x)
         times.append(time.perf_counter() - t0)
     return times
 
 
-def cpu_baseline_record(cfg, budget_bytes=6.5e9, reps=1):
+def cpu_baseline_record(cfg, budget_bytes=6.5e9, reps=1, min_seconds=10.0):
     q, n, depth, fb = oracle_sample(cfg, budget_bytes)
-    times = run_oracle_sample(cfg, q, n, depth, reps, cfg.nrhs)
+    times = run_oracle_sample(cfg, q, n, depth, reps, cfg.nrhs, min_seconds)
+    reps = len(times)
     t = float(np.median(times))
     gbps = fb / t / 1e9
     per_matvec = cfg.factor_bytes
