@@ -81,6 +81,7 @@ def alg_bytes(cfg, n_rows, nrhs):
     return {"project": project, "expand": expand, "factor": factor, "total": factor + 16 * n_rows * nrhs}
 
 
+DMMA_MIN_RHS = 9  # the library's default HMAT_DMMA_MIN: from 9 rhs the FP64 tensor-core path runs
 FP64_PEAK_TFLOPS = 37.07  # scripts/fp64_peak.cu, DMMA m8n8k4, this pool (profiles/r01_fp64_peak.txt)
 # Read-only stream ceiling: scripts/hbm_read_peak.cu (bulk-TMA ring, random fp64 data,
 # 800 back-to-back launches under the 1000 W cap), profiles/r01_hbm_read_peak.txt.
@@ -302,7 +303,7 @@ def run_ours(args):
     t_setup = time.perf_counter()
     # the in-kernel peer exchange serves the single-rhs weak path; the standard
     # structure and the many-rhs tensor-core path exchange through NCCL
-    exchange = ("nccl" if (cfg.adm or nrhs >= 16) else args.exchange) if world > 1 else "none"
+    exchange = ("nccl" if (cfg.adm or nrhs >= DMMA_MIN_RHS) else args.exchange) if world > 1 else "none"
     h = None
     if exchange == "peer":
         # mailboxes connected once through CUDA IPC handles (hmat_peer_export/_import)
@@ -434,7 +435,7 @@ def run_ours(args):
             per_kernel[ph] = {"avg_ms": ms / nl, "launches": nl, "alg_bytes_per_launch": ab[ph] / max(1, (nl // args.steps)),
                               "GBps": ab[ph] / (ms / nl * 1e-3) / 1e9 / max(1, (nl // args.steps))}
     dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_ms"])
-    if nrhs >= 16:
+    if nrhs >= DMMA_MIN_RHS:
         # many right-hand sides: a dense FP64 contraction on the DMMA tensor pipe
         fl = alg_flops(cfg, n, nrhs)
         for ph, d in per_kernel.items():

@@ -61,7 +61,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.max_nr = env_int("HMAT_MAX_NR", o.max_nr);
   o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
   o.dmma_off = env_int("HMAT_DMMA_OFF", 0);
-  o.dmma_min = env_int("HMAT_DMMA_MIN", 16);
+  o.dmma_min = env_int("HMAT_DMMA_MIN", 9);
   o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);

@@ -81,7 +81,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 16, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 9, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
@@ -104,7 +104,7 @@ struct PlanOptions {
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
   // per-call switches, read once at hmat_create (HMAT_* environment)
-  int dmma_off = 0, dmma_min = 16;  // tensor-core path off / from this many rhs
+  int dmma_off = 0, dmma_min = 9;   // tensor-core path off / from this many rhs (measured crossover)
   int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)
   int expand_chunk = -1;            // expand items per dynamic chunk (-1 = default, 0 = static)
   int project_dyn = 1;              // project's last level in dynamic chunks
