@@ -81,7 +81,7 @@ def alg_bytes(cfg, n_rows, nrhs):
     return {"project": project, "expand": expand, "factor": factor, "total": factor + 16 * n_rows * nrhs}
 
 
-DMMA_MIN_RHS = 9  # the library's default HMAT_DMMA_MIN: from 9 rhs the FP64 tensor-core path runs
+DMMA_MIN_RHS = 5  # the library's default HMAT_DMMA_MIN: from 5 rhs the FP64 tensor-core path runs
 FP64_PEAK_TFLOPS = 37.07  # scripts/fp64_peak.cu, DMMA m8n8k4, this pool (profiles/r01_fp64_peak.txt)
 # Read-only stream ceiling: scripts/hbm_read_peak.cu (bulk-TMA ring, random fp64 data,
 # 800 back-to-back launches under the 1000 W cap), profiles/r01_hbm_read_peak.txt.

@@ -61,12 +61,13 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.max_nr = env_int("HMAT_MAX_NR", o.max_nr);
   o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
   o.dmma_off = env_int("HMAT_DMMA_OFF", 0);
-  o.dmma_min = env_int("HMAT_DMMA_MIN", 9);
+  o.dmma_min = env_int("HMAT_DMMA_MIN", 5);
   o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
+  o.dmma_nb32 = env_int("HMAT_DMMA_NB32", o.dmma_nb32);
   return o;
 }
 
@@ -312,7 +313,8 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       // z rows: padding columns (odd W) are multiplied by zero padding of U, so keep them finite
       (e = cudaMemsetAsync(H->zloc, 0, std::max<size_t>(256, size_t(p.z_local_rows) * zrow), H->stream)) ||
       (e = cudaMemsetAsync(H->zex, 0, std::max<size_t>(256, size_t(p.z_exch_rows) * zrow), H->stream)) ||
-      (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(p.dsmem_p, p.dsmem_e))) ||
+      (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(64, p.dl[1].dsmem_p, p.dl[1].dsmem_e))) ||
+      (p.dmma_ok && p.dl[0].ok && (e = hmat::configure_dmma(32, p.dl[0].dsmem_p, p.dl[0].dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   H->external = p.P > 1 && dist->exchange == HMAT_EXCHANGE_EXTERNAL;
@@ -416,11 +418,11 @@ hmat_status ensure_dmma(hmat_s* H) {
   if (H->cnt_d) return HMAT_OK;
   const hmat::Plan& p = H->plan;
   const size_t zrow = size_t(p.W) * hmat::kDmmaNB * sizeof(double);
-  const size_t tickets = size_t(p.dgrid_p) * p.L * sizeof(int) + 256;
+  const size_t tickets = size_t(p.dgrid_p_max) * p.L * sizeof(int) + 256;
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zloc_d), std::max<size_t>(256, size_t(p.z_local_rows) * zrow)));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zex_d), std::max<size_t>(256, size_t(p.z_exch_rows) * zrow)));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->part_d),
-                      std::max<size_t>(256, size_t(p.dgrid_p) * p.L * 2 * p.Wp * hmat::kDmmaNB * sizeof(double))));
+                      std::max<size_t>(256, size_t(p.dgrid_p_max) * p.L * 2 * p.Wp * hmat::kDmmaNB * sizeof(double))));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->cnt_d), tickets));
   CUDA_TRY(cudaMemsetAsync(H->cnt_d, 0, tickets, H->stream));
   return HMAT_OK;
@@ -752,12 +754,6 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     a.dkr = p.dkr;
     a.dkc = p.dkc;
     a.dnw = p.dnw;
-    a.nstage_p = p.dns_p;
-    a.stage_bytes_p = p.dstage_p;
-    a.bar_off_p = p.dns_p * p.dstage_p;
-    a.nstage_e = p.dns_e;
-    a.stage_bytes_e = p.dstage_e;
-    a.bar_off_e = p.dns_e * p.dstage_e;
     a.part = H->part_d;
     a.cnt = H->cnt_d;
     if (p.L > 0) {  // V-role panels [L][N_loc][Wp], box [1][dkr][vp]
@@ -778,29 +774,38 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     for (int c0 = 0; c0 < nrhs; c0 += hmat::kDmmaNB) {
       a.nr = nrhs - c0 < hmat::kDmmaNB ? nrhs - c0 : hmat::kDmmaNB;
+      // the pass width: 32 when at most 32 rhs remain (half the work), else 64
+      const hmat::Plan::DmmaLayout& dl = p.dmma_layout(a.nr);
+      const int nb = dl.nb;
+      a.nstage_p = dl.dns_p;
+      a.stage_bytes_p = dl.dstage_p;
+      a.bar_off_p = dl.dns_p * dl.dstage_p;
+      a.nstage_e = dl.dns_e;
+      a.stage_bytes_e = dl.dstage_e;
+      a.bar_off_e = dl.dns_e * dl.dstage_e;
       a.x = xd + c0 * ldx;
       a.y = yd + c0 * n;
-      {  // this pass's x columns [nr][N_loc] (ld = ldx), box [64][dkr + 4]
+      {  // this pass's x columns [nr][N_loc] (ld = ldx), box [nb][dkr + 4] (rows >= nr zero-filled)
         const uint64_t dims[2] = {uint64_t(n), uint64_t(a.nr)};
         const uint64_t strides[1] = {uint64_t(ldx) * 8};
-        const uint32_t box[2] = {uint32_t(p.dkr + 4), uint32_t(hmat::kDmmaNB)};
+        const uint32_t box[2] = {uint32_t(p.dkr + 4), uint32_t(nb)};
         hmat_status st3 = encode_map(&a.tm_x, 2, a.x, dims, strides, box);
         if (st3 != HMAT_OK) return st3;
-        const uint32_t xbox[2] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaNB)};
+        const uint32_t xbox[2] = {uint32_t(p.dkc + 4), uint32_t(nb)};
         if ((st3 = encode_map(&a.tm_xe, 2, a.x, dims, strides, xbox)) != HMAT_OK) return st3;
       }
       for (int l = 1; l <= p.L; ++l) {
         hmat::LevelArgs& lv = a.lv[l];
         lv.m = p.m[l];
         lv.seg_rows = p.m[l] < n ? p.m[l] : n;
-        lv.zt = (l <= p.cross ? H->zex_d : H->zloc_d) + p.zt_off[l] * p.W * hmat::kDmmaNB;
+        lv.zt = (l <= p.cross ? H->zex_d : H->zloc_d) + p.zt_off[l] * p.W * nb;
         lv.tbase = p.zt_tbase[l];
       }
-      const size_t exch = size_t(p.z_exch_rows) * p.W * hmat::kDmmaNB;
+      const size_t exch = size_t(p.z_exch_rows) * p.W * nb;
       hmat_status st2 = pass(
-          H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, p.dgrid_p, p.dsmem_p, H->stream); },
-          [&] { return hmat::launch_expand_dmma(a, p.dgrid_e, p.dsmem_e, H->stream); }, p.dgrid_p > 0, p.dgrid_p,
-          p.dgrid_e, [] { return cudaSuccess; }, [] { return cudaSuccess; });
+          H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, nb, dl.dgrid_p, dl.dsmem_p, H->stream); },
+          [&] { return hmat::launch_expand_dmma(a, nb, dl.dgrid_e, dl.dsmem_e, H->stream); }, dl.dgrid_p > 0,
+          dl.dgrid_p, dl.dgrid_e, [] { return cudaSuccess; }, [] { return cudaSuccess; });
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -921,7 +926,7 @@ hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count) {
   const hmat::Plan& p = H->plan;
   if (use_dmma(p, nrhs)) {
     if (nrhs > hmat::kDmmaNB) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
-    *count = p.P > 1 ? p.z_exch_rows * p.W * hmat::kDmmaNB : 0;
+    *count = p.P > 1 ? p.z_exch_rows * p.W * p.dmma_layout(nrhs).nb : 0;
   } else {
     if (nrhs > p.max_nr) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
     *count = p.P > 1 ? (H->sx ? H->sx->doubles(nr_cap(nrhs), p.r) : p.z_exch_rows * p.Wp * nr_cap(nrhs)) : 0;

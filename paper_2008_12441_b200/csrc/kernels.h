@@ -114,9 +114,10 @@ cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t sm
 // Launch one expand pass.  grid = plan.grid_e.
 cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
 // FP64 tensor-core (DMMA) passes of kDmmaNB right-hand sides (kernels_dmma.cu).
-cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
-cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s);
-cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e);
+// nb: the pass width (32 or 64 right-hand sides; plan.h DmmaLayout).
+cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
+cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
+cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e);
 // Standard admissibility: upload the interaction-list slot tables (plan.h
 // std_slot_tables) to the project kernel's constant memory (per device).
 cudaError_t init_std_tables(const int16_t* code, const int16_t* slot);

@@ -6,7 +6,9 @@
 //   expand  (Step 5, eq:prod-yuz, eq:prod-ydz):      Y_tile (64 x NB) = sum_l U_l[tile] (64 x W) Zt_l[t] (W x NB)
 //                                                                       + D[tile] (64 x b) X_leaf (b x NB)
 // computed with warp-level mma.sync.m8n8k4.f64 (SASS DMMA; tcgen05 has no
-// f64 kind on sm_100a).  Measured on this B200: DMMA 37.1 TFLOP/s, DFMA 36.5
+// f64 kind on sm_100a).  A pass is NB = 64 columns wide, or NB = 32 when at most
+// 32 right-hand sides remain (a pass computes all NB columns, so a narrower one
+// halves the work of 9..32 rhs).  Measured on this B200: DMMA 37.1 TFLOP/s, DFMA 36.5
 // (scripts/fp64_peak.cu), so the tensor path's gain is issue slots and
 // operand reuse, not a higher peak.
 //
@@ -27,7 +29,6 @@ constexpr int NCW = CT / 32;
 // project: 16 warps (4 per SM sub-partition), no producer warp
 constexpr int kDmmaProjWarps = 16;
 constexpr int kMaxThreadsP = kDmmaProjWarps * 32;
-constexpr int NB = kDmmaNB;   // right-hand sides per pass
 constexpr int kThreadsE = 256;  // expand: 8 warps, no producer warp
 constexpr int RE = kDmmaRE;   // expand: rows per item
 
@@ -39,6 +40,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 
 // Fragment-major position of element (w, n) of one target's Zt block (W x NB):
 // k-step kb = w/4, N-tile pair np = n/16, lane = (n%8)*4 + w%4, half = (n/8)%2.
+template <int NB>
 __device__ __forceinline__ int64_t zfrag(int w, int n) {
   return ((((int64_t)(w >> 2) * (NB / 16) + (n >> 4)) * 32 + (n & 7) * 4 + (w & 3)) << 1) + ((n >> 3) & 1);
 }
@@ -49,13 +51,14 @@ __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { r
 // t's column qt r + aa (qt = slot of sg in t's list).  Returns the Zt block of t
 // with the column's fragment-major base folded in: element (w, n) then sits at
 // + zfrag(0, n) (zfrag is additive in its w and n parts).
+template <int NB>
 __device__ __forceinline__ double* zt_column(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int q, int aa) {
   const int d = __ffs(a.c) - 1;
   const int me = static_cast<int>(sg & (a.c - 1));
   const int64_t t = ((sg >> d) << d) + (q < me ? q : q + 1);
   const int tc = static_cast<int>(t & (a.c - 1));
   const int qt = me < tc ? me : me - 1;
-  return lv.zt + (t - lv.tbase) * (int64_t)a.W * NB + zfrag(qt * a.r + aa, 0);
+  return lv.zt + (t - lv.tbase) * (int64_t)a.W * NB + zfrag<NB>(qt * a.r + aa, 0);
 }
 
 // ============================ project ========================================
@@ -74,10 +77,11 @@ __device__ __forceinline__ double* zt_column(const StreamArgs& a, const LevelArg
 // NW warps per CTA: 16 (one CTA per SM) or 8 (two CTAs per SM, used for
 // W % 32 != 0 so that a warp still holds 2 N-tiles: MT + 2 fragment loads per
 // 2 MT DMMAs instead of MT + 1 per MT).
-template <int KR, int MT, int NT, int NW>
+template <int KR, int MT, int NT, int NW, int NB>
 __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int XPP = KR + 4;
-  constexpr int NG = 8 / NT, MG = NW / NG;
+  constexpr int NG = NB / 8 / NT, MG = NW / NG;
+  static_assert(NG * MG == NW, "warp grid");
   constexpr int NCW = NW;
   constexpr int CTP = NCW * 32;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -198,13 +202,13 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
           // column w = q r + aa; rhs n = 8 NT ng + 8 nt + 2 tq + h
           const int w = (mg * MT + mt) * 8 + g;
           const int q = w / a.r;
-          double* zc = zt_column(a, lv, sg, q, w - q * a.r);
+          double* zc = zt_column<NB>(a, lv, sg, q, w - q * a.r);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int n = (ng * NT + nt) * 8 + tq * 2 + h;
-              if (n < a.nr) zc[zfrag(0, n)] = acc[mt][nt][h];
+              if (n < a.nr) zc[zfrag<NB>(0, n)] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
           const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
           // thread: rhs n = tid % NB, columns w = tid / NB, + CTP / NB, ... (CTP is a multiple of NB)
           const int n = tid % NB, wstep = CTP / NB;
-          const int64_t zn = zfrag(0, n);
+          const int64_t zn = zfrag<NB>(0, n);
           int w = tid / NB, q = w / a.r, aa = w - q * a.r;
           const int64_t ps = (int64_t)Wp * NB;
           const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
           for (; w < W; w += wstep) {
             const int64_t off = (int64_t)w * NB + n;
             const double v = dev::sum_cg(dev::ld_cg(p0 + off), p1 + off, 2 * ps, b1 - b0);
-            if (n < a.nr) zt_column(a, lv, sg, q, aa)[zn] = v;
+            if (n < a.nr) zt_column<NB>(a, lv, sg, q, aa)[zn] = v;
             for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
           }
           if (tid == 0) *ticket = 0;
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 
 // ============================ expand =========================================
 // CTA item: RE = 64 rows x NB rhs; warp owns rows [wm*16, wm*16+16) (2 M-tiles)
-// and rhs [wn*32, wn*32+32) (4 N-tiles).  A stage is one k-chunk of KC
+// and rhs [wn*NB/2, (wn+1)*NB/2) (NTW = NB/16 N-tiles: 4 for NB = 64, 2 for 32).  A stage is one k-chunk of KC
 // columns: the RE x (KC+4) box of U_l (tm_u) + the chunk of the target's
 // fragment-major Zt (one bulk copy), or of D (tm_d) + the (KC+4) x NB box of
 // the leaf's x (tm_xe); the extra 4 columns / rows give the conflict-free
@@ -265,9 +269,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 // the last of the 8 warps to finish a slot refills it.
 // KC: k-columns per stage (32, or 16 when W % 32 != 0); the staged U / D row
 // chunks and x columns have pitch KC + 4 (= 4 mod 16 doubles).
-template <int KC>
+template <int KC, int NB>
 __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int NCW = kThreadsE / 32;
+  constexpr int NTW = NB / 16;  // N-tiles per warp (NTW / 2 fragment-major pairs)
   constexpr int AP = KC + 4, XP = KC + 4;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -338,11 +343,11 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   uint32_t phase = 0;
   for (int64_t j = j0; j < j1; ++j) {
     const int64_t i0 = j * RE;
-    double acc[2][4][2];
+    double acc[2][NTW][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+      for (int k = 0; k < NTW; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
     for (int l = 1; l <= L + 1; ++l) {
       const bool is_d = (l == L + 1);
       if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
@@ -356,33 +361,34 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
         if (!is_d) {
 #pragma unroll
           for (int ks = 0; ks < KC / 4; ++ks) {
-            double av[2], bv[4];
+            double av[2], bv[NTW];
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
-            // fragment-major Zt chunk: k-step ks, N-tile pairs wn*2, wn*2+1
+            // fragment-major Zt chunk: k-step ks, N-tile pairs wn*NTW/2 .. + NTW/2 - 1
 #pragma unroll
-            for (int np = 0; np < 2; ++np) {
-              const double2 v = reinterpret_cast<const double2*>(Bs)[(ks * (NB / 16) + wn * 2 + np) * 32 + lane];
+            for (int np = 0; np < NTW / 2; ++np) {
+              const double2 v =
+                  reinterpret_cast<const double2*>(Bs)[(ks * (NB / 16) + wn * (NTW / 2) + np) * 32 + lane];
               bv[np * 2] = v.x;
               bv[np * 2 + 1] = v.y;
             }
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-              for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+              for (int nt = 0; nt < NTW; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
           }
         } else {
 #pragma unroll
           for (int ks = 0; ks < KC / 4; ++ks) {
-            double av[2], bv[4];
+            double av[2], bv[NTW];
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) bv[nt] = Bs[((wn * 4 + nt) * 8 + g) * XP + ks * 4 + tq];
+            for (int nt = 0; nt < NTW; ++nt) bv[nt] = Bs[((wn * NTW + nt) * 8 + g) * XP + ks * 4 + tq];
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-              for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
+              for (int nt = 0; nt < NTW; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
           }
         }
         // release: the last of the NCW warps refills the slot NS stages ahead
@@ -408,10 +414,10 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     for (int mt = 0; mt < 2; ++mt) {
       const int64_t row = i0 + wm * 16 + mt * 8 + g;
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+      for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int n = (wn * 4 + nt) * 8 + tq * 2 + h;
+          const int n = (wn * NTW + nt) * 8 + tq * 2 + h;
           if (n < a.nr) {
             double* yp = a.y + n * a.ldy + row;
             *yp = a.beta == 0.0 ? a.alpha * acc[mt][nt][h] : a.alpha * acc[mt][nt][h] + a.beta * *yp;
@@ -421,68 +427,105 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   }
 }
 
-template <int MT, int NT, int NW = kDmmaProjWarps>
+template <int MT, int NT, int NW, int NB>
 void launch_p(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  project_dmma_kernel<kDmmaKR, MT, NT, NW><<<grid, NW * 32, smem, s>>>(a);
+  project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<grid, NW * 32, smem, s>>>(a);
 }
 
-template <int MT, int NT, int NW = kDmmaProjWarps>
+template <int MT, int NT, int NW, int NB>
 cudaError_t set_p(int64_t smem) {
-  return cudaFuncSetAttribute(project_dmma_kernel<kDmmaKR, MT, NT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem);
+  return cudaFuncSetAttribute(project_dmma_kernel<kDmmaKR, MT, NT, NW, NB>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// The warp grid of a project pass (plan.cpp: dmma_project_warps picks NW):
+//   NB = 64: W % 32 == 0: NT = 2, MT = W / 32, NW = 16; W % 16 == 0: MT = W / 16,
+//            NT = 2 with NW = 8 (two CTAs per SM) or NT = 1 with NW = 16
+//   NB = 32: NT = 1; W % 32 == 0: MT = W / 32, NW = 16; W % 16 == 0: MT = W / 16, NW = 8
+template <int NB>
+void launch_p_nb(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  constexpr int NT64 = NB == 64 ? 2 : 1;
+  if (a.W % 32 == 0) {
+    switch (a.W / 32) {
+      case 1: launch_p<1, NT64, 16, NB>(a, grid, smem, s); break;
+      case 2: launch_p<2, NT64, 16, NB>(a, grid, smem, s); break;
+      case 3: launch_p<3, NT64, 16, NB>(a, grid, smem, s); break;
+      case 4: launch_p<4, NT64, 16, NB>(a, grid, smem, s); break;
+      case 5: launch_p<5, NT64, 16, NB>(a, grid, smem, s); break;
+      case 6: launch_p<6, NT64, 16, NB>(a, grid, smem, s); break;
+      default: launch_p<7, NT64, 16, NB>(a, grid, smem, s); break;
+    }
+  } else if (a.dnw == 8) {  // 2 column groups (W/16 M-tiles) x NB/8/NT rhs groups, 2 CTAs per SM
+    switch (a.W / 16) {
+      case 1: launch_p<1, NT64, 8, NB>(a, grid, smem, s); break;
+      case 3: launch_p<3, NT64, 8, NB>(a, grid, smem, s); break;
+      case 5: launch_p<5, NT64, 8, NB>(a, grid, smem, s); break;
+      default: launch_p<7, NT64, 8, NB>(a, grid, smem, s); break;
+    }
+  } else if constexpr (NB == 64) {  // (NB = 32 needs dnw = 8 here: plan.cpp)
+    switch (a.W / 16) {
+      case 1: launch_p<1, 1, 16, 64>(a, grid, smem, s); break;
+      case 3: launch_p<3, 1, 16, 64>(a, grid, smem, s); break;
+      case 5: launch_p<5, 1, 16, 64>(a, grid, smem, s); break;
+      default: launch_p<7, 1, 16, 64>(a, grid, smem, s); break;
+    }
+  }
+}
+
+template <int NB>
+cudaError_t set_p_nb(int64_t smem) {
+  constexpr int NT64 = NB == 64 ? 2 : 1;
+  cudaError_t e;
+  if ((e = set_p<1, NT64, 16, NB>(smem)) || (e = set_p<2, NT64, 16, NB>(smem)) || (e = set_p<3, NT64, 16, NB>(smem)) ||
+      (e = set_p<4, NT64, 16, NB>(smem)) || (e = set_p<5, NT64, 16, NB>(smem)) || (e = set_p<6, NT64, 16, NB>(smem)) ||
+      (e = set_p<7, NT64, 16, NB>(smem)) || (e = set_p<1, NT64, 8, NB>(smem)) || (e = set_p<3, NT64, 8, NB>(smem)) ||
+      (e = set_p<5, NT64, 8, NB>(smem)) || (e = set_p<7, NT64, 8, NB>(smem)))
+    return e;
+  return cudaSuccess;
 }
 
 }  // namespace
 
-// W % 32 == 0: NT = 2, MT = W / 32 (1..7); else W % 16 == 0: NT = 1, MT = W / 16 (1, 3, 5, 7)
-cudaError_t launch_project_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  if (a.W % 32 == 0) {
-    switch (a.W / 32) {
-      case 1: launch_p<1, 2>(a, grid, smem, s); break;
-      case 2: launch_p<2, 2>(a, grid, smem, s); break;
-      case 3: launch_p<3, 2>(a, grid, smem, s); break;
-      case 4: launch_p<4, 2>(a, grid, smem, s); break;
-      case 5: launch_p<5, 2>(a, grid, smem, s); break;
-      case 6: launch_p<6, 2>(a, grid, smem, s); break;
-      default: launch_p<7, 2>(a, grid, smem, s); break;
-    }
-  } else if (a.dnw == 8) {  // 2 column groups (W/16 M-tiles) x 4 rhs groups (2 N-tiles), 2 CTAs per SM
-    switch (a.W / 16) {
-      case 1: launch_p<1, 2, 8>(a, grid, smem, s); break;
-      case 3: launch_p<3, 2, 8>(a, grid, smem, s); break;
-      case 5: launch_p<5, 2, 8>(a, grid, smem, s); break;
-      default: launch_p<7, 2, 8>(a, grid, smem, s); break;
-    }
+cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
+  if (nb == 32)
+    launch_p_nb<32>(a, grid, smem, s);
+  else
+    launch_p_nb<64>(a, grid, smem, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
+  if (nb == 32) {
+    if (a.dkc == 16)
+      expand_dmma_kernel<16, 32><<<grid, kThreadsE, smem, s>>>(a);
+    else
+      expand_dmma_kernel<32, 32><<<grid, kThreadsE, smem, s>>>(a);
   } else {
-    switch (a.W / 16) {
-      case 1: launch_p<1, 1>(a, grid, smem, s); break;
-      case 3: launch_p<3, 1>(a, grid, smem, s); break;
-      case 5: launch_p<5, 1>(a, grid, smem, s); break;
-      default: launch_p<7, 1>(a, grid, smem, s); break;
-    }
+    if (a.dkc == 16)
+      expand_dmma_kernel<16, 64><<<grid, kThreadsE, smem, s>>>(a);
+    else
+      expand_dmma_kernel<32, 64><<<grid, kThreadsE, smem, s>>>(a);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand_dmma(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  if (a.dkc == 16)
-    expand_dmma_kernel<16><<<grid, kThreadsE, smem, s>>>(a);
-  else
-    expand_dmma_kernel<32><<<grid, kThreadsE, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t configure_dmma(int64_t smem_p, int64_t smem_e) {
+cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e) {
   cudaError_t e;
-  if ((e = set_p<1, 2>(smem_p)) || (e = set_p<2, 2>(smem_p)) || (e = set_p<3, 2>(smem_p)) ||
-      (e = set_p<4, 2>(smem_p)) || (e = set_p<5, 2>(smem_p)) || (e = set_p<6, 2>(smem_p)) ||
-      (e = set_p<7, 2>(smem_p)) || (e = set_p<1, 1>(smem_p)) || (e = set_p<3, 1>(smem_p)) ||
-      (e = set_p<5, 1>(smem_p)) || (e = set_p<7, 1>(smem_p)) || (e = set_p<1, 2, 8>(smem_p)) ||
-      (e = set_p<3, 2, 8>(smem_p)) || (e = set_p<5, 2, 8>(smem_p)) || (e = set_p<7, 2, 8>(smem_p)))
+  if (nb == 32) {
+    if ((e = set_p_nb<32>(smem_p))) return e;
+  } else {
+    if ((e = set_p_nb<64>(smem_p)) || (e = set_p<1, 1, 16, 64>(smem_p)) || (e = set_p<3, 1, 16, 64>(smem_p)) ||
+        (e = set_p<5, 1, 16, 64>(smem_p)) || (e = set_p<7, 1, 16, 64>(smem_p)))
+      return e;
+  }
+  if (nb == 32) {
+    if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
+      return e;
+    return cudaFuncSetAttribute(expand_dmma_kernel<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+  }
+  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
     return e;
-  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
-    return e;
-  return cudaFuncSetAttribute(expand_dmma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+  return cudaFuncSetAttribute(expand_dmma_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
 }
 
 }  // namespace hmat

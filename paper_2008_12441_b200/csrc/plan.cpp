@@ -215,21 +215,28 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
               leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
-    // V rows + the 64 x columns (pitch dkr + 4 = 4 mod 16 doubles)
-    p.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(kDmmaNB) * (p.dkr + 4) * 8, 128);
-    p.dstage_e = round_up(int64_t(kDmmaRE) * (p.dkc + 4) * 8 +
-                              std::max(int64_t(p.dkc) * kDmmaNB * 8, int64_t(kDmmaNB) * (p.dkc + 4) * 8),
-                          128);
     p.dnw = (p.W % 32 != 0 && opt.dmma_nw == 8) ? 8 : 16;
     const int64_t pbudget = p.dnw == 8 ? 112 * 1024 : 226 * 1024;  // 2 CTAs per SM with 8 warps
-    p.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / p.dstage_p));
-    p.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 32 ? 3 : 5, (112 * 1024 - bar_bytes) / p.dstage_e));
-    p.dsmem_p = p.dns_p * p.dstage_p + bar_bytes;
-    p.dsmem_e = p.dns_e * p.dstage_e + bar_bytes;
-    p.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * (p.dnw == 8 ? 2 : 1),
-                                                   depth > 0 ? p.N_loc / p.dkr : 0));
-    p.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * 2, p.N_loc / kDmmaRE));
-    if (p.dns_p < 2 || p.dns_e < 2) p.dmma_ok = false;
+    for (int li = 0; li < 2; ++li) {
+      Plan::DmmaLayout& d = p.dl[li];
+      d.nb = li == 0 ? 32 : kDmmaNB;
+      // V rows + the nb x columns (pitch dkr + 4 = 4 mod 16 doubles)
+      d.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(d.nb) * (p.dkr + 4) * 8, 128);
+      d.dstage_e = round_up(int64_t(kDmmaRE) * (p.dkc + 4) * 8 +
+                                std::max(int64_t(p.dkc) * d.nb * 8, int64_t(d.nb) * (p.dkc + 4) * 8),
+                            128);
+      d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / d.dstage_p));
+      d.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 32 ? 3 : 5, (112 * 1024 - bar_bytes) / d.dstage_e));
+      d.dsmem_p = d.dns_p * d.dstage_p + bar_bytes;
+      d.dsmem_e = d.dns_e * d.dstage_e + bar_bytes;
+      d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * (p.dnw == 8 ? 2 : 1),
+                                                     depth > 0 ? p.N_loc / p.dkr : 0));
+      d.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * 2, p.N_loc / kDmmaRE));
+      // (a 32-wide project pass with W % 32 != 0 needs the 8-warp grid: kernels_dmma.cu)
+      d.ok = d.dns_p >= 2 && d.dns_e >= 2 && (d.nb == kDmmaNB || ((p.W % 32 == 0 || p.dnw == 8) && opt.dmma_nb32));
+      p.dgrid_p_max = std::max(p.dgrid_p_max, d.dgrid_p);
+    }
+    if (!p.dl[1].ok) p.dmma_ok = false;
   }
   *out = p;
   return "";

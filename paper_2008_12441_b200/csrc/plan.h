@@ -81,14 +81,22 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 9, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 5, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
   int dnw = 16;                     // project: warps per CTA (16 at 1 CTA/SM, or 8 at 2 CTAs/SM)
-  int dns_p = 0, dns_e = 0;
-  int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
-  int dgrid_p = 0, dgrid_e = 0;
+  // one layout per pass width: dl[0] = 32 right-hand sides, dl[1] = 64
+  struct DmmaLayout {
+    bool ok = false;
+    int nb = 0;
+    int dns_p = 0, dns_e = 0;
+    int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
+    int dgrid_p = 0, dgrid_e = 0;
+  } dl[2];
+  int dgrid_p_max = 0;              // partial-sum / ticket slots to allocate (max over dl)
+  // the layout of a pass of `nr` right-hand sides: 32 wide when nr <= 32 and it fits
+  const DmmaLayout& dmma_layout(int nr) const { return nr <= 32 && dl[0].ok ? dl[0] : dl[1]; }
 };
 
 // index into Plan::lay of a right-hand-side capacity 1, 2, 4 or 8
@@ -104,7 +112,7 @@ struct PlanOptions {
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
   // per-call switches, read once at hmat_create (HMAT_* environment)
-  int dmma_off = 0, dmma_min = 9;   // tensor-core path off / from this many rhs (measured crossover)
+  int dmma_off = 0, dmma_min = 5;   // tensor-core path off / from this many rhs (measured crossover)
   int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)
   int expand_chunk = -1;            // expand items per dynamic chunk (-1 = default, 0 = static)
   int project_dyn = 1;              // project's last level in dynamic chunks
@@ -113,6 +121,7 @@ struct PlanOptions {
   int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
+  int dmma_nb32 = 1;                // DMMA: 32-wide passes for <= 32 remaining rhs
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.
