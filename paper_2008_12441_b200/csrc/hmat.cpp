@@ -67,7 +67,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
-  o.dmma_nb32 = env_int("HMAT_DMMA_NB32", o.dmma_nb32);
+  o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   return o;
 }
 
@@ -313,8 +313,9 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       // z rows: padding columns (odd W) are multiplied by zero padding of U, so keep them finite
       (e = cudaMemsetAsync(H->zloc, 0, std::max<size_t>(256, size_t(p.z_local_rows) * zrow), H->stream)) ||
       (e = cudaMemsetAsync(H->zex, 0, std::max<size_t>(256, size_t(p.z_exch_rows) * zrow), H->stream)) ||
-      (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(64, p.dl[1].dsmem_p, p.dl[1].dsmem_e))) ||
-      (p.dmma_ok && p.dl[0].ok && (e = hmat::configure_dmma(32, p.dl[0].dsmem_p, p.dl[0].dsmem_e))) ||
+      (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(64, p.dl[2].dsmem_p, p.dl[2].dsmem_e))) ||
+      (p.dmma_ok && p.dl[1].ok && (e = hmat::configure_dmma(32, p.dl[1].dsmem_p, p.dl[1].dsmem_e))) ||
+      (p.dmma_ok && p.dl[0].ok && (e = hmat::configure_dmma(16, p.dl[0].dsmem_p, p.dl[0].dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   H->external = p.P > 1 && dist->exchange == HMAT_EXCHANGE_EXTERNAL;
@@ -753,7 +754,6 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     a.vp = p.vp;
     a.dkr = p.dkr;
     a.dkc = p.dkc;
-    a.dnw = p.dnw;
     a.part = H->part_d;
     a.cnt = H->cnt_d;
     if (p.L > 0) {  // V-role panels [L][N_loc][Wp], box [1][dkr][vp]
@@ -777,6 +777,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       // the pass width: 32 when at most 32 rhs remain (half the work), else 64
       const hmat::Plan::DmmaLayout& dl = p.dmma_layout(a.nr);
       const int nb = dl.nb;
+      a.dnw = dl.nw;
       a.nstage_p = dl.dns_p;
       a.stage_bytes_p = dl.dstage_p;
       a.bar_off_p = dl.dns_p * dl.dstage_p;

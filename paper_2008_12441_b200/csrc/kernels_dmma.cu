@@ -6,9 +6,9 @@
 //   expand  (Step 5, eq:prod-yuz, eq:prod-ydz):      Y_tile (64 x NB) = sum_l U_l[tile] (64 x W) Zt_l[t] (W x NB)
 //                                                                       + D[tile] (64 x b) X_leaf (b x NB)
 // computed with warp-level mma.sync.m8n8k4.f64 (SASS DMMA; tcgen05 has no
-// f64 kind on sm_100a).  A pass is NB = 64 columns wide, or NB = 32 when at most
-// 32 right-hand sides remain (a pass computes all NB columns, so a narrower one
-// halves the work of 9..32 rhs).  Measured on this B200: DMMA 37.1 TFLOP/s, DFMA 36.5
+// f64 kind on sm_100a).  A pass is NB = 64 columns wide, or NB = 32 / 16 when at
+// most 32 / 16 right-hand sides remain (a pass computes all NB columns, so a
+// narrower one cuts the work of a few rhs).  Measured on this B200: DMMA 37.1 TFLOP/s, DFMA 36.5
 // (scripts/fp64_peak.cu), so the tensor path's gain is issue slots and
 // operand reuse, not a higher peak.
 //
@@ -260,8 +260,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 }
 
 // ============================ expand =========================================
-// CTA item: RE = 64 rows x NB rhs; warp owns rows [wm*16, wm*16+16) (2 M-tiles)
-// and rhs [wn*NB/2, (wn+1)*NB/2) (NTW = NB/16 N-tiles: 4 for NB = 64, 2 for 32).  A stage is one k-chunk of KC
+// CTA item: RE = 64 rows x NB rhs over WM x WN warps: warp (wm, wn) owns rows
+// [wm*8*MT, (wm+1)*8*MT) (MT M-tiles) and NTW N-tiles of rhs from wn*NTW*8:
+// NB = 64: 4 x 2 warps, MT = 2, NTW = 4; NB = 32: 4 x 2, MT = 2, NTW = 2;
+// NB = 16: 8 x 1, MT = 1, NTW = 2.  A stage is one k-chunk of KC
 // columns: the RE x (KC+4) box of U_l (tm_u) + the chunk of the target's
 // fragment-major Zt (one bulk copy), or of D (tm_d) + the (KC+4) x NB box of
 // the leaf's x (tm_xe); the extra 4 columns / rows give the conflict-free
@@ -272,7 +274,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 template <int KC, int NB>
 __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int NCW = kThreadsE / 32;
-  constexpr int NTW = NB / 16;  // N-tiles per warp (NTW / 2 fragment-major pairs)
+  constexpr int WM = NB == 16 ? 8 : 4, WN = NCW / WM;  // warp grid over rows x rhs
+  constexpr int MT = RE / 8 / WM;                      // M-tiles (8 rows) per warp
+  constexpr int NTW = NB / 8 / WN;                     // N-tiles per warp (NTW / 2 fragment-major pairs)
+  static_assert(NTW % 2 == 0 && MT * WM * 8 == RE, "expand warp grid");
   constexpr int AP = KC + 4, XP = KC + 4;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -337,15 +342,15 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     advance();
   }
 
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % WM, wn = warp / WM;
   const int g = lane >> 2, tq = lane & 3;
   int slot = 0;
   uint32_t phase = 0;
   for (int64_t j = j0; j < j1; ++j) {
     const int64_t i0 = j * RE;
-    double acc[2][NTW][2];
+    double acc[MT][NTW][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int k = 0; k < NTW; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
     for (int l = 1; l <= L + 1; ++l) {
@@ -361,9 +366,9 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
         if (!is_d) {
 #pragma unroll
           for (int ks = 0; ks < KC / 4; ++ks) {
-            double av[2], bv[NTW];
+            double av[MT], bv[NTW];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
+            for (int mt = 0; mt < MT; ++mt) av[mt] = As[(wm * 8 * MT + mt * 8 + g) * AP + ks * 4 + tq];
             // fragment-major Zt chunk: k-step ks, N-tile pairs wn*NTW/2 .. + NTW/2 - 1
 #pragma unroll
             for (int np = 0; np < NTW / 2; ++np) {
@@ -373,20 +378,20 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
               bv[np * 2 + 1] = v.y;
             }
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
               for (int nt = 0; nt < NTW; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
           }
         } else {
 #pragma unroll
           for (int ks = 0; ks < KC / 4; ++ks) {
-            double av[2], bv[NTW];
+            double av[MT], bv[NTW];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) av[mt] = As[(wm * 16 + mt * 8 + g) * AP + ks * 4 + tq];
+            for (int mt = 0; mt < MT; ++mt) av[mt] = As[(wm * 8 * MT + mt * 8 + g) * AP + ks * 4 + tq];
 #pragma unroll
             for (int nt = 0; nt < NTW; ++nt) bv[nt] = Bs[((wn * NTW + nt) * 8 + g) * XP + ks * 4 + tq];
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt)
+            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
               for (int nt = 0; nt < NTW; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av[mt], bv[nt]);
           }
@@ -411,8 +416,8 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
       }
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      const int64_t row = i0 + wm * 16 + mt * 8 + g;
+    for (int mt = 0; mt < MT; ++mt) {
+      const int64_t row = i0 + wm * 8 * MT + mt * 8 + g;
 #pragma unroll
       for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
@@ -486,8 +491,43 @@ cudaError_t set_p_nb(int64_t smem) {
 
 }  // namespace
 
+// NB = 16: NT = 1 (2 rhs groups); W % 32 == 0: MT = W / 32 over 4 column groups,
+// NW = 8; W % 16 == 0: MT = W / 16 over 2 column groups, NW = 4
+void launch_p16(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.W % 32 == 0) {
+    switch (a.W / 32) {
+      case 1: launch_p<1, 1, 8, 16>(a, grid, smem, s); break;
+      case 2: launch_p<2, 1, 8, 16>(a, grid, smem, s); break;
+      case 3: launch_p<3, 1, 8, 16>(a, grid, smem, s); break;
+      case 4: launch_p<4, 1, 8, 16>(a, grid, smem, s); break;
+      case 5: launch_p<5, 1, 8, 16>(a, grid, smem, s); break;
+      case 6: launch_p<6, 1, 8, 16>(a, grid, smem, s); break;
+      default: launch_p<7, 1, 8, 16>(a, grid, smem, s); break;
+    }
+  } else {
+    switch (a.W / 16) {
+      case 1: launch_p<1, 1, 4, 16>(a, grid, smem, s); break;
+      case 3: launch_p<3, 1, 4, 16>(a, grid, smem, s); break;
+      case 5: launch_p<5, 1, 4, 16>(a, grid, smem, s); break;
+      default: launch_p<7, 1, 4, 16>(a, grid, smem, s); break;
+    }
+  }
+}
+
+cudaError_t set_p16(int64_t smem) {
+  cudaError_t e;
+  if ((e = set_p<1, 1, 8, 16>(smem)) || (e = set_p<2, 1, 8, 16>(smem)) || (e = set_p<3, 1, 8, 16>(smem)) ||
+      (e = set_p<4, 1, 8, 16>(smem)) || (e = set_p<5, 1, 8, 16>(smem)) || (e = set_p<6, 1, 8, 16>(smem)) ||
+      (e = set_p<7, 1, 8, 16>(smem)) || (e = set_p<1, 1, 4, 16>(smem)) || (e = set_p<3, 1, 4, 16>(smem)) ||
+      (e = set_p<5, 1, 4, 16>(smem)) || (e = set_p<7, 1, 4, 16>(smem)))
+    return e;
+  return cudaSuccess;
+}
+
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
-  if (nb == 32)
+  if (nb == 16)
+    launch_p16(a, grid, smem, s);
+  else if (nb == 32)
     launch_p_nb<32>(a, grid, smem, s);
   else
     launch_p_nb<64>(a, grid, smem, s);
@@ -495,7 +535,12 @@ cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t s
 }
 
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
-  if (nb == 32) {
+  if (nb == 16) {
+    if (a.dkc == 16)
+      expand_dmma_kernel<16, 16><<<grid, kThreadsE, smem, s>>>(a);
+    else
+      expand_dmma_kernel<32, 16><<<grid, kThreadsE, smem, s>>>(a);
+  } else if (nb == 32) {
     if (a.dkc == 16)
       expand_dmma_kernel<16, 32><<<grid, kThreadsE, smem, s>>>(a);
     else
@@ -511,6 +556,12 @@ cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t sm
 
 cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e) {
   cudaError_t e;
+  if (nb == 16) {
+    if ((e = set_p16(smem_p))) return e;
+    if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
+      return e;
+    return cudaFuncSetAttribute(expand_dmma_kernel<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+  }
   if (nb == 32) {
     if ((e = set_p_nb<32>(smem_p))) return e;
   } else {

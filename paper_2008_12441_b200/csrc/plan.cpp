@@ -216,27 +216,35 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
     p.dnw = (p.W % 32 != 0 && opt.dmma_nw == 8) ? 8 : 16;
-    const int64_t pbudget = p.dnw == 8 ? 112 * 1024 : 226 * 1024;  // 2 CTAs per SM with 8 warps
-    for (int li = 0; li < 2; ++li) {
+    for (int li = 0; li < 3; ++li) {
       Plan::DmmaLayout& d = p.dl[li];
-      d.nb = li == 0 ? 32 : kDmmaNB;
+      d.nb = 16 << li;
+      // project warps: 64 / 32 wide as p.dnw; 16 wide: 8 (W % 32 == 0) or 4 (kernels_dmma.cu)
+      d.nw = d.nb == 16 ? (p.W % 32 == 0 ? 8 : 4) : p.dnw;
       // V rows + the nb x columns (pitch dkr + 4 = 4 mod 16 doubles)
       d.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(d.nb) * (p.dkr + 4) * 8, 128);
       d.dstage_e = round_up(int64_t(kDmmaRE) * (p.dkc + 4) * 8 +
                                 std::max(int64_t(p.dkc) * d.nb * 8, int64_t(d.nb) * (p.dkc + 4) * 8),
                             128);
-      d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / d.dstage_p));
+      // project CTAs per SM: 16 warps' worth (1 CTA of 16, 2 of 8, 4 of 4), fewer if
+      // two stages do not fit (64 / 32 wide keep their measured budgets)
+      int ctas = 16 / d.nw;
+      for (;; --ctas) {
+        const int64_t pbudget = d.nb == 16 ? 227 * 1024 / ctas - 1024 : (p.dnw == 8 ? 112 * 1024 : 226 * 1024);
+        d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / d.dstage_p));
+        if (d.dns_p >= 2 || ctas == 1) break;
+      }
       d.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 32 ? 3 : 5, (112 * 1024 - bar_bytes) / d.dstage_e));
       d.dsmem_p = d.dns_p * d.dstage_p + bar_bytes;
       d.dsmem_e = d.dns_e * d.dstage_e + bar_bytes;
-      d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * (p.dnw == 8 ? 2 : 1),
-                                                     depth > 0 ? p.N_loc / p.dkr : 0));
+      d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas, depth > 0 ? p.N_loc / p.dkr : 0));
       d.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * 2, p.N_loc / kDmmaRE));
       // (a 32-wide project pass with W % 32 != 0 needs the 8-warp grid: kernels_dmma.cu)
-      d.ok = d.dns_p >= 2 && d.dns_e >= 2 && (d.nb == kDmmaNB || ((p.W % 32 == 0 || p.dnw == 8) && opt.dmma_nb32));
+      const bool narrow_on = d.nb == kDmmaNB || (d.nb == 32 ? opt.dmma_narrow >= 1 : opt.dmma_narrow >= 2);
+      d.ok = d.dns_p >= 2 && d.dns_e >= 2 && narrow_on && (d.nb != 32 || p.W % 32 == 0 || p.dnw == 8);
       p.dgrid_p_max = std::max(p.dgrid_p_max, d.dgrid_p);
     }
-    if (!p.dl[1].ok) p.dmma_ok = false;
+    if (!p.dl[2].ok) p.dmma_ok = false;
   }
   *out = p;
   return "";

@@ -86,17 +86,20 @@ struct Plan {
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
   int dnw = 16;                     // project: warps per CTA (16 at 1 CTA/SM, or 8 at 2 CTAs/SM)
-  // one layout per pass width: dl[0] = 32 right-hand sides, dl[1] = 64
+  // one layout per pass width: dl[0] = 16 right-hand sides, dl[1] = 32, dl[2] = 64
   struct DmmaLayout {
     bool ok = false;
     int nb = 0;
+    int nw = 0;                     // project warps per CTA
     int dns_p = 0, dns_e = 0;
     int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
     int dgrid_p = 0, dgrid_e = 0;
-  } dl[2];
+  } dl[3];
   int dgrid_p_max = 0;              // partial-sum / ticket slots to allocate (max over dl)
-  // the layout of a pass of `nr` right-hand sides: 32 wide when nr <= 32 and it fits
-  const DmmaLayout& dmma_layout(int nr) const { return nr <= 32 && dl[0].ok ? dl[0] : dl[1]; }
+  // the layout of a pass of `nr` right-hand sides: the narrowest that holds them
+  const DmmaLayout& dmma_layout(int nr) const {
+    return nr <= 16 && dl[0].ok ? dl[0] : nr <= 32 && dl[1].ok ? dl[1] : dl[2];
+  }
 };
 
 // index into Plan::lay of a right-hand-side capacity 1, 2, 4 or 8
@@ -121,7 +124,7 @@ struct PlanOptions {
   int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
-  int dmma_nb32 = 1;                // DMMA: 32-wide passes for <= 32 remaining rhs
+  int dmma_narrow = 2;              // DMMA narrow last passes: 0 = none, 1 = 32 wide, 2 = 32 or 16 wide
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.

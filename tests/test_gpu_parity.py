@@ -198,11 +198,11 @@ DMMA = [HConfig("d3L2", d=3, L=2, b=64, r=32, seed=501), HConfig("d3L3", d=3, L=
 
 
 @pytest.mark.parametrize("cfg", DMMA, ids=lambda c: c.name)
-@pytest.mark.parametrize("nrhs", [5, 9, 16, 32, 33, 64, 70, 96])
+@pytest.mark.parametrize("nrhs", [5, 16, 17, 32, 33, 64, 70, 96])
 def test_dmma_many_rhs(cfg, nrhs):
     """FP64 tensor-core path (nrhs >= 5, W % 16 == 0, 64 | b): passes of 64
-    right-hand sides, a last pass 32 wide when at most 32 remain (9, 16, 32,
-    70 = 64 + 6, 96 = 64 + 32), ragged passes, vs the oracle."""
+    right-hand sides, the last one 16 or 32 wide when at most 16 / 32 remain
+    (5, 16 | 17, 32 | 70 = 64 + 6 | 96 = 64 + 32), ragged passes, vs the oracle."""
     U, V, D, x = host_case(cfg, nrhs)
     ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
     h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
