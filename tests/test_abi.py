@@ -105,3 +105,30 @@ def test_nccl_unique_id_resolves_the_runtime():
     import torch  # noqa: F401  (loads torch's libnccl first, as bench.py does)
     a, b = hm.hmat_nccl_unique_id(), hm.hmat_nccl_unique_id()
     assert len(a) == 128 and len(b) == 128 and a != b and any(a)
+
+
+def _build_c_example(tmp_path):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "matvec_c")
+    lib = os.path.join(root, "paper_2008_12441_b200")
+    subprocess.run(["gcc", "-std=c99", "-pedantic", "-Wall", "-Wextra", "-Werror", "-O2", "-I" + os.path.join(root, "include"),
+                    os.path.join(root, "examples", "matvec.c"), "-L" + lib, "-lhmat", "-Wl,-rpath," + lib, "-lm",
+                    "-o", exe], check=True)
+    return exe
+
+
+def test_c_example_compiles_as_plain_c(tmp_path):
+    """include/hmat.h is a C header (extern "C", plain pointers): a C99 program
+    compiles against it with -pedantic -Werror and links libhmat.so."""
+    _build_c_example(tmp_path)
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    """examples/matvec.c on the GPU: linearity and the dense part alone."""
+    import subprocess
+    out = subprocess.run([_build_c_example(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.strip().endswith("ok")
