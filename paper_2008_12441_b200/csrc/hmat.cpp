@@ -68,6 +68,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
+  o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
   return o;
 }
 
@@ -768,7 +769,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     {  // D-role panel [N_loc][Dp], box [64][KC+4]
       const uint64_t dims[2] = {uint64_t(p.Dp), uint64_t(n)};
       const uint64_t strides[1] = {uint64_t(p.Dp) * 8};
-      const uint32_t box[2] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaRE)};
+      const uint32_t box[2] = {uint32_t((p.dkc == 16 ? 16 : 32) + 4), uint32_t(hmat::kDmmaRE)};  // dense stage columns
       hmat_status st3 = encode_map(&a.tm_d, 2, a.D, dims, strides, box);
       if (st3 != HMAT_OK) return st3;
     }
@@ -792,7 +793,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         const uint32_t box[2] = {uint32_t(p.dkr + 4), uint32_t(nb)};
         hmat_status st3 = encode_map(&a.tm_x, 2, a.x, dims, strides, box);
         if (st3 != HMAT_OK) return st3;
-        const uint32_t xbox[2] = {uint32_t(p.dkc + 4), uint32_t(nb)};
+        const uint32_t xbox[2] = {uint32_t((p.dkc == 16 ? 16 : 32) + 4), uint32_t(nb)};
         if ((st3 = encode_map(&a.tm_xe, 2, a.x, dims, strides, xbox)) != HMAT_OK) return st3;
       }
       for (int l = 1; l <= p.L; ++l) {

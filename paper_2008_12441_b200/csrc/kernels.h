@@ -66,7 +66,7 @@ struct StreamArgs {
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows
   int dkr;             // DMMA project: V rows per stage (32)
-  int dkc;             // DMMA expand: k-columns per stage (32, or 16 when W % 32 != 0)
+  int dkc;             // DMMA expand: k-columns per level stage (32; 48 at W = 48; else 16)
   int dnw;             // DMMA project: warps per CTA (16, or 8 with two CTAs per SM)
   int dbg;             // diagnostics only (HMAT_DEBUG_SKIP): bit 0 skips project's math, bit 1 expand's
   int snake;           // project: even levels stream their range backwards (x tail reused from L2)

@@ -278,7 +278,10 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   constexpr int MT = RE / 8 / WM;                      // M-tiles (8 rows) per warp
   constexpr int NTW = NB / 8 / WN;                     // N-tiles per warp (NTW / 2 fragment-major pairs)
   static_assert(NTW % 2 == 0 && MT * WM * 8 == RE, "expand warp grid");
-  constexpr int AP = KC + 4, XP = KC + 4;
+  // level stages: KC columns of U (pitch AP = KC + 4); dense stages: KD columns
+  // of D (pitch APD) and the KD x NB box of x (pitch XP): KD = 16 with KC = 16, else 32
+  constexpr int KD = KC == 16 ? 16 : 32;
+  constexpr int AP = KC + 4, APD = KD + 4, XP = KD + 4;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -287,8 +290,8 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   const int64_t items = a.N_loc / RE;
   const int64_t j0 = items * bid / G, j1 = items * (bid + 1) / G;
   const int NS = a.nstage_e;
-  const int kcw = W / KC, kcd = b / KC;      // k-chunks per level / for the dense block
-  const int64_t abytes = (int64_t)RE * AP * 8;
+  const int kcw = W / KC, kcd = b / KD;      // k-chunks per level / for the dense block
+  const int64_t abytes = (int64_t)RE * AP * 8, abytes_d = (int64_t)RE * APD * 8;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
   int* done = reinterpret_cast<int*>(full + NS);
   const uint64_t pol_stream = dev::policy_evict_first();
@@ -317,9 +320,9 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     unsigned char* st = smem + sl * a.stage_bytes_e;
     const int i0 = static_cast<int>(jr * RE);
     if (lr == L + 1) {
-      dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes + NB * XP * 8));
-      dev::tma_load_2d(st, &a.tm_d, kcr * KC, i0, &full[sl], pol_stream);
-      dev::tma_load_2d(st + abytes, &a.tm_xe, (i0 / b) * b + kcr * KC, 0, &full[sl], pol_keep);
+      dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes_d + NB * XP * 8));
+      dev::tma_load_2d(st, &a.tm_d, kcr * KD, i0, &full[sl], pol_stream);
+      dev::tma_load_2d(st + abytes_d, &a.tm_xe, (i0 / b) * b + kcr * KD, 0, &full[sl], pol_keep);
     } else {
       const LevelArgs& lv = a.lv[lr];
       const double* zt = lv.zt + ((a.row0 + i0) / lv.m - lv.tbase) * (int64_t)W * NB;
@@ -360,7 +363,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
       for (int kc = 0; kc < nkc; ++kc) {
         dev::mbar_wait(&full[slot], phase);
         const double* As = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e);
-        const double* Bs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e + abytes);
+        const double* Bs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_e + (is_d ? abytes_d : abytes));
         // two copies of the k loop (U / Zt stage, D / x stage), so the compiler
         // does not if-convert the B loads of both layouts into every k-step
         if (!is_d) {
@@ -384,10 +387,10 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
           }
         } else {
 #pragma unroll
-          for (int ks = 0; ks < KC / 4; ++ks) {
+          for (int ks = 0; ks < KD / 4; ++ks) {
             double av[MT], bv[NTW];
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt) av[mt] = As[(wm * 8 * MT + mt * 8 + g) * AP + ks * 4 + tq];
+            for (int mt = 0; mt < MT; ++mt) av[mt] = As[(wm * 8 * MT + mt * 8 + g) * APD + ks * 4 + tq];
 #pragma unroll
             for (int nt = 0; nt < NTW; ++nt) bv[nt] = Bs[((wn * NTW + nt) * 8 + g) * XP + ks * 4 + tq];
 #pragma unroll
@@ -534,23 +537,32 @@ cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t s
   return cudaGetLastError();
 }
 
+template <int NB>
+void launch_e(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.dkc == 16)
+    expand_dmma_kernel<16, NB><<<grid, kThreadsE, smem, s>>>(a);
+  else if (a.dkc == 48)
+    expand_dmma_kernel<48, NB><<<grid, kThreadsE, smem, s>>>(a);
+  else
+    expand_dmma_kernel<32, NB><<<grid, kThreadsE, smem, s>>>(a);
+}
+
+template <int NB>
+cudaError_t set_e(int64_t smem) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
+      (e = cudaFuncSetAttribute(expand_dmma_kernel<48, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+    return e;
+  return cudaFuncSetAttribute(expand_dmma_kernel<32, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
-  if (nb == 16) {
-    if (a.dkc == 16)
-      expand_dmma_kernel<16, 16><<<grid, kThreadsE, smem, s>>>(a);
-    else
-      expand_dmma_kernel<32, 16><<<grid, kThreadsE, smem, s>>>(a);
-  } else if (nb == 32) {
-    if (a.dkc == 16)
-      expand_dmma_kernel<16, 32><<<grid, kThreadsE, smem, s>>>(a);
-    else
-      expand_dmma_kernel<32, 32><<<grid, kThreadsE, smem, s>>>(a);
-  } else {
-    if (a.dkc == 16)
-      expand_dmma_kernel<16, 64><<<grid, kThreadsE, smem, s>>>(a);
-    else
-      expand_dmma_kernel<32, 64><<<grid, kThreadsE, smem, s>>>(a);
-  }
+  if (nb == 16)
+    launch_e<16>(a, grid, smem, s);
+  else if (nb == 32)
+    launch_e<32>(a, grid, smem, s);
+  else
+    launch_e<64>(a, grid, smem, s);
   return cudaGetLastError();
 }
 
@@ -558,25 +570,16 @@ cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e) {
   cudaError_t e;
   if (nb == 16) {
     if ((e = set_p16(smem_p))) return e;
-    if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
-      return e;
-    return cudaFuncSetAttribute(expand_dmma_kernel<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+    return set_e<16>(smem_e);
   }
   if (nb == 32) {
     if ((e = set_p_nb<32>(smem_p))) return e;
-  } else {
-    if ((e = set_p_nb<64>(smem_p)) || (e = set_p<1, 1, 16, 64>(smem_p)) || (e = set_p<3, 1, 16, 64>(smem_p)) ||
-        (e = set_p<5, 1, 16, 64>(smem_p)) || (e = set_p<7, 1, 16, 64>(smem_p)))
-      return e;
+    return set_e<32>(smem_e);
   }
-  if (nb == 32) {
-    if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
-      return e;
-    return cudaFuncSetAttribute(expand_dmma_kernel<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
-  }
-  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e)))
+  if ((e = set_p_nb<64>(smem_p)) || (e = set_p<1, 1, 16, 64>(smem_p)) || (e = set_p<3, 1, 16, 64>(smem_p)) ||
+      (e = set_p<5, 1, 16, 64>(smem_p)) || (e = set_p<7, 1, 16, 64>(smem_p)))
     return e;
-  return cudaFuncSetAttribute(expand_dmma_kernel<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+  return set_e<64>(smem_e);
 }
 
 }  // namespace hmat

@@ -210,7 +210,11 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   // W % 32 == 0: 4 column groups of W/32 M-tiles, 32-column expand chunks;
   // W % 16 == 0: 2 column groups of W/16 M-tiles (<= 7), 16-column chunks
   p.dkr = kDmmaKR;
-  p.dkc = p.W % 32 == 0 ? 32 : 16;
+  // expand k-chunk of a level stage: 32 columns (W % 32 == 0), the whole level at
+  // W = 48 (the c2 / c4 shape: a third of the stages of 16-column chunks), else 16;
+  // dense stages are 32 columns of D (kernels_dmma.cu KD)
+  p.dkc = opt.dmma_kc > 0 ? opt.dmma_kc : p.W % 32 == 0 ? 32 : p.W == 48 ? 48 : 16;
+  if (p.W % p.dkc != 0 || (p.dkc != 16 && p.dkc != 32 && p.dkc != 48)) p.dkc = p.W % 32 == 0 ? 32 : 16;
   p.dmma_ok = p.adm == 0 && !opt.peer && p.W % 16 == 0 && (p.W % 32 == 0 ? p.W <= 224 : p.W <= 112) &&
               leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
@@ -223,8 +227,9 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       d.nw = d.nb == 16 ? (p.W % 32 == 0 ? 8 : 4) : p.dnw;
       // V rows + the nb x columns (pitch dkr + 4 = 4 mod 16 doubles)
       d.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(d.nb) * (p.dkr + 4) * 8, 128);
-      d.dstage_e = round_up(int64_t(kDmmaRE) * (p.dkc + 4) * 8 +
-                                std::max(int64_t(p.dkc) * d.nb * 8, int64_t(d.nb) * (p.dkc + 4) * 8),
+      const int64_t kd = p.dkc == 16 ? 16 : 32;  // dense-stage columns (kernels_dmma.cu KD)
+      d.dstage_e = round_up(std::max(int64_t(kDmmaRE) * (p.dkc + 4) * 8 + int64_t(p.dkc) * d.nb * 8,
+                                     int64_t(kDmmaRE) * (kd + 4) * 8 + int64_t(d.nb) * (kd + 4) * 8),
                             128);
       // project CTAs per SM: 16 warps' worth (1 CTA of 16, 2 of 8, 4 of 4), fewer if
       // two stages do not fit (64 / 32 wide keep their measured budgets)
@@ -234,7 +239,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
         d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / d.dstage_p));
         if (d.dns_p >= 2 || ctas == 1) break;
       }
-      d.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 32 ? 3 : 5, (112 * 1024 - bar_bytes) / d.dstage_e));
+      d.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 16 ? 5 : 3, (112 * 1024 - bar_bytes) / d.dstage_e));
       d.dsmem_p = d.dns_p * d.dstage_p + bar_bytes;
       d.dsmem_e = d.dns_e * d.dstage_e + bar_bytes;
       d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas, depth > 0 ? p.N_loc / p.dkr : 0));

@@ -84,7 +84,7 @@ struct Plan {
   int dmma_off = 0, dmma_min = 5, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
-  int dkc = kDmmaKC;                // expand: k-columns per stage (32, or 16 when W % 32 != 0)
+  int dkc = kDmmaKC;                // expand: k-columns per level stage (32; 48 at W = 48; else 16)
   int dnw = 16;                     // project: warps per CTA (16 at 1 CTA/SM, or 8 at 2 CTAs/SM)
   // one layout per pass width: dl[0] = 16 right-hand sides, dl[1] = 32, dl[2] = 64
   struct DmmaLayout {
@@ -125,6 +125,7 @@ struct PlanOptions {
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
   int dmma_narrow = 2;              // DMMA narrow last passes: 0 = none, 1 = 32 wide, 2 = 32 or 16 wide
+  int dmma_kc = 0;                  // DMMA expand k-columns per level stage (0 = auto: 32 / 48 / 16)
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.
