@@ -24,11 +24,7 @@
 namespace hmat {
 namespace {
 
-constexpr int CT = kConsumerThreads;   // expand: 8 consumer warps
-constexpr int NCW = CT / 32;
-// project: 16 warps (4 per SM sub-partition), no producer warp
-constexpr int kDmmaProjWarps = 16;
-constexpr int kMaxThreadsP = kDmmaProjWarps * 32;
+// project: 16 warps (4 per SM sub-partition) or 8, no producer warp (launch_p)
 constexpr int kThreadsE = 256;  // expand: 8 warps, no producer warp
 constexpr int RE = kDmmaRE;   // expand: rows per item
 
