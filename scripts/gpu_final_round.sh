@@ -19,3 +19,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pro
 echo "full c2 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"dmma" -s 2 -c 2 -o gpurun_out/prof_c5_full python scripts/kernel_sweep.py c5 "" > gpurun_out/ncu_c5.log 2>&1
 echo "ncu c5 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"project_kernel|expand_kernel" -s 4 -c 2 -o gpurun_out/prof_c4_full python scripts/kernel_sweep.py c4 "" > gpurun_out/ncu_c4.log 2>&1
+echo "full c4 rc=$?"

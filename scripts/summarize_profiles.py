@@ -86,4 +86,14 @@ if os.path.exists(rep):
             for h, v in sorted(st, key=lambda t: -float(t[1]))[:6]:
                 f.write(f"    {h[len('smsp__pcsamp_warps_issue_stalled_'):]:30s} {100 * float(v) / tot:5.1f}%\n")
             f.write("\n")
+# 4. full captures of the bench's workload (c4) and of the DMMA kernels (c5): summaries,
+#    reports, and their per-launch DRAM traffic (replaces step 2's entry for c4)
+for cfg, what in (("c5", "python scripts/kernel_sweep.py c5 (full c5: N=2^21, W=224, 64 rhs)"),
+                  ("c4", "python scripts/kernel_sweep.py c4 (full c4: N=2^24, W=48, 1 rhs; the bench's workload)")):
+    rep = os.path.join(G, f"prof_{cfg}_full.ncu-rep")
+    if os.path.exists(rep):
+        subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "summarize_ncu.py"), rep,
+                        os.path.join(P, f"{rnd}_ncu_full_{cfg}_summary.txt"), f"{what}, {rnd}", "--traffic", cfg],
+                       check=True, capture_output=True)
+        subprocess.run(["cp", rep, os.path.join(P, f"{rnd}_prof_{cfg}_full.ncu-rep")], check=True)
 print("ok")
