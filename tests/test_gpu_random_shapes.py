@@ -89,3 +89,46 @@ def test_random_strict(d, L, b, r, nrhs):
         assert_parity(yd.t().cpu().numpy(), oracle.matvec_strict(d, L, b, r, U, V, Dc, x))
     finally:
         hm.hmat_destroy(h)
+
+
+def _dmma_shapes(n, seed):
+    """Random shapes the tensor-core path takes (W % 16 == 0 within its limits,
+    64 | b), with right-hand-side counts hitting every pass width (16 / 32 / 64
+    wide, ragged, several passes)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        d = int(rng.integers(1, 4))
+        c1 = (1 << d) - 1
+        r = int(rng.choice([16, 32, 48, 64, 80]))
+        W = c1 * r
+        if W % 16 or (W % 32 == 0 and W > 224) or (W % 32 and W > 112):
+            continue
+        b = int(rng.choice([64, 128]))
+        L = int(rng.integers(1, {1: 6, 2: 4, 3: 3}[d] + 1))
+        N = b * (1 << d) ** L
+        if N > 1 << 15:
+            continue
+        nrhs = int(rng.choice([5, 11, 16, 17, 29, 32, 40, 64, 65, 81, 100]))
+        out.append((d, L, b, r, nrhs))
+    return out
+
+
+@pytest.mark.parametrize("d,L,b,r,nrhs", _dmma_shapes(14, 515), ids=lambda v: str(v))
+def test_random_dmma(d, L, b, r, nrhs):
+    cfg = HConfig("rndm", d=d, L=L, b=b, r=r, seed=5000 + 97 * d + 13 * L + b + r)
+    U, V, D = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs)
+    h = hm.hmat_create(L, d, b, r, U, V, D)
+    try:
+        assert hm.hmat_launches_per_matvec(h, nrhs) == 2 * ((nrhs + 63) // 64)  # the DMMA passes
+        xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        yd = torch.full_like(xd, float("nan"))
+        hm.hmat_matvec(h, xd.t(), yd.t(), nrhs)
+        torch.cuda.synchronize()
+        assert_parity(yd.t().cpu().numpy(), oracle.matvec(d, L, b, r, U, V, D, x))
+        hm.hmat_gemv(h, 1, 1.0, xd.t(), 0.0, yd.t(), nrhs)             # H^T on the same passes
+        torch.cuda.synchronize()
+        assert_parity(yd.t().cpu().numpy(), oracle.matvec_t(d, L, b, r, U, V, D, x))
+    finally:
+        hm.hmat_destroy(h)
