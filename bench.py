@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
-                    help="N > 1: in-kernel exchange over NVLink peer memory (default) or ncclAllReduce")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "tree"],
+                    help="N > 1: in-kernel exchange over NVLink peer memory (default), ncclAllReduce, or the "
+                         "paper's tree-structured exchange (recursive doubling over ncclSend/ncclRecv)")
     return ap.parse_args()
 
 
@@ -303,7 +304,9 @@ def run_ours(args):
     t_setup = time.perf_counter()
     # the in-kernel peer exchange serves the single-rhs weak path; the standard
     # structure and the many-rhs tensor-core path exchange through NCCL
-    exchange = ("nccl" if (cfg.adm or nrhs >= DMMA_MIN_RHS) else args.exchange) if world > 1 else "none"
+    exchange = args.exchange if world > 1 else "none"
+    if exchange == "peer" and (cfg.adm or nrhs >= DMMA_MIN_RHS):
+        exchange = "nccl"  # the peer exchange serves the single-rhs weak path only
     h = None
     if exchange == "peer":
         # mailboxes connected once through CUDA IPC handles (hmat_peer_export/_import)
@@ -326,7 +329,8 @@ def run_ours(args):
             h = None
             exchange = "nccl (peer unavailable: " + [e for e in errs if e][0][:120] + ")"
     if h is None:
-        dd = hm._dist(nranks=world, rank=rank, nccl_unique_id=nid, cuda_stream=sptr, device=local)
+        dd = hm._dist(nranks=world, rank=rank, nccl_unique_id=nid, cuda_stream=sptr, device=local,
+                      exchange=hm.HMAT_EXCHANGE_TREE if exchange == "tree" else hm.HMAT_EXCHANGE_NCCL)
         h = create(cfg.L, cfg.d, cfg.b, cfg.r, dd)
     r0, r1 = hm.hmat_local_rows(h)
     n = r1 - r0

@@ -90,10 +90,17 @@ typedef struct {
  *            Mailboxes are connected once with hmat_peer_export/_import (CUDA
  *            IPC, one process per GPU) or hmat_peer_connect_local (one process).
  *            No host or NCCL call per matvec; the many-rhs tensor-core path is
- *            not used in this mode. */
+ *            not used in this mode.
+ *   TREE     the paper's tree-structured Steps 2-4 over NCCL point-to-point
+ *            (needs nccl_unique_id): log2 P rounds of recursive doubling on
+ *            the hypercube of ranks, round j swapping the packed buffer with
+ *            rank ^ 2^j (ncclSend/ncclRecv) and adding the partner's copy;
+ *            every rank ends with bit-identical sums (IEEE addition is
+ *            commutative), whatever algorithm NCCL would pick for an allreduce. */
 #define HMAT_EXCHANGE_NCCL 0
 #define HMAT_EXCHANGE_EXTERNAL 1
 #define HMAT_EXCHANGE_PEER 2
+#define HMAT_EXCHANGE_TREE 3
 
 /* Build H from canonical panels (see above).  U and V are arrays of `depth`
  * pointers (ignored when depth == 0); each panel and D may be host (pageable or
@@ -236,8 +243,10 @@ hmat_status hmat_nccl_unique_id(void* out128);
 /* Diagnostic: runs the library's NCCL layer end to end on ONE GPU -- a fresh
  * unique id, a one-rank communicator on `device`, an in-place sum of `count`
  * doubles (the call every multi-GPU matvec makes on its packed exchange
- * buffer), destroy -- and checks the buffer is unchanged
- * (a one-rank sum is the identity).  HMAT_ERR_NCCL / HMAT_ERR_CUDA on failure,
+ * buffer) checked unchanged (a one-rank sum is the
+ * identity), then one round of the TREE exchange with this rank as its own
+ * partner (ncclSend + ncclRecv in a group, then the add) checked to double
+ * every value, destroy.  HMAT_ERR_NCCL / HMAT_ERR_CUDA on failure,
  * HMAT_ERR_INVALID for count < 1. */
 hmat_status hmat_nccl_selftest(int device, int64_t count);
 

@@ -19,6 +19,10 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   std::string error;
 };
 
@@ -40,7 +44,12 @@ NcclApi& api() {
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(a.handle, "ncclAllReduce"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.handle, "ncclCommDestroy"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(a.handle, "ncclGetErrorString"));
-    if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.GetErrorString)
+    a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(a.handle, "ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(a.handle, "ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.handle, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.handle, "ncclGroupEnd"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.GetErrorString || !a.Send ||
+        !a.Recv || !a.GroupStart || !a.GroupEnd)
       a.error = "libnccl is missing a required symbol";
   });
   return a;
@@ -86,6 +95,31 @@ std::string comm_allreduce_sum(Comm* c, double* buf, size_t count, cudaStream_t 
   if (count == 0) return "";
   ncclResult_t r = api().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, stream);
   if (r != ncclSuccess) return nccl_err("ncclAllReduce", r);
+  return "";
+}
+
+std::string comm_swap_round(Comm* c, const double* buf, double* tmp, size_t count, int partner, cudaStream_t stream) {
+  NcclApi& a = api();
+  ncclResult_t r = a.GroupStart();
+  if (r != ncclSuccess) return nccl_err("ncclGroupStart", r);
+  ncclResult_t rs = a.Send(buf, count, ncclFloat64, partner, c->comm, stream);
+  ncclResult_t rr = a.Recv(tmp, count, ncclFloat64, partner, c->comm, stream);
+  r = a.GroupEnd();
+  if (rs != ncclSuccess) return nccl_err("ncclSend", rs);
+  if (rr != ncclSuccess) return nccl_err("ncclRecv", rr);
+  if (r != ncclSuccess) return nccl_err("ncclGroupEnd", r);
+  return "";
+}
+
+std::string comm_tree_allreduce_sum(Comm* c, double* buf, double* tmp, size_t count, int nranks, int rank,
+                                    cudaStream_t stream) {
+  if (count == 0) return "";
+  for (int bit = 1; bit < nranks; bit <<= 1) {
+    std::string m = comm_swap_round(c, buf, tmp, count, rank ^ bit, stream);
+    if (!m.empty()) return m;
+    cudaError_t e = launch_add_inplace(buf, tmp, count, stream);
+    if (e != cudaSuccess) return std::string("add_inplace: ") + cudaGetErrorString(e);
+  }
   return "";
 }
 

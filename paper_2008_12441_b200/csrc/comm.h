@@ -22,6 +22,21 @@ std::string comm_unique_id(void* out128);
 std::string comm_create(const void* id128, int nranks, int rank, Comm** out);
 // In-place sum of `count` doubles over all ranks, on `stream`.
 std::string comm_allreduce_sum(Comm* c, double* buf, size_t count, cudaStream_t stream);
+// The paper's tree-structured Steps 2-4 (reduce to group leaders, leader to
+// leader, broadcast back) on the hypercube of the P = 2^k
+// ranks: log2 P rounds of recursive doubling, round j swapping the whole packed
+// buffer with rank ^ 2^j (ncclSend + ncclRecv in one group) and adding the
+// partner's copy (launch_add_inplace).  IEEE addition is commutative, so both
+// partners hold bit-identical sums after every round, and after the last one
+// every rank holds the same total -- deterministic, unlike an allreduce whose
+// algorithm NCCL picks.  tmp: count doubles of scratch.
+std::string comm_tree_allreduce_sum(Comm* c, double* buf, double* tmp, size_t count, int nranks, int rank,
+                                    cudaStream_t stream);
+// One round: buf -> partner, partner's buf -> tmp (partner may be this rank).
+std::string comm_swap_round(Comm* c, const double* buf, double* tmp, size_t count, int partner, cudaStream_t stream);
 void comm_destroy(Comm* c);
+
+// buf[i] += add[i] (kernels_aux.cu)
+cudaError_t launch_add_inplace(double* buf, const double* add, size_t n, cudaStream_t s);
 
 }  // namespace hmat

@@ -145,6 +145,10 @@ struct hmat_s {
   int64_t* pack_d = nullptr;
   int32_t* halo_of_d = nullptr;
   bool external = false;  // P > 1 with a caller-provided exchange (split-phase API)
+  // HMAT_EXCHANGE_TREE: recursive doubling over NCCL point-to-point; scratch buffer
+  bool tree = false;
+  double* xtmp = nullptr;
+  size_t xtmp_cap = 0;
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): this rank's mailbox
   // [2 parities][P slots][mb] doubles + [2][P] uint64 flags, and the device
   // table of every rank's mailbox address (peer memory)
@@ -173,6 +177,7 @@ void release(hmat_s* H) {
   cudaSetDevice(H->device);
   if (H->stream) cudaStreamSynchronize(H->stream);
   cudaFree(H->trace);
+  cudaFree(H->xtmp);
   cudaFree(H->U);
   cudaFree(H->V);
   cudaFree(H->D);
@@ -224,10 +229,11 @@ hmat_status validate_dist(const hmat_dist_t* dist, int* P, int* rank) {
   if (!dist) return HMAT_OK;
   *P = dist->nranks;
   *rank = dist->rank;
-  if (dist->exchange < HMAT_EXCHANGE_NCCL || dist->exchange > HMAT_EXCHANGE_PEER)
-    return fail(HMAT_ERR_INVALID, "exchange must be HMAT_EXCHANGE_NCCL, _EXTERNAL or _PEER");
-  if (dist->nranks > 1 && dist->exchange == HMAT_EXCHANGE_NCCL && !dist->nccl_unique_id)
-    return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1 and the NCCL exchange");
+  if (dist->exchange < HMAT_EXCHANGE_NCCL || dist->exchange > HMAT_EXCHANGE_TREE)
+    return fail(HMAT_ERR_INVALID, "exchange must be HMAT_EXCHANGE_NCCL, _EXTERNAL, _PEER or _TREE");
+  if (dist->nranks > 1 && (dist->exchange == HMAT_EXCHANGE_NCCL || dist->exchange == HMAT_EXCHANGE_TREE) &&
+      !dist->nccl_unique_id)
+    return fail(HMAT_ERR_INVALID, "nccl_unique_id is NULL with nranks > 1 and an NCCL exchange");
   if (dist->device < 0) return fail(HMAT_ERR_INVALID, "device ordinal must be >= 0");
   return HMAT_OK;
 }
@@ -320,6 +326,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   H->external = p.P > 1 && dist->exchange == HMAT_EXCHANGE_EXTERNAL;
+  H->tree = p.P > 1 && dist->exchange == HMAT_EXCHANGE_TREE;
   H->peer = peer;
   if (peer) {
     H->mb = (p.z_exch_rows * p.Wp * hmat::kMaxNR + 15) / 16 * 16;
@@ -734,7 +741,14 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     if ((phases & kPhaseExchange) && !H->external && !H->peer && p.P > 1 && exch) {
       prof_begin(H, 1, &ep);
-      std::string m = hmat::comm_allreduce_sum(H->comm, zex, exch, H->stream);
+      std::string m;
+      if (H->tree) {
+        hmat_status st = ensure_buf(&H->xtmp, &H->xtmp_cap, exch);
+        if (st != HMAT_OK) return st;
+        m = hmat::comm_tree_allreduce_sum(H->comm, zex, H->xtmp, exch, p.P, p.rank, H->stream);
+      } else {
+        m = hmat::comm_allreduce_sum(H->comm, zex, exch, H->stream);
+      }
       if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
       prof_end(H, &ep);
     }
@@ -1038,12 +1052,25 @@ hmat_status hmat_nccl_selftest(int device, int64_t count) {
   if (e == cudaSuccess) m = hmat::comm_allreduce_sum(c, d, static_cast<size_t>(count), s);
   if (e == cudaSuccess && m.empty()) e = cudaStreamSynchronize(s);
   if (e == cudaSuccess && m.empty()) e = cudaMemcpy(back.data(), d, bytes, cudaMemcpyDeviceToHost);
+  bool same = back == h;
+  // one TREE round with this rank as its own partner: the buffer doubles
+  double* t = nullptr;
+  std::vector<double> twice(static_cast<size_t>(count));
+  if (e == cudaSuccess && m.empty()) e = cudaMalloc(&t, bytes);
+  if (e == cudaSuccess && m.empty()) m = hmat::comm_swap_round(c, d, t, static_cast<size_t>(count), 0, s);
+  if (e == cudaSuccess && m.empty()) e = hmat::launch_add_inplace(d, t, static_cast<size_t>(count), s);
+  if (e == cudaSuccess && m.empty()) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && m.empty()) e = cudaMemcpy(twice.data(), d, bytes, cudaMemcpyDeviceToHost);
   if (s) cudaStreamDestroy(s);
   if (d) cudaFree(d);
+  if (t) cudaFree(t);
   hmat::comm_destroy(c);
   if (e != cudaSuccess) return cuda_fail(e, "hmat_nccl_selftest");
   if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
-  if (back != h) return fail(HMAT_ERR_NCCL, "one-rank ncclAllReduce changed the buffer");
+  if (!same) return fail(HMAT_ERR_NCCL, "one-rank ncclAllReduce changed the buffer");
+  for (int64_t i = 0; i < count; ++i)
+    if (twice[static_cast<size_t>(i)] != 2.0 * h[static_cast<size_t>(i)])
+      return fail(HMAT_ERR_NCCL, "tree round (send/recv to self + add) gave a wrong value");
   return HMAT_OK;
 }
 

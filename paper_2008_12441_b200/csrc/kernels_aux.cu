@@ -4,6 +4,7 @@
 // PAPER.md:961-969): H^T has the same block structure with U and V exchanged
 // and every dense leaf block transposed, so the expand kernel runs unchanged on
 // (V, U, D^T).
+#include "comm.h"
 #include "geometry.cuh"
 #include "kernels.h"
 
@@ -74,12 +75,24 @@ __global__ void std_unpack_z_kernel(double* __restrict__ zt, const double* __res
   }
 }
 
+// buf += add, elementwise (the tree exchange's combine, comm.h)
+__global__ void add_inplace_kernel(double* __restrict__ buf, const double* __restrict__ add, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] += add[i];
+}
+
 int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   return static_cast<int>(g < 1 ? 1 : g > 148 * 16 ? 148 * 16 : g);
 }
 
 }  // namespace
+
+cudaError_t launch_add_inplace(double* buf, const double* add, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  add_inplace_kernel<<<grid_for(static_cast<int64_t>(n)), 256, 0, s>>>(buf, add, static_cast<int64_t>(n));
+  return cudaGetLastError();
+}
 
 cudaError_t launch_std_pack_x(double* halo, const double* x, int64_t ldx, const int64_t* pack, int64_t n_pack, int cap,
                               int nr, int b, int bpad, cudaStream_t s) {

@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 HMAT_OK, HMAT_ERR_INVALID, HMAT_ERR_NOMEM, HMAT_ERR_CUDA, HMAT_ERR_NCCL, HMAT_ERR_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 HMAT_NUM_PHASES = 4
-HMAT_EXCHANGE_NCCL, HMAT_EXCHANGE_EXTERNAL, HMAT_EXCHANGE_PEER = 0, 1, 2
+HMAT_EXCHANGE_NCCL, HMAT_EXCHANGE_EXTERNAL, HMAT_EXCHANGE_PEER, HMAT_EXCHANGE_TREE = 0, 1, 2, 3
 PHASES = ("project", "exchange", "expand", "copies")
 
 # Every symbol include/hmat.h declares (checked by tests/test_abi.py).

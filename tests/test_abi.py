@@ -69,8 +69,12 @@ def test_create_rejects_invalid_before_device_work():
     h = ctypes.c_void_p()
     assert hm._lib.hmat_create(2, 2, 4, 2, None, None, None, None, ctypes.byref(h)) == hm.HMAT_ERR_INVALID
     assert hm._lib.hmat_create(2, 2, 4, 2, None, None, None, None, None) == hm.HMAT_ERR_INVALID
-    # P > 1 needs an NCCL id
+    # P > 1 needs an NCCL id (allreduce and tree exchanges); exchange modes are 0..3
     d = hm._dist(nranks=2, rank=0, device=0)
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_create_uninit, 3, 2, 64, 8, d)
+    d = hm._dist(nranks=2, rank=0, device=0, exchange=hm.HMAT_EXCHANGE_TREE)
+    expect(hm.HMAT_ERR_INVALID, hm.hmat_create_uninit, 3, 2, 64, 8, d)
+    d = hm._dist(nranks=2, rank=0, device=0, exchange=4)
     expect(hm.HMAT_ERR_INVALID, hm.hmat_create_uninit, 3, 2, 64, 8, d)
 
 
