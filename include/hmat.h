@@ -185,7 +185,7 @@ hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, cons
  *   the caller sums exchange over all ranks (Steps 2-4);
  *   hmat_expand: reads the summed exchange, Step 5: y = H x.
  * With HMAT_EXCHANGE_NCCL hmat_matvec does exactly this with an
- * in-place ncclAllReduce.  With HMAT_EXCHANGE_PEER `exchange` is ignored (may
+ * in-place ncclAllReduce (HMAT_EXCHANGE_TREE: the recursive-doubling rounds).  With HMAT_EXCHANGE_PEER `exchange` is ignored (may
  * be NULL): the kernels exchange through the connected mailboxes. */
 hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count);
 hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange);
