@@ -41,6 +41,14 @@
  * y it returns after y is complete.  With nranks > 1 hmat_matvec is a
  * collective: every rank calls it with the same nrhs in the same order.
  *
+ * CUDA GRAPHS: with device x/y (16-byte aligned), profiling off, and one GPU or
+ * the NCCL / TREE exchange, a call enqueues only kernels, memsets and NCCL calls
+ * on H's stream, so it may be stream-captured (set H's stream to the capturing
+ * stream with hmat_set_stream, and make one uncaptured call first: buffers are
+ * allocated lazily) and replayed; the kernels re-arm their own work counters.
+ * Host vectors and the PEER exchange (a host-side pass counter) are not
+ * capture-safe.
+ *
  * ERRORS: every entry point returns HMAT_OK or a negative hmat_status and sets
  * a thread-local message readable with hmat_last_error().  Argument checks
  * happen before any device work.  No C++ exception crosses this ABI.

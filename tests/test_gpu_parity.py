@@ -460,3 +460,43 @@ def test_host_async_pipeline_bitwise_at_c2_size():
     finally:
         hm.hmat_destroy(h)
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("nrhs", [1, 64])
+def test_cuda_graph_capture_and_replay(nrhs):
+    """A matvec is capture-safe (P = 1): warmed up once (lazy buffers), captured
+    into a CUDA graph on the capturing stream (hmat_set_stream), replayed on new x
+    -- same bits as direct calls (the dynamic work counters re-arm inside the
+    kernels, so replays need no host work)."""
+    cfg = HConfig("graph", d=2, L=4, b=64, r=16, seed=1601)           # W = 48: nrhs 64 takes DMMA
+    U, V, D = hgen.inputs(cfg)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        xs = [torch.from_numpy(np.ascontiguousarray(hgen.xblock(cfg, nrhs=nrhs, vec=v).T)).cuda() for v in range(3)]
+        x = torch.empty_like(xs[0])
+        y = torch.empty_like(xs[0])
+        s = torch.cuda.Stream()
+        hm.hmat_set_stream(h, s.cuda_stream)
+        with torch.cuda.stream(s):
+            x.copy_(xs[0])
+            hm.hmat_matvec(h, x.t(), y.t(), nrhs)                      # warm-up: lazy allocations
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            hm.hmat_matvec(h, x.t(), y.t(), nrhs)
+        for v in (1, 2, 1):
+            x.copy_(xs[v])
+            g.replay()
+            torch.cuda.synchronize()
+            want = torch.empty_like(y)
+            with torch.cuda.stream(s):
+                hm.hmat_matvec(h, xs[v].t(), want.t(), nrhs)
+            s.synchronize()
+            assert torch.equal(y, want)
+        ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, xs[1].t().cpu().numpy())
+        x.copy_(xs[1])
+        g.replay()
+        torch.cuda.synchronize()
+        assert_parity(y.t().cpu().numpy(), ref)
+    finally:
+        hm.hmat_destroy(h)
