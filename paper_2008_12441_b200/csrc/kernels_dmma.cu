@@ -488,8 +488,6 @@ cudaError_t set_p_nb(int64_t smem) {
   return cudaSuccess;
 }
 
-}  // namespace
-
 // NB = 16: NT = 1 (2 rhs groups); W % 32 == 0: MT = W / 32 over 4 column groups,
 // NW = 8; W % 16 == 0: MT = W / 16 over 2 column groups, NW = 4
 void launch_p16(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
@@ -523,16 +521,6 @@ cudaError_t set_p16(int64_t smem) {
   return cudaSuccess;
 }
 
-cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
-  if (nb == 16)
-    launch_p16(a, grid, smem, s);
-  else if (nb == 32)
-    launch_p_nb<32>(a, grid, smem, s);
-  else
-    launch_p_nb<64>(a, grid, smem, s);
-  return cudaGetLastError();
-}
-
 template <int NB>
 void launch_e(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
   if (a.dkc == 16)
@@ -550,6 +538,18 @@ cudaError_t set_e(int64_t smem) {
       (e = cudaFuncSetAttribute(expand_dmma_kernel<48, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
     return e;
   return cudaFuncSetAttribute(expand_dmma_kernel<32, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+}  // namespace
+
+cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
+  if (nb == 16)
+    launch_p16(a, grid, smem, s);
+  else if (nb == 32)
+    launch_p_nb<32>(a, grid, smem, s);
+  else
+    launch_p_nb<64>(a, grid, smem, s);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
