@@ -277,7 +277,10 @@ hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches);
 hmat_status hmat_cta_trace(hmat_t H, int enable);
 hmat_status hmat_cta_trace_read(hmat_t H, int kernel, int64_t* out, int max_ctas, int* n_ctas);
 
-/* Kernel launches one hmat_matvec(nrhs) performs on this rank. */
+/* Launches of this library's kernels one hmat_matvec(nrhs) performs on this
+ * rank: per pass of right-hand sides, project + expand, + pack / unpack with
+ * standard admissibility and P > 1, + log2 P adds with the TREE exchange (NCCL's
+ * own kernels and memsets not counted). */
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs);
 
 /* Host-only description of a shard's plan (no GPU needed). */

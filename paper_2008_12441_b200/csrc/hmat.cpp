@@ -1180,9 +1180,15 @@ hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches) {
 
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs) {
   if (!H || nrhs < 1) return -1;
-  const int per = use_dmma(H->plan, nrhs) ? hmat::kDmmaNB : H->plan.max_nr;
+  const hmat::Plan& p = H->plan;
+  const int per = use_dmma(p, nrhs) ? hmat::kDmmaNB : p.max_nr;
   const int64_t passes = (nrhs + per - 1) / per;
-  return passes * ((H->plan.stages_p > 0 ? 1 : 0) + 1);
+  int per_pass = (p.stages_p > 0 ? 1 : 0) + 1;  // project (if any level) + expand
+  if (H->sx) per_pass += 2;                     // standard admissibility, P > 1: pack x, unpack z
+  if (H->tree) {                                // one add kernel per recursive-doubling round
+    for (int bit = 1; bit < p.P; bit <<= 1) ++per_pass;
+  }
+  return passes * per_pass;
 }
 
 hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
