@@ -17,6 +17,13 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 }
 
 // Make mbarrier inits visible to the async (TMA) proxy.
+// Programmatic dependent launch (PDL): the expand kernel is launched with
+// programmatic stream serialisation, so its CTAs may start (and run their
+// prologue) while project's last CTAs finish; it waits for project's completion
+// and memory before its first dependent read.  Project lets it launch early.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

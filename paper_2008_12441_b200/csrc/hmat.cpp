@@ -66,6 +66,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
+  o.pdl = env_int("HMAT_PDL", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
@@ -712,6 +713,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.zex_base = H->zex;
   a.dbg = p.dbg;
   a.snake = p.snake;
+  // PDL (expand's launch and prologue overlap project's tail) for whole products;
+  // off while the per-kernel profiler brackets the kernels with events
+  // and the CTA trace (its memsets sit between the kernels)
+  a.pdl = p.pdl && !H->prof && !H->trace && phases == kPhaseAll;
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.

@@ -70,6 +70,7 @@ struct StreamArgs {
   int dnw;             // DMMA project: warps per CTA (16, or 8 with two CTAs per SM)
   int dbg;             // diagnostics only (HMAT_DEBUG_SKIP): bit 0 skips project's math, bit 1 expand's
   int snake;           // project: even levels stream their range backwards (x tail reused from L2)
+  int pdl;             // expand launched as a programmatic dependent of project (HMAT_PDL)
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
   // CTA pushes this rank's exchange levels into slot `rank` of every rank's
   // mailbox and raises its flag there; expand sums the P slots in rank order
@@ -114,6 +115,24 @@ cudaError_t launch_project(const StreamArgs& a, int nr_cap, int grid, int64_t sm
 // Launch one expand pass.  grid = plan.grid_e.
 cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t smem, cudaStream_t s);
 // FP64 tensor-core (DMMA) passes of kDmmaNB right-hand sides (kernels_dmma.cu).
+// Launch `kernel(a)` as a programmatic dependent of the previous kernel on `s`
+// (PDL: its CTAs may start while that kernel's last CTAs finish; the kernel
+// calls griddepcontrol.wait before reading what the previous one wrote).
+template <typename Kernel>
+cudaError_t launch_pdl(Kernel kernel, const StreamArgs& a, int grid, int threads, int64_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 // nb: the pass width (32 or 64 right-hand sides; plan.h DmmaLayout).
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);

@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
     dev::fence_mbar_init();
   }
   __syncthreads();
+  if (a.pdl) dev::pdl_launch_dependents();  // expand may launch as SMs free up
   const dev::CtaTrace trace_scope(a.trace, bid);
   if (bid >= GL) return;
   advance();  // first stage
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     dev::fence_mbar_init();
   }
   __syncthreads();
+  if (a.pdl) dev::pdl_wait();  // project (Zt) complete and visible
   const dev::CtaTrace trace_scope(a.trace, bid);
   for (int i = 0; i < NS && jr < j1; ++i) {
     if (tid == 0) issue(i);
@@ -521,14 +523,22 @@ cudaError_t set_p16(int64_t smem) {
   return cudaSuccess;
 }
 
+template <int KC, int NB>
+void launch_e_kc(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.pdl)
+    launch_pdl(expand_dmma_kernel<KC, NB>, a, grid, kThreadsE, smem, s);
+  else
+    expand_dmma_kernel<KC, NB><<<grid, kThreadsE, smem, s>>>(a);
+}
+
 template <int NB>
 void launch_e(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
   if (a.dkc == 16)
-    expand_dmma_kernel<16, NB><<<grid, kThreadsE, smem, s>>>(a);
+    launch_e_kc<16, NB>(a, grid, smem, s);
   else if (a.dkc == 48)
-    expand_dmma_kernel<48, NB><<<grid, kThreadsE, smem, s>>>(a);
+    launch_e_kc<48, NB>(a, grid, smem, s);
   else
-    expand_dmma_kernel<32, NB><<<grid, kThreadsE, smem, s>>>(a);
+    launch_e_kc<32, NB>(a, grid, smem, s);
 }
 
 template <int NB>

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     dev::fence_mbar_init();
   }
   __syncthreads();
+  if (a.pdl) dev::pdl_wait();  // project (Zt, x staging) complete and visible
   const dev::CtaTrace trace_scope(a.trace, bid);
 
   if (warp == 0) {
@@ -486,8 +487,11 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
 
 template <int NR>
 cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  expand_kernel<NR><<<grid, kThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  if (!a.pdl) {
+    expand_kernel<NR><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  return launch_pdl(expand_kernel<NR>, a, grid, kThreads, smem, s);
 }
 
 }  // namespace

@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     dev::fence_mbar_init();
   }
   __syncthreads();
+  if (a.pdl) dev::pdl_launch_dependents();  // expand may launch as SMs free up
   const dev::CtaTrace trace_scope(a.trace, bid);
   if (bid >= GL) return;
   // every level is split evenly over the GL CTAs, so each CTA streams the same

@@ -75,6 +75,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.expand_chunk = opt.expand_chunk;
   p.project_dyn = opt.project_dyn;
   p.snake = opt.snake;
+  p.pdl = opt.pdl;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;
