@@ -67,6 +67,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.pdl = env_int("HMAT_PDL", 1);
+  o.lpar = env_int("HMAT_PROJECT_LPAR", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
@@ -853,7 +854,13 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     // stages), when it is local (no exchange) and has at least 2 chunks per CTA
     a.dyn_level = 0;
     a.sched_p = H->sched + 4;
-    if (level_mask && p.project_dyn) {
+    // small operators (every active level's stages fit the grid at once, one GPU):
+    // level-parallel project, one stage of one level per CTA (kernels_project.cu)
+    const int64_t SL = p.N_loc / p.Rp;
+    const int nact = __builtin_popcountll(level_mask);
+    a.lpar = p.lpar && p.P == 1 && nact >= 2 && SL * nact <= int64_t(ly.grid_p_slots) && SL <= p.grid_p_max ? 1 : 0;
+    const int grid_p = a.lpar ? static_cast<int>(SL * nact) : ly.grid_p;
+    if (level_mask && p.project_dyn && !a.lpar) {
       const int ll = 64 - __builtin_clzll(level_mask);
       const int64_t SLs = p.N_loc / p.Rp, seg = std::min<int64_t>(p.m[ll], p.N_loc) / p.Rp;
       int64_t ch = seg;
@@ -899,8 +906,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       H->zt_cap = cap;
     }
     hmat_status st2 = pass(
-        H->zex, exch, [&] { return hmat::launch_project(a, cap, ly.grid_p, ly.smem_p, H->stream); },
-        [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0, ly.grid_p,
+        H->zex, exch, [&] { return hmat::launch_project(a, cap, grid_p, ly.smem_p, H->stream); },
+        [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0, grid_p,
         ly.grid_e, pack_x, unpack_z);
     if (st2 != HMAT_OK) return st2;
   }

@@ -138,7 +138,25 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   const int64_t G = gridDim.x, bid = blockIdx.x;
   const int Rp = a.Rp, W = a.W, Wp = a.Wp, L = a.L;
   const int64_t SL = a.N_loc / Rp;      // stages per level
-  const int64_t GL = G < SL ? G : SL;   // CTAs active at each level
+  // Level-parallel mode (a.lpar, small operators): CTA b serves ONE stage of ONE
+  // level -- the (b / SL)-th active level, stage b % SL -- so the levels' stage
+  // loads and node flushes run side by side instead of one after the other in
+  // every CTA (the whole pass is a few latencies long).  Otherwise each level is
+  // split evenly over the GL CTAs.
+  const bool lpar = a.lpar != 0;
+  const int64_t GL = lpar ? SL : (G < SL ? G : SL);  // CTAs sharing a level
+  const int64_t GS = lpar ? SL : G;                  // partial / ticket slots per level
+  int my_level = 0;
+  int64_t jb = bid;                                  // this CTA's index among GL
+  if (lpar) {
+    int nth = static_cast<int>(bid / SL);
+    jb = bid - int64_t(nth) * SL;
+    for (int l = 1; l <= L; ++l)
+      if (((a.level_mask >> (l - 1)) & 1ull) && nth-- == 0) {
+        my_level = l;
+        break;
+      }
+  }
   const int NS = a.nstage_p;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_p);
   uint64_t* empty = full + NS;
@@ -160,10 +178,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   __syncthreads();
   if (a.pdl) dev::pdl_launch_dependents();  // expand may launch as SMs free up
   const dev::CtaTrace trace_scope(a.trace, bid);
-  if (bid >= GL) return;
+  if (lpar ? my_level == 0 : bid >= GL) return;
   // every level is split evenly over the GL CTAs, so each CTA streams the same
   // mix of coarse and fine levels (fine levels flush a node per stage)
-  const int64_t k0 = SL * bid / GL, k1 = SL * (bid + 1) / GL;  // this CTA's stages of each level
+  const int64_t k0 = SL * jb / GL, k1 = SL * (jb + 1) / GL;  // this CTA's stages of each level
 
   if (warp == 0) {
     // ---------------- producer: one lane streams V_l rows + x segments -------
@@ -174,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       int slot = 0;
       uint32_t phase = 0;
       for (int l = 1; l <= L; ++l) {
-        if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+        if (!((a.level_mask >> (l - 1)) & 1ull) || (lpar && l != my_level)) continue;
         const double* Vl = a.V + (l - 1) * a.panel_stride;
         const bool dyn = l == dyn_level;
         const bool rev = a.snake && !dyn && !(l & 1);  // even levels: the range backwards
@@ -264,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   int slot = 0;
   uint32_t phase = 0;
   for (int l = 1; l <= L; ++l) {
-    if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+    if (!((a.level_mask >> (l - 1)) & 1ull) || (lpar && l != my_level)) continue;
     const LevelArgs& lv = a.lv[l];
     const bool dyn = l == dyn_level;
     // Even levels stream the CTA's range backwards: the x segments read last at
@@ -380,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         // partial node sum of this CTA: slot 0 if the node holds our first
         // stage of the level, slot 1 otherwise (it then holds our last one)
         const int myslot = sa <= k0 ? 0 : 1;
-        double* pp = a.part + (((int64_t)(l - 1) * G + bid) * 2 + myslot) * (int64_t)Wp * NR;
+        double* pp = a.part + (((int64_t)(l - 1) * GS + jb) * 2 + myslot) * (int64_t)Wp * NR;
         for (int o = t; o < W * NR; o += CT) {
           const int kk = o / W, col = o - kk * W;
           double v = 0.0;
@@ -390,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         __threadfence();
         dev::named_bar_sync(1, CT);
         const int64_t b0 = owner_of(sa, SL, GL), b1 = owner_of(sb - 1, SL, GL);
-        int* ticket = a.cnt + (int64_t)(l - 1) * G + b1;
+        int* ticket = a.cnt + (int64_t)(l - 1) * GS + b1;
         if (t == 0) {
           const int prev = atomicAdd(ticket, 1);
           *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
@@ -402,8 +420,8 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           // consecutive CTAs' slot-0 partials are 2 ps doubles apart
           const int slot0 = (sa == SL * b0 / GL) ? 0 : 1;
           const int64_t ps = (int64_t)Wp * NR, nb = b1 - b0;
-          const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
-          const double* p1 = a.part + (((int64_t)(l - 1) * G + b0 + 1) * 2) * ps;
+          const double* p0 = a.part + (((int64_t)(l - 1) * GS + b0) * 2 + slot0) * ps;
+          const double* p1 = a.part + (((int64_t)(l - 1) * GS + b0 + 1) * 2) * ps;
           const int WN = W * NR;
           // few outputs (W NR < CT): spl threads per output, thread s summing the
           // partials i = s mod spl in order, then the spl sums in order (smem)

@@ -76,6 +76,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.project_dyn = opt.project_dyn;
   p.snake = opt.snake;
   p.pdl = opt.pdl;
+  p.lpar = opt.lpar;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;
@@ -203,6 +204,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
     y.smem_p = y.bar_off_p + bar_bytes;
     y.smem_e = y.bar_off_e + bar_bytes;
     const int64_t slots = int64_t(opt.num_sms) * y.ctas_per_sm;
+    y.grid_p_slots = static_cast<int>(slots);
     y.grid_p = static_cast<int>(std::min<int64_t>(slots, depth > 0 ? p.N_loc / p.Rp : 0));
     y.grid_e = static_cast<int>(std::min<int64_t>(slots, p.items_e));
     p.grid_p_max = std::max(p.grid_p_max, y.grid_p);

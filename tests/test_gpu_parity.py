@@ -500,3 +500,23 @@ def test_cuda_graph_capture_and_replay(nrhs):
         assert_parity(y.t().cpu().numpy(), ref)
     finally:
         hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("cfg", [HConfig("lp1", d=2, L=3, b=64, r=8, seed=1701),     # c1's shape
+                                 HConfig("lp2", d=3, L=2, b=16, r=4, seed=1702),     # nodes over many CTAs
+                                 HConfig("lp3", d=1, L=6, b=8, r=3, seed=1703)], ids=lambda c: c.name)
+def test_project_level_parallel_mode(cfg, monkeypatch):
+    """Small operators: project in level-parallel mode (one stage of one level per
+    CTA, HMAT_PROJECT_LPAR) equals the oracle, the per-level pieces too (a
+    subset of active levels), and the default split bit for bit (same CTA
+    partition of each level when every level fits the grid)."""
+    U, V, D, x = host_case(cfg, nrhs=3)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    monkeypatch.setenv("HMAT_PROJECT_LPAR", "1")
+    y1 = gpu_matvec(cfg, U, V, D, x)
+    assert_parity(y1, ref)
+    mask = 0b101 if cfg.L >= 3 else 0b11
+    assert_parity(gpu_matvec(cfg, U, V, D, x, level_mask=mask, dense=False),
+                  oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x, level_mask=mask, dense=False))
+    monkeypatch.setenv("HMAT_PROJECT_LPAR", "0")
+    assert np.array_equal(gpu_matvec(cfg, U, V, D, x), y1)
