@@ -35,6 +35,16 @@ int main() {
   const double enq = std::chrono::duration<double, std::micro>(t1 - t0).count() / calls;
   const double wall = std::chrono::duration<double, std::micro>(t2 - t0).count() / calls;
   std::printf("c1 shape from C: host enqueue %.2f us/call, wall incl. GPU %.2f us/call\n", enq, wall);
+  // host cost alone: a burst short enough not to fill the launch queue
+  {
+    cudaDeviceSynchronize();
+    auto b0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < 100; ++i) hmat_matvec(H, x, y, 1);
+    auto b1 = std::chrono::steady_clock::now();
+    cudaDeviceSynchronize();
+    std::printf("host cost of a call (burst of 100, queue not full): %.2f us\n",
+                std::chrono::duration<double, std::micro>(b1 - b0).count() / 100);
+  }
   // GPU time alone: 100 matvecs captured in a CUDA graph, replayed
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
