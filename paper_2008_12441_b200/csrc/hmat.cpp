@@ -66,7 +66,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
-  o.pdl = env_int("HMAT_PDL", 1);
+  o.pdl = env_int("HMAT_PDL", 2);
   o.lpar = env_int("HMAT_PROJECT_LPAR", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
@@ -718,6 +718,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   // off while the per-kernel profiler brackets the kernels with events
   // and the CTA trace (its memsets sit between the kernels)
   a.pdl = p.pdl && !H->prof && !H->trace && phases == kPhaseAll;
+  // project as a programmatic dependent of whatever kernel precedes it (it waits
+  // for that kernel's completion before any global access): one GPU, no memset
+  // or event wait of this call in between
+  a.pdl_p = a.pdl && p.pdl >= 2 && p.P == 1 && !async_io ? 1 : 0;
 
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.

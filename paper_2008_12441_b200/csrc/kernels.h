@@ -72,6 +72,7 @@ struct StreamArgs {
   int snake;           // project: even levels stream their range backwards (x tail reused from L2)
   int pdl;             // expand launched as a programmatic dependent of project (HMAT_PDL)
   int lpar;            // project: level-parallel mode (one stage of one level per CTA)
+  int pdl_p;           // project launched as a programmatic dependent of the previous kernel
   // in-kernel peer exchange (HMAT_EXCHANGE_PEER): the last project
   // CTA pushes this rank's exchange levels into slot `rank` of every rank's
   // mailbox and raises its flag there; expand sums the P slots in rank order

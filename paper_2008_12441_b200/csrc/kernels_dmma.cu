@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
     dev::fence_mbar_init();
   }
   __syncthreads();
+  if (a.pdl_p) dev::pdl_wait();  // the previous kernel (e.g. last product's expand) complete
   if (a.pdl) dev::pdl_launch_dependents();  // expand may launch as SMs free up
   const dev::CtaTrace trace_scope(a.trace, bid);
   if (bid >= GL) return;
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   }
   __syncthreads();
   if (a.pdl) dev::pdl_wait();  // project (Zt) complete and visible
+  if (a.pdl_p) dev::pdl_launch_dependents();  // the next product's project may launch early
   const dev::CtaTrace trace_scope(a.trace, bid);
   for (int i = 0; i < NS && jr < j1; ++i) {
     if (tid == 0) issue(i);
@@ -435,7 +437,10 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
 
 template <int MT, int NT, int NW, int NB>
 void launch_p(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<grid, NW * 32, smem, s>>>(a);
+  if (a.pdl_p)
+    launch_pdl(project_dmma_kernel<kDmmaKR, MT, NT, NW, NB>, a, grid, NW * 32, smem, s);
+  else
+    project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<grid, NW * 32, smem, s>>>(a);
 }
 
 template <int MT, int NT, int NW, int NB>

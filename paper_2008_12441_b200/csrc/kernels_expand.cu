@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   }
   __syncthreads();
   if (a.pdl) dev::pdl_wait();  // project (Zt, x staging) complete and visible
+  if (a.pdl_p) dev::pdl_launch_dependents();  // the next product's project may launch as SMs free up
   const dev::CtaTrace trace_scope(a.trace, bid);
 
   if (warp == 0) {

@@ -176,6 +176,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     dev::fence_mbar_init();
   }
   __syncthreads();
+  // PDL: wait for the previous kernel (e.g. the last product's expand, which may
+  // have written this x) before any global access; let expand launch early
+  if (a.pdl_p) dev::pdl_wait();
   if (a.pdl) dev::pdl_launch_dependents();  // expand may launch as SMs free up
   const dev::CtaTrace trace_scope(a.trace, bid);
   if (lpar ? my_level == 0 : bid >= GL) return;
@@ -468,6 +471,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
 
 template <int NR>
 cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.pdl_p)
+    return (a.Wp >> 1) <= CT ? launch_pdl(project_kernel<NR, 1>, a, grid, kThreads, smem, s)
+                             : launch_pdl(project_kernel<NR, 2>, a, grid, kThreads, smem, s);
   if ((a.Wp >> 1) <= CT)
     project_kernel<NR, 1><<<grid, kThreads, smem, s>>>(a);
   else

@@ -520,3 +520,66 @@ def test_project_level_parallel_mode(cfg, monkeypatch):
                   oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x, level_mask=mask, dense=False))
     monkeypatch.setenv("HMAT_PROJECT_LPAR", "0")
     assert np.array_equal(gpu_matvec(cfg, U, V, D, x), y1)
+
+
+@pytest.mark.parametrize("pdl", ["0", "1", "2"])
+def test_power_iteration_chains_products(pdl, monkeypatch):
+    """x_{k+1} = H x_k with the buffers swapped between calls and no host sync:
+    each product's project reads what the previous expand wrote (the hazard the
+    programmatic dependent launches must respect, HMAT_PDL).  Every setting gives
+    the same bits, and the oracle's iterates."""
+    monkeypatch.setenv("HMAT_PDL", pdl)
+    cfg = HConfig("pw", d=2, L=3, b=64, r=8, seed=1801)            # c1's shape (level-parallel project)
+    U, V, D = hgen.inputs(cfg)
+    x0 = hgen.xblock(cfg, nrhs=1)[:, 0]
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        a = torch.from_numpy(x0.copy()).cuda()
+        b = torch.empty_like(a)
+        iters = 12
+        for k in range(iters):
+            hm.hmat_matvec(h, a, b)
+            a, b = b, a
+            a.mul_(1.0 / 8.0)                                          # keep the iterates bounded (a torch kernel in between)
+        torch.cuda.synchronize()
+        got = a.cpu().numpy()
+    finally:
+        hm.hmat_destroy(h)
+    ref = x0.copy()
+    for k in range(iters):
+        ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, ref) / 8.0
+    assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(ref)
+    tag = f"pw_{pdl}"
+    test_power_iteration_chains_products.results = getattr(test_power_iteration_chains_products, "results", {})
+    test_power_iteration_chains_products.results[tag] = got
+    if len(test_power_iteration_chains_products.results) == 3:
+        vals = list(test_power_iteration_chains_products.results.values())
+        assert all(np.array_equal(v, vals[0]) for v in vals)
+
+
+def test_power_iteration_back_to_back_products(monkeypatch):
+    """The same chain with nothing between the products (expand k -> project k+1
+    directly: the programmatic launch edge itself), iterates compared bit for
+    bit with HMAT_PDL=0."""
+    cfg = HConfig("pw2", d=2, L=3, b=64, r=8, seed=1802)
+    U, V, D = hgen.inputs(cfg)
+    x0 = hgen.xblock(cfg, nrhs=1)[:, 0] / 64.0
+    outs = []
+    for pdl in ("0", "2"):
+        monkeypatch.setenv("HMAT_PDL", pdl)
+        h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+        try:
+            a = torch.from_numpy(x0.copy()).cuda()
+            b = torch.empty_like(a)
+            for k in range(10):
+                hm.hmat_matvec(h, a, b)
+                a, b = b, a
+            torch.cuda.synchronize()
+            outs.append(a.cpu().numpy())
+        finally:
+            hm.hmat_destroy(h)
+    assert np.array_equal(outs[0], outs[1])
+    ref = x0.copy()
+    for k in range(10):
+        ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, ref)
+    assert np.linalg.norm(outs[1] - ref) <= 1e-11 * np.linalg.norm(ref)
