@@ -131,7 +131,10 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
                        int64_t* ld);
 
 /* y = H x for nrhs right-hand sides (the whole hot path: project, on-chip
- * reduction, cross-GPU exchange when P > 1, fused expand + dense). */
+ * reduction, cross-GPU exchange when P > 1, fused expand + dense).  1-4 rhs run
+ * on the SIMT streaming kernels; from 5 rhs, where W % 16 == 0 (W <= 224, or
+ * <= 112 if W % 32 != 0) and 64 | leaf_size, on the FP64 tensor cores in passes
+ * of 64 rhs, the last one 16 or 32 wide when at most 16 / 32 remain. */
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
 
 /* GEMV form y = alpha op(H) x + beta y ("do not initialize y
@@ -181,7 +184,9 @@ hmat_status hmat_create_standard_uninit(int depth, int dim, int leaf_size, int r
 hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
                                const double* const* V, const double* Dc, const hmat_dist_t* dist, hmat_t* out);
 
-/* Split-phase form (one pass: nrhs <= 8, or <= 64 on the tensor-core path), for
+/* Split-phase form (one pass of right-hand sides: nrhs <= the SIMT pass width,
+ * 4 by default, or <= 64 where the tensor-core path takes the product: from 5
+ * rhs when W % 16 == 0 within its limits and 64 | leaf_size), for
  * a caller-provided exchange (hmat_dist_t.exchange = HMAT_EXCHANGE_EXTERNAL: MPI,
  * torch.distributed, ...) or to overlap other work.  x, y, exchange are device
  * pointers on H's device; work is enqueued on H's stream.
