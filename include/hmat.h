@@ -133,7 +133,8 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
 /* y = H x for nrhs right-hand sides (the whole hot path: project, on-chip
  * reduction, cross-GPU exchange when P > 1, fused expand + dense).  1-4 rhs run
  * on the SIMT streaming kernels; from 5 rhs, where W % 16 == 0 (W <= 224, or
- * <= 112 if W % 32 != 0) and 64 | leaf_size, on the FP64 tensor cores in passes
+ * <= 112 if W % 32 != 0), 64 | leaf_size, weak admissibility and no PEER
+ * exchange, on the FP64 tensor cores in passes
  * of 64 rhs, the last one 16 or 32 wide when at most 16 / 32 remain. */
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
 
