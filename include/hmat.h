@@ -298,6 +298,11 @@ typedef struct {
   int64_t level_rows_offset[64]; /* first exchange row of level l (l = 1..cross)    */
   int Rp, Re, tpr, nstage_p, nstage_e, grid_p, grid_e;
   int64_t smem_p, smem_e;
+  int max_nr;                 /* widest SIMT pass of right-hand sides                */
+  int dmma;                   /* 1: the FP64 tensor-core path serves >= 5 rhs         */
+  /* tensor-core pass layouts, [0] = 16, [1] = 32, [2] = 64 rhs wide (ok = 0: unused) */
+  int dmma_ok[3], dmma_grid_p[3], dmma_grid_e[3], dmma_stages_p[3], dmma_stages_e[3];
+  int64_t dmma_smem_p[3], dmma_smem_e[3];
 } hmat_plan_info_t;
 
 /* Validates (depth, dim, leaf_size, rank, nranks, rank_id) exactly like

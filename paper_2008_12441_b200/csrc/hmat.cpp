@@ -1232,6 +1232,18 @@ hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nra
   info->grid_e = p.lay[0].grid_e;
   info->smem_p = p.lay[0].smem_p;
   info->smem_e = p.lay[0].smem_e;
+  info->max_nr = p.max_nr;
+  info->dmma = use_dmma(p, p.dmma_min) ? 1 : 0;
+  for (int i = 0; i < 3; ++i) {
+    const hmat::Plan::DmmaLayout& d = p.dl[i];
+    info->dmma_ok[i] = p.dmma_ok && d.ok ? 1 : 0;
+    info->dmma_grid_p[i] = d.dgrid_p;
+    info->dmma_grid_e[i] = d.dgrid_e;
+    info->dmma_stages_p[i] = d.dns_p;
+    info->dmma_stages_e[i] = d.dns_e;
+    info->dmma_smem_p[i] = d.dsmem_p;
+    info->dmma_smem_e[i] = d.dsmem_e;
+  }
   return HMAT_OK;
 }
 
