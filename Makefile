@@ -16,7 +16,7 @@ CSRC      := $(PKG)/csrc
 
 HMAT_SRC  := $(CSRC)/hmat.cpp $(CSRC)/plan.cpp $(CSRC)/comm.cpp $(CSRC)/std_exchange.cpp \
              $(CSRC)/kernels_project.cu $(CSRC)/kernels_expand.cu $(CSRC)/kernels_dmma.cu $(CSRC)/kernels_aux.cu
-HMAT_HDR  := include/hmat.h $(CSRC)/plan.h $(CSRC)/kernels.h $(CSRC)/comm.h $(CSRC)/device_utils.cuh $(CSRC)/std_exchange.h $(CSRC)/geometry.cuh
+HMAT_HDR  := include/hmat.h $(CSRC)/plan.h $(CSRC)/kernels.h $(CSRC)/comm.h $(CSRC)/device_utils.cuh $(CSRC)/std_exchange.h $(CSRC)/geometry.cuh $(CSRC)/peer.cuh
 
 all: $(PKG)/libhmat.so oracle/liboracle.so gen/libhgen.so gen/libhgen_dev.so
 

@@ -302,11 +302,11 @@ def run_ours(args):
         nid = obj[0]
     create = hm.hmat_create_standard_uninit if cfg.adm else hm.hmat_create_uninit
     t_setup = time.perf_counter()
-    # the in-kernel peer exchange serves the single-rhs weak path; the standard
-    # structure and the many-rhs tensor-core path exchange through NCCL
+    # the in-kernel peer exchange serves the weak structure (SIMT and tensor-core
+    # paths); the standard structure exchanges through NCCL
     exchange = args.exchange if world > 1 else "none"
-    if exchange == "peer" and (cfg.adm or nrhs >= DMMA_MIN_RHS):
-        exchange = "nccl"  # the peer exchange serves the single-rhs weak path only
+    if exchange == "peer" and cfg.adm:
+        exchange = "nccl"  # the peer exchange serves the weak-admissibility structure
     h = None
     if exchange == "peer":
         # mailboxes connected once through CUDA IPC handles (hmat_peer_export/_import)

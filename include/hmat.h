@@ -97,8 +97,10 @@ typedef struct {
  *            kernel waits for the P flags and sums the P slots in rank order.
  *            Mailboxes are connected once with hmat_peer_export/_import (CUDA
  *            IPC, one process per GPU) or hmat_peer_connect_local (one process).
- *            No host or NCCL call per matvec; the many-rhs tensor-core path is
- *            not used in this mode.
+ *            No host or NCCL call per matvec.  On the many-rhs tensor-core
+ *            path the project kernel pushes the same way and a small kernel
+ *            sums the P slots in rank order before expand.  Not with
+ *            standard admissibility.
  *   TREE     the paper's tree-structured Steps 2-4 over NCCL point-to-point
  *            (needs nccl_unique_id): log2 P rounds of recursive doubling on
  *            the hypercube of ranks, round j swapping the packed buffer with
@@ -133,8 +135,8 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
 /* y = H x for nrhs right-hand sides (the whole hot path: project, on-chip
  * reduction, cross-GPU exchange when P > 1, fused expand + dense).  1-4 rhs run
  * on the SIMT streaming kernels; from 5 rhs, where W % 16 == 0 (W <= 224, or
- * <= 112 if W % 32 != 0), 64 | leaf_size, weak admissibility and no PEER
- * exchange, on the FP64 tensor cores in passes
+ * <= 112 if W % 32 != 0), 64 | leaf_size and weak admissibility, on the FP64
+ * tensor cores in passes
  * of 64 rhs, the last one 16 or 32 wide when at most 16 / 32 remain. */
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
 
@@ -285,8 +287,9 @@ hmat_status hmat_cta_trace_read(hmat_t H, int kernel, int64_t* out, int max_ctas
 
 /* Launches of this library's kernels one hmat_matvec(nrhs) performs on this
  * rank: per pass of right-hand sides, project + expand, + pack / unpack with
- * standard admissibility and P > 1, + log2 P adds with the TREE exchange (NCCL's
- * own kernels and memsets not counted). */
+ * standard admissibility and P > 1, + log2 P adds with the TREE exchange, + the
+ * mailbox sum on the tensor-core path with the PEER exchange (NCCL's own kernels
+ * and memsets not counted). */
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs);
 
 /* Host-only description of a shard's plan (no GPU needed). */

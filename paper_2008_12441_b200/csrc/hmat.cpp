@@ -331,7 +331,8 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   H->tree = p.P > 1 && dist->exchange == HMAT_EXCHANGE_TREE;
   H->peer = peer;
   if (peer) {
-    H->mb = (p.z_exch_rows * p.Wp * hmat::kMaxNR + 15) / 16 * 16;
+    // one slot holds the widest pass's exchange levels (SIMT: kMaxNR rhs; tensor-core: 64)
+    H->mb = (p.z_exch_rows * p.Wp * (p.dmma_ok ? std::max(hmat::kMaxNR, hmat::kDmmaNB) : hmat::kMaxNR) + 15) / 16 * 16;
     const size_t mbytes = (size_t(2) * p.P * H->mb + size_t(2) * p.P) * sizeof(double);
     if ((e = cudaMalloc(reinterpret_cast<void**>(&H->mbox), mbytes)) ||
         (e = cudaMalloc(reinterpret_cast<void**>(&H->mbox_dev), size_t(p.P) * sizeof(double*))) ||
@@ -828,10 +829,13 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         lv.tbase = p.zt_tbase[l];
       }
       const size_t exch = size_t(p.z_exch_rows) * p.W * nb;
+      a.zex_base = H->zex_d;  // PEER: the project's last CTA pushes this region to every mailbox
       hmat_status st2 = pass(
           H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, nb, dl.dgrid_p, dl.dsmem_p, H->stream); },
           [&] { return hmat::launch_expand_dmma(a, nb, dl.dgrid_e, dl.dsmem_e, H->stream); }, dl.dgrid_p > 0,
-          dl.dgrid_p, dl.dgrid_e, [] { return cudaSuccess; }, [] { return cudaSuccess; });
+          dl.dgrid_p, dl.dgrid_e, [] { return cudaSuccess; },
+          // PEER: the rank-ordered sum of the P mailbox slots into the exchange levels
+          [&] { return H->peer ? hmat::launch_peer_sum(a, H->zex_d, H->stream) : cudaSuccess; });
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -1201,6 +1205,7 @@ int64_t hmat_launches_per_matvec(hmat_t H, int nrhs) {
   const int64_t passes = (nrhs + per - 1) / per;
   int per_pass = (p.stages_p > 0 ? 1 : 0) + 1;  // project (if any level) + expand
   if (H->sx) per_pass += 2;                     // standard admissibility, P > 1: pack x, unpack z
+  if (H->peer && use_dmma(p, nrhs)) per_pass += 1;  // tensor-core path with PEER: the mailbox sum
   if (H->tree) {                                // one add kernel per recursive-doubling round
     for (int bit = 1; bit < p.P; bit <<= 1) ++per_pass;
   }

@@ -139,6 +139,9 @@ cudaError_t launch_pdl(Kernel kernel, const StreamArgs& a, int grid, int threads
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
 cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e);
+// PEER exchange on the tensor-core path: wait for the P ranks' flags of this
+// pass, then out[0..a.exch) = the rank-ordered sum of this rank's P mailbox slots.
+cudaError_t launch_peer_sum(const StreamArgs& a, double* out, cudaStream_t s);
 // Standard admissibility: upload the interaction-list slot tables (plan.h
 // std_slot_tables) to the project kernel's constant memory (per device).
 cudaError_t init_std_tables(const int16_t* code, const int16_t* slot);

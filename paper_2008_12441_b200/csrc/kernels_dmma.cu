@@ -20,6 +20,7 @@
 // partials are the same as in the single-vector kernels.
 #include "device_utils.cuh"
 #include "kernels.h"
+#include "peer.cuh"
 
 namespace hmat {
 namespace {
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
       }
     }
   }
+  if (a.peer) peer_push<NW * 32>(a, tid, GL, flag);  // this rank's exchange levels -> every mailbox
 }
 
 // ============================ expand =========================================
@@ -555,6 +557,29 @@ cudaError_t set_e(int64_t smem) {
   return cudaFuncSetAttribute(expand_dmma_kernel<32, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// Wait for the P ranks' flags of this pass, then exchange[o] = sum over ranks g
+// (in rank order) of slot g of this rank's mailbox: the summed exchange levels
+// the tensor-core expand reads.  Bounded wait (~2^35 cycles): never a hung GPU.
+__global__ void peer_sum_kernel(const __grid_constant__ StreamArgs a, double* __restrict__ out) {
+  const int par = static_cast<int>(a.epoch & 1);
+  const double* mb = a.mbox[a.rank] + (int64_t)par * a.P * a.mb;
+  if (threadIdx.x == 0) {
+    const uint64_t* fl = reinterpret_cast<const uint64_t*>(a.mbox[a.rank] + 2 * a.P * a.mb) + par * a.P;
+    const long long t0 = clock64();
+    for (int g = 0; g < a.P; ++g)
+      while (dev::ld_acquire_sys(fl + g) != a.epoch) {
+        __nanosleep(256);
+        if (clock64() - t0 > (1ll << 35)) __trap();
+      }
+  }
+  __syncthreads();
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < a.exch; o += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int g = 0; g < a.P; ++g) v += dev::ld_cg(mb + (int64_t)g * a.mb + o);
+    out[o] = v;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
@@ -574,6 +599,14 @@ cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t sm
     launch_e<32>(a, grid, smem, s);
   else
     launch_e<64>(a, grid, smem, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_sum(const StreamArgs& a, double* out, cudaStream_t s) {
+  if (a.exch <= 0) return cudaSuccess;
+  int64_t grid = (a.exch + 255) / 256;
+  if (grid > 148) grid = 148;
+  peer_sum_kernel<<<static_cast<int>(grid), 256, 0, s>>>(a, out);
   return cudaGetLastError();
 }
 

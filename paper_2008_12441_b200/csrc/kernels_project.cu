@@ -28,6 +28,7 @@
 #include "device_utils.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
+#include "peer.cuh"
 
 namespace hmat {
 namespace {
@@ -96,38 +97,6 @@ __device__ __forceinline__ void scatter_z(const StreamArgs& a, const LevelArgs& 
   const int tc = static_cast<int>(t & (a.c - 1));
   const int qt = me < tc ? me : me - 1;
   lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)kk * a.Wp + qt * a.r + aa] = v;  // [t][rhs][col]
-}
-
-// Peer exchange (the device-side Steps 2-4):
-// the last CTA to finish pushes this rank's exchange levels (complete sums of
-// its own sources, partial sums of sources spanning ranks, zeros elsewhere)
-// into slot `rank` of every rank's mailbox over NVLink peer memory, then raises
-// its flag there (system-scope release).  Readers sum the P slots in rank order,
-// so the result is deterministic and equal on every rank.  Consumer threads only.
-__device__ __forceinline__ void peer_push(const StreamArgs& a, int t, int64_t GL, volatile int* flag) {
-  dev::named_bar_sync(1, CT);
-  __threadfence();
-  if (t == 0) {
-    const unsigned int prev = atomicAdd(a.done, 1u);
-    *flag = (prev + 1 == static_cast<unsigned int>(GL)) ? 1 : 0;
-  }
-  dev::named_bar_sync(1, CT);
-  if (!*flag) return;
-  __threadfence();
-  const int par = static_cast<int>(a.epoch & 1);
-  for (int p = 0; p < a.P; ++p) {
-    double* dst = a.mbox[p] + ((int64_t)par * a.P + a.rank) * a.mb;
-    for (int64_t o = t; o < a.exch; o += CT) dst[o] = dev::ld_cg(a.zex_base + o);
-  }
-  __threadfence_system();
-  dev::named_bar_sync(1, CT);
-  if (t == 0) {
-    for (int p = 0; p < a.P; ++p) {
-      uint64_t* fl = reinterpret_cast<uint64_t*>(a.mbox[p] + 2 * a.P * a.mb) + par * a.P + a.rank;
-      dev::st_release_sys(fl, a.epoch);
-    }
-    *a.done = 0u;  // re-arm for the next pass
-  }
 }
 
 template <int NR, int PAIRS>
@@ -466,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     }
     }
   }
-  if (a.peer) peer_push(a, t, GL, flag);
+  if (a.peer) peer_push<CT>(a, t, GL, flag);
 }
 
 template <int NR>

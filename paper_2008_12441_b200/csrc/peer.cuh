@@ -1,0 +1,44 @@
+// peer.cuh -- the device side of the in-kernel NVLink peer exchange
+// (HMAT_EXCHANGE_PEER): the push at the end of a project kernel
+// (SIMT and tensor-core).
+#pragma once
+#include "device_utils.cuh"
+#include "kernels.h"
+
+namespace hmat {
+
+// Peer exchange (the device-side Steps 2-4):
+// the last CTA to finish pushes this rank's exchange levels (complete sums of
+// its own sources, partial sums of sources spanning ranks, zeros elsewhere)
+// into slot `rank` of every rank's mailbox over NVLink peer memory, then raises
+// its flag there (system-scope release).  Readers sum the P slots in rank order,
+// so the result is deterministic and equal on every rank.  Consumer threads only.
+template <int NTH>  // threads taking part (all consumer threads of the CTA)
+__device__ __forceinline__ void peer_push(const StreamArgs& a, int t, int64_t GL, volatile int* flag) {
+  dev::named_bar_sync(1, NTH);
+  __threadfence();
+  if (t == 0) {
+    const unsigned int prev = atomicAdd(a.done, 1u);
+    *flag = (prev + 1 == static_cast<unsigned int>(GL)) ? 1 : 0;
+  }
+  dev::named_bar_sync(1, NTH);
+  if (!*flag) return;
+  __threadfence();
+  const int par = static_cast<int>(a.epoch & 1);
+  for (int p = 0; p < a.P; ++p) {
+    double* dst = a.mbox[p] + ((int64_t)par * a.P + a.rank) * a.mb;
+    for (int64_t o = t; o < a.exch; o += NTH) dst[o] = dev::ld_cg(a.zex_base + o);
+  }
+  __threadfence_system();
+  dev::named_bar_sync(1, NTH);
+  if (t == 0) {
+    for (int p = 0; p < a.P; ++p) {
+      uint64_t* fl = reinterpret_cast<uint64_t*>(a.mbox[p] + 2 * a.P * a.mb) + par * a.P + a.rank;
+      dev::st_release_sys(fl, a.epoch);
+    }
+    *a.done = 0u;  // re-arm for the next pass
+  }
+}
+
+
+}  // namespace hmat

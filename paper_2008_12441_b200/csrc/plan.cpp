@@ -218,7 +218,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   // dense stages are 32 columns of D (kernels_dmma.cu KD)
   p.dkc = opt.dmma_kc > 0 ? opt.dmma_kc : p.W % 32 == 0 ? 32 : p.W == 48 ? 48 : 16;
   if (p.W % p.dkc != 0 || (p.dkc != 16 && p.dkc != 32 && p.dkc != 48)) p.dkc = p.W % 32 == 0 ? 32 : 16;
-  p.dmma_ok = p.adm == 0 && !opt.peer && p.W % 16 == 0 && (p.W % 32 == 0 ? p.W <= 224 : p.W <= 112) &&
+  p.dmma_ok = p.adm == 0 && p.W % 16 == 0 && (p.W % 32 == 0 ? p.W <= 224 : p.W <= 112) &&
               leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;

@@ -162,6 +162,10 @@ def peer_split_matvec(cfg, P, nrhs, reps=2):
     (HConfig("q3d", d=3, L=3, b=8, r=3, seed=402), 4, 2),
     (HConfig("q3d", d=3, L=3, b=64, r=32, seed=403), 8, 1),
     (HConfig("q1d", d=1, L=7, b=4, r=2, seed=404), 16, 8),
+    # tensor-core path: the project's last CTA pushes, a rank-ordered sum kernel precedes expand
+    (HConfig("q3d", d=3, L=3, b=64, r=32, seed=403), 2, 64),
+    (HConfig("q3d", d=3, L=3, b=64, r=32, seed=403), 8, 20),     # 32-wide pass
+    (HConfig("qw48", d=2, L=4, b=64, r=16, seed=405), 4, 7),     # W = 48, 16-wide pass
 ], ids=lambda v: getattr(v, "name", str(v)))
 def test_peer_exchange_matches_oracle(cfg, P, nrhs):
     outs = peer_split_matvec(cfg, P, nrhs)

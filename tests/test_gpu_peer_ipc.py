@@ -73,6 +73,7 @@ def _worker(rank, world, port, cfg, nrhs, reps, out_q):
 @pytest.mark.parametrize("cfg,P,nrhs", [
     (HConfig("ipc2d", d=2, L=4, b=16, r=4, seed=501), 2, 1),
     (HConfig("ipc3d", d=3, L=3, b=8, r=3, seed=502), 4, 3),
+    (HConfig("ipcdm", d=2, L=4, b=64, r=16, seed=503), 2, 16),   # tensor-core path (16-wide pass)
 ], ids=lambda v: getattr(v, "name", str(v)))
 def test_peer_exchange_ipc_processes(cfg, P, nrhs):
     import torch.multiprocessing as mp
