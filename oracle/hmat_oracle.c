@@ -5,7 +5,10 @@
  * bench.py's cpu_baseline / --impl reference legs may load this library.  It
  * shares no code with the CUDA path (paper_2008_12441_b200/csrc); its only
  * shared dependency is the seeded input generator gen/hgen.h, used by
- * oracle_rows_generated() to produce factor entries on demand.
+ * oracle_rows_generated() and the generated form of oracle_matvec_rows_par()
+ * to produce factor entries on demand (full-size operators without factor
+ * memory).  oracle_matvec_rows_par() is also the all-cores block loop timed as
+ * the CPU baseline; it is bit-identical to oracle_matvec().
  *
  * Plain, slow, obviously correct fp64 loops, written from the paper:
  *   - structure: Def 2.4 (\label{def:hmat}) on the 2^d-ary
@@ -336,6 +339,115 @@ void oracle_dense_matvec(int64_t N, const double* A, const double* x, double* y,
       for (int64_t j = 0; j < N; ++j) acc += A[i * N + j] * x[(int64_t)k * N + j];
       y[(int64_t)k * N + i] = acc;
     }
+}
+
+/* ---- the block loop on all host cores (SURVEY §8(d) "oracle_allcores") ----
+ * The arithmetic of oracle_matvec_masked (eq:hmat-vec-add),
+ * element for element in the same order, so the output is BIT-IDENTICAL to the
+ * one-thread block loop for any thread count:
+ *   y_i = 0;  y_i += D_k[i, j] x_{k b + j}  for j = 0..b-1          (dense leaf)
+ *   for l = 1..L, q = 0..c-2, a = 0..r-1:  y_i += U_{t,s_q}[i, a] z_{t,q}[a]
+ *   with z_{t,q}[a] = sum_{j = 0..m-1} V_{t,s_q}[j, a] x_{s_q m + j}  (V_ts^T x_s)
+ * Only the distribution of the work over threads differs: per level, (A) every
+ * z_{t,q}[a] of the level's targets is an independent dot product (one thread
+ * each), then (B) every row i adds its sum over q and a.  Rows [r0, r1) of y
+ * only (an aligned shard, a chunk); y is (r1 - r0) x nrhs column-major with
+ * leading dimension ldy, x the full N x nrhs block (ld N).
+ * Factor entries come from the canonical panels (U, V, D non-NULL) or, with
+ * U == NULL, straight from the seeded generator (gen/hgen.h):
+ * U_l / V_l entry (row, col) = normal(stream(seed, U|V, l), row W + col) / sqrt(m_l),
+ * D entry (row, col) = normal(stream(seed, D, 0), row b + col) / 8 -- the values
+ * hgen_fill_rowmajor writes, so both sources give the same y bits.  The
+ * generated form needs no factor memory: full-size operators (124.55 GB at
+ * BASELINE configs[3]) are checked in full on the host. */
+#define ORACLE_ZCAP ((int64_t)1 << 25) /* doubles of z per target chunk (256 MB) */
+
+void oracle_matvec_rows_par(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                            const double* D, uint64_t seed, const double* x, int nrhs, int64_t r0, int64_t r1,
+                            double* y, int64_t ldy, uint64_t level_mask, int dense, int nthreads) {
+  const int c = 1 << d;
+  const int64_t N = (int64_t)b * ipow(c, L);
+  const int W = (c - 1) * r;
+  const int gen = (U == NULL);
+  const int nt = nthreads > 0 ? nthreads : 1;
+  const uint64_t stD = hgen_stream(seed, HGEN_TAG_D, 0, 0);
+  if (r1 <= r0) return;
+  /* x and y with the right-hand sides innermost (xr[j nrhs + k], yr[(i - r0) nrhs + k]):
+   * a data layout only -- column-major blocks put the nrhs values of one row
+   * N doubles apart, on the same cache set */
+  const int64_t nl = r1 - r0;
+  double* xr = (double*)malloc(sizeof(double) * (size_t)N * (size_t)nrhs);
+  double* yr = (double*)malloc(sizeof(double) * (size_t)nl * (size_t)nrhs);
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t j = 0; j < N; ++j)
+    for (int k = 0; k < nrhs; ++k) xr[j * nrhs + k] = x[(int64_t)k * N + j];
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t i = r0; i < r1; ++i) { /* y = 0, then the dense leaf block */
+    const int64_t leaf = i / b;
+    double* yi = yr + (i - r0) * nrhs;
+    for (int k = 0; k < nrhs; ++k) yi[k] = 0.0;
+    if (!dense) continue;
+    for (int j = 0; j < b; ++j) {
+      const double dv = gen ? hgen_normal(stD, (uint64_t)(i * b + j)) * 0.125 : D[i * b + j];
+      const double* xj = xr + (leaf * b + j) * nrhs;
+      for (int k = 0; k < nrhs; ++k) yi[k] += dv * xj[k];
+    }
+  }
+  const int64_t per_t = (int64_t)W * nrhs; /* z doubles per target: [q][a][k] */
+  double* Z = (double*)malloc(sizeof(double) * (size_t)(per_t < ORACLE_ZCAP ? ORACLE_ZCAP : per_t));
+  for (int l = 1; l <= L; ++l) {
+    if (!((level_mask >> (l - 1)) & 1ull)) continue;
+    const int64_t m = N / ipow(c, l);
+    const double scale = 1.0 / sqrt((double)m);
+    const uint64_t stU = hgen_stream(seed, HGEN_TAG_U, (uint64_t)l, 0);
+    const uint64_t stV = hgen_stream(seed, HGEN_TAG_V, (uint64_t)l, 0);
+    const double* Ul = gen ? NULL : U[l - 1];
+    const double* Vl = gen ? NULL : V[l - 1];
+    const int64_t t_lo = r0 / m, t_hi = (r1 - 1) / m + 1;
+    int64_t chunk = ORACLE_ZCAP / per_t;
+    if (chunk < 1) chunk = 1;
+    for (int64_t tc = t_lo; tc < t_hi; tc += chunk) {
+      const int64_t te = tc + chunk < t_hi ? tc + chunk : t_hi;
+      const int64_t items = (te - tc) * (c - 1) * r;
+      /* (A) z_{t,q}[a] = V_{t,s_q}[:, a]^T x_{s_q}, one dot product per item */
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1)
+      for (int64_t it = 0; it < items; ++it) {
+        const int64_t t = tc + it / ((int64_t)(c - 1) * r);
+        const int q = (int)((it / r) % (c - 1));
+        const int a = (int)(it % r);
+        const int64_t s = oracle_sibling(c, t, q); /* block (t, s) */
+        const int qs = oracle_slot(c, s, t);       /* t's slot in s's list: V_ts columns */
+        double* z = Z + (((t - tc) * (c - 1) + q) * r + a) * (int64_t)nrhs;
+        for (int k = 0; k < nrhs; ++k) z[k] = 0.0;
+        for (int64_t j = 0; j < m; ++j) {
+          const int64_t idx = (s * m + j) * W + qs * r + a;
+          const double v = gen ? hgen_normal(stV, (uint64_t)idx) * scale : Vl[idx];
+          const double* xj = xr + (s * m + j) * nrhs;
+          for (int k = 0; k < nrhs; ++k) z[k] += v * xj[k];
+        }
+      }
+      /* (B) y_i += U_{t,s_q}[i, :] z_{t,q} for every row of these targets */
+      const int64_t i_lo = tc * m > r0 ? tc * m : r0, i_hi = te * m < r1 ? te * m : r1;
+#pragma omp parallel for num_threads(nt) schedule(static)
+      for (int64_t i = i_lo; i < i_hi; ++i) {
+        const int64_t t = i / m;
+        double* yi = yr + (i - r0) * nrhs;
+        for (int q = 0; q < c - 1; ++q)
+          for (int a = 0; a < r; ++a) {
+            const int64_t idx = i * W + q * r + a;
+            const double u = gen ? hgen_normal(stU, (uint64_t)idx) * scale : Ul[idx];
+            const double* z = Z + (((t - tc) * (c - 1) + q) * r + a) * (int64_t)nrhs;
+            for (int k = 0; k < nrhs; ++k) yi[k] += u * z[k];
+          }
+      }
+    }
+  }
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t i = r0; i < r1; ++i)
+    for (int k = 0; k < nrhs; ++k) y[(int64_t)k * ldy + (i - r0)] = yr[(i - r0) * nrhs + k];
+  free(Z);
+  free(xr);
+  free(yr);
 }
 
 /* ---- sampled rows at any size, factors generated on demand ---------------

@@ -61,8 +61,18 @@ def _load():
         lib.oracle_rows_generated.restype = None
         lib.oracle_rows_generated.argtypes = [ctypes.c_int] * 4 + [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int,
                                                                   ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_matvec_rows_par.restype = None
+        lib.oracle_matvec_rows_par.argtypes = [ctypes.c_int] * 4 + [pp, pp, ctypes.c_void_p, ctypes.c_uint64,
+                                                                    ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                                                    ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                                                    ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
         _lib = lib
     return _lib
+
+
+def host_threads() -> int:
+    """Host cores this process may use (cgroup / taskset aware)."""
+    return len(os.sched_getaffinity(0))
 
 
 def _c(a: np.ndarray) -> np.ndarray:
@@ -151,6 +161,41 @@ def rows_generated(cfg, x, rows) -> np.ndarray:
     _load().oracle_rows_generated(cfg.d, cfg.L, cfg.b, cfg.r, cfg.seed, xc.ctypes.data, nrhs, len(rows),
                                   rows.ctypes.data, out.ctypes.data)
     return out[:, 0] if np.ndim(x) == 1 else out
+
+
+def matvec_par(d: int, L: int, b: int, r: int, U, V, D, x, threads: int | None = None, row_begin: int = 0,
+               row_end: int | None = None, level_mask: int = (1 << 64) - 1, dense: bool = True) -> np.ndarray:
+    """Rows [row_begin, row_end) of y = H x: the block loop of `matvec` on all
+    host cores (bit-identical to it for any thread count, oracle_matvec_rows_par)."""
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    r1 = N if row_end is None else row_end
+    y = np.zeros((r1 - row_begin, nrhs), dtype=np.float64, order="F")
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dc = _c(D)
+    _load().oracle_matvec_rows_par(d, L, b, r, up, vp, Dc.ctypes.data, 0, xc.ctypes.data, nrhs, row_begin, r1,
+                                   y.ctypes.data, max(1, r1 - row_begin), level_mask & ((1 << 64) - 1), int(dense),
+                                   threads or host_threads())
+    return y[:, 0] if np.ndim(x) == 1 else y
+
+
+def matvec_generated(cfg, x, row_begin: int = 0, row_end: int | None = None, threads: int | None = None,
+                     level_mask: int = (1 << 64) - 1, dense: bool = True) -> np.ndarray:
+    """Rows [row_begin, row_end) of y = H x for the seeded synthetic H-matrix of
+    `cfg` (gen/hgen.h), every factor entry generated on demand (no factor memory:
+    full-size BASELINE operators on the host), all host cores; bit-identical to
+    `matvec` on the panels of hgen.inputs(cfg).  x: (N,) or (N, nrhs), full."""
+    xc = _colmajor(x)
+    N, nrhs = xc.shape
+    assert N == cfg.N
+    r1 = N if row_end is None else row_end
+    y = np.zeros((r1 - row_begin, nrhs), dtype=np.float64, order="F")
+    null = ctypes.POINTER(_dp)()
+    _load().oracle_matvec_rows_par(cfg.d, cfg.L, cfg.b, cfg.r, null, null, None, cfg.seed, xc.ctypes.data, nrhs,
+                                   row_begin, r1, y.ctypes.data, max(1, r1 - row_begin),
+                                   level_mask & ((1 << 64) - 1), int(dense), threads or host_threads())
+    return y[:, 0] if np.ndim(x) == 1 else y
 
 
 def block_census_strict(d: int, L: int):

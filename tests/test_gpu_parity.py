@@ -148,46 +148,6 @@ def test_device_generator_matches_host_bitwise():
     assert np.array_equal(xd.cpu().numpy().T, hgen.xblock(cfg, nrhs=3, vec=7, row_begin=5000, row_end=6000))
 
 
-def sample_rows(cfg, rng):
-    """Rows spread over the first and last level-1 nodes plus random ones,
-    grouped so the oracle reuses z of shared ancestors."""
-    N, b = cfg.N, cfg.b
-    rows = [0, 1, b - 1, b, 2 * b + 5] + [N - 1, N - b, N - 2 * b - 3]
-    rows += list(rng.integers(0, N, 4))
-    return np.array(sorted(set(int(r) for r in rows)))
-
-
-@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c2strict"])
-def test_full_size_sampled_rows(name):
-    """BASELINE configs (and the bench's c2strict line: leaf 256, dense blocks in
-    64-column chunks) at full size, in the bench's launch configuration
-    (device-generated panels, default plan): sampled y rows vs the oracle,
-    which recomputes each row from eq:hmat-vec-add with on-demand factors."""
-    cfg = {**CONFIGS, **hgen.EXTRA_CONFIGS}[name]
-    free, _ = torch.cuda.mem_get_info()
-    if free < cfg.factor_bytes * 1.05:
-        pytest.skip(f"needs {cfg.factor_bytes / 1e9:.0f} GB of device memory")
-    h = device_operator(cfg, hm)
-    try:
-        x = torch.empty(cfg.N, dtype=torch.float64, device="cuda")
-        hgen.dev_fill_x(cfg, 1, 3, 0, cfg.N, x.data_ptr(), cfg.N)
-        y = torch.empty_like(x)
-        hm.hmat_matvec(h, x, y)
-        torch.cuda.synchronize()
-        xh = x.cpu().numpy()
-        assert np.array_equal(xh, hgen.xblock(cfg, nrhs=1, vec=3)[:, 0])
-        rows = sample_rows(cfg, np.random.default_rng(1))
-        ref = oracle.rows_generated(cfg, xh, rows)
-        got = y.cpu().numpy()[rows]
-        # per-row check against the column's scale (the oracle only sees rows)
-        scale = np.abs(y.cpu().numpy()).max()
-        assert np.abs(got - ref).max() <= 1e-12 * scale
-        assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
-    finally:
-        hm.hmat_destroy(h)
-        torch.cuda.empty_cache()
-
-
 DMMA = [HConfig("d3L2", d=3, L=2, b=64, r=32, seed=501), HConfig("d3L3", d=3, L=3, b=64, r=32, seed=502),
         HConfig("d2L3", d=2, L=3, b=64, r=32, seed=503), HConfig("d2b128", d=2, L=3, b=128, r=64, seed=504),
         # W % 32 != 0: 2 column groups x 8 rhs groups, 16-column expand chunks
@@ -212,34 +172,6 @@ def test_dmma_many_rhs(cfg, nrhs):
         hm.hmat_destroy(h)
     assert_parity(gpu_matvec(cfg, U, V, D, x), ref)
 
-
-def test_c5_full_size_sampled_rows():
-    """BASELINE configs[4] (N = 2^21, 64 right-hand sides) at full size through
-    the DMMA path: sampled rows of all 64 columns vs the oracle."""
-    cfg = CONFIGS["c5"]
-    free, _ = torch.cuda.mem_get_info()
-    if free < cfg.factor_bytes * 1.2:
-        pytest.skip("not enough device memory")
-    h = device_operator(cfg, hm)
-    try:
-        n = cfg.N
-        X = torch.empty(cfg.nrhs, n, dtype=torch.float64, device="cuda")
-        hgen.dev_fill_x(cfg, cfg.nrhs, 0, 0, n, X.data_ptr(), n)
-        Y = torch.empty_like(X)
-        hm.hmat_matvec(h, X.t(), Y.t())
-        torch.cuda.synchronize()
-        assert hm.hmat_launches_per_matvec(h, cfg.nrhs) == 2
-        xh = X.t().cpu().numpy()
-        rows = np.array([0, 63, 64, 1000, n - 1])
-        ref = oracle.rows_generated(cfg, np.asfortranarray(xh), rows)
-        yall = Y.t().cpu().numpy()
-        got = yall[rows]
-        for k in range(cfg.nrhs):
-            scale = np.abs(yall[:, k]).max()
-            assert np.abs(got[:, k] - ref[:, k]).max() <= 1e-12 * scale
-    finally:
-        hm.hmat_destroy(h)
-        torch.cuda.empty_cache()
 
 
 def _dev_cols(x):

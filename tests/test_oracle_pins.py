@@ -360,3 +360,44 @@ def test_unit_columns_at_scale(d, L, b, r):
     Y = oracle.matvec(d, L, b, r, U, V, D, X)
     for k, j in enumerate(js):
         assert rel(Y[:, k], unit_column(d, L, b, r, U, V, D, int(j))) < 1e-14
+
+
+# -- the all-cores block loop and its generated-factor form (full-size parity) --
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 5, 3, 2), (2, 3, 4, 3), (2, 4, 8, 2), (3, 2, 4, 2), (2, 0, 5, 2)])
+@pytest.mark.parametrize("nrhs", [1, 3])
+def test_matvec_par_bitwise_equals_block_loop(d, L, b, r, nrhs):
+    """oracle_matvec_rows_par does the block loop's arithmetic element for
+    element in the same order, only split over threads: bit-identical to
+    `matvec` for any thread count, any row range and any level selection.  A
+    dropped level, a wrong z (t/s or slot transposition), a race or an
+    off-by-one in the row range shows as a bit difference."""
+    U, V, D = rand_panels(d, L, b, r, 1000 + 7 * d + L)
+    N = len(D)
+    x = np.random.default_rng(77).standard_normal((N, nrhs))
+    ref = oracle.matvec(d, L, b, r, U, V, D, x)
+    for th in (1, 3, 8):
+        assert np.array_equal(oracle.matvec_par(d, L, b, r, U, V, D, x, threads=th), ref)
+    for r0, r1 in [(0, N // 3), (N // 3, N - 1), (min(b + 1, N - 2), min(b + 2, N - 1)), (N - 1, N)]:
+        got = oracle.matvec_par(d, L, b, r, U, V, D, x, threads=4, row_begin=r0, row_end=r1)
+        assert np.array_equal(got, ref[r0:r1])
+    if L >= 2:
+        mask = 0b10
+        assert np.array_equal(oracle.matvec_par(d, L, b, r, U, V, D, x, level_mask=mask, dense=False),
+                              oracle.matvec(d, L, b, r, U, V, D, x, level_mask=mask, dense=False))
+
+
+@pytest.mark.parametrize("cfg", [CONFIGS["c1"], HConfig("g3", d=3, L=2, b=8, r=3, seed=71),
+                                 HConfig("g1", d=1, L=6, b=4, r=5, seed=72),
+                                 HConfig("gs", d=2, L=2, b=256, r=16, seed=73)], ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 2, 64])
+def test_matvec_generated_bitwise_equals_block_loop(cfg, nrhs):
+    """The generated-factor form (the full-size parity oracle) equals the block
+    loop run on the panels hgen writes, bit for bit, so the pins of the block
+    loop carry over to it; any row range gives the same rows."""
+    U, V, D = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs, vec=2)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    assert np.array_equal(oracle.matvec_generated(cfg, x, threads=5), ref)
+    r0, r1 = cfg.N // 4 + 3, cfg.N // 2 + 1
+    assert np.array_equal(oracle.matvec_generated(cfg, x, r0, r1, threads=2), ref[r0:r1])

@@ -235,3 +235,55 @@ def test_std_rows_generated_equals_assembled_matrix(cfg):
     yr = oracle.std_rows_generated(cfg, x, rows)
     assert rel(yr, (A @ x)[rows]) < 1e-13
     assert rel(yr, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x)[rows]) < 1e-13
+
+
+@pytest.mark.parametrize("d,level", [(1, 3), (1, 6), (2, 3), (2, 4), (3, 3)])
+def test_std_slot_order_rederived_from_the_header(d, level):
+    """oracle_std_slot against the slot order as include/hmat.h states it,
+    re-derived here in plain Python with no call into the oracle: for target t
+    (coordinates X, parent P = X >> 1), the candidates are the boxes
+    S = 2 (P + eps) + sigma for eps in {-1,0,1}^d, sigma in {0,1}^d, taken in
+    increasing (sum_i (eps_i + 1) 3^i) 2^d + sum_i sigma_i 2^i; the ones that
+    touch t (every |S_i - X_i| <= 1) are skipped; the others are numbered
+    0, 1, ... whether or not they lie inside the domain.  Every ordered pair
+    (t, s) of boxes of the level is checked: s gets its number in t's list if it
+    is a candidate that does not touch t, else -1 (not in the interaction list:
+    eq:standard-ad-cond with the parent-neighbour rule, PAPER.md:279-297,
+    615-620).  A dropped out-of-domain candidate, a wrong key order or a wrong
+    touch test shifts the numbers and fails here."""
+    n = 1 << level
+
+    def coords(k):
+        return tuple(sum(((k >> (j * d + i)) & 1) << j for j in range(level)) for i in range(d))
+
+    def morton(xs):
+        return sum(((xs[i] >> j) & 1) << (j * d + i) for j in range(level) for i in range(d))
+
+    def eps_list():
+        out = [()]
+        for _ in range(d):
+            out = [e + (v,) for e in out for v in (-1, 0, 1)]
+        return out
+
+    M = 6 ** d - 3 ** d
+    for t in range(n ** d):
+        X = coords(t)
+        P = tuple(v >> 1 for v in X)
+        keyed = []
+        for eps in eps_list():
+            for sig in range(1 << d):
+                S = tuple(2 * (P[i] + eps[i]) + ((sig >> i) & 1) for i in range(d))
+                key = sum((eps[i] + 1) * 3 ** i for i in range(d)) * (1 << d) + sig
+                keyed.append((key, S))
+        keyed.sort()
+        expect = {}
+        q = 0
+        for _, S in keyed:
+            if all(abs(S[i] - X[i]) <= 1 for i in range(d)):
+                continue
+            if all(0 <= S[i] < n for i in range(d)):
+                expect[morton(S)] = q
+            q += 1
+        assert q == M
+        for s in range(n ** d):
+            assert oracle.std_slot(d, level, t, s) == expect.get(s, -1), (t, s)
