@@ -53,6 +53,13 @@
  * a thread-local message readable with hmat_last_error().  Argument checks
  * happen before any device work.  No C++ exception crosses this ABI.
  * Asynchronous device faults surface as HMAT_ERR_CUDA at a later call.
+ * Asynchronous EXCHANGE failures surface as HMAT_ERR_NCCL at the next call on
+ * H (or at hmat_synchronize / hmat_comm_info): an NCCL communicator error
+ * (ncclCommGetAsyncError is polled on every call), or, with the PEER exchange,
+ * a flag wait that timed out (HMAT_PEER_TIMEOUT_MS, default 10000): the waiting
+ * kernel records the missing rank in a host-mapped error word and finishes
+ * without trapping, so the CUDA context stays usable; that product's y is
+ * invalid and the error is reported once.
  */
 #ifndef HMAT_H
 #define HMAT_H
@@ -70,13 +77,15 @@ typedef enum {
   HMAT_ERR_INVALID = -1,     /* bad argument (message says which) */
   HMAT_ERR_NOMEM = -2,       /* device allocation failed */
   HMAT_ERR_CUDA = -3,        /* CUDA runtime error (incl. asynchronous faults) */
-  HMAT_ERR_NCCL = -4,        /* NCCL load/initialisation/collective error */
+  HMAT_ERR_NCCL = -4,        /* cross-GPU exchange error: NCCL load / init / collective /
+                                asynchronous error, or a PEER flag wait that timed out */
   HMAT_ERR_UNSUPPORTED = -5  /* valid but outside the implemented envelope */
 } hmat_status;
 
-/* Multi-GPU placement of one rank.  NULL => one GPU, the current device,
- * N_loc = N, a library-owned stream (a blocking stream, so it is ordered with
- * work on the legacy default stream). */
+/* Multi-GPU placement of one rank (PAPER.md:413-501 process tree on an ideal
+ * domain; block-row distribution of the vectors).  NULL =>
+ * one GPU, the current device, N_loc = N, a library-owned stream (a blocking
+ * stream, so it is ordered with work on the legacy default stream). */
 typedef struct {
   int nranks;                 /* P: a power of two <= c^L                            */
   int rank;                   /* 0 <= rank < P; owns Morton rows [rank N/P, ...)     */
@@ -106,38 +115,58 @@ typedef struct {
  *            the hypercube of ranks, round j swapping the packed buffer with
  *            rank ^ 2^j (ncclSend/ncclRecv) and adding the partner's copy;
  *            every rank ends with bit-identical sums (IEEE addition is
- *            commutative), whatever algorithm NCCL would pick for an allreduce. */
+ *            commutative), whatever algorithm NCCL would pick for an allreduce.
+ *            The recommended exchange (bench.py's default for P > 1). */
 #define HMAT_EXCHANGE_NCCL 0
 #define HMAT_EXCHANGE_EXTERNAL 1
 #define HMAT_EXCHANGE_PEER 2
 #define HMAT_EXCHANGE_TREE 3
 
-/* Build H from canonical panels (see above).  U and V are arrays of `depth`
+/* Build H from canonical panels (see above): the H-matrix of Def 2.4
+ * on the ideal domain tree under weak
+ * admissibility, factors U_ts V_ts^T,
+ * O(r N log N) storage.  U and V are arrays of `depth`
  * pointers (ignored when depth == 0); each panel and D may be host (pageable or
  * pinned) or device memory; the library copies them into its own 128-byte
  * aligned per-level device panels, so the caller may free them on return.
- * dim in {1,2,3}; depth >= 0; leaf_size >= 1; rank >= 1; N < 2^62.
- * HMAT_ERR_UNSUPPORTED if (2^dim - 1) * rank > 1024. */
+ * With dist->nranks = P > 1 each rank passes its rows only.
+ * HMAT_ERR_INVALID: dim not in {1,2,3}, depth < 0, leaf_size < 1, rank < 1,
+ * N >= 2^62, a NULL pointer, P not a power of two, P > c^L, rank out of range.
+ * HMAT_ERR_UNSUPPORTED if (2^dim - 1) * rank > 1024.  HMAT_ERR_NOMEM if the
+ * panels do not fit.  HMAT_ERR_NCCL if the NCCL communicator cannot be made. */
 hmat_status hmat_create(int depth, int dim, int leaf_size, int rank, const double* const* U,
                         const double* const* V, const double* D, const hmat_dist_t* dist, hmat_t* out);
 
-/* Same as hmat_create but leaves the panels uninitialised (zero); fill them in
- * place through hmat_panel() (no second copy of a 125 GB operator). */
+/* Same as hmat_create but leaves the panels uninitialised
+ * (zero); fill them in place through hmat_panel() (no second copy of a 125 GB
+ * operator).  Same errors as hmat_create. */
 hmat_status hmat_create_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist,
                                hmat_t* out);
 
-/* Device address of one of H's panels: kind 0 = U_level, 1 = V_level (level in
- * 1..depth), 2 = D (level ignored).  *rows = N_loc, *cols = W (or b), *ld =
- * row pitch in doubles (>= cols; padding columns are never read). */
+/* Device address of one of H's panels (the per-level factor layout of the
+ * blocks U_ts, V_ts; dense leaf blocks):
+ * kind 0 = U_level, 1 = V_level (level in 1..depth), 2 = D (level ignored; the
+ * dense panel index with standard admissibility).  *rows = N_loc, *cols = W (or
+ * b), *ld = row pitch in doubles (>= cols; padding columns are never read).
+ * HMAT_ERR_INVALID for a bad kind or level.  The pointer stays valid until
+ * hmat_destroy; writes must be complete before the next product is enqueued. */
 hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* rows, int64_t* cols,
                        int64_t* ld);
 
-/* y = H x for nrhs right-hand sides (the whole hot path: project, on-chip
- * reduction, cross-GPU exchange when P > 1, fused expand + dense).  1-4 rhs run
- * on the SIMT streaming kernels; from 5 rhs, where W % 16 == 0 (W <= 224, or
+/* y = H x for nrhs right-hand sides: eq:hmat-vec-add with
+ * y initialised to zero, computed by the paper's five steps
+ * (PAPER.md:652-663): project z_ts = V_ts^T x_s (Step 1, eq:prod-vx,
+ * PAPER.md:701-713), on-chip and cross-GPU reduction / transfer / broadcast of
+ * the z of blocks whose parent spans ranks (Steps 2-4), then
+ * y_t = sum U_ts z_ts + D_t x_t (Step 5, eq:prod-yuz / eq:prod-ydz,
+ * PAPER.md:907-959), expand fused over all levels and the dense leaf blocks.
+ * x, y: N_loc x nrhs column-major, device or host.  1-4 rhs
+ * run on the SIMT streaming kernels; from 5 rhs, where W % 16 == 0 (W <= 224, or
  * <= 112 if W % 32 != 0), 64 | leaf_size and weak admissibility, on the FP64
- * tensor cores in passes
- * of 64 rhs, the last one 16 or 32 wide when at most 16 / 32 remain. */
+ * tensor cores in passes of 64 rhs, the last one 16 or 32 wide when at most
+ * 16 / 32 remain.  HMAT_ERR_INVALID: NULL H/x/y, nrhs < 1, x aliasing y.
+ * With P > 1 a collective (same nrhs, same order on every rank); with the
+ * EXTERNAL exchange use hmat_project / hmat_expand (HMAT_ERR_UNSUPPORTED). */
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
 
 /* GEMV form y = alpha op(H) x + beta y ("do not initialize y
@@ -169,7 +198,10 @@ hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double
  * hmat_gemv(trans = 1) applies H^T (the interaction relation is symmetric, so
  * U and V swap roles; the near-field panels of H^T, (D_{t+eps,t})^T, are built
  * once on the first transposed call: 3^dim N leaf_size more doubles).
- * One GPU only (HMAT_ERR_UNSUPPORTED for nranks > 1); M rank <= 1024.
+ * nranks > 1 is supported with the NCCL, TREE and EXTERNAL exchanges: the
+ * cross-rank pairs along the slice boundaries and the near-field halo travel in
+ * one packed buffer (hmat_std_exchange_query).  Not
+ * supported (HMAT_ERR_UNSUPPORTED): the PEER exchange.  M rank <= 1024.
  * hmat_panel(kind 2, level e) returns dense panel e. */
 hmat_status hmat_create_standard(int depth, int dim, int leaf_size, int rank, const double* const* U,
                                  const double* const* V, const double* Dn, const hmat_dist_t* dist, hmat_t* out);
@@ -183,7 +215,8 @@ hmat_status hmat_create_standard_uninit(int depth, int dim, int leaf_size, int r
  * canonical panels (levels 1..depth-1); Dc: N_loc x (2^dim leaf_size), row i
  * of leaf-parent p = i / (2^dim leaf_size) holds row i - p 2^dim leaf_size of
  * p's dense diagonal block.  This is the structure of hmat_create(depth - 1,
- * dim, 2^dim leaf_size, ...) and is built as such.  depth >= 1. */
+ * dim, 2^dim leaf_size, ...) and is built as such.  depth >= 1
+ * (HMAT_ERR_INVALID otherwise); other errors as hmat_create. */
 hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
                                const double* const* V, const double* Dc, const hmat_dist_t* dist, hmat_t* out);
 
@@ -200,45 +233,63 @@ hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, cons
  *     contributions (partial node sums, zeros elsewhere) to exchange[0..count).
  *   the caller sums exchange over all ranks (Steps 2-4);
  *   hmat_expand: reads the summed exchange, Step 5: y = H x.
- * With HMAT_EXCHANGE_NCCL hmat_matvec does exactly this with an
- * in-place ncclAllReduce (HMAT_EXCHANGE_TREE: the recursive-doubling rounds).  With HMAT_EXCHANGE_PEER `exchange` is ignored (may
- * be NULL): the kernels exchange through the connected mailboxes. */
+ * With HMAT_EXCHANGE_NCCL hmat_matvec does exactly this with an in-place
+ * ncclAllReduce (HMAT_EXCHANGE_TREE: the recursive-doubling rounds).  With
+ * HMAT_EXCHANGE_PEER `exchange` is ignored (may be NULL): the kernels exchange
+ * through the connected mailboxes.  HMAT_ERR_INVALID: more than one pass of
+ * rhs, host x / y, NULL exchange where count > 0. */
 hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count);
 hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange);
 hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, double* y, int nrhs);
 
-/* PEER exchange set-up (collective in spirit: every rank must connect before
- * the first product).  hmat_peer_export writes the 64-byte CUDA IPC handle of
+/* PEER exchange set-up (the fused Steps 2-4, over NVLink
+ * peer memory; collective in spirit: every rank must connect before the first
+ * product).  hmat_peer_export writes the 64-byte CUDA IPC handle of
  * H's mailbox; after gathering all ranks' handles (rank order), each rank calls
  * hmat_peer_import with them.  hmat_peer_connect_local connects the P handles of
  * ONE process directly (e.g. P shards on one GPU; only the split-phase calls
  * may then be used, projects of all ranks before any expand, since an expand
- * waits for every rank's project). */
+ * waits for every rank's project); ranks on other devices of the process get
+ * peer access enabled (HMAT_ERR_UNSUPPORTED if the devices cannot reach each
+ * other).  HMAT_ERR_INVALID: H not a PEER handle, ranks[g] not rank g's handle
+ * of the same operator. */
 hmat_status hmat_peer_export(hmat_t H, void* handle64);
 hmat_status hmat_peer_import(hmat_t H, const void* handles);
 hmat_status hmat_peer_connect_local(hmat_t H, const hmat_t* ranks);
 
-/* Diagnostic form: only the low-rank levels l with bit (l-1) of level_mask set
- * and, if dense != 0, the dense leaf blocks: y = y_D + sum_{l in mask} y_l. */
+/* Diagnostic form of eq:hmat-vec-add restricted to some
+ * blocks: only the low-rank levels l with bit (l-1) of level_mask set and, if
+ * dense != 0, the dense leaf blocks: y = y_D + sum_{l in mask} y_l.  Errors as
+ * hmat_matvec. */
 hmat_status hmat_matvec_parts(hmat_t H, const double* x, double* y, int nrhs, uint64_t level_mask,
                               int dense);
 
-/* Frees everything H owns (collective when P > 1).  hmat_destroy(NULL) is OK. */
+/* Frees everything H owns (device panels of PAPER.md:316-339, buffers, the
+ * communicator; collective when P > 1).  Waits for H's
+ * stream first.  hmat_destroy(NULL) is OK.  Always returns HMAT_OK. */
 hmat_status hmat_destroy(hmat_t H);
 
-/* Thread-local message of the last failing call on this thread ("" if none). */
+/* Thread-local message of the last failing call on this thread ("" if none);
+ * the text names the failed check or call (SPEC's "dimension mismatch -> error"
+ * of the sequential matvec, PAPER.md:363-372 for the operation's shapes). */
 const char* hmat_last_error(void);
 
-/* N (global number of points), or -1 if H is NULL. */
+/* N = b c^L, the global number of points of the domain tree,
+ * or -1 if H is NULL. */
 int64_t hmat_num_points(hmat_t H);
 
-/* This rank's Morton rows [begin, end). */
+/* This rank's Morton rows [begin, end) = [rank N/P, (rank+1) N/P): the block-row
+ * ownership of x, y and the panels.  HMAT_ERR_INVALID
+ * for NULL arguments. */
 hmat_status hmat_local_rows(hmat_t H, int64_t* begin, int64_t* end);
 
-/* Make H enqueue on `stream` (a cudaStream_t on H's device) from now on. */
+/* Make H enqueue on `stream` (a cudaStream_t on H's device) from now on; waits
+ * for H's current stream first.  (Execution plumbing of the matvec of
+ * PAPER.md:363-388; no paper counterpart.)  HMAT_ERR_INVALID if H is NULL. */
 hmat_status hmat_set_stream(hmat_t H, void* stream);
 
-/* Asynchronous host-pointer mode (enable = 1): hmat_matvec / hmat_gemv with a
+/* Asynchronous host-pointer mode (enable = 1) for the products of
+ * PAPER.md:363-388 with host vectors: hmat_matvec / hmat_gemv with a
  * host x or y return as soon as the work is enqueued.  x is copied in on a
  * copy stream, the kernels run on H's stream, y is copied out on another copy
  * stream; the staging buffers alternate between consecutive calls, so one
@@ -249,11 +300,14 @@ hmat_status hmat_set_stream(hmat_t H, void* stream);
  * pointers are unaffected.  Disabling drains the pipeline.  Default: off. */
 hmat_status hmat_set_host_async(hmat_t H, int enable);
 
-/* Wait for all work of H (copies in, kernels, copies out). */
+/* Wait for all work of H (copies in, kernels, copies out; the exchange of
+ * PAPER.md:746-904 included), then report any asynchronous exchange error
+ * (HMAT_ERR_NCCL, see ERRORS above). */
 hmat_status hmat_synchronize(hmat_t H);
 
 /* 128 bytes of a fresh ncclUniqueId for hmat_dist_t (call on one rank and
- * broadcast).  HMAT_ERR_NCCL if NCCL cannot be loaded. */
+ * broadcast): the communicator of the cross-GPU Steps 2-4.
+ * HMAT_ERR_NCCL if NCCL cannot be loaded, HMAT_ERR_INVALID for NULL. */
 hmat_status hmat_nccl_unique_id(void* out128);
 
 /* Diagnostic: runs the library's NCCL layer end to end on ONE GPU -- a fresh
@@ -266,30 +320,39 @@ hmat_status hmat_nccl_unique_id(void* out128);
  * HMAT_ERR_INVALID for count < 1. */
 hmat_status hmat_nccl_selftest(int device, int64_t count);
 
-/* Kernel timing: when enabled, CUDA events bracket every kernel/collective of
- * each matvec on H's stream.  hmat_profile_read() synchronises, returns the
+/* The communicator H exchanges over (Steps 2-4): *nranks
+ * and *rank as NCCL reports them (ncclCommCount / ncclCommUserRank) for the
+ * NCCL and TREE exchanges, else the plan's P and rank.  Also reports pending
+ * asynchronous exchange errors (HMAT_ERR_NCCL).  HMAT_ERR_INVALID for NULL. */
+hmat_status hmat_comm_info(hmat_t H, int* nranks, int* rank);
+
+/* Kernel timing of the steps of PAPER.md:652-663: when enabled, CUDA events
+ * bracket every kernel/collective of each matvec on H's stream.  hmat_profile_read() synchronises, returns the
  * accumulated milliseconds and launch counts per phase since the last read
  * (phase 0 = project, 1 = exchange, 2 = expand, 3 = host<->device copies) and
- * resets them.  ms and launches point to HMAT_NUM_PHASES entries. */
+ * resets them.  ms and launches point to HMAT_NUM_PHASES entries.
+ * HMAT_ERR_INVALID for NULL arguments. */
 #define HMAT_NUM_PHASES 4
 hmat_status hmat_profile(hmat_t H, int enable);
 hmat_status hmat_profile_read(hmat_t H, double* ms, int64_t* launches);
 
-/* Per-CTA trace (load-balance diagnostics).  hmat_cta_trace(H, 1) allocates a
+/* Per-CTA trace (load-balance diagnostics of the balanced work split the paper
+ * argues for).  hmat_cta_trace(H, 1) allocates a
  * device buffer; every later project / expand launch on H then records, per CTA
  * b, [start ns, end ns, SM id] (%globaltimer at the CTA's start and at its last
  * warp's exit; end is 0 for a CTA that did not run).  hmat_cta_trace(H, 0) frees
  * it.  hmat_cta_trace_read synchronises H's stream and copies the records of the
  * LAST launch of `kernel` (0 = project, 1 = expand) into out[3 * b + 0..2] for
- * b < min(grid, max_ctas, 8192); *n_ctas = that count. */
+ * b < min(grid, max_ctas, 8192); *n_ctas = that count.  HMAT_ERR_INVALID for a
+ * bad kernel index or when tracing is off. */
 hmat_status hmat_cta_trace(hmat_t H, int enable);
 hmat_status hmat_cta_trace_read(hmat_t H, int kernel, int64_t* out, int max_ctas, int* n_ctas);
 
 /* Launches of this library's kernels one hmat_matvec(nrhs) performs on this
- * rank: per pass of right-hand sides, project + expand, + pack / unpack with
+ * rank (the steps of PAPER.md:652-663 as kernels): per pass of right-hand sides, project + expand, + pack / unpack with
  * standard admissibility and P > 1, + log2 P adds with the TREE exchange, + the
  * mailbox sum on the tensor-core path with the PEER exchange (NCCL's own kernels
- * and memsets not counted). */
+ * and memsets not counted).  -1 for NULL H or nrhs < 1. */
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs);
 
 /* Host-only description of a shard's plan (no GPU needed). */
@@ -309,7 +372,9 @@ typedef struct {
 } hmat_plan_info_t;
 
 /* Validates (depth, dim, leaf_size, rank, nranks, rank_id) exactly like
- * hmat_create and describes the plan a B200 (148 SMs) would use.  The exchange
+ * hmat_create (same HMAT_ERR_INVALID / _UNSUPPORTED) and describes the plan a
+ * B200 (148 SMs) would use: the partition of PAPER.md:434-501 and the packed
+ * exchange of Steps 2-4.  The exchange
  * buffer is level-major, then target-major: row (level_rows_offset[l] + t)
  * holds, in columns [q r, (q+1) r), z_{t, s_q} = V_{t,s_q}^T x_{s_q}, summed over
  * all ranks. */
@@ -328,6 +393,7 @@ hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nra
  *                           another rank, in Morton order,
  * the second part starting at E rank cap rounded up to even; every rank writes
  * what it owns, zeros elsewhere, and the buffer is summed over the ranks.
+ * (PAPER.md:606-629 for where the pairs lie; errors as hmat_plan_query.)
  * Tables of THIS rank (filled when the caller's array is non-NULL and its
  * capacity is large enough; the n_* fields always receive the lengths):
  *   src_entry  [node - first local node][M] per level l at src_off[l]: entry of

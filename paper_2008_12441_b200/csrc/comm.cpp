@@ -23,6 +23,9 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int*) = nullptr;
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   std::string error;
 };
 
@@ -48,8 +51,11 @@ NcclApi& api() {
     a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(a.handle, "ncclRecv"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.handle, "ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.handle, "ncclGroupEnd"));
+    a.CommGetAsyncError = reinterpret_cast<decltype(a.CommGetAsyncError)>(dlsym(a.handle, "ncclCommGetAsyncError"));
+    a.CommCount = reinterpret_cast<decltype(a.CommCount)>(dlsym(a.handle, "ncclCommCount"));
+    a.CommUserRank = reinterpret_cast<decltype(a.CommUserRank)>(dlsym(a.handle, "ncclCommUserRank"));
     if (!a.GetUniqueId || !a.CommInitRank || !a.AllReduce || !a.CommDestroy || !a.GetErrorString || !a.Send ||
-        !a.Recv || !a.GroupStart || !a.GroupEnd)
+        !a.Recv || !a.GroupStart || !a.GroupEnd || !a.CommGetAsyncError || !a.CommCount || !a.CommUserRank)
       a.error = "libnccl is missing a required symbol";
   });
   return a;
@@ -120,6 +126,24 @@ std::string comm_tree_allreduce_sum(Comm* c, double* buf, double* tmp, size_t co
     cudaError_t e = launch_add_inplace(buf, tmp, count, stream);
     if (e != cudaSuccess) return std::string("add_inplace: ") + cudaGetErrorString(e);
   }
+  return "";
+}
+
+std::string comm_async_error(Comm* c) {
+  if (!c || !c->comm) return "";
+  ncclResult_t st = ncclSuccess;
+  ncclResult_t r = api().CommGetAsyncError(c->comm, &st);
+  if (r != ncclSuccess) return nccl_err("ncclCommGetAsyncError", r);
+  if (st != ncclSuccess && st != ncclInProgress) return nccl_err("NCCL asynchronous error", st);
+  return "";
+}
+
+std::string comm_info(Comm* c, int* nranks, int* rank) {
+  NcclApi& a = api();
+  ncclResult_t r = a.CommCount(c->comm, nranks);
+  if (r != ncclSuccess) return nccl_err("ncclCommCount", r);
+  r = a.CommUserRank(c->comm, rank);
+  if (r != ncclSuccess) return nccl_err("ncclCommUserRank", r);
   return "";
 }
 

@@ -34,6 +34,11 @@ std::string comm_tree_allreduce_sum(Comm* c, double* buf, double* tmp, size_t co
                                     cudaStream_t stream);
 // One round: buf -> partner, partner's buf -> tmp (partner may be this rank).
 std::string comm_swap_round(Comm* c, const double* buf, double* tmp, size_t count, int partner, cudaStream_t stream);
+// ncclCommGetAsyncError: "" while the communicator is healthy (or still
+// progressing), else the error (a peer died, a network/NVLink fault, ...).
+std::string comm_async_error(Comm* c);
+// ncclCommCount / ncclCommUserRank of the library's communicator.
+std::string comm_info(Comm* c, int* nranks, int* rank);
 void comm_destroy(Comm* c);
 
 // buf[i] += add[i] (kernels_aux.cu)

@@ -158,6 +158,11 @@ struct hmat_s {
   double* mbox = nullptr;
   double** mbox_dev = nullptr;
   unsigned int* done = nullptr;
+  // error word of the bounded flag waits (peer.cuh): host-mapped, written by a
+  // kernel whose wait timed out, read (and cleared) by the next call
+  unsigned int* err_host = nullptr;
+  unsigned int* err_dev = nullptr;
+  int64_t peer_timeout_ns = 0;
   int64_t mb = 0;
   uint64_t epoch = 0;
   std::vector<void*> opened;  // IPC mappings to close
@@ -215,6 +220,7 @@ void release(hmat_s* H) {
   cudaFree(H->mbox);
   cudaFree(H->mbox_dev);
   cudaFree(H->done);
+  if (H->err_host) cudaFreeHost(H->err_host);
   for (auto& e : H->ev) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -338,8 +344,13 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
         (e = cudaMalloc(reinterpret_cast<void**>(&H->mbox_dev), size_t(p.P) * sizeof(double*))) ||
         (e = cudaMalloc(reinterpret_cast<void**>(&H->done), 256)) ||
         (e = cudaMemset(H->mbox, 0, mbytes)) || (e = cudaMemset(H->mbox_dev, 0, size_t(p.P) * sizeof(double*))) ||
-        (e = cudaMemset(H->done, 0, 256)))
+        (e = cudaMemset(H->done, 0, 256)) ||
+        (e = cudaHostAlloc(reinterpret_cast<void**>(&H->err_host), 64, cudaHostAllocMapped | cudaHostAllocPortable)))
       return bail(cuda_fail(e, "allocating the peer mailbox"));
+    *reinterpret_cast<volatile unsigned int*>(H->err_host) = 0u;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&H->err_dev), H->err_host, 0)))
+      return bail(cuda_fail(e, "mapping the peer error word"));
+    H->peer_timeout_ns = int64_t(std::max(1, env_int("HMAT_PEER_TIMEOUT_MS", 10000))) * 1000000;
   }
   if (H->sx) {  // device copies of the exchange tables
     const hmat::StdExchange& X = *H->sx;
@@ -447,6 +458,28 @@ hmat_status ensure_buf(double** buf, size_t* cap, size_t n) {
   *cap = 0;
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(buf), n * sizeof(double)));
   *cap = n;
+  return HMAT_OK;
+}
+
+// Asynchronous failures of earlier work on H: a peer flag wait that timed out
+// (the kernels' error word, cleared once reported) and NCCL's asynchronous
+// communicator errors (ncclCommGetAsyncError).  Both map to HMAT_ERR_NCCL.
+hmat_status check_async(hmat_s* H) {
+  if (H->err_host) {
+    volatile unsigned int* w = reinterpret_cast<volatile unsigned int*>(H->err_host);
+    const unsigned int v = *w;
+    if (v) {
+      *w = 0u;
+      return fail(HMAT_ERR_NCCL, "peer exchange: rank " + std::to_string((v >> 16) & 0x7fffu) +
+                                     "'s flag of pass " + std::to_string(v & 0xffffu) + " (mod 2^16) not raised within " +
+                                     std::to_string(H->peer_timeout_ns / 1000000) +
+                                     " ms (late or missing peer; that product's y is invalid)");
+    }
+  }
+  if (H->comm) {
+    std::string m = hmat::comm_async_error(H->comm);
+    if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  }
   return HMAT_OK;
 }
 
@@ -573,6 +606,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     return fail(HMAT_ERR_INVALID, "x and y alias");
   const hmat::Plan& p = H->plan;
   CUDA_TRY(cudaSetDevice(H->device));
+  {
+    hmat_status sa = check_async(H);
+    if (sa != HMAT_OK) return sa;
+  }
   if (trans && p.adm && p.P > 1)
     return fail(HMAT_ERR_UNSUPPORTED, "transposed product with standard admissibility and nranks > 1");
   if (trans) {
@@ -712,6 +749,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.mbox = H->mbox_dev;
   a.mb = H->mb;
   a.done = H->done;
+  a.err = H->err_dev;
+  a.peer_timeout_ns = H->peer_timeout_ns;
   a.zex_base = H->zex;
   a.dbg = p.dbg;
   a.snake = p.snake;
@@ -834,8 +873,12 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
           H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, nb, dl.dgrid_p, dl.dsmem_p, H->stream); },
           [&] { return hmat::launch_expand_dmma(a, nb, dl.dgrid_e, dl.dsmem_e, H->stream); }, dl.dgrid_p > 0,
           dl.dgrid_p, dl.dgrid_e, [] { return cudaSuccess; },
-          // PEER: the rank-ordered sum of the P mailbox slots into the exchange levels
-          [&] { return H->peer ? hmat::launch_peer_sum(a, H->zex_d, H->stream) : cudaSuccess; });
+          // PEER: the rank-ordered sum of the P mailbox slots into the exchange levels,
+          // when this pass ran a project (whose last CTA raised the flags)
+          [&] {
+            return H->peer && dl.dgrid_p > 0 && level_mask ? hmat::launch_peer_sum(a, H->zex_d, H->stream)
+                                                            : cudaSuccess;
+          });
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -936,7 +979,11 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
     prof_end(H, &ep);
   }
-  if (host_io) CUDA_TRY(cudaStreamSynchronize(H->stream));
+  if (host_io) {
+    CUDA_TRY(cudaStreamSynchronize(H->stream));
+    hmat_status sa = check_async(H);
+    if (sa != HMAT_OK) return sa;
+  }
   CUDA_TRY(cudaGetLastError());
   return HMAT_OK;
 }
@@ -1032,7 +1079,7 @@ hmat_status hmat_synchronize(hmat_t H) {
   if (H->s_in) CUDA_TRY(cudaStreamSynchronize(H->s_in));
   CUDA_TRY(cudaStreamSynchronize(H->stream));
   if (H->s_out) CUDA_TRY(cudaStreamSynchronize(H->s_out));
-  return HMAT_OK;
+  return check_async(H);
 }
 
 hmat_status hmat_set_stream(hmat_t H, void* stream) {
@@ -1133,15 +1180,39 @@ hmat_status hmat_peer_connect_local(hmat_t H, const hmat_t* ranks) {
   if (!H->peer) return fail(HMAT_ERR_INVALID, "H does not use the peer exchange");
   const int P = H->plan.P;
   std::vector<double*> ptrs(P);
+  CUDA_TRY(cudaSetDevice(H->device));
   for (int g = 0; g < P; ++g) {
     if (!ranks[g] || !ranks[g]->peer || ranks[g]->plan.P != P || ranks[g]->plan.rank != g)
       return fail(HMAT_ERR_INVALID, "ranks[g] must be rank g's handle of the same peer-exchange operator");
+    if (ranks[g]->mb != H->mb)
+      return fail(HMAT_ERR_INVALID, "ranks[g]'s mailbox slot size differs (not the same operator)");
+    if (ranks[g]->device != H->device) {  // this rank's kernels store into that device's memory
+      int ok = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&ok, H->device, ranks[g]->device));
+      if (!ok) return fail(HMAT_ERR_UNSUPPORTED, "no peer access from this device to rank " + std::to_string(g) + "'s");
+      cudaError_t pe = cudaDeviceEnablePeerAccess(ranks[g]->device, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else if (pe != cudaSuccess)
+        return cuda_fail(pe, "cudaDeviceEnablePeerAccess");
+    }
     ptrs[g] = ranks[g]->mbox;
   }
-  CUDA_TRY(cudaSetDevice(H->device));
   CUDA_TRY(cudaMemcpy(H->mbox_dev, ptrs.data(), P * sizeof(double*), cudaMemcpyHostToDevice));
   H->connected = true;
   return HMAT_OK;
+}
+
+hmat_status hmat_comm_info(hmat_t H, int* nranks, int* rank) {
+  if (!H || !nranks || !rank) return fail(HMAT_ERR_INVALID, "NULL argument");
+  *nranks = H->plan.P;
+  *rank = H->plan.rank;
+  if (H->comm) {  // the NCCL communicator's own view
+    CUDA_TRY(cudaSetDevice(H->device));
+    std::string m = hmat::comm_info(H->comm, nranks, rank);
+    if (!m.empty()) return fail(HMAT_ERR_NCCL, m);
+  }
+  return check_async(H);
 }
 
 hmat_status hmat_profile(hmat_t H, int enable) {

@@ -559,19 +559,12 @@ cudaError_t set_e(int64_t smem) {
 
 // Wait for the P ranks' flags of this pass, then exchange[o] = sum over ranks g
 // (in rank order) of slot g of this rank's mailbox: the summed exchange levels
-// the tensor-core expand reads.  Bounded wait (~2^35 cycles): never a hung GPU.
+// the tensor-core expand reads.  Bounded wait: a timeout is reported through
+// the handle's error word (peer_wait_flags), never a trap or a hung GPU.
 __global__ void peer_sum_kernel(const __grid_constant__ StreamArgs a, double* __restrict__ out) {
   const int par = static_cast<int>(a.epoch & 1);
   const double* mb = a.mbox[a.rank] + (int64_t)par * a.P * a.mb;
-  if (threadIdx.x == 0) {
-    const uint64_t* fl = reinterpret_cast<const uint64_t*>(a.mbox[a.rank] + 2 * a.P * a.mb) + par * a.P;
-    const long long t0 = clock64();
-    for (int g = 0; g < a.P; ++g)
-      while (dev::ld_acquire_sys(fl + g) != a.epoch) {
-        __nanosleep(256);
-        if (clock64() - t0 > (1ll << 35)) __trap();
-      }
-  }
+  if (threadIdx.x == 0) peer_wait_flags(a);
   __syncthreads();
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < a.exch; o += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;

@@ -21,6 +21,7 @@
 #include "device_utils.cuh"
 #include "geometry.cuh"
 #include "kernels.h"
+#include "peer.cuh"
 
 namespace hmat {
 
@@ -179,13 +180,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
               const int par = static_cast<int>(a.epoch & 1);
               const double* mb = a.mbox[a.rank] + (int64_t)par * a.P * a.mb;
               if (!peers_ready) {
-                const uint64_t* fl = reinterpret_cast<const uint64_t*>(a.mbox[a.rank] + 2 * a.P * a.mb) + par * a.P;
-                const long long t0 = clock64();
-                for (int g = 0; g < a.P; ++g)
-                  while (dev::ld_acquire_sys(fl + g) != a.epoch) {
-                    __nanosleep(256);
-                    if (clock64() - t0 > (1ll << 35)) __trap();  // ~17 s: never hang the GPU
-                  }
+                peer_wait_flags(a);  // bounded; a timeout is reported through a.err
                 dev::fence_proxy_async_global();
                 peers_ready = true;
               }

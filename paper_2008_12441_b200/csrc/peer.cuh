@@ -40,5 +40,29 @@ __device__ __forceinline__ void peer_push(const StreamArgs& a, int t, int64_t GL
   }
 }
 
+// Bounded wait (one thread) for the P ranks' flags of this pass in this rank's
+// mailbox.  Returns true when all are raised.  On timeout (a.peer_timeout_ns,
+// HMAT_PEER_TIMEOUT_MS) it records the first missing rank in the handle's
+// host-mapped error word -- the host reports it as HMAT_ERR_NCCL on the next
+// call or at hmat_synchronize -- and returns false; the caller then finishes
+// with whatever the mailbox holds (a wrong but finite y, flagged as an error):
+// no __trap, so a late or missing peer never poisons the CUDA context.
+__device__ __forceinline__ bool peer_wait_flags(const StreamArgs& a) {
+  const int par = static_cast<int>(a.epoch & 1);
+  const uint64_t* fl = reinterpret_cast<const uint64_t*>(a.mbox[a.rank] + 2 * a.P * a.mb) + par * a.P;
+  const uint64_t t0 = dev::globaltimer_ns();
+  for (int g = 0; g < a.P; ++g)
+    while (dev::ld_acquire_sys(fl + g) != a.epoch) {
+      __nanosleep(256);
+      if (static_cast<int64_t>(dev::globaltimer_ns() - t0) > a.peer_timeout_ns) {
+        // error word: bit 31 | missing rank << 16 | low 16 bits of the pass number
+        atomicCAS(a.err, 0u, 0x80000000u | (static_cast<unsigned int>(g) << 16) |
+                                 static_cast<unsigned int>(a.epoch & 0xffffu));
+        __threadfence_system();
+        return false;
+      }
+    }
+  return true;
+}
 
 }  // namespace hmat

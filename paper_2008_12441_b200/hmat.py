@@ -34,7 +34,8 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_nccl_selftest",
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
            "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local", "hmat_cta_trace",
-           "hmat_cta_trace_read", "hmat_std_exchange_query", "hmat_set_host_async", "hmat_synchronize")
+           "hmat_cta_trace_read", "hmat_std_exchange_query", "hmat_set_host_async", "hmat_synchronize",
+           "hmat_comm_info")
 
 
 class hmat_std_exchange_t(ctypes.Structure):
@@ -101,6 +102,7 @@ _sigs = {
     "hmat_std_exchange_query": (_i, [_i, _i, _i, _i, _i, _i, ctypes.POINTER(hmat_std_exchange_t)]),
     "hmat_set_host_async": (_i, [_H, _i]),
     "hmat_synchronize": (_i, [_H]),
+    "hmat_comm_info": (_i, [_H, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "hmat_peer_export": (_i, [_H, _P]),
     "hmat_cta_trace": (_i, [_H, _i]),
     "hmat_cta_trace_read": (_i, [_H, _i, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(ctypes.c_int)]),
@@ -354,6 +356,14 @@ def hmat_set_host_async(h, enable: bool = True) -> None:
 
 def hmat_synchronize(h) -> None:
     _check(_lib.hmat_synchronize(h), "hmat_synchronize")
+
+
+def hmat_comm_info(h):
+    """(nranks, rank) of the communicator h exchanges over (NCCL's own view for
+    the NCCL / TREE exchanges); raises on a pending asynchronous exchange error."""
+    n, r = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.hmat_comm_info(h, ctypes.byref(n), ctypes.byref(r)), "hmat_comm_info")
+    return n.value, r.value
 
 
 def hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id) -> dict:

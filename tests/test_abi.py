@@ -155,3 +155,24 @@ def test_plan_query_reports_tensor_core_layouts(L, d, b, r, dmma, narrow):
             assert 2 <= info.dmma_stages_p[i] and 2 <= info.dmma_stages_e[i]
             assert info.dmma_smem_p[i] <= 227 * 1024 and info.dmma_smem_e[i] <= 227 * 1024
             assert info.dmma_grid_p[i] % 148 == 0 and info.dmma_grid_e[i] == 296
+
+
+def test_every_declaration_cites_the_paper():
+    """Each exported declaration of include/hmat.h is preceded by a comment that
+    cites the paper passage it implements or serves (PAPER.md:<line>)."""
+    src = open(os.path.join(ROOT, "include", "hmat.h")).read()
+    missing = []
+    for name in declared_symbols():
+        m = re.search(r"^[\w\s\*]*\b" + name + r"\s*\(", src, flags=re.M)
+        assert m, name
+        before = src[:m.start()]
+        # the comment block that precedes the declaration (possibly shared by a
+        # run of consecutive declarations)
+        end = before.rfind("*/")
+        start = before.rfind("/*", 0, end)
+        between = before[end + 2:]
+        decls_between = re.findall(r"\bhmat_[a-z_0-9]+\s*\(", re.sub(r"/\*.*?\*/", "", between, flags=re.S))
+        comment = before[start:end]
+        if "PAPER.md:" not in comment or len(decls_between) > 3:
+            missing.append(name)
+    assert not missing, f"declarations without a PAPER.md: citation: {missing}"

@@ -262,3 +262,92 @@ def test_standard_sharded_transpose_unsupported():
         assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
     finally:
         hm.hmat_destroy(h)
+
+
+# ---- failure behaviour of the PEER exchange ------------------------------------------
+
+def _peer_pair(cfg, monkeypatch, timeout_ms):
+    monkeypatch.setenv("HMAT_PEER_TIMEOUT_MS", str(timeout_ms))
+    P = 2
+    hs, xs = [], []
+    for g in range(P):
+        r0, r1 = g * cfg.N // P, (g + 1) * cfg.N // P
+        U, V, D = hgen.inputs(cfg, r0, r1)
+        hs.append(hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D,
+                                 hm._dist(nranks=P, rank=g, device=0, exchange=hm.HMAT_EXCHANGE_PEER)))
+        xs.append((r0, r1))
+    for h in hs:
+        hm.hmat_peer_connect_local(h, hs)
+    return hs, xs
+
+
+@pytest.mark.parametrize("cfg,nrhs", [(HConfig("t2d", d=2, L=3, b=16, r=4, seed=421), 1),        # SIMT expand waits
+                                      (HConfig("t3d", d=3, L=2, b=64, r=32, seed=422), 64)],     # tensor-core peer_sum waits
+                         ids=["simt", "dmma"])
+def test_peer_flag_timeout_is_an_error_not_a_fault(cfg, nrhs, monkeypatch):
+    """A rank whose peer never raises its flag: the bounded wait gives up after
+    HMAT_PEER_TIMEOUT_MS, the handle reports HMAT_ERR_NCCL (naming the missing
+    rank) at hmat_synchronize, once, and the CUDA context stays usable (no trap):
+    later work on the device, including another H-matvec, is correct."""
+    hs, rows = _peer_pair(cfg, monkeypatch, 300)
+    try:
+        r0, r1 = rows[0]
+        x = torch.from_numpy(np.ascontiguousarray(hgen.xblock(cfg, nrhs=nrhs, row_begin=r0, row_end=r1).T)).cuda()
+        y = torch.empty_like(x)
+        hm.hmat_project(hs[0], x.t(), None, nrhs)          # rank 0 pushes and raises its flags
+        hm.hmat_expand(hs[0], x.t(), None, y.t(), nrhs)    # ... and waits for rank 1's, which never come
+        with pytest.raises(hm.HMatError) as ei:
+            hm.hmat_synchronize(hs[0])
+        assert ei.value.status == hm.HMAT_ERR_NCCL
+        assert "rank 1" in str(ei.value) and "not raised" in str(ei.value)
+        hm.hmat_synchronize(hs[0])                          # reported once
+        assert torch.isfinite(y).all()
+    finally:
+        for h in hs:
+            hm.hmat_destroy(h)
+    assert float(torch.ones(1000, device="cuda", dtype=torch.float64).sum()) == 1000.0
+    c = HConfig("after", d=2, L=3, b=16, r=4, seed=423)
+    U, V, D = hgen.inputs(c)
+    x = hgen.xblock(c, nrhs=1)[:, 0]
+    h = hm.hmat_create(c.L, c.d, c.b, c.r, U, V, D)
+    try:
+        xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        yd = torch.empty_like(xd)
+        hm.hmat_matvec(h, xd, yd)
+        assert_parity(yd.cpu().numpy(), oracle.matvec(c.d, c.L, c.b, c.r, U, V, D, x))
+    finally:
+        hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("cfg,nrhs", [(HConfig("m2d", d=2, L=3, b=16, r=4, seed=424), 2),
+                                      (HConfig("m3d", d=3, L=2, b=64, r=32, seed=425), 8)],
+                         ids=["simt", "dmma"])
+def test_peer_dense_only_parts_do_not_wait(cfg, nrhs, monkeypatch):
+    """hmat_matvec_parts(mask = 0, dense = 1) on a PEER handle runs no project,
+    so no rank raises a flag: nothing may wait for one (the tensor-core path
+    skips its mailbox sum).  Rank 0 alone gets y = D x of its rows, no error."""
+    hs, rows = _peer_pair(cfg, monkeypatch, 2000)
+    try:
+        r0, r1 = rows[0]
+        xh = hgen.xblock(cfg, nrhs=nrhs)
+        x = torch.from_numpy(np.ascontiguousarray(xh[r0:r1].T)).cuda()
+        y = torch.empty_like(x)
+        hm.hmat_matvec_parts(hs[0], x.t(), y.t(), 0, True, nrhs)
+        hm.hmat_synchronize(hs[0])
+        U, V, D = hgen.inputs(cfg)
+        ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, xh, level_mask=0, dense=True)
+        assert_parity(y.t().cpu().numpy(), ref[r0:r1])
+    finally:
+        for h in hs:
+            hm.hmat_destroy(h)
+
+
+def test_comm_info_without_nccl():
+    cfg = HConfig("ci", d=2, L=2, b=4, r=2, seed=426)
+    U, V, D = hgen.inputs(cfg, cfg.N // 4, cfg.N // 2)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D, hm._dist(nranks=4, rank=1, device=0,
+                                                                       external_exchange=True))
+    try:
+        assert hm.hmat_comm_info(h) == (4, 1)
+    finally:
+        hm.hmat_destroy(h)
