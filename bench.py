@@ -11,9 +11,13 @@ r = 16, 124.55 GB of factors), the configuration BASELINE.json quotes the
 generated in place on the device (gen/), distinct x per step; the working set
 (125 GB) is far larger than L2 (126 MB), so no flush is needed.
 
-N > 1: launched by torch.distributed.run, one rank per GPU; each rank owns the
-Morton rows [g N/P, (g+1) N/P) of every panel (strong scaling of one operator)
-and the library sums the cross-GPU z vectors with NCCL.  Time = max over ranks.
+N > 1: one rank per GPU.  Launched by torch.distributed.run (the driver), or
+`python bench.py --gpus N` re-executes itself under torch.distributed.run with
+N local ranks; a world size different from --gpus is an error (rc 2).  Each
+rank owns the Morton rows [g N/P, (g+1) N/P) of every panel (strong scaling of
+one operator) and the library exchanges the cross-GPU z vectors with the
+paper's tree-structured Steps 2-4 over NCCL (--exchange tree, the default;
+PAPER.md:746-904).  Time = max over ranks.
 
 Rank 0 prints one JSON line (see DESIGN.md §7 for every field).
 """
@@ -49,10 +53,43 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl", "tree"],
-                    help="N > 1: in-kernel exchange over NVLink peer memory (default), ncclAllReduce, or the "
-                         "paper's tree-structured exchange (recursive doubling over ncclSend/ncclRecv)")
+    ap.add_argument("--exchange", default="tree", choices=["tree", "nccl", "peer"],
+                    help="N > 1: the paper's tree-structured exchange (recursive doubling over ncclSend/ncclRecv, "
+                         "default), one ncclAllReduce, or the in-kernel exchange over NVLink peer memory (opt-in)")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="host-only: start the ranks (gloo), report the world each one sees, exit")
     return ap.parse_args()
+
+
+def self_launch(args):
+    """`--gpus N` (N > 1) outside torch.distributed: re-execute this script under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous) and return its
+    exit code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launcher_check(args):
+    """The ranks self_launch / the driver started: each joins a gloo group and
+    rank 0 prints what every rank saw (a host test of the launcher)."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    seen = [(rank, world, int(os.environ.get("LOCAL_RANK", "0")))]
+    if world > 1:
+        dist.init_process_group("gloo")
+        allv = [None] * world
+        dist.all_gather_object(allv, seen[0])
+        seen = allv
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"launcher_check": True, "gpus": args.gpus, "world": world,
+                          "ranks": sorted(s[0] for s in seen), "worlds": sorted(set(s[1] for s in seen))}), flush=True)
 
 
 def workload_desc(cfg):
@@ -177,11 +214,16 @@ class ClockSampler:
 # CPU oracle baseline: the oracle as it stands, single-threaded, on a bounded sample
 # --------------------------------------------------------------------------------------
 
-def oracle_sample(cfg, budget_bytes):
-    """The leading diagonal sub-H-matrix of `cfg` rooted at level q (rows
-    [0, N/c^q)): exactly the blocks of cfg at levels q+1..L inside that
-    diagonal block plus its dense leaves -- an H-matrix of depth L-q with the
-    same b, r, d.  q is the smallest level whose factor bytes fit the budget."""
+SAMPLE_BYTES = 1.5e9  # factor bytes of the oracle's bounded sample of a workload
+
+
+def oracle_sample(cfg, budget_bytes=SAMPLE_BYTES):
+    """The bounded sample the CPU oracle is timed on (cpu_baseline AND the
+    reference arm: the same sample): the leading diagonal sub-H-matrix of `cfg`
+    rooted at level q (rows [0, N/c^q)) -- exactly the blocks of cfg at levels
+    q+1..L inside that diagonal block plus its dense leaves, an H-matrix of depth
+    L-q with the same b, r, d -- for the smallest q whose factor bytes fit the
+    budget.  Values are extrapolated to the whole workload by factor bytes."""
     for q in range(0, cfg.L + 1):
         n = cfg.N // cfg.c ** q
         depth = cfg.L - q
@@ -191,82 +233,107 @@ def oracle_sample(cfg, budget_bytes):
     return cfg.L, cfg.b, 0, 8 * cfg.b * cfg.b
 
 
-def run_oracle_sample(cfg, q, n, depth, reps, nrhs, min_seconds=0.0):
-    """Times `reps` oracle passes over the sample, more (up to 50) until they add
-    up to min_seconds."""
-    from oracle import oracle
+def sample_desc(cfg, q, n, depth, fb):
+    return (f"the leading level-{q} diagonal sub-H-matrix of {cfg.name} (rows [0,{n}), its blocks at levels "
+            f"{q + 1}..{cfg.L} + dense leaves = an H-matrix of depth {depth}, {fb / 1e9:.3f} GB of factors, "
+            f"nrhs={cfg.nrhs}); value extrapolated by factor bytes to {cfg.factor_bytes / 1e9:.2f} GB per matvec")
 
-    def more(times):
-        return len(times) < reps or (sum(times) < min_seconds and len(times) < 50)
-    if cfg.adm:
-        # standard admissibility: a standalone operator of depth L-q with the same
-        # b, r, d (a sub-block is not an H-matrix of the same kind at the boundary)
+
+class OracleSample:
+    """Panels of the sample (generated from the full operator's streams: the same
+    values as the GPU operator's rows) and a timer of the oracle on them."""
+
+    def __init__(self, cfg):
         import dataclasses
-        sub = dataclasses.replace(cfg, L=depth)
-        U, V, D = hgen.inputs(sub)
-        x = hgen.xblock(sub, nrhs=nrhs)
-        times = []
-        while more(times):
-            t0 = time.perf_counter()
-            oracle.std_matvec(sub.d, sub.L, sub.b, sub.r, U, V, D, x)
-            times.append(time.perf_counter() - t0)
-        return times
-    # panels of levels q+1..L restricted to rows [0, n): generated from the full
-    # operator's streams (same values as the GPU operator)
-    U = [hgen.panel(cfg, hgen.TAG_U, q + l, 0, n) for l in range(1, depth + 1)]
-    V = [hgen.panel(cfg, hgen.TAG_V, q + l, 0, n) for l in range(1, depth + 1)]
-    D = hgen.panel(cfg, hgen.TAG_D, 0, 0, n)
-    x = hgen.xblock(cfg, nrhs=nrhs, vec=0, row_begin=0, row_end=n)
-    times = []
-    while more(times):
+        self.cfg = cfg
+        self.q, self.n, self.depth, self.fb = oracle_sample(cfg)
+        if cfg.adm:
+            # standard admissibility: a standalone operator of depth L-q with the same
+            # b, r, d (a sub-block is not an H-matrix of the same kind at the boundary)
+            sub = dataclasses.replace(cfg, L=self.depth)
+            self.U, self.V, self.D = hgen.inputs(sub)
+            self.x = hgen.xblock(sub, nrhs=cfg.nrhs)
+        else:
+            q = self.q
+            self.U = [hgen.panel(cfg, hgen.TAG_U, q + l, 0, self.n) for l in range(1, self.depth + 1)]
+            self.V = [hgen.panel(cfg, hgen.TAG_V, q + l, 0, self.n) for l in range(1, self.depth + 1)]
+            self.D = hgen.panel(cfg, hgen.TAG_D, 0, 0, self.n)
+            self.x = hgen.xblock(cfg, nrhs=cfg.nrhs, vec=0, row_begin=0, row_end=self.n)
+
+    def once(self, threads):
+        """Seconds of one oracle matvec over the sample on `threads` host threads
+        (1: the plain block loop; more: its all-cores form, bit-identical)."""
+        from oracle import oracle
+        c = self.cfg
         t0 = time.perf_counter()
-        oracle.matvec(cfg.d, depth, cfg.b, cfg.r, U, V, D, x)
-        times.append(time.perf_counter() - t0)
-    return times
+        if c.adm:
+            oracle.std_matvec(c.d, self.depth, c.b, c.r, self.U, self.V, self.D, self.x)
+        elif threads == 1:
+            oracle.matvec(c.d, self.depth, c.b, c.r, self.U, self.V, self.D, self.x)
+        else:
+            oracle.matvec_par(c.d, self.depth, c.b, c.r, self.U, self.V, self.D, self.x, threads=threads)
+        return time.perf_counter() - t0
+
+    def timed(self, threads, min_seconds, max_reps):
+        times = []
+        while not times or (sum(times) < min_seconds and len(times) < max_reps):
+            times.append(self.once(threads))
+        return times
+
+    def value(self, t):
+        """matvec/s of the whole workload from the seconds of one sample pass."""
+        return (self.fb / t) / self.cfg.factor_bytes
 
 
-def cpu_baseline_record(cfg, budget_bytes=6.5e9, reps=1, min_seconds=10.0):
-    q, n, depth, fb = oracle_sample(cfg, budget_bytes)
-    times = run_oracle_sample(cfg, q, n, depth, reps, cfg.nrhs, min_seconds)
-    reps = len(times)
-    t = float(np.median(times))
-    gbps = fb / t / 1e9
-    per_matvec = cfg.factor_bytes
+def cpu_baseline_record(cfg):
+    """The oracle (as it stands) on the box's host cores, on the bounded sample:
+    all cores (OpenMP block loop; the standard-admissibility oracle is single
+    threaded) and, beside it, the plain one-thread loop."""
+    from oracle import oracle
+    smp = OracleSample(cfg)
+    cores = 1 if cfg.adm else oracle.host_threads()
+    t_all = smp.timed(cores, 8.0, 400)
+    t_one = smp.timed(1, 8.0, 40) if cores > 1 else t_all
+    med_all, med_one = float(np.median(t_all)), float(np.median(t_one))
     return {
-        "value": (fb / t) / per_matvec,
+        "value": smp.value(med_all),
         "unit": "matvec/s",
-        "cores": 1,
+        "cores": cores,
         "kind": "oracle",
         "host_cores_available": len(os.sched_getaffinity(0)),
-        "sample": (f"oracle block loop (1 thread) over the leading level-{q} diagonal sub-H-matrix of {cfg.name} "
-                   f"(rows [0,{n}), levels {q + 1}..{cfg.L} + dense leaves, {fb / 1e9:.2f} GB of factors, "
-                   f"nrhs={cfg.nrhs}), {reps} rep(s), median {t:.2f} s; value = sample factor GB/s / "
-                   f"{per_matvec / 1e9:.2f} GB per full matvec"),
-        "factor_GBps": gbps,
+        "sample": f"{sample_desc(cfg, smp.q, smp.n, smp.depth, smp.fb)}; median of {len(t_all)} passes "
+                  f"({med_all:.3f} s each) on {cores} host thread(s)",
+        "factor_GBps": smp.fb / med_all / 1e9,
+        "one_core": {"value": smp.value(med_one), "cores": 1, "factor_GBps": smp.fb / med_one / 1e9,
+                     "reps": len(t_one), "median_s": med_one},
     }
 
 
+def workload_config(cfg):
+    """The `config` object of both arms (same workload, same keys)."""
+    return {"workload": workload_desc(cfg), "N": cfg.N, "nrhs": cfg.nrhs, "factor_bytes": cfg.factor_bytes,
+            "l2": "working set >> L2 (126 MB) except c1; no flush between steps"}
+
+
 def run_reference(args):
-    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    """--impl reference: the oracle timed on the host cores (rank 0 only), each
+    step one pass over the same bounded sample cpu_baseline uses."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import oracle
     cfg = ALL_CONFIGS[args.config]
-    steps, warm = args.steps, args.warmup
-    # size each step so the whole run stays within ~2-3 minutes at ~1.5 GB/s
-    budget = max(64e6, min(6.5e9, 150e9 / (steps + warm)))
-    q, n, depth, fb = oracle_sample(cfg, budget)
-    times = run_oracle_sample(cfg, q, n, depth, warm + steps, cfg.nrhs)[warm:]
+    smp = OracleSample(cfg)
+    cores = 1 if cfg.adm else oracle.host_threads()
+    times = [smp.once(cores) for _ in range(args.warmup + args.steps)][args.warmup:]
     t = float(np.sum(times))
-    value = steps * fb / t / cfg.factor_bytes
-    cpu = {"value": value, "unit": "matvec/s", "cores": 1, "kind": "oracle",
-           "sample": f"per step: oracle over the leading level-{q} diagonal sub-H-matrix of {cfg.name} "
-                     f"({fb / 1e9:.3f} GB of factors, rows [0,{n})), extrapolated by factor bytes"}
+    value = args.steps * smp.fb / t / cfg.factor_bytes
+    cpu = {"value": value, "unit": "matvec/s", "cores": cores, "kind": "oracle",
+           "sample": f"per step: {sample_desc(cfg, smp.q, smp.n, smp.depth, smp.fb)}; {cores} host thread(s)"}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": args.gpus,
-            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * t / steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "parallelism": "1 host thread"},
-            "cpu_baseline": cpu,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(cfg), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -284,8 +351,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    if local >= torch.cuda.device_count():
+        print(f"error: rank {rank} has LOCAL_RANK {local} but {torch.cuda.device_count()} visible GPU(s)",
+              file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -334,8 +403,16 @@ def run_ours(args):
         h = create(cfg.L, cfg.d, cfg.b, cfg.r, dd)
     r0, r1 = hm.hmat_local_rows(h)
     n = r1 - r0
+    comm_nranks, comm_rank = hm.hmat_comm_info(h)
     hgen.dev_fill_operator(cfg, lambda kind, level: hm.hmat_panel(h, kind, level), r0, r1, sptr)
-    nvec = max(1, min(args.steps + args.warmup, 8))
+    # distinct seeded x per timed step, up to the paper's 128 vectors,
+    # as many as fit in a third of the free device memory (same count on every rank)
+    free, _ = torch.cuda.mem_get_info()
+    nvec = int(max(1, min(128, args.steps, free // 3 // max(1, 8 * n * nrhs))))
+    if world > 1:
+        tv = torch.tensor([nvec], device="cuda")
+        dist.all_reduce(tv, op=dist.ReduceOp.MIN)
+        nvec = int(tv.item())
     X = [torch.empty(nrhs, n, dtype=torch.float64, device="cuda") for _ in range(nvec)]
     for v, xv in enumerate(X):
         hgen.dev_fill_x(cfg, nrhs, v, r0, r1, xv.data_ptr(), n, sptr)
@@ -359,6 +436,7 @@ def run_ours(args):
     for i in range(args.warmup):
         hm.hmat_matvec(h, xs[i % nvec], ys, nrhs)
     torch.cuda.synchronize()
+    hm.hmat_synchronize(h)  # raises on an asynchronous exchange error
 
     # ---------------- timed region (device, CUDA events on the launch stream) ----------
     # The K steps exactly as a user runs them (no per-kernel events: the library then
@@ -382,13 +460,33 @@ def run_ours(args):
         barrier()
         return ev0.elapsed_time(ev1)
 
+    def per_step_times():
+        """The same K steps with an event after each: per-step durations (max over
+        ranks per step) for the median / min / max beside the mean."""
+        barrier()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for i in range(args.steps):
+            hm.hmat_matvec(h, xs[i % nvec], ys, nrhs)
+            evs[i + 1].record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)], dtype=torch.float64,
+                         device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        barrier()
+        return t.cpu().numpy()
+
     ms_local = timed_steps()
+    step_ms = per_step_times()
     hm.hmat_profile(h, True)
     hm.hmat_profile_read(h)  # reset
     ms_profiled = timed_steps()
     prof = hm.hmat_profile_read(h)
     hm.hmat_profile(h, False)
     clk = clocks.stop()
+    hm.hmat_synchronize(h)  # raises on an asynchronous exchange error
     ms_total = max_over_ranks(ms_local)
     ms_step = ms_total / args.steps
     ms_prof_step = max_over_ranks(ms_profiled) / args.steps  # (collective: every rank)
@@ -475,6 +573,11 @@ def run_ours(args):
                 "read_stream_source": "scripts/hbm_read_peak.cu sustained bulk-TMA read ring (profiles/r01_hbm_read_peak.txt)"}
 
     value = 1e3 / ms_step  # matvecs/s of the whole job (one operator across all ranks)
+    # every rank's communicator spans the whole job (NCCL's own count for NCCL / TREE)
+    cn = torch.tensor([comm_nranks], device="cuda")
+    if world > 1:
+        dist.all_reduce(cn, op=dist.ReduceOp.MIN)
+    comm_nranks_ok = int(cn.item()) == world and comm_nranks == world
     factor_gbps = alg_bytes(cfg, cfg.N, nrhs)["factor"] / (ms_step * 1e-3) / 1e9
     if rank == 0:
         cpu = None
@@ -484,10 +587,14 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "matvec/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_desc(cfg), "N": cfg.N, "nrhs": nrhs,
-                       "factor_bytes": cfg.factor_bytes, "parallelism": f"subtree shards x{world} (Morton rows)",
-                       "l2": "working set 1000x L2; no flush needed", "distinct_x": nvec,
-                       "exchange": exchange},
+            "config": workload_config(cfg),
+            "parallelism": f"Morton-row subtree shards x{world}, one rank per GPU",
+            "exchange": exchange, "comm_nranks": comm_nranks, "comm_nranks_ok": bool(comm_nranks_ok),
+            "distinct_x": nvec,
+            "step_ms": {"mean": float(step_ms.mean()), "median": float(np.median(step_ms)),
+                        "min": float(step_ms.min()), "max": float(step_ms.max()), "n": int(len(step_ms)),
+                        "how": "a second pass of the K steps with a CUDA event after each step, max over ranks "
+                               f"per step; {nvec} distinct seeded x (PAPER.md:1129-1130 averages 128)"},
             "factor_GBps": factor_gbps,
             "alg_GBps": ab["total"] * world / (ms_step * 1e-3) / 1e9,
             "roofline": roof,
@@ -508,7 +615,15 @@ def run_ours(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1 and args.impl == "ours":
+        sys.exit(self_launch(args))     # one rank per GPU under torch.distributed.run
+    if world is not None and int(world) != args.gpus:
+        print(f"error: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.launcher_check:
+        launcher_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

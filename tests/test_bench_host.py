@@ -63,3 +63,46 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["workload"].startswith("c1")
+
+
+def _clean_env():
+    return {k: v for k, v in os.environ.items()
+            if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR", "MASTER_PORT")}
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_gpus_n_starts_n_ranks(n):
+    """`python bench.py --gpus N` outside torch.distributed re-executes itself
+    under torch.distributed.run with N ranks: every rank sees WORLD_SIZE = N
+    and ranks 0..N-1 all report (gloo, host only)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--launcher-check"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=_clean_env())
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["launcher_check"] and line["gpus"] == n and line["world"] == n
+    assert line["ranks"] == list(range(n)) and line["worlds"] == [n]
+
+
+def test_world_size_mismatch_is_an_error():
+    """Under a launcher whose world differs from --gpus, bench.py refuses (rc 2)
+    instead of silently measuring another GPU count."""
+    env = _clean_env()
+    env.update(WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--launcher-check"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE=2" in out.stderr
+
+
+def test_reference_arm_same_config_and_sample_as_cpu_baseline():
+    """Both CPU-oracle legs use one sample of the workload, and the reference
+    arm's `config` is exactly the GPU arm's (same keys and values)."""
+    cfg = CONFIGS["c4"]
+    q, n, depth, fb = bench.oracle_sample(cfg)
+    assert (q, n, depth) == (3, cfg.N // 64, 6) and fb <= bench.SAMPLE_BYTES
+    assert bench.workload_config(cfg)["factor_bytes"] == cfg.factor_bytes
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "1", "--config", "c2"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["config"] == json.loads(json.dumps(bench.workload_config(CONFIGS["c2"])))
+    assert "leading level-1 diagonal sub-H-matrix of c2" in line["cpu_baseline"]["sample"]
