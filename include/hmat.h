@@ -208,6 +208,20 @@ hmat_status hmat_create_standard(int depth, int dim, int leaf_size, int rank, co
 hmat_status hmat_create_standard_uninit(int depth, int dim, int leaf_size, int rank, const hmat_dist_t* dist,
                                         hmat_t* out);
 
+/* Standard admissibility with Def 2.4 read LITERALLY (the
+ * three conditions "in the given order", leaf first; the literal alternative to
+ * hmat_create_standard's reading, R17): at the leaf level every child
+ * pair of two touching leaf-parents is dense (near field AND the leaf-level
+ * interaction list), low-rank blocks exist at levels 2..depth-1.  U, V: depth-1
+ * canonical standard panels (levels 1..depth-1); Dc: N_loc x (3^dim 2^dim
+ * leaf_size): row i of leaf-parent p, columns [e 2^dim b, (e+1) 2^dim b) = row
+ * i - p 2^dim b of the dense block of (p, p + eps), e = sum_i (eps_i + 1) 3^i.
+ * This is the structure of hmat_create_standard(depth - 1, dim, 2^dim leaf_size,
+ * ...) and is built as such (same envelope and errors); depth >= 1. */
+hmat_status hmat_create_standard_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                                        const double* const* V, const double* Dc, const hmat_dist_t* dist,
+                                        hmat_t* out);
+
 /* The paper-strict reading of Def 2.4 (conditions checked in
  * order, "leaf" first): every child pair of a leaf-parent is dense, so each
  * leaf-parent diagonal block (2^dim leaf_size square) is dense and low-rank

@@ -786,6 +786,146 @@ void oracle_std_matvec_t(int d, int L, int b, int r, const double* const* U, con
   free(mv.z);
 }
 
+/* ---- standard admissibility, Def 2.4 read LITERALLY (leaf check first) ------
+ * PAPER.md:316-339 checks the three conditions "in the given order": (1) a child
+ * pair with a leaf is dense, (2) else an admissible pair is low rank, (3) else
+ * recurse.  So at the leaf level EVERY child pair of a hierarchical (touching)
+ * parent pair is dense -- the near field AND the leaf-level interaction list --
+ * and low-rank blocks exist at levels 2..L-1 only.  (R17 checks
+ * admissibility first, like R1 for the weak structure; this is the literal
+ * alternative, SURVEY §8 f3 with the f2 reading.)
+ * Panels: U, V as the standard canonical panels (levels 1..L-1 used); the dense
+ * blocks of leaf-parent p (level L-1) against its neighbour p + eps form one
+ * (c b) x (c b) block, stored like the standard near field one level up:
+ *   Dc (N x 3^d c b): row i of leaf-parent p, columns [e c b, (e+1) c b) = row
+ *   i - p c b of the dense block of (p, p + eps), e = sum_i (eps_i + 1) 3^i;
+ *   the leaf pair (t, s), t in p, s in p + eps, is its sub-block at column
+ *   offset (s - c (p + eps)) b. */
+static void visit_std_strict(int d, int L, int level, int64_t pt, int64_t ps, block_fn fn, void* ctx) {
+  const int c = 1 << d;
+  for (int a = 0; a < c; ++a)
+    for (int bb = 0; bb < c; ++bb) {
+      int64_t t = pt * c + a, s = ps * c + bb;
+      int64_t xt[3], xs[3];
+      morton_decode(d, t, level + 1, xt);
+      morton_decode(d, s, level + 1, xs);
+      if (level + 1 == L) fn(ctx, 0, level + 1, t, s);                 /* (1) leaves: dense */
+      else if (std_admissible(d, xt, xs)) fn(ctx, 1, level + 1, t, s); /* (2) admissible: low rank */
+      else visit_std_strict(d, L, level + 1, t, s, fn, ctx);          /* (3) hierarchical */
+    }
+}
+
+static void visit_root_std_strict(int d, int L, block_fn fn, void* ctx) {
+  if (L == 0) fn(ctx, 0, 0, 0, 0);
+  else visit_std_strict(d, L, 0, 0, 0, fn, ctx);
+}
+
+void oracle_std_census_strict(int d, int L, int64_t* n_lowrank, int64_t* n_dense) {
+  std_census_t cs = {0, 0, -1, -1, 0};
+  visit_root_std_strict(d, L, std_census_cb, &cs);
+  *n_lowrank = cs.lowrank; *n_dense = cs.dense;
+}
+
+void oracle_std_cover_count_strict(int d, int L, int b, int32_t* count) {
+  cover_t cv;
+  cv.c = 1 << d; cv.L = L; cv.b = b; cv.N = (int64_t)b * ipow(cv.c, L); cv.count = count;
+  memset(count, 0, sizeof(int32_t) * (size_t)(cv.N * cv.N));
+  visit_root_std_strict(d, L, cover_cb, &cv);
+}
+
+/* column of entry (row of t, column j of s) of a leaf pair in the Dc panel */
+static int64_t std_strict_dcol(int d, int L, int b, int64_t t, int64_t s, int j) {
+  const int c = 1 << d;
+  if (L == 0) return j; /* the root is the only leaf: Dc is N x b */
+  const int64_t pt = t / c, ps = s / c;
+  const int e = std_neighbour_index(d, pt, ps, L - 1);
+  return (int64_t)e * c * b + (s - ps * c) * b + j;
+}
+
+typedef struct {
+  int d, L, b, r, M, ND, nrhs, c; int64_t N, ldd;
+  const double* const* U; const double* const* V; const double* Dc; const double* x; double* y; double* z;
+  double* A;
+} std_strict_t;
+
+static void std_strict_assemble_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_strict_t* as = (std_strict_t*)ctx;
+  const int64_t N = as->N;
+  if (kind == 0) {
+    for (int i = 0; i < as->b; ++i)
+      for (int j = 0; j < as->b; ++j)
+        as->A[(t * as->b + i) * N + (s * as->b + j)] =
+            as->Dc[(t * as->b + i) * as->ldd + std_strict_dcol(as->d, as->L, as->b, t, s, j)];
+    return;
+  }
+  const int64_t m = N / ipow(as->c, level);
+  const int qt = oracle_std_slot(as->d, level, t, s), qs = oracle_std_slot(as->d, level, s, t);
+  const int W = as->M * as->r;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < m; ++j) {
+      double acc = 0.0;
+      for (int a = 0; a < as->r; ++a)
+        acc += as->U[level - 1][(t * m + i) * W + qt * as->r + a] * as->V[level - 1][(s * m + j) * W + qs * as->r + a];
+      as->A[(t * m + i) * N + (s * m + j)] = acc;
+    }
+}
+
+static void std_strict_init(std_strict_t* st, int d, int L, int b, int r, const double* const* U,
+                            const double* const* V, const double* Dc) {
+  st->d = d; st->L = L; st->b = b; st->r = r; st->c = 1 << d;
+  st->M = oracle_std_slots(d); st->ND = (int)ipow(3, d);
+  st->N = (int64_t)b * ipow(st->c, L);
+  st->ldd = L == 0 ? b : (int64_t)st->ND * st->c * b;
+  st->U = U; st->V = V; st->Dc = Dc;
+}
+
+void oracle_std_assemble_strict(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                                const double* Dc, double* A) {
+  std_strict_t as;
+  std_strict_init(&as, d, L, b, r, U, V, Dc);
+  as.A = A;
+  memset(A, 0, sizeof(double) * (size_t)(as.N * as.N));
+  visit_root_std_strict(d, L, std_strict_assemble_cb, &as);
+}
+
+/* y = H x, eq:hmat-vec-add over the literal-order blocks */
+static void std_strict_mv_cb(void* ctx, int kind, int level, int64_t t, int64_t s) {
+  std_strict_t* mv = (std_strict_t*)ctx;
+  const int64_t N = mv->N;
+  for (int k = 0; k < mv->nrhs; ++k) {
+    const double* xk = mv->x + (int64_t)k * N;
+    double* yk = mv->y + (int64_t)k * N;
+    if (kind == 0) { /* y_t += D_ts x_s */
+      for (int i = 0; i < mv->b; ++i)
+        for (int j = 0; j < mv->b; ++j)
+          yk[t * mv->b + i] += mv->Dc[(t * mv->b + i) * mv->ldd + std_strict_dcol(mv->d, mv->L, mv->b, t, s, j)] *
+                               xk[s * mv->b + j];
+      continue;
+    }
+    const int64_t m = N / ipow(mv->c, level);
+    const int qt = oracle_std_slot(mv->d, level, t, s), qs = oracle_std_slot(mv->d, level, s, t);
+    const int W = mv->M * mv->r;
+    const double* Ul = mv->U[level - 1];
+    const double* Vl = mv->V[level - 1];
+    for (int a = 0; a < mv->r; ++a) mv->z[a] = 0.0;
+    for (int64_t j = 0; j < m; ++j)   /* z = V_ts^T x_s */
+      for (int a = 0; a < mv->r; ++a) mv->z[a] += Vl[(s * m + j) * W + qs * mv->r + a] * xk[s * m + j];
+    for (int64_t i = 0; i < m; ++i)   /* y_t += U_ts z */
+      for (int a = 0; a < mv->r; ++a) yk[t * m + i] += Ul[(t * m + i) * W + qt * mv->r + a] * mv->z[a];
+  }
+}
+
+void oracle_std_matvec_strict(int d, int L, int b, int r, const double* const* U, const double* const* V,
+                              const double* Dc, const double* x, double* y, int nrhs) {
+  std_strict_t mv;
+  std_strict_init(&mv, d, L, b, r, U, V, Dc);
+  mv.nrhs = nrhs; mv.x = x; mv.y = y;
+  mv.z = (double*)malloc(sizeof(double) * (size_t)(r > 0 ? r : 1));
+  for (int64_t i = 0; i < mv.N * nrhs; ++i) y[i] = 0.0;
+  visit_root_std_strict(d, L, std_strict_mv_cb, &mv);
+  free(mv.z);
+}
+
 /* Sampled rows of the SEEDED standard-admissibility operator (gen/hgen.h, the
  * canonical standard panels above, entries generated on demand), so that full
  * bench-size operators (s2: 55.6 GB of factors) can be checked row by row:

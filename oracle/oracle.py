@@ -268,6 +268,14 @@ def _std_lib():
         lib.oracle_std_matvec_t.argtypes = lib.oracle_std_matvec.argtypes
         lib.oracle_std_rows_generated.restype = None
         lib.oracle_std_rows_generated.argtypes = lib.oracle_rows_generated.argtypes
+        lib.oracle_std_census_strict.restype = None
+        lib.oracle_std_census_strict.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.POINTER(ctypes.c_int64)] * 2
+        lib.oracle_std_cover_count_strict.restype = None
+        lib.oracle_std_cover_count_strict.argtypes = lib.oracle_std_cover_count.argtypes
+        lib.oracle_std_assemble_strict.restype = None
+        lib.oracle_std_assemble_strict.argtypes = lib.oracle_std_assemble.argtypes
+        lib.oracle_std_matvec_strict.restype = None
+        lib.oracle_std_matvec_strict.argtypes = lib.oracle_std_matvec.argtypes
         lib._std_ready = True
     return lib
 
@@ -315,6 +323,36 @@ def std_matvec_t(d: int, L: int, b: int, r: int, U, V, Dn, x) -> np.ndarray:
     """y = H^T x by the transposed standard-admissibility block loop."""
     _std_lib()
     return _mv(_load().oracle_std_matvec_t, d, L, b, r, U, V, Dn, x)
+
+
+def std_census_strict(d: int, L: int):
+    """(#low-rank, #dense) blocks of the literal-order (leaf-first) standard structure."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _std_lib().oracle_std_census_strict(d, L, ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
+
+
+def std_cover_count_strict(d: int, L: int, b: int) -> np.ndarray:
+    N = b * (1 << d) ** L
+    out = np.zeros((N, N), dtype=np.int32)
+    _std_lib().oracle_std_cover_count_strict(d, L, b, out.ctypes.data)
+    return out
+
+
+def std_assemble_strict(d: int, L: int, b: int, r: int, U, V, Dc) -> np.ndarray:
+    N = b * (1 << d) ** L
+    A = np.zeros((N, N), dtype=np.float64)
+    ua, up = _panel_ptrs(U)
+    va, vp = _panel_ptrs(V)
+    Dc = _c(Dc)
+    _std_lib().oracle_std_assemble_strict(d, L, b, r, up, vp, Dc.ctypes.data, A.ctypes.data)
+    return A
+
+
+def std_matvec_strict(d: int, L: int, b: int, r: int, U, V, Dc, x) -> np.ndarray:
+    """y = H x for the literal-order (leaf-first) standard structure."""
+    _std_lib()
+    return _mv(_load().oracle_std_matvec_strict, d, L, b, r, U, V, Dc, x)
 
 
 def std_rows_generated(cfg, x, rows) -> np.ndarray:

@@ -68,6 +68,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.pdl = env_int("HMAT_PDL", 2);
   o.lpar = env_int("HMAT_PROJECT_LPAR", 1);
+  o.early = env_int("HMAT_PROJECT_EARLY", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
@@ -754,6 +755,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.zex_base = H->zex;
   a.dbg = p.dbg;
   a.snake = p.snake;
+  a.early = p.early;
   // PDL (expand's launch and prologue overlap project's tail) for whole products;
   // off while the per-kernel profiler brackets the kernels with events
   // and the CTA trace (its memsets sit between the kernels)
@@ -1043,6 +1045,20 @@ hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, cons
   if (dim < 1 || dim > 3) return fail(HMAT_ERR_INVALID, "dim must be 1, 2 or 3 (ideal domains, PAPER.md:243-246)");
   if (leaf_size < 1 || leaf_size > (1 << 28)) return fail(HMAT_ERR_INVALID, "leaf_size must be >= 1");
   return hmat_create(depth - 1, dim, leaf_size << dim, rank, U, V, Dc, dist, out);
+}
+
+hmat_status hmat_create_standard_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
+                                        const double* const* V, const double* Dc, const hmat_dist_t* dist,
+                                        hmat_t* out) {
+  // Def 2.4 read literally under standard admissibility: at the leaf level every
+  // child pair of two touching leaf-parents is dense, low-rank blocks exist at
+  // levels 2..depth-1 -- the standard structure of depth-1 with leaf 2^dim leaf_size
+  // (its near field = the touching leaf-parents' (2^dim b)^2 blocks).
+  if (out) *out = nullptr;
+  if (depth < 1) return fail(HMAT_ERR_INVALID, "strict structure needs depth >= 1");
+  if (dim < 1 || dim > 3) return fail(HMAT_ERR_INVALID, "dim must be 1, 2 or 3 (ideal domains, PAPER.md:243-246)");
+  if (leaf_size < 1 || leaf_size > (1 << 28)) return fail(HMAT_ERR_INVALID, "leaf_size must be >= 1");
+  return hmat_create_standard(depth - 1, dim, leaf_size << dim, rank, U, V, Dc, dist, out);
 }
 
 hmat_status hmat_destroy(hmat_t H) {

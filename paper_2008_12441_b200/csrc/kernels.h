@@ -83,6 +83,7 @@ struct StreamArgs {
   unsigned int* done;        // project CTAs finished (last one pushes)
   unsigned int* err;         // host-mapped error word: a flag wait that timed out (peer.cuh)
   int64_t peer_timeout_ns;   // bound on a flag wait (HMAT_PEER_TIMEOUT_MS)
+  int early;                 // project: release a ring slot before the FMAs (HMAT_PROJECT_EARLY)
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
   int64_t exch;              // doubles of this pass's exchange levels
   int cross;                 // levels 1..cross are exchange levels

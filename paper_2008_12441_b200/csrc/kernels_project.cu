@@ -35,6 +35,7 @@ namespace {
 
 constexpr int CT = kConsumerThreads;
 constexpr int NCW = CT / 32;
+constexpr int kEarlyRows = 7;  // rows per consumer thread and stage on the early-release path
 
 // CTA owning stage k under the even split [S b / G, S (b+1) / G).
 __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { return ((k + 1) * G - 1) / S; }
@@ -241,6 +242,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   const int rho = PAIRS == 1 ? t / NP : 0;
   const int cp0 = PAIRS == 1 ? t - rho * NP : t;
   const bool active = PAIRS == 1 ? rho < RG : true;
+  // single rhs, one column pair per thread, at most 8 rows per thread per stage:
+  // the early-release path (a.early, HMAT_PROJECT_EARLY)
+  const bool early = NR == 1 && PAIRS == 1 && a.early && Rp <= kEarlyRows * RG;
   const int64_t red_elems = (int64_t)RG * Wp * NR;  // one of two alternating buffers
   double* red_base = reinterpret_cast<double*>(smem + a.red_off_p);
   int64_t* nbr_base = reinterpret_cast<int64_t*>(smem + a.bar_off_p + 256);  // 2 x 32 entries
@@ -299,7 +303,29 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       int xo[NR];
 #pragma unroll
       for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
-      if (active && !(a.dbg & 1)) {
+      if (NR == 1 && PAIRS == 1 && early) {
+        // early release: the thread's rows of the stage (<= kEarlyRows) go to
+        // registers, the slot is handed back to the producer, then the FMAs run --
+        // the ring slot is held for the shared-memory loads only, not for the math
+        double2 v[kEarlyRows];
+        double xv[kEarlyRows];
+#pragma unroll
+        for (int i = 0; i < kEarlyRows; ++i) {
+          const int row = min(rho + i * RG, Rp - 1);  // clamped: in-bounds, unused beyond Rp
+          v[i] = V2[row * NP + cp0];
+          xv[i] = xs[xo[0] + row];
+        }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&empty[slot]);
+        if (active && !(a.dbg & 1)) {
+#pragma unroll
+          for (int i = 0; i < kEarlyRows; ++i) {
+            const double xi = rho + i * RG < Rp ? xv[i] : 0.0;
+            acc[0][0].x = fma(v[i].x, xi, acc[0][0].x);
+            acc[0][0].y = fma(v[i].y, xi, acc[0][0].y);
+          }
+        }
+      } else if (active && !(a.dbg & 1)) {
 #pragma unroll 4
         for (int row = rho; row < Rp; row += RG) {
           double xv[NR];
@@ -319,8 +345,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      if (!(NR == 1 && PAIRS == 1 && early)) {
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      }
       if (++slot == NS) {
         slot = 0;
         phase ^= 1;

@@ -77,6 +77,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.snake = opt.snake;
   p.pdl = opt.pdl;
   p.lpar = opt.lpar;
+  p.early = opt.early;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;

@@ -28,6 +28,7 @@ PHASES = ("project", "exchange", "expand", "copies")
 
 # Every symbol include/hmat.h declares (checked by tests/test_abi.py).
 EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_create_standard",
+           "hmat_create_standard_strict",
            "hmat_create_standard_uninit", "hmat_panel", "hmat_matvec", "hmat_gemv",
            "hmat_exchange_size", "hmat_project", "hmat_expand", "hmat_matvec_parts", "hmat_destroy",
            "hmat_last_error", "hmat_num_points", "hmat_local_rows", "hmat_set_stream", "hmat_nccl_unique_id",
@@ -83,6 +84,7 @@ _sigs = {
     "hmat_gemv": (_i, [_H, _i, ctypes.c_double, _P, ctypes.c_double, _P, _i]),
     "hmat_create_strict": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
     "hmat_create_standard": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
+    "hmat_create_standard_strict": (_i, [_i, _i, _i, _i, _P, _P, _P, _P, ctypes.POINTER(_H)]),
     "hmat_create_standard_uninit": (_i, [_i, _i, _i, _i, _P, ctypes.POINTER(_H)]),
     "hmat_exchange_size": (_i, [_H, _i, ctypes.POINTER(_i64)]),
     "hmat_project": (_i, [_H, _P, _i, _P]),
@@ -214,6 +216,19 @@ def hmat_create_standard(depth, dim, leaf_size, rank, U, V, Dn, dist: hmat_dist_
     _check(_lib.hmat_create_standard(depth, dim, leaf_size, rank, ctypes.cast(Up, _P), ctypes.cast(Vp, _P),
                                      _ptr(Dn), ctypes.byref(dist) if dist is not None else None, ctypes.byref(h)),
            "hmat_create_standard")
+    return h
+
+
+def hmat_create_standard_strict(depth, dim, leaf_size, rank, U, V, Dc, dist: hmat_dist_t | None = None):
+    """Standard admissibility with Def 2.4 read literally (leaf first): U, V = depth-1
+    standard panels, Dc = N x (3^dim 2^dim leaf) leaf-parent near-field panel."""
+    Up = (ctypes.c_void_p * max(1, len(U)))(*[_ptr(u) for u in U])
+    Vp = (ctypes.c_void_p * max(1, len(V)))(*[_ptr(v) for v in V])
+    h = _H()
+    _check(_lib.hmat_create_standard_strict(depth, dim, leaf_size, rank, ctypes.cast(Up, _P), ctypes.cast(Vp, _P),
+                                            _ptr(Dc), ctypes.byref(dist) if dist is not None else None,
+                                            ctypes.byref(h)),
+           "hmat_create_standard_strict")
     return h
 
 

@@ -20,10 +20,17 @@ from paper_2008_12441_b200 import hmat as hm  # noqa: E402
 def run(cfg, setting, reps=10):
     import dataclasses
     keys = []
+    warm = 3
     for kv in filter(None, setting.split(",")):
         k, v = kv.split("=")
         if k == "NRHS":  # override the config's right-hand-side count
             cfg = dataclasses.replace(cfg, nrhs=int(v))
+            continue
+        if k == "REPS":  # timed matvecs
+            reps = int(v)
+            continue
+        if k == "WARM":  # untimed matvecs first (e.g. enough to reach the sustained power cap)
+            warm = int(v)
             continue
         os.environ[k] = v
         keys.append(k)
@@ -37,7 +44,7 @@ def run(cfg, setting, reps=10):
         hgen.dev_fill_x(cfg, cfg.nrhs, 0, r0, r1, x.data_ptr(), n, 0)
         y = torch.empty_like(x)
         torch.cuda.synchronize()
-        for _ in range(3):
+        for _ in range(warm):
             hm.hmat_matvec(h, x.t(), y.t(), cfg.nrhs)
         hm.hmat_profile(h, True)
         hm.hmat_profile_read(h)

@@ -174,3 +174,29 @@ def test_s2_full_size_sampled_rows():
     finally:
         hm.hmat_destroy(h)
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("d,L,b,r,nrhs", [(2, 4, 4, 2, 1), (2, 3, 16, 4, 3), (1, 6, 8, 3, 2), (3, 3, 2, 1, 1),
+                                          (2, 5, 16, 8, 1)])
+def test_standard_literal_order_parity(d, L, b, r, nrhs):
+    """hmat_create_standard_strict (Def 2.4 checked leaf first under standard
+    admissibility) vs the literal-order oracle block loop, for H and H^T."""
+    c = 1 << d
+    N = b * c ** L
+    rng = np.random.default_rng(1000 + 10 * d + L)
+    M = 6 ** d - 3 ** d
+    U = [rng.standard_normal((N, M * r)) / 8 for _ in range(L - 1)]
+    V = [rng.standard_normal((N, M * r)) / 8 for _ in range(L - 1)]
+    Dc = rng.standard_normal((N, 3 ** d * c * b)) / 8
+    x = rng.uniform(-1, 1, (N, nrhs))
+    h = hm.hmat_create_standard_strict(L, d, b, r, U, V, Dc)
+    try:
+        y = np.zeros((N, nrhs), order="F")
+        hm.hmat_matvec(h, np.asfortranarray(x), y, nrhs)
+        assert_parity(y, oracle.std_matvec_strict(d, L, b, r, U, V, Dc, x))
+        yt = np.zeros((N, nrhs), order="F")
+        hm.hmat_gemv(h, 1, 1.0, np.asfortranarray(x), 0.0, yt, nrhs)
+        A = oracle.std_assemble_strict(d, L, b, r, U, V, Dc)
+        assert_parity(yt, A.T @ x)
+    finally:
+        hm.hmat_destroy(h)

@@ -287,3 +287,60 @@ def test_std_slot_order_rederived_from_the_header(d, level):
         assert q == M
         for s in range(n ** d):
             assert oracle.std_slot(d, level, t, s) == expect.get(s, -1), (t, s)
+
+
+# ---- Def 2.4 read literally (leaf check first) under standard admissibility ----
+
+def _std_counts_closed_form(d, L, strict):
+    """Ordered box pairs per level, from the geometry alone: with n = 2^l boxes
+    per side, pairs whose parents touch number ((3 n/2 - 2) 4)^d and touching
+    pairs (3 n - 2)^d (per dimension 3k - 2 ordered pairs of positions within
+    one step among k, then 2 x 2 children per parent pair; dimensions multiply).
+    Low rank at level l = parents touch but the boxes do not (eq:standard-ad-cond
+    with rho = sqrt(d) on an ideal domain).  Dense blocks: the touching leaf
+    pairs (R17), or -- leaf checked first -- every leaf pair whose parents touch."""
+    def par(l):
+        return ((3 * 2 ** (l - 1) - 2) * 4) ** d
+
+    def touch(l):
+        return (3 * 2 ** l - 2) ** d
+    if L == 0:
+        return 0, 1
+    last = L - 1 if strict else L
+    lowrank = sum(par(l) - touch(l) for l in range(2, last + 1))
+    dense = par(L) if strict else touch(L)
+    return lowrank, dense
+
+
+@pytest.mark.parametrize("d,L", [(1, 1), (1, 4), (1, 7), (2, 1), (2, 2), (2, 3), (2, 5), (3, 2), (3, 3)])
+def test_std_census_closed_forms(d, L):
+    """Block counts by walking Def 2.4 (both orders) vs the closed forms."""
+    assert oracle.std_census(d, L)[:2] == _std_counts_closed_form(d, L, strict=False)
+    assert oracle.std_census_strict(d, L) == _std_counts_closed_form(d, L, strict=True)
+
+
+@pytest.mark.parametrize("d,L,b", [(1, 4, 2), (2, 3, 1), (2, 2, 3), (3, 2, 1)])
+def test_std_strict_tiles_exactly_once(d, L, b):
+    assert np.all(oracle.std_cover_count_strict(d, L, b) == 1)
+
+
+@pytest.mark.parametrize("d,L,b,r", [(1, 5, 2, 2), (2, 3, 2, 1), (2, 4, 1, 2), (3, 2, 1, 1), (2, 1, 3, 2)])
+def test_std_strict_block_loop_equals_brute_force_and_coarse_structure(d, L, b, r):
+    """The literal-order block loop = A x of its assembled matrix; and the
+    literal-order structure of depth L, leaf b IS the R17 structure of depth
+    L - 1, leaf 2^d b on the same panels (the leaf-level blocks of two touching
+    parents tile the parents' near-field block): the two recursions assemble
+    the same matrix entry for entry."""
+    c = 1 << d
+    U, V, _ = std_panels(d, L - 1, c * b, r, 40 + 3 * d + L)
+    N = b * c ** L
+    Dc = np.random.default_rng(41 + L).standard_normal((N, 3 ** d * c * b))
+    A = oracle.std_assemble_strict(d, L, b, r, U, V, Dc)
+    assert np.array_equal(A, oracle.std_assemble(d, L - 1, c * b, r, U, V, Dc))
+    x = np.random.default_rng(42).standard_normal((N, 2))
+    assert rel(oracle.std_matvec_strict(d, L, b, r, U, V, Dc, x), A @ x) < 1e-13
+    # the leaf level holds interaction-list pairs as dense blocks: more dense
+    # entries than the R17 structure of the same depth and leaf
+    lr_s, dn_s = oracle.std_census_strict(d, L)
+    lr, dn = oracle.std_census(d, L)[:2]
+    assert dn_s >= dn and lr_s <= lr and (L < 2 or dn_s > dn)
