@@ -198,10 +198,11 @@ hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double
  * hmat_gemv(trans = 1) applies H^T (the interaction relation is symmetric, so
  * U and V swap roles; the near-field panels of H^T, (D_{t+eps,t})^T, are built
  * once on the first transposed call: 3^dim N leaf_size more doubles).
- * nranks > 1 is supported with the NCCL, TREE and EXTERNAL exchanges: the
- * cross-rank pairs along the slice boundaries and the near-field halo travel in
- * one packed buffer (hmat_std_exchange_query).  Not
- * supported (HMAT_ERR_UNSUPPORTED): the PEER exchange.  M rank <= 1024.
+ * nranks > 1 is supported with the NCCL, TREE and EXTERNAL exchanges, for H
+ * and H^T: the cross-rank pairs along the slice boundaries and the near-field
+ * halo (x for H, the products (D_{S,T})^T x_S for H^T) travel in one packed
+ * buffer (hmat_std_exchange_query).  Not supported
+ * (HMAT_ERR_UNSUPPORTED): the PEER exchange.  M rank <= 1024.
  * hmat_panel(kind 2, level e) returns dense panel e. */
 hmat_status hmat_create_standard(int depth, int dim, int leaf_size, int rank, const double* const* U,
                                  const double* const* V, const double* Dn, const hmat_dist_t* dist, hmat_t* out);
@@ -255,6 +256,17 @@ hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, cons
 hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count);
 hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange);
 hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, double* y, int nrhs);
+
+/* The split-phase form of the GEMV y = alpha op(H) x + beta y,
+ * op = H (trans = 0: exactly the three calls above) or H^T (trans = 1; with
+ * standard admissibility and P > 1 the buffer's second part carries the
+ * products (D_{S,T})^T x_S of the cross-rank near-field pairs instead of halo
+ * x, and hmat_expand_op adds the incoming ones after its kernel).  Same rules
+ * and errors as above; HMAT_ERR_INVALID for trans not in {0, 1}. */
+hmat_status hmat_exchange_size_op(hmat_t H, int trans, int nrhs, int64_t* count);
+hmat_status hmat_project_op(hmat_t H, int trans, const double* x, int nrhs, double* exchange);
+hmat_status hmat_expand_op(hmat_t H, int trans, double alpha, const double* x, const double* exchange, double beta,
+                           double* y, int nrhs);
 
 /* PEER exchange set-up (the fused Steps 2-4, over NVLink
  * peer memory; collective in spirit: every rank must connect before the first
@@ -415,7 +427,14 @@ hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nra
  *   unpack     pairs {entry, Zt row * 256 + slot}: entries of this rank's targets,
  *              Zt row = zt_row_offset[l] + target - first local node of level l;
  *   pack       pairs {halo index, local leaf}: this rank's leaves others need;
- *   halo_of    [local leaf][3^dim]: halo index of near-field neighbour e, or -1. */
+ *   halo_of    [local leaf][3^dim]: halo index of near-field neighbour e, or -1.
+ * H^T (the second part holds [Hp pairs][cap][bpad] products instead of halo x):
+ *   Hp         cross near-field pairs (S, T), owner(S) != owner(T), numbered over
+ *              leaves S in Morton order, then neighbour e (T = S + eps_e);
+ *   tpack      triples {pair, local leaf S, e}: this rank's outgoing pairs, whose
+ *              product (D_{S,T})^T x_S it writes;
+ *   tadd_leaf / tadd_off / tadd_pair  CSR of this rank's leaves T with incoming
+ *              pairs (local leaf, offsets, ascending pair indices). */
 typedef struct {
   int64_t E, Hn;
   int bpad, M;
@@ -424,6 +443,11 @@ typedef struct {
   int64_t* unpack;    int64_t unpack_cap, n_unpack;
   int64_t* pack;      int64_t pack_cap, n_pack;
   int32_t* halo_of;   int64_t halo_of_cap, n_halo_of;
+  int64_t Hp;
+  int64_t* tpack;     int64_t tpack_cap, n_tpack;
+  int64_t* tadd_leaf; int64_t tadd_leaf_cap, n_tadd_leaf;
+  int64_t* tadd_off;  int64_t tadd_off_cap, n_tadd_off;
+  int64_t* tadd_pair; int64_t tadd_pair_cap, n_tadd_pair;
 } hmat_std_exchange_t;
 hmat_status hmat_std_exchange_query(int depth, int dim, int leaf_size, int rank, int nranks, int rank_id,
                                     hmat_std_exchange_t* q);

@@ -65,10 +65,13 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
+  o.project_chunk = env_int("HMAT_PROJECT_CHUNK", 4);
   o.snake = env_int("HMAT_PROJECT_SNAKE", 1);
   o.pdl = env_int("HMAT_PDL", 2);
   o.lpar = env_int("HMAT_PROJECT_LPAR", 1);
   o.early = env_int("HMAT_PROJECT_EARLY", 1);
+  o.dmma_ileave = env_int("HMAT_DMMA_ILEAVE", 1);
+  o.aflush = env_int("HMAT_PROJECT_AFLUSH", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
@@ -147,6 +150,10 @@ struct hmat_s {
   int64_t* unpack_d = nullptr;
   int64_t* pack_d = nullptr;
   int32_t* halo_of_d = nullptr;
+  int64_t* tpack_d = nullptr;   // H^T, P > 1: outgoing cross near-field pairs
+  int64_t* tadd_leaf_d = nullptr;
+  int64_t* tadd_off_d = nullptr;
+  int64_t* tadd_pair_d = nullptr;
   bool external = false;  // P > 1 with a caller-provided exchange (split-phase API)
   // HMAT_EXCHANGE_TREE: recursive doubling over NCCL point-to-point; scratch buffer
   bool tree = false;
@@ -216,6 +223,10 @@ void release(hmat_s* H) {
   cudaFree(H->unpack_d);
   cudaFree(H->pack_d);
   cudaFree(H->halo_of_d);
+  cudaFree(H->tpack_d);
+  cudaFree(H->tadd_leaf_d);
+  cudaFree(H->tadd_off_d);
+  cudaFree(H->tadd_pair_d);
   delete H->sx;
   for (void* q : H->opened) cudaIpcCloseMemHandle(q);
   cudaFree(H->mbox);
@@ -313,7 +324,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = alloc(reinterpret_cast<void**>(&H->D), size_t(p.nd) * p.d_stride * sizeof(double), "D")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zloc), size_t(p.z_local_rows) * zrow, "z")) ||
       (e = alloc(reinterpret_cast<void**>(&H->zex),
-                 H->sx ? size_t(H->sx->doubles(hmat::kMaxNR, p.r)) * sizeof(double) : size_t(p.z_exch_rows) * zrow,
+                 H->sx ? size_t(H->sx->doubles_max(hmat::kMaxNR, p.r)) * sizeof(double) : size_t(p.z_exch_rows) * zrow,
                  "exchange")) ||
       (e = alloc(reinterpret_cast<void**>(&H->part), size_t(p.grid_p_max) * p.L * 2 * zrow, "partials")) ||
       (e = alloc(reinterpret_cast<void**>(&H->cnt), size_t(p.grid_p_max) * p.L * sizeof(int) + 256, "tickets")) ||
@@ -363,7 +374,11 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
     if ((e = up(reinterpret_cast<void**>(&H->xent_d), X.src_entry.data(), X.src_entry.size() * sizeof(int32_t))) ||
         (e = up(reinterpret_cast<void**>(&H->unpack_d), X.unpack.data(), X.unpack.size() * sizeof(int64_t))) ||
         (e = up(reinterpret_cast<void**>(&H->pack_d), X.pack.data(), X.pack.size() * sizeof(int64_t))) ||
-        (e = up(reinterpret_cast<void**>(&H->halo_of_d), X.halo_of.data(), X.halo_of.size() * sizeof(int32_t))))
+        (e = up(reinterpret_cast<void**>(&H->halo_of_d), X.halo_of.data(), X.halo_of.size() * sizeof(int32_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->tpack_d), X.tpack.data(), X.tpack.size() * sizeof(int64_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->tadd_leaf_d), X.tadd_leaf.data(), X.tadd_leaf.size() * sizeof(int64_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->tadd_off_d), X.tadd_off.data(), X.tadd_off.size() * sizeof(int64_t))) ||
+        (e = up(reinterpret_cast<void**>(&H->tadd_pair_d), X.tadd_pair.data(), X.tadd_pair.size() * sizeof(int64_t))))
       return bail(cuda_fail(e, "uploading the standard-admissibility exchange tables"));
   }
   if (p.adm) {  // interaction-list slot tables for the project kernel's scatter
@@ -582,9 +597,9 @@ hmat_status ensure_dt(hmat_s* H) {
   const size_t bytes = size_t(p.nd) * p.d_stride * sizeof(double);
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->Dt), bytes));
   CUDA_TRY(cudaMemsetAsync(H->Dt, 0, bytes, H->stream));
-  if (p.adm)  // standard admissibility: nd near-field panels (one GPU: N_loc = N)
-    CUDA_TRY(hmat::launch_transpose_near_field(H->D, H->Dt, p.N_loc / p.b, p.d, p.L, p.b, p.Dp, p.d_stride, p.nd,
-                                               H->stream));
+  if (p.adm)  // standard admissibility: nd near-field panels of this rank's leaves
+    CUDA_TRY(hmat::launch_transpose_near_field(H->D, H->Dt, p.N_loc / p.b, p.row0 / p.b, p.d, p.L, p.b, p.Dp,
+                                               p.d_stride, p.nd, H->stream));
   else
     CUDA_TRY(hmat::launch_transpose_leaf_blocks(H->D, H->Dt, p.N_loc / p.b, p.b, p.Dp, H->stream));
   return HMAT_OK;
@@ -611,8 +626,6 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     hmat_status sa = check_async(H);
     if (sa != HMAT_OK) return sa;
   }
-  if (trans && p.adm && p.P > 1)
-    return fail(HMAT_ERR_UNSUPPORTED, "transposed product with standard admissibility and nranks > 1");
   if (trans) {
     hmat_status st = ensure_dt(H);
     if (st != HMAT_OK) return st;
@@ -756,6 +769,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.dbg = p.dbg;
   a.snake = p.snake;
   a.early = p.early;
+  a.dmma_ileave = p.dmma_ileave;
+  a.aflush = p.aflush;
   // PDL (expand's launch and prologue overlap project's tail) for whole products;
   // off while the per-kernel profiler brackets the kernels with events
   // and the CTA trace (its memsets sit between the kernels)
@@ -768,7 +783,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
   auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project, int gp, int ge,
-                  auto&& before_project, auto&& before_expand) -> hmat_status {
+                  auto&& before_project, auto&& before_expand, auto&& after_expand) -> hmat_status {
     const size_t bytes = exch * sizeof(double);
     // optional per-CTA trace: zeroed slots, filled by the kernels
     auto trace = [&](int ph, int grid) -> cudaError_t {
@@ -811,6 +826,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       prof_begin(H, 2, &ep);
       CUDA_TRY(expand());
       prof_end(H, &ep);
+      CUDA_TRY(after_expand());
     }
     return HMAT_OK;
   };
@@ -880,7 +896,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
           [&] {
             return H->peer && dl.dgrid_p > 0 && level_mask ? hmat::launch_peer_sum(a, H->zex_d, H->stream)
                                                             : cudaSuccess;
-          });
+          },
+          [] { return cudaSuccess; });
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -917,7 +934,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       const int ll = 64 - __builtin_clzll(level_mask);
       const int64_t SLs = p.N_loc / p.Rp, seg = std::min<int64_t>(p.m[ll], p.N_loc) / p.Rp;
       int64_t ch = seg;
-      while (ch < 4) ch += seg;
+      while (ch < p.project_chunk) ch += seg;
       if (ll > p.cross && SLs / ch >= 2 * int64_t(ly.grid_p)) {
         a.dyn_level = ll;
         a.dyn_chunk = ch;
@@ -933,7 +950,9 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     size_t exch = size_t(p.z_exch_rows) * p.Wp * cap;
     if (H->sx) {  // standard admissibility, P > 1: the packed cross-rank buffer
       const hmat::StdExchange& X = *H->sx;
-      exch = size_t(X.doubles(cap, p.r));
+      // H^T: products of the cross near-field pairs instead of the halo x
+      exch = size_t(trans ? X.doubles_t(cap, p.r) : X.doubles(cap, p.r));
+      a.skip_remote = trans ? 1 : 0;
       a.xchg = H->zex;
       a.halo_of = H->halo_of_d;
       a.halo_base = X.halo_base(cap, p.r);
@@ -942,8 +961,16 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     auto pack_x = [&]() -> cudaError_t {
       if (!H->sx) return cudaSuccess;
+      if (trans)  // H^T: c_{S,T} = (D_{S,T})^T x_S of this rank's outgoing near-field pairs (forward D)
+        return hmat::launch_std_tpack(H->zex + a.halo_base, H->D, p.d_stride, p.Dp, a.x, ldx, H->tpack_d,
+                                      int64_t(H->sx->tpack.size() / 3), cap, nr, p.b, a.bpad, H->stream);
       return hmat::launch_std_pack_x(H->zex + a.halo_base, a.x, ldx, H->pack_d, int64_t(H->sx->pack.size() / 2), cap,
                                      nr, p.b, a.bpad, H->stream);
+    };
+    auto add_t = [&]() -> cudaError_t {  // H^T: the incoming near-field products, in pair order
+      if (!H->sx || !trans || !dense) return cudaSuccess;
+      return hmat::launch_std_tadd(a.y, n, alpha, H->zex + a.halo_base, H->tadd_leaf_d, H->tadd_off_d, H->tadd_pair_d,
+                                   int64_t(H->sx->tadd_leaf.size()), cap, nr, p.b, a.bpad, H->stream);
     };
     auto unpack_z = [&]() -> cudaError_t {
       if (!H->sx) return cudaSuccess;
@@ -961,7 +988,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     hmat_status st2 = pass(
         H->zex, exch, [&] { return hmat::launch_project(a, cap, grid_p, ly.smem_p, H->stream); },
         [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0, grid_p,
-        ly.grid_e, pack_x, unpack_z);
+        ly.grid_e, pack_x, unpack_z, add_t);
     if (st2 != HMAT_OK) return st2;
   }
   if (async_io) {  // y out on s_out once the kernels are done; no host wait
@@ -1006,33 +1033,48 @@ hmat_status hmat_gemv(hmat_t H, int trans, double alpha, const double* x, double
   return run(H, trans, alpha, x, beta, y, nrhs, ~0ull, 1);
 }
 
-hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count) {
+hmat_status hmat_exchange_size_op(hmat_t H, int trans, int nrhs, int64_t* count) {
   if (!H || !count || nrhs < 1) return fail(HMAT_ERR_INVALID, "NULL argument or nrhs < 1");
+  if (trans != 0 && trans != 1) return fail(HMAT_ERR_INVALID, "trans must be 0 (H) or 1 (H^T)");
   const hmat::Plan& p = H->plan;
   if (use_dmma(p, nrhs)) {
     if (nrhs > hmat::kDmmaNB) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
     *count = p.P > 1 ? p.z_exch_rows * p.W * p.dmma_layout(nrhs).nb : 0;
   } else {
     if (nrhs > p.max_nr) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
-    *count = p.P > 1 ? (H->sx ? H->sx->doubles(nr_cap(nrhs), p.r) : p.z_exch_rows * p.Wp * nr_cap(nrhs)) : 0;
+    const int cap = nr_cap(nrhs);
+    *count = p.P > 1 ? (H->sx ? (trans ? H->sx->doubles_t(cap, p.r) : H->sx->doubles(cap, p.r))
+                              : p.z_exch_rows * p.Wp * cap)
+                     : 0;
   }
   return HMAT_OK;
 }
 
-hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange) {
+hmat_status hmat_exchange_size(hmat_t H, int nrhs, int64_t* count) { return hmat_exchange_size_op(H, 0, nrhs, count); }
+
+hmat_status hmat_project_op(hmat_t H, int trans, const double* x, int nrhs, double* exchange) {
   int64_t count = 0;
-  hmat_status st = hmat_exchange_size(H, nrhs, &count);
+  hmat_status st = hmat_exchange_size_op(H, trans, nrhs, &count);
   if (st != HMAT_OK) return st;
   if (count && !exchange && !H->peer) return fail(HMAT_ERR_INVALID, "exchange is NULL");
-  return run(H, 0, 1.0, x, 0.0, nullptr, nrhs, ~0ull, 1, kPhaseProject, exchange, nullptr);
+  return run(H, trans, 1.0, x, 0.0, nullptr, nrhs, ~0ull, 1, kPhaseProject, exchange, nullptr);
+}
+
+hmat_status hmat_project(hmat_t H, const double* x, int nrhs, double* exchange) {
+  return hmat_project_op(H, 0, x, nrhs, exchange);
+}
+
+hmat_status hmat_expand_op(hmat_t H, int trans, double alpha, const double* x, const double* exchange, double beta,
+                           double* y, int nrhs) {
+  int64_t count = 0;
+  hmat_status st = hmat_exchange_size_op(H, trans, nrhs, &count);
+  if (st != HMAT_OK) return st;
+  if (count && !exchange && !H->peer) return fail(HMAT_ERR_INVALID, "exchange is NULL");
+  return run(H, trans, alpha, x, beta, y, nrhs, ~0ull, 1, kPhaseExpand, nullptr, exchange);
 }
 
 hmat_status hmat_expand(hmat_t H, const double* x, const double* exchange, double* y, int nrhs) {
-  int64_t count = 0;
-  hmat_status st = hmat_exchange_size(H, nrhs, &count);
-  if (st != HMAT_OK) return st;
-  if (count && !exchange && !H->peer) return fail(HMAT_ERR_INVALID, "exchange is NULL");
-  return run(H, 0, 1.0, x, 0.0, y, nrhs, ~0ull, 1, kPhaseExpand, nullptr, exchange);
+  return hmat_expand_op(H, 0, 1.0, x, exchange, 0.0, y, nrhs);
 }
 
 hmat_status hmat_create_strict(int depth, int dim, int leaf_size, int rank, const double* const* U,
@@ -1368,6 +1410,11 @@ hmat_status hmat_std_exchange_query(int depth, int dim, int leaf_size, int rank,
   give(X.unpack, q->unpack, q->unpack_cap, &q->n_unpack);
   give(X.pack, q->pack, q->pack_cap, &q->n_pack);
   give(X.halo_of, q->halo_of, q->halo_of_cap, &q->n_halo_of);
+  q->Hp = X.Hp;
+  give(X.tpack, q->tpack, q->tpack_cap, &q->n_tpack);
+  give(X.tadd_leaf, q->tadd_leaf, q->tadd_leaf_cap, &q->n_tadd_leaf);
+  give(X.tadd_off, q->tadd_off, q->tadd_off_cap, &q->n_tadd_off);
+  give(X.tadd_pair, q->tadd_pair, q->tadd_pair_cap, &q->n_tadd_pair);
   return HMAT_OK;
 }
 

@@ -84,6 +84,9 @@ struct StreamArgs {
   unsigned int* err;         // host-mapped error word: a flag wait that timed out (peer.cuh)
   int64_t peer_timeout_ns;   // bound on a flag wait (HMAT_PEER_TIMEOUT_MS)
   int early;                 // project: release a ring slot before the FMAs (HMAT_PROJECT_EARLY)
+  int dmma_ileave;           // tensor-core expand: interleaved item order (HMAT_DMMA_ILEAVE)
+  int skip_remote;           // standard H^T, P > 1: expand skips near-field blocks of remote neighbours
+  int aflush;                // project: asynchronous node flushes (HMAT_PROJECT_AFLUSH)
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
   int64_t exch;              // doubles of this pass's exchange levels
   int cross;                 // levels 1..cross are exchange levels
@@ -155,9 +158,20 @@ cudaError_t launch_std_pack_x(double* xchg_halo, const double* x, int64_t ldx, c
                               int cap, int nr, int b, int bpad, cudaStream_t s);
 cudaError_t launch_std_unpack_z(double* zt, const double* xchg, const int64_t* unpack, int64_t n_unpack, int cap,
                                 int nr, int Wp, int r, cudaStream_t s);
-// Standard admissibility: the transposed near-field panels of H^T (one-time helper).
-cudaError_t launch_transpose_near_field(const double* D, double* Dt, int64_t n_leaves, int d, int L, int b, int Dp,
-                                        int64_t d_stride, int nd, cudaStream_t s);
+// Standard admissibility: the transposed near-field panels of H^T (one-time
+// helper); leaves lbase .. lbase + n_leaves - 1 of this rank, blocks whose
+// neighbour lies on another rank stay zero (their products travel in the exchange).
+cudaError_t launch_transpose_near_field(const double* D, double* Dt, int64_t n_leaves, int64_t lbase, int d, int L,
+                                        int b, int Dp, int64_t d_stride, int nd, cudaStream_t s);
+// Standard admissibility, H^T with P > 1 (std_exchange.h): the products
+// c_{S,T} = (D_{S,T})^T x_S of this rank's outgoing cross near-field pairs into the
+// packed buffer (before project), and y_T += alpha sum c_{S,T} of the incoming
+// ones in pair order (after expand).
+cudaError_t launch_std_tpack(double* out, const double* D, int64_t d_stride, int Dp, const double* x, int64_t ldx,
+                             const int64_t* tpack, int64_t n_pairs, int cap, int nr, int b, int bpad, cudaStream_t s);
+cudaError_t launch_std_tadd(double* y, int64_t ldy, double alpha, const double* in, const int64_t* leaf,
+                            const int64_t* off, const int64_t* pairs, int64_t n_leaves, int cap, int nr, int b,
+                            int bpad, cudaStream_t s);
 // D^T of every dense leaf block (for H^T x); one-time helper.
 cudaError_t launch_transpose_leaf_blocks(const double* D, double* Dt, int64_t n_leaves, int b, int Dp, cudaStream_t s);
 // Opt the kernels into large dynamic shared memory (once per device).

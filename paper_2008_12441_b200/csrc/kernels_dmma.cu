@@ -288,7 +288,14 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   const int64_t G = gridDim.x, bid = blockIdx.x;
   const int W = a.W, b = a.b, L = a.L;
   const int64_t items = a.N_loc / RE;
-  const int64_t j0 = items * bid / G, j1 = items * (bid + 1) / G;
+  // item order: interleaved (CTA b takes items b, b + G, b + 2G, ...: the G CTAs
+  // work on G consecutive tiles at any time, so the coarse levels' Zt chunks they
+  // share stay in L2 -- a handful of nodes instead of one per CTA, which at c5
+  // (296 x 4 coarse levels x 114 KB) exceeded L2 and re-read Zt from DRAM), or
+  // contiguous ranges (a.dmma_ileave = 0)
+  const bool ilv = a.dmma_ileave != 0;
+  const int64_t j0 = ilv ? bid : items * bid / G, j1 = ilv ? items : items * (bid + 1) / G;
+  const int64_t jst = ilv ? G : 1;
   const int NS = a.nstage_e;
   const int kcw = W / KC, kcd = b / KD;      // k-chunks per level / for the dense block
   const int64_t abytes = (int64_t)RE * AP * 8, abytes_d = (int64_t)RE * APD * 8;
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     do {
       if (++lr > L + 1) {
         lr = 1;
-        ++jr;
+        jr += jst;
       }
     } while (!level_on(lr));
   };
@@ -328,7 +335,8 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
       const double* zt = lv.zt + ((a.row0 + i0) / lv.m - lv.tbase) * (int64_t)W * NB;
       dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes + KC * NB * 8));
       dev::tma_load_3d(st, &a.tm_u, kcr * KC, i0, lr - 1, &full[sl], pol_stream);
-      dev::bulk_g2s(st + abytes, zt + (int64_t)kcr * KC * NB, KC * NB * 8, &full[sl], pol_keep);
+      // a node of at most one tile is read once: stream it; coarser nodes' Zt is shared
+      dev::bulk_g2s(st + abytes, zt + (int64_t)kcr * KC * NB, KC * NB * 8, &full[sl], lv.m <= RE ? pol_stream : pol_keep);
     }
   };
   if (tid == 0) {
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   const int g = lane >> 2, tq = lane & 3;
   int slot = 0;
   uint32_t phase = 0;
-  for (int64_t j = j0; j < j1; ++j) {
+  for (int64_t j = j0; j < j1; j += jst) {
     const int64_t i0 = j * RE;
     double acc[MT][NTW][2];
 #pragma unroll

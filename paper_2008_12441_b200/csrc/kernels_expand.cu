@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       if (!((geo::near_mask(a.d, lx, 1 << L) >> lane) & 1u)) return kNone;
       if (a.halo_of) {
         const int h = a.halo_of[(leaf_idx - a.row0 / b) * a.nd + lane];
+        if (h >= 0 && a.skip_remote) return kNone;  // H^T: that product arrives in the exchange
         if (h >= 0) {
           xsrc = a.xchg + a.halo_base;
           xld = a.bpad;
@@ -317,6 +318,11 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       for (int e = 0; e < a.nd; ++e) m |= (a.halo_of[(leaf_idx - lbase) * a.nd + e] >= 0 ? 1u : 0u) << e;
     return m;
   };
+  // H^T with P > 1: remote neighbours' blocks are skipped (added after the kernel)
+  auto present = [&]() -> uint32_t {
+    const uint32_t m = geo::near_mask(a.d, lx, 1 << L);
+    return a.skip_remote ? m & ~hmask : m;
+  };
   int slot = 0;
   uint32_t phase = 0;
   int64_t cj0 = j0, cj1 = j1;
@@ -342,8 +348,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   leaf_idx = (a.row0 + leaf0) / b;
   if (a.adm) {
     geo::morton_decode(a.d, leaf_idx, L, lx);
-    nmask = geo::near_mask(a.d, lx, 1 << L);
     hmask = halo_mask();
+    nmask = present();
   }
   for (int64_t j = cj0; j < cj1; ++j) {
     const int64_t i0 = j * Re;
@@ -473,8 +479,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       if (a.adm) {
         ++leaf_idx;
         geo::morton_decode(a.d, leaf_idx, L, lx);
-        nmask = geo::near_mask(a.d, lx, 1 << L);
         hmask = halo_mask();
+        nmask = present();
       }
     }
   }

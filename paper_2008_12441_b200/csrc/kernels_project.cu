@@ -132,6 +132,12 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   uint64_t* empty = full + NS;
   volatile int* flag = reinterpret_cast<volatile int*>(empty + NS);
   volatile int* chunk_q = reinterpret_cast<volatile int*>(smem + a.bar_off_p + 768);  // [NS] chunk ids
+  // asynchronous node flush (see the consumers): per reduction buffer, "all
+  // consumer warps wrote their partials" and "its summing warps are done"
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + a.bar_off_p + 160);
+  uint64_t* rempty = rfull + 2;
+  // summing warps per node: enough warps for the W NR outputs
+  const int nsw = min(NCW, (W * NR + 31) / 32);
   // The last active level (a.dyn_level; 0 = none) is handed out dynamically in
   // chunks of a.dyn_chunk stages (whole nodes: no partial sums) from a global
   // counter, so CTAs that streamed the earlier levels faster take more of it
@@ -142,6 +148,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     for (int i = 0; i < NS; ++i) {
       dev::mbar_init(&full[i], 1);
       dev::mbar_init(&empty[i], NCW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      dev::mbar_init(&rfull[i], NCW);
+      dev::mbar_init(&rempty[i], nsw);
     }
     dev::fence_mbar_init();
   }
@@ -164,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       const uint32_t vbytes = static_cast<uint32_t>(Rp * Wp * 8);
       int slot = 0;
       uint32_t phase = 0;
+      int next_c = -1;  // dynamic level: the chunk claimed ahead (its atomic's latency hidden)
       for (int l = 1; l <= L; ++l) {
         if (!((a.level_mask >> (l - 1)) & 1ull) || (lpar && l != my_level)) continue;
         const double* Vl = a.V + (l - 1) * a.panel_stride;
@@ -173,7 +184,9 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         int chunk = -1;
         for (bool first_range = true;; first_range = false) {
         if (dyn) {
-          const int c = atomicAdd(a.sched_p, 1);
+          const int c = next_c >= 0 ? next_c : atomicAdd(a.sched_p, 1);
+          // claim the following chunk now: its round trip overlaps this chunk's copies
+          next_c = int64_t(c) * a.dyn_chunk < SL ? atomicAdd(a.sched_p, 1) : -1;
           if (int64_t(c) * a.dyn_chunk >= SL) {
             // end of work: an empty phase with chunk id -1 tells the consumers
             dev::mbar_wait(&empty[slot], phase ^ 1);
@@ -249,6 +262,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   double* red_base = reinterpret_cast<double*>(smem + a.red_off_p);
   int64_t* nbr_base = reinterpret_cast<int64_t*>(smem + a.bar_off_p + 256);  // 2 x 32 entries
   int red_buf = 0;
+  uint32_t ph_f[2] = {0u, 0u}, ph_e[2] = {0u, 0u};  // async flush phases per buffer (all threads)
+  int nflush = 0;                                   // async flushes so far (rotates the summing warps)
+  const int cw = warp - 1;                          // consumer warp index
+  const bool async_flush = a.aflush != 0;
   double2 acc[PAIRS][NR];
 #pragma unroll
   for (int j = 0; j < PAIRS; ++j)
@@ -361,14 +378,19 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         sl += dk;
       }
       if (!node_end && n != 1) continue;
+      if ((a.dbg & 4) && node_end) continue;  // diagnostics: skip node flushes entirely (wrong z)
 
       // ---- end of a (local) node, or end of this CTA's range of the level ----
       const int64_t sa = this_sl * seg, sb = sa + seg;  // the node's stages
       const bool complete = sa >= rk0 && sb <= rk1;
       const int64_t sg = sg0 + this_sl;                 // global source node
-      double* red = red_base + red_buf * red_elems;
-      int64_t* nbr = nbr_base + red_buf * 32;  // standard admissibility: parent's neighbours
+      const int rb = red_buf;
+      double* red = red_base + rb * red_elems;
+      int64_t* nbr = nbr_base + rb * 32;  // standard admissibility: parent's neighbours
       red_buf ^= 1;  // alternate buffers: one barrier per complete node suffices
+      // the buffer is free once the summing warps of its last asynchronous use
+      // are done (a fresh barrier's parity 1 passes at once)
+      dev::mbar_wait(&rempty[rb], ph_e[rb] ^ 1);
       if (a.adm) std_parent_neighbours(a, sg, l, t, nbr);
       if (active) {
 #pragma unroll
@@ -383,7 +405,37 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           }
         }
       }
+      if (complete && async_flush) {
+        // Asynchronous flush of a complete node: every warp posts its partials
+        // and moves on to the next stage; only this node's nsw summing warps
+        // (rotating, so the work spreads over all warps) wait for the other
+        // warps' partials, sum the RG row groups and scatter z.  No CTA-wide
+        // barrier per node: at the finest level (one node per stage) the
+        // barrier held every warp to the slowest one each stage.
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&rfull[rb]);
+        const int rel = (cw - nflush * nsw % NCW + NCW) % NCW;
+        if (rel < nsw) {
+          dev::mbar_wait(&rfull[rb], ph_f[rb]);
+          for (int o = rel * 32 + lane; o < W * NR; o += nsw * 32) {
+            const int kk = o / W, col = o - kk * W;
+            double v = 0.0;
+            for (int g = 0; g < RG; ++g) v += red[((int64_t)g * NR + kk) * Wp + col];
+            if (kk < a.nr) {
+              if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);
+              else scatter_z<NR>(a, lv, sg, col, kk, v);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive(&rempty[rb]);
+        }
+        ph_f[rb] ^= 1u;
+        ph_e[rb] ^= 1u;
+        ++nflush;
+        continue;
+      }
       dev::named_bar_sync(1, CT);
+      if (complete && (a.dbg & 8)) continue;  // diagnostics: barrier only, no reduction / store
       if (complete) {
         for (int o = t; o < W * NR; o += CT) {
           const int kk = o / W, col = o - kk * W;

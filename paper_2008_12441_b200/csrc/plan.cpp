@@ -78,6 +78,9 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.pdl = opt.pdl;
   p.lpar = opt.lpar;
   p.early = opt.early;
+  p.dmma_ileave = opt.dmma_ileave;
+  p.project_chunk = opt.project_chunk;
+  p.aflush = opt.aflush;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;

@@ -114,6 +114,28 @@ std::string std_exchange_build(const Plan& p, StdExchange* out) {
           static_cast<int32_t>(hidx[static_cast<size_t>(s)]);
     }
   }
+  // ---- H^T: cross near-field pairs (S, T) carrying c_{S,T} = (D_{S,T})^T x_S ----
+  std::vector<std::vector<int64_t>> incoming(static_cast<size_t>(lcnt));
+  for (int64_t s = 0; s < leaves; ++s) {
+    int64_t xs[3];
+    decode(d, s, L, xs);
+    const int64_t os = owner(s * p.b);
+    for (int e = 0; e < nd; ++e) {
+      const int64_t t = shifted(d, xs, e, L);
+      if (t < 0 || owner(t * p.b) == os) continue;
+      const int64_t pair = X.Hp++;
+      if (os == me) X.tpack.insert(X.tpack.end(), {pair, s - lbase, e});
+      if (owner(t * p.b) == me) incoming[static_cast<size_t>(t - lbase)].push_back(pair);
+    }
+  }
+  X.tadd_off.push_back(0);
+  for (int64_t t = 0; t < lcnt; ++t) {
+    const auto& v = incoming[static_cast<size_t>(t)];
+    if (v.empty()) continue;
+    X.tadd_leaf.push_back(t);
+    X.tadd_pair.insert(X.tadd_pair.end(), v.begin(), v.end());
+    X.tadd_off.push_back(static_cast<int64_t>(X.tadd_pair.size()));
+  }
   *out = std::move(X);
   return "";
 }

@@ -21,6 +21,16 @@
 // reads halo x directly from the buffer.  A pair is "cross" unless target and
 // source lie inside the same rank (pairs touching a node that spans ranks are
 // always cross: its z is a sum of per-rank partials).
+//
+// The transposed product H^T (GEMV "T") has the same
+// interaction pairs (the relation is symmetric), so the z entries and their
+// tables serve it unchanged with U and V swapping roles.  Its near field is
+// y_T += (D_{S,T})^T x_S, and for S on another rank the block D_{S,T} lives
+// there (row block S): instead of the halo x, the buffer's second part carries
+// one product per cross near-field pair, computed by the rank owning S,
+//   [Hp pairs][cap rhs][bpad]        c_{S,T} = (D_{S,T})^T x_S,
+// and the rank owning T adds its incoming c's to y_T after the expand kernel
+// (which skips the remote blocks), in pair order: deterministic.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -45,9 +55,18 @@ struct StdExchange {
   std::vector<int64_t> pack;
   // [local leaf][3^d]: halo index of neighbour e, -1 when local / outside the domain
   std::vector<int32_t> halo_of;
+  // H^T: cross near-field pairs (S, T), owner(S) != owner(T), numbered over leaves S
+  // in Morton order then neighbour e (T = S + eps_e)
+  int64_t Hp = 0;
+  std::vector<int64_t> tpack;     // this rank's outgoing pairs: {pair, local leaf S, e}
+  std::vector<int64_t> tadd_leaf; // this rank's leaves T with incoming pairs (local index)
+  std::vector<int64_t> tadd_off;  // CSR offsets into tadd_pair (size tadd_leaf + 1)
+  std::vector<int64_t> tadd_pair; // incoming pair indices, ascending per leaf
   // doubles of the packed buffer for a pass of `cap` right-hand sides
   int64_t halo_base(int cap, int r) const { return (E * r * cap + 1) / 2 * 2; }  // 16-byte aligned
   int64_t doubles(int cap, int r) const { return halo_base(cap, r) + Hn * bpad * cap; }
+  int64_t doubles_t(int cap, int r) const { return halo_base(cap, r) + Hp * bpad * cap; }  // H^T
+  int64_t doubles_max(int cap, int r) const { return halo_base(cap, r) + (Hn > Hp ? Hn : Hp) * bpad * cap; }
 };
 
 // Requires p.adm == 1 (standard admissibility).  Returns "" on success.

@@ -36,7 +36,7 @@ EXPORTS = ("hmat_create", "hmat_create_uninit", "hmat_create_strict", "hmat_crea
            "hmat_profile", "hmat_profile_read", "hmat_launches_per_matvec", "hmat_plan_query",
            "hmat_peer_export", "hmat_peer_import", "hmat_peer_connect_local", "hmat_cta_trace",
            "hmat_cta_trace_read", "hmat_std_exchange_query", "hmat_set_host_async", "hmat_synchronize",
-           "hmat_comm_info")
+           "hmat_comm_info", "hmat_exchange_size_op", "hmat_project_op", "hmat_expand_op")
 
 
 class hmat_std_exchange_t(ctypes.Structure):
@@ -45,7 +45,12 @@ class hmat_std_exchange_t(ctypes.Structure):
                 ("src_entry", ctypes.c_void_p), ("src_entry_cap", ctypes.c_int64), ("n_src_entry", ctypes.c_int64),
                 ("unpack", ctypes.c_void_p), ("unpack_cap", ctypes.c_int64), ("n_unpack", ctypes.c_int64),
                 ("pack", ctypes.c_void_p), ("pack_cap", ctypes.c_int64), ("n_pack", ctypes.c_int64),
-                ("halo_of", ctypes.c_void_p), ("halo_of_cap", ctypes.c_int64), ("n_halo_of", ctypes.c_int64)]
+                ("halo_of", ctypes.c_void_p), ("halo_of_cap", ctypes.c_int64), ("n_halo_of", ctypes.c_int64),
+                ("Hp", ctypes.c_int64),
+                ("tpack", ctypes.c_void_p), ("tpack_cap", ctypes.c_int64), ("n_tpack", ctypes.c_int64),
+                ("tadd_leaf", ctypes.c_void_p), ("tadd_leaf_cap", ctypes.c_int64), ("n_tadd_leaf", ctypes.c_int64),
+                ("tadd_off", ctypes.c_void_p), ("tadd_off_cap", ctypes.c_int64), ("n_tadd_off", ctypes.c_int64),
+                ("tadd_pair", ctypes.c_void_p), ("tadd_pair_cap", ctypes.c_int64), ("n_tadd_pair", ctypes.c_int64)]
 
 
 class HMatError(RuntimeError):
@@ -105,6 +110,9 @@ _sigs = {
     "hmat_set_host_async": (_i, [_H, _i]),
     "hmat_synchronize": (_i, [_H]),
     "hmat_comm_info": (_i, [_H, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "hmat_exchange_size_op": (_i, [_H, _i, _i, ctypes.POINTER(_i64)]),
+    "hmat_project_op": (_i, [_H, _i, _P, _i, _P]),
+    "hmat_expand_op": (_i, [_H, _i, ctypes.c_double, _P, _P, ctypes.c_double, _P, _i]),
     "hmat_peer_export": (_i, [_H, _P]),
     "hmat_cta_trace": (_i, [_H, _i]),
     "hmat_cta_trace_read": (_i, [_H, _i, ctypes.POINTER(ctypes.c_int64), _i, ctypes.POINTER(ctypes.c_int)]),
@@ -302,6 +310,33 @@ def hmat_expand(h, x, exchange, y, nrhs: int | None = None):
     _check(_lib.hmat_expand(h, xp, _ptr(exchange), yp, nrhs), "hmat_expand")
 
 
+def hmat_exchange_size_op(h, trans: int, nrhs: int) -> int:
+    """doubles of one pass's packed exchange buffer for op(H) (0 when P = 1)."""
+    cnt = _i64()
+    _check(_lib.hmat_exchange_size_op(h, int(trans), nrhs, ctypes.byref(cnt)), "hmat_exchange_size_op")
+    return cnt.value
+
+
+def hmat_project_op(h, trans: int, x, exchange, nrhs: int | None = None):
+    """Split phase 1 of y = alpha op(H) x + beta y."""
+    n = hmat_local_rows(h)
+    n = n[1] - n[0]
+    xp, kx = _vec(x, n)
+    nrhs = kx if nrhs is None else nrhs
+    _check(_lib.hmat_project_op(h, int(trans), xp, nrhs, _ptr(exchange)), "hmat_project_op")
+
+
+def hmat_expand_op(h, trans: int, alpha: float, x, exchange, beta: float, y, nrhs: int | None = None):
+    """Split phase 3: y = alpha op(H) x + beta y from the exchange summed over all ranks."""
+    n = hmat_local_rows(h)
+    n = n[1] - n[0]
+    xp, kx = _vec(x, n)
+    yp, ky = _vec(y, n)
+    nrhs = kx if nrhs is None else nrhs
+    _check(_lib.hmat_expand_op(h, int(trans), float(alpha), xp, _ptr(exchange), float(beta), yp, nrhs),
+           "hmat_expand_op")
+
+
 def hmat_matvec_parts(h, x, y, level_mask: int, dense: bool, nrhs: int | None = None):
     n = hmat_local_rows(h)
     n = n[1] - n[0]
@@ -396,12 +431,21 @@ def hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id) -> dic
     q.unpack, q.unpack_cap = unp.ctypes.data, unp.size
     q.pack, q.pack_cap = pk.ctypes.data, pk.size
     q.halo_of, q.halo_of_cap = ho.ctypes.data, ho.size
+    tp = np.zeros(max(1, q.n_tpack), dtype=np.int64)
+    tl = np.zeros(max(1, q.n_tadd_leaf), dtype=np.int64)
+    to = np.zeros(max(1, q.n_tadd_off), dtype=np.int64)
+    tq = np.zeros(max(1, q.n_tadd_pair), dtype=np.int64)
+    q.tpack, q.tpack_cap = tp.ctypes.data, tp.size
+    q.tadd_leaf, q.tadd_leaf_cap = tl.ctypes.data, tl.size
+    q.tadd_off, q.tadd_off_cap = to.ctypes.data, to.size
+    q.tadd_pair, q.tadd_pair_cap = tq.ctypes.data, tq.size
     _check(_lib.hmat_std_exchange_query(depth, dim, leaf_size, rank, nranks, rank_id, ctypes.byref(q)),
            "hmat_std_exchange_query")
     return {"E": q.E, "Hn": q.Hn, "bpad": q.bpad, "M": q.M, "src_off": list(q.src_off)[:depth + 1],
             "zt_row_offset": list(q.zt_row_offset)[:depth + 1], "src_entry": src[:q.n_src_entry],
             "unpack": unp[:q.n_unpack].reshape(-1, 2), "pack": pk[:q.n_pack].reshape(-1, 2),
-            "halo_of": ho[:q.n_halo_of]}
+            "halo_of": ho[:q.n_halo_of], "Hp": q.Hp, "tpack": tp[:q.n_tpack].reshape(-1, 3),
+            "tadd_leaf": tl[:q.n_tadd_leaf], "tadd_off": to[:q.n_tadd_off], "tadd_pair": tq[:q.n_tadd_pair]}
 
 
 class HMatrix:

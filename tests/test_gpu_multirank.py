@@ -250,18 +250,49 @@ def test_standard_sharded_split_phase_matches_oracle(cfg, P, nrhs):
     assert cnt > 0
 
 
-def test_standard_sharded_transpose_unsupported():
-    cfg = HConfig("s2t", d=2, L=3, b=4, r=2, adm=1, seed=316)
-    U, V, Dn = hgen.inputs(cfg, 0, cfg.N // 2)
-    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn,
-                                hm._dist(nranks=2, rank=0, device=0, external_exchange=True))
+def sharded_std_gemv_t(cfg, P, nrhs, alpha, beta, y0):
+    """H^T with P shards, rank after rank through the split-phase op calls: the
+    buffer carries the z entries and the products (D_{S,T})^T x_S of the cross
+    near-field pairs; hmat_expand_op adds the incoming ones."""
+    hs, xs, ys = [], [], []
+    for g in range(P):
+        r0, r1 = g * cfg.N // P, (g + 1) * cfg.N // P
+        U, V, Dn = hgen.inputs(cfg, r0, r1)
+        d = hm._dist(nranks=P, rank=g, device=0, external_exchange=True)
+        hs.append(hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn, d))
+        x = hgen.xblock(cfg, nrhs=nrhs, row_begin=r0, row_end=r1)
+        xs.append(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())
+        ys.append(torch.from_numpy(np.ascontiguousarray(y0[r0:r1].T)).cuda())
     try:
-        x = torch.zeros(cfg.N // 2, dtype=torch.float64, device="cuda")
-        with pytest.raises(hm.HMatError) as ei:
-            hm.hmat_gemv(h, 1, 1.0, x, 0.0, torch.empty_like(x))
-        assert ei.value.status == hm.HMAT_ERR_UNSUPPORTED
+        cnt = hm.hmat_exchange_size_op(hs[0], 1, nrhs)
+        assert all(hm.hmat_exchange_size_op(h, 1, nrhs) == cnt for h in hs)
+        ex = [torch.zeros(max(cnt, 1), dtype=torch.float64, device="cuda") for _ in range(P)]
+        for g in range(P):
+            hm.hmat_project_op(hs[g], 1, xs[g].t(), ex[g], nrhs)
+        torch.cuda.synchronize()
+        total = torch.stack(ex).sum(dim=0)
+        for g in range(P):
+            hm.hmat_expand_op(hs[g], 1, alpha, xs[g].t(), total, beta, ys[g].t(), nrhs)
+        torch.cuda.synchronize()
+        return torch.cat(ys, dim=1).t().cpu().numpy(), cnt
     finally:
-        hm.hmat_destroy(h)
+        for h in hs:
+            hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("cfg,P,nrhs", [STD_CASES[0], STD_CASES[1], STD_CASES[3], STD_CASES[4], STD_CASES[5],
+                                        STD_CASES[6], STD_CASES[8], STD_CASES[9]],
+                         ids=lambda v: getattr(v, "name", str(v)))
+def test_standard_sharded_transpose_matches_oracle(cfg, P, nrhs):
+    """Standard admissibility, H^T with P > 1 (PAPER.md:961-969 GEMV "T"): the
+    shards' y = alpha H^T x + beta y0 vs the transposed oracle block loop."""
+    rng = np.random.default_rng(7)
+    y0 = rng.standard_normal((cfg.N, nrhs))
+    y, cnt = sharded_std_gemv_t(cfg, P, nrhs, 0.75, -0.5, y0)
+    U, V, Dn = hgen.inputs(cfg)
+    ref = 0.75 * oracle.std_matvec_t(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, hgen.xblock(cfg, nrhs=nrhs)) - 0.5 * y0
+    assert_parity(y, ref)
+    assert cnt > 0
 
 
 # ---- failure behaviour of the PEER exchange ------------------------------------------

@@ -193,3 +193,43 @@ def test_gloo_standard_exchange_matches_oracle(cfg, world, nrhs):
     U, V, Dn = hgen.inputs(cfg)
     ref = oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, hgen.xblock(cfg, nrhs=nrhs))
     assert np.linalg.norm(y - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("d,L,b,P", [(2, 3, 4, 2), (2, 4, 2, 8), (1, 6, 2, 8), (3, 2, 2, 8), (2, 3, 4, 16)])
+def test_transposed_near_field_pairs(d, L, b, P):
+    """H^T with P > 1: the cross near-field pairs (S, T) -- touching leaves on
+    different ranks -- counted by brute force from the leaf geometry; every pair
+    is written by exactly one rank (the owner of S, with T = S + eps_e, e the
+    near-field code of T - S) and added by exactly one rank (the owner of T)."""
+    c = 1 << d
+    N = b * c ** L
+    n_loc = N // P
+    leaves = c ** L
+    pairs = {}
+    for s in range(leaves):
+        xs = morton_decode(d, s, L)
+        for e in range(3 ** d):
+            eps = [(e // 3 ** i) % 3 - 1 for i in range(d)]
+            xt = [xs[i] + eps[i] for i in range(d)]
+            if not all(0 <= v < (1 << L) for v in xt):
+                continue
+            t = sum(((xt[i] >> j) & 1) << (j * d + i) for j in range(L) for i in range(d))
+            if (s * b) // n_loc != (t * b) // n_loc:
+                pairs[len(pairs)] = (s, t, e)
+    written, added = {}, {}
+    for g in range(P):
+        q = hm.hmat_std_exchange_query(L, d, b, 2, P, g)
+        assert q["Hp"] == len(pairs)
+        lbase = g * n_loc // b
+        for pair, sl, e in q["tpack"]:
+            assert pair not in written and pairs[pair] == (lbase + sl, pairs[pair][1], e)
+            written[pair] = g
+        off = q["tadd_off"]
+        assert len(off) == len(q["tadd_leaf"]) + 1 and off[0] == 0
+        for k, tl in enumerate(q["tadd_leaf"]):
+            pl = list(q["tadd_pair"][off[k]:off[k + 1]])
+            assert pl == sorted(pl) and len(pl) > 0
+            for pair in pl:
+                assert pair not in added and pairs[pair][1] == lbase + tl
+                added[pair] = g
+    assert sorted(written) == sorted(added) == list(range(len(pairs)))
