@@ -100,7 +100,20 @@ __device__ __forceinline__ void scatter_z(const StreamArgs& a, const LevelArgs& 
   lv.zt[(t - lv.tbase) * (int64_t)a.Wp * NR + (int64_t)kk * a.Wp + qt * a.r + aa] = v;  // [t][rhs][col]
 }
 
-template <int NR, int PAIRS>
+// Compile-time consumer shapes (SH > 0, single rhs, one column pair per thread):
+// the stage's row offsets become immediates and only the last row of a thread
+// can fall outside the stage.  SH = 1: W = 48 (2D, r = 16: the c2 / c4 panels),
+// 64-row stages; SH = 2: W = 224 (3D, r = 32: c3), 16-row stages.  SH = 0: any
+// shape, from the runtime plan.
+template <int SH>
+struct ProjShape {
+  static constexpr int NP = SH == 1 ? 24 : SH == 2 ? 112 : 0;  // column pairs (Wp / 2)
+  static constexpr int RP = SH == 1 ? 64 : SH == 2 ? 16 : 0;   // rows per stage
+  static constexpr int RG = NP ? kConsumerThreads / (NP ? NP : 1) : 0;  // row groups
+  static constexpr int ROWS = NP ? (RP + RG - 1) / (RG ? RG : 1) : 0;   // rows per thread
+};
+
+template <int NR, int PAIRS, int SH = 0>
 __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_constant__ StreamArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -250,19 +263,22 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   const int t = tid - 32;
   // each thread owns column pair(s) cp (columns 2cp, 2cp+1; Wp is even) and,
   // when the pairs fit in one pass (PAIRS == 1), the rows rho, rho+RG, ...
-  const int NP = Wp >> 1;
-  const int RG = PAIRS == 1 ? CT / NP : 1;
+  using Sh = ProjShape<SH>;
+  const int NP = SH ? Sh::NP : Wp >> 1;
+  const int RG = SH ? Sh::RG : PAIRS == 1 ? CT / NP : 1;
   const int rho = PAIRS == 1 ? t / NP : 0;
   const int cp0 = PAIRS == 1 ? t - rho * NP : t;
   const bool active = PAIRS == 1 ? rho < RG : true;
   // single rhs, one column pair per thread, at most 8 rows per thread per stage:
   // the early-release path (a.early, HMAT_PROJECT_EARLY)
-  const bool early = NR == 1 && PAIRS == 1 && a.early && Rp <= kEarlyRows * RG;
+  const bool early = SH || (NR == 1 && PAIRS == 1 && a.early && Rp <= kEarlyRows * RG);
   const int64_t red_elems = (int64_t)RG * Wp * NR;  // one of two alternating buffers
   double* red_base = reinterpret_cast<double*>(smem + a.red_off_p);
   int64_t* nbr_base = reinterpret_cast<int64_t*>(smem + a.bar_off_p + 256);  // 2 x 32 entries
   int red_buf = 0;
-  uint32_t ph_f[2] = {0u, 0u}, ph_e[2] = {0u, 0u};  // async flush phases per buffer (all threads)
+  // async flush phases (all threads): bit b = rfull[b]'s, bit 2 + b = rempty[b]'s
+  // (one register: a per-buffer array indexed at run time would live in local memory)
+  uint32_t ph_bits = 0u;
   int nflush = 0;                                   // async flushes so far (rotates the summing warps)
   const int cw = warp - 1;                          // consumer warp index
   const bool async_flush = a.aflush != 0;
@@ -306,21 +322,48 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
     }
     // (32-bit cursors: stages per level and per node fit; fewer live registers)
     const int dk = rev ? -1 : 1;
-    const int pend = rev ? 0 : static_cast<int>(seg) - 1;  // position of a node's last stage in stream order
     int64_t k = rev ? rk1 - 1 : rk0;
     int64_t sl = k / seg;
-    int pos = static_cast<int>(k - sl * seg);
+    const int pos0 = static_cast<int>(k - sl * seg);
+    int left = rev ? pos0 + 1 : static_cast<int>(seg) - pos0;  // stages to the node's end, stream order
     for (int n = static_cast<int>(rk1 - rk0); n > 0; --n, k += dk) {
       if (!peeked) dev::mbar_wait(&full[slot], phase);
       peeked = false;
       const int64_t i0 = k * Rp;
       const unsigned char* st = smem + slot * a.stage_bytes_p;
       const double2* V2 = reinterpret_cast<const double2*>(st);
-      const double* xs = reinterpret_cast<const double*>(st + Rp * Wp * 8);
+      const double* xs = reinterpret_cast<const double*>(st + (SH ? Sh::RP * Sh::NP * 16 : Rp * Wp * 8));
       int xo[NR];
 #pragma unroll
-      for (int kk = 0; kk < NR; ++kk) xo[kk] = kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
-      if (NR == 1 && PAIRS == 1 && early) {
+      for (int kk = 0; kk < NR; ++kk)  // (one rhs, even stage rows: the segment starts aligned)
+        xo[kk] = SH ? 0 : kk * a.xs_p + static_cast<int>((kk * a.ldx + i0) & 1);
+      if (SH) {
+        // compile-time shape: immediate row offsets; rows below the last one are
+        // always inside the stage
+        constexpr int RWS = Sh::ROWS > 0 ? Sh::ROWS : 1;
+        double2 v[RWS];
+        double xv[RWS];
+        const double2* vp = V2 + rho * Sh::NP + cp0;
+        const double* xp = xs + rho;
+#pragma unroll
+        for (int i = 0; i < RWS; ++i) {
+          const bool last = (i + 1) * Sh::RG > Sh::RP;  // may pass the stage's end
+          const int off = last ? min(i * Sh::RG, Sh::RP - 1 - rho) : i * Sh::RG;
+          v[i] = vp[off * Sh::NP];
+          xv[i] = xp[off];
+        }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&empty[slot]);
+        if (active && !(a.dbg & 1)) {
+#pragma unroll
+          for (int i = 0; i < RWS; ++i) {
+            const bool last = (i + 1) * Sh::RG > Sh::RP;
+            const double xi = (!last || rho + i * Sh::RG < Sh::RP) ? xv[i] : 0.0;
+            acc[0][0].x = fma(v[i].x, xi, acc[0][0].x);
+            acc[0][0].y = fma(v[i].y, xi, acc[0][0].y);
+          }
+        }
+      } else if (NR == 1 && PAIRS == 1 && early) {
         // early release: the thread's rows of the stage (<= kEarlyRows) go to
         // registers, the slot is handed back to the producer, then the FMAs run --
         // the ring slot is held for the shared-memory loads only, not for the math
@@ -362,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           }
         }
       }
-      if (!(NR == 1 && PAIRS == 1 && early)) {
+      if (!(SH || (NR == 1 && PAIRS == 1 && early))) {
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&empty[slot]);
       }
@@ -370,11 +413,10 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         slot = 0;
         phase ^= 1;
       }
-      const bool node_end = pos == pend;
+      const bool node_end = --left == 0;
       const int64_t this_sl = sl;
-      pos += dk;
       if (node_end) {
-        pos = static_cast<int>(seg) - 1 - pend;
+        left = static_cast<int>(seg);
         sl += dk;
       }
       if (!node_end && n != 1) continue;
@@ -390,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
       red_buf ^= 1;  // alternate buffers: one barrier per complete node suffices
       // the buffer is free once the summing warps of its last asynchronous use
       // are done (a fresh barrier's parity 1 passes at once)
-      dev::mbar_wait(&rempty[rb], ph_e[rb] ^ 1);
+      dev::mbar_wait(&rempty[rb], ((ph_bits >> (2 + rb)) & 1u) ^ 1u);
       if (a.adm) std_parent_neighbours(a, sg, l, t, nbr);
       if (active) {
 #pragma unroll
@@ -416,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
         if (lane == 0) dev::mbar_arrive(&rfull[rb]);
         const int rel = (cw - nflush * nsw % NCW + NCW) % NCW;
         if (rel < nsw) {
-          dev::mbar_wait(&rfull[rb], ph_f[rb]);
+          dev::mbar_wait(&rfull[rb], (ph_bits >> rb) & 1u);
           for (int o = rel * 32 + lane; o < W * NR; o += nsw * 32) {
             const int kk = o / W, col = o - kk * W;
             double v = 0.0;
@@ -429,8 +471,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
           __syncwarp();
           if (lane == 0) dev::mbar_arrive(&rempty[rb]);
         }
-        ph_f[rb] ^= 1u;
-        ph_e[rb] ^= 1u;
+        ph_bits ^= 5u << rb;  // flip bits rb and 2 + rb
         ++nflush;
         continue;
       }
@@ -518,22 +559,41 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
   if (a.peer) peer_push<CT>(a, t, GL, flag);
 }
 
+template <int NR, int PAIRS, int SH>
+cudaError_t launch_sh(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.pdl_p) return launch_pdl(project_kernel<NR, PAIRS, SH>, a, grid, kThreads, smem, s);
+  project_kernel<NR, PAIRS, SH><<<grid, kThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// compile-time shape of this launch (ProjShape), 0 = generic
+int project_shape(const StreamArgs& a, int nr_cap) {
+  if (nr_cap != 1 || !a.early || a.adm || a.lpar) return 0;
+  if (a.Wp == 2 * ProjShape<1>::NP && a.Rp == ProjShape<1>::RP) return 1;
+  if (a.Wp == 2 * ProjShape<2>::NP && a.Rp == ProjShape<2>::RP) return 2;
+  return 0;
+}
+
 template <int NR>
 cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  if (a.pdl_p)
-    return (a.Wp >> 1) <= CT ? launch_pdl(project_kernel<NR, 1>, a, grid, kThreads, smem, s)
-                             : launch_pdl(project_kernel<NR, 2>, a, grid, kThreads, smem, s);
-  if ((a.Wp >> 1) <= CT)
-    project_kernel<NR, 1><<<grid, kThreads, smem, s>>>(a);
-  else
-    project_kernel<NR, 2><<<grid, kThreads, smem, s>>>(a);
-  return cudaGetLastError();
+  if (NR == 1) {
+    const int sh = project_shape(a, NR);
+    if (sh == 1) return launch_sh<NR, 1, 1>(a, grid, smem, s);
+    if (sh == 2) return launch_sh<NR, 1, 2>(a, grid, smem, s);
+  }
+  if ((a.Wp >> 1) <= CT) return launch_sh<NR, 1, 0>(a, grid, smem, s);
+  return launch_sh<NR, 2, 0>(a, grid, smem, s);
 }
 
 template <int NR>
 cudaError_t configure_nr(int64_t smem) {
   cudaError_t e = cudaFuncSetAttribute(project_kernel<NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (NR == 1) {
+    if ((e = cudaFuncSetAttribute(project_kernel<NR, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
+        (e = cudaFuncSetAttribute(project_kernel<NR, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+      return e;
+  }
   return cudaFuncSetAttribute(project_kernel<NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
