@@ -111,7 +111,22 @@ struct ProjShape {
   static constexpr int RP = SH == 1 ? 64 : SH == 2 ? 16 : 0;   // rows per stage
   static constexpr int RG = NP ? kConsumerThreads / (NP ? NP : 1) : 0;  // row groups
   static constexpr int ROWS = NP ? (RP + RG - 1) / (RG ? RG : 1) : 0;   // rows per thread
+  static constexpr int D = SH == 1 ? 2 : SH == 2 ? 3 : 0;               // dimension
+  static constexpr int R = SH == 1 ? 16 : SH == 2 ? 32 : 0;             // rank
 };
+
+// scatter_z with the dimension and rank known at compile time (ProjShape)
+template <int NR, int D, int R>
+__device__ __forceinline__ void scatter_z_c(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int col, int kk,
+                                            double v) {
+  constexpr int C = 1 << D, WP = (C - 1) * R;
+  const int q = col / R, aa = col % R;
+  const int me = static_cast<int>(sg & (C - 1));
+  const int64_t t = ((sg >> D) << D) + (q < me ? q : q + 1);
+  const int tc = static_cast<int>(t & (C - 1));
+  const int qt = me < tc ? me : me - 1;
+  lv.zt[(t - lv.tbase) * (int64_t)(WP * NR) + kk * WP + qt * R + aa] = v;  // [t][rhs][col]
+}
 
 template <int NR, int PAIRS, int SH = 0>
 __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_constant__ StreamArgs a) {
@@ -464,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
             double v = 0.0;
             for (int g = 0; g < RG; ++g) v += red[((int64_t)g * NR + kk) * Wp + col];
             if (kk < a.nr) {
-              if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);
+              if (SH) scatter_z_c<NR, Sh::D, Sh::R>(a, lv, sg, col, kk, v);
+              else if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);
               else scatter_z<NR>(a, lv, sg, col, kk, v);
             }
           }
@@ -569,8 +585,10 @@ cudaError_t launch_sh(const StreamArgs& a, int grid, int64_t smem, cudaStream_t 
 // compile-time shape of this launch (ProjShape), 0 = generic
 int project_shape(const StreamArgs& a, int nr_cap) {
   if (nr_cap != 1 || !a.early || a.adm || a.lpar) return 0;
-  if (a.Wp == 2 * ProjShape<1>::NP && a.Rp == ProjShape<1>::RP) return 1;
-  if (a.Wp == 2 * ProjShape<2>::NP && a.Rp == ProjShape<2>::RP) return 2;
+  if (a.Wp == 2 * ProjShape<1>::NP && a.Rp == ProjShape<1>::RP && a.d == ProjShape<1>::D && a.r == ProjShape<1>::R)
+    return 1;
+  if (a.Wp == 2 * ProjShape<2>::NP && a.Rp == ProjShape<2>::RP && a.d == ProjShape<2>::D && a.r == ProjShape<2>::R)
+    return 2;
   return 0;
 }
 

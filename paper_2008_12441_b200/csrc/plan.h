@@ -111,7 +111,7 @@ struct PlanOptions {
   int ctas_per_sm = 2;
   int stage_cap_bytes = 36 * 1024;  // upper bound on the factor bytes of one stage
   int smem_budget = 200 * 1024;     // dynamic smem per CTA for the pipeline
-  int max_stages_p = 2;             // project: measured best at 2 stages x 2 CTAs per SM
+  int max_stages_p = 3;             // project: measured best at 3 stages x 2 CTAs per SM (early slot release)
   int max_stages_e = 3;             // expand: measured best at 3 stages x 2 CTAs per SM
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
