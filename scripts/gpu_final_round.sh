@@ -1,14 +1,19 @@
 #!/bin/bash
-# Round-end evidence: GPU tests, smoke, bench lines of every config, the c4 launch
-# list and DRAM traffic, full ncu captures of the c2 single-rhs and c5 DMMA kernels.
+# Round-end evidence: GPU tests, smoke, bench lines of every config, the FP64 peak
+# probe, the c4 launch list and DRAM traffic, full ncu captures of the c2 / c4
+# single-rhs kernels and the c5 DMMA kernels.  Then (here, on CPU):
+#   python scripts/summarize_profiles.py r02 && python scripts/summary_table.py r02
 set -u
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+nproc > gpurun_out/nproc.txt
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-timeout 900 python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "bench c4 rc=$?"
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "bench c4 rc=$?"
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref_c4.json 2> gpurun_out/bench_ref_c4.err; echo "ref c4 rc=$?"
 for c in c5 c1 c2 c3 s2 c2strict; do
-  timeout 900 python bench.py --config $c --steps 20 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c rc=$?"
+  timeout 900 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c rc=$?"
 done
+(cd scripts && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu && ./fp64_peak) > gpurun_out/fp64_peak.txt 2>&1; echo "fp64 rc=$?"
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 600 $CMD > gpurun_out/plain_bench.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD > gpurun_out/ncu_launches.log 2>&1

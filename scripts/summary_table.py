@@ -20,7 +20,7 @@ for c in ["c1", "c2", "c3", "c4", "c5", "s2", "c2strict"]:
                 f"{e['value']:,.1f} / {e['blocking']['value']:,.1f} | {cpu['value']:.4g} | "
                 f"{clk['sm_mhz']:.0f}, {', '.join(clk['reasons']) or '-'} |")
 hdr = ("| cfg | matvec/s | ms/step | bound | dominant kernel | achieved | peak | frac | frac of 7.3 TB/s read stream "
-       "| project ms | expand ms | e2e streaming / blocking (matvec/s) | CPU oracle (matvec/s, 1 core) | SM MHz, throttle |\n"
+       "| project ms | expand ms | e2e streaming / blocking (matvec/s) | CPU oracle (matvec/s, all cores) | SM MHz, throttle |\n"
        "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
 print(hdr)
 print("\n".join(rows))
