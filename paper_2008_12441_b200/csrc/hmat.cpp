@@ -72,6 +72,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.early = env_int("HMAT_PROJECT_EARLY", 1);
   o.dmma_ileave = env_int("HMAT_DMMA_ILEAVE", 1);
   o.aflush = env_int("HMAT_PROJECT_AFLUSH", 1);
+  o.dmma_upol = env_int("HMAT_DMMA_UPOL", 0);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
@@ -771,6 +772,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.early = p.early;
   a.dmma_ileave = p.dmma_ileave;
   a.aflush = p.aflush;
+  a.dmma_upol = p.dmma_upol;
   // PDL (expand's launch and prologue overlap project's tail) for whole products;
   // off while the per-kernel profiler brackets the kernels with events
   // and the CTA trace (its memsets sit between the kernels)

@@ -87,6 +87,7 @@ struct StreamArgs {
   int dmma_ileave;           // tensor-core expand: interleaved item order (HMAT_DMMA_ILEAVE)
   int skip_remote;           // standard H^T, P > 1: expand skips near-field blocks of remote neighbours
   int aflush;                // project: asynchronous node flushes (HMAT_PROJECT_AFLUSH)
+  int dmma_upol;             // tensor-core expand: L2 policy of the U / D boxes (HMAT_DMMA_UPOL)
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
   int64_t exch;              // doubles of this pass's exchange levels
   int cross;                 // levels 1..cross are exchange levels

@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   const int64_t abytes = (int64_t)RE * AP * 8, abytes_d = (int64_t)RE * APD * 8;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
   int* done = reinterpret_cast<int*>(full + NS);
-  const uint64_t pol_stream = dev::policy_evict_first();
+  // U / D boxes: read once, but each 36-column box overlaps the next chunk's
+  // first 4 columns, so a policy that keeps them in L2 a little longer saves the
+  // re-read (a.dmma_upol: 0 evict_first, 1 evict_normal)
+  const uint64_t pol_stream = a.dmma_upol == 1 ? dev::policy_evict_normal() : dev::policy_evict_first();
   const uint64_t pol_keep = dev::policy_evict_last();
   auto level_on = [&](int l) -> bool {
     return l == L + 1 ? a.dense != 0 : ((a.level_mask >> (l - 1)) & 1ull) != 0;

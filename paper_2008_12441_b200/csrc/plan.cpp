@@ -81,6 +81,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.dmma_ileave = opt.dmma_ileave;
   p.project_chunk = opt.project_chunk;
   p.aflush = opt.aflush;
+  p.dmma_upol = opt.dmma_upol;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;
