@@ -72,7 +72,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.early = env_int("HMAT_PROJECT_EARLY", 1);
   o.dmma_ileave = env_int("HMAT_DMMA_ILEAVE", 1);
   o.aflush = env_int("HMAT_PROJECT_AFLUSH", 1);
-  o.dmma_upol = env_int("HMAT_DMMA_UPOL", 0);
+  o.dmma_upol = env_int("HMAT_DMMA_UPOL", 1);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
