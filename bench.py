@@ -119,7 +119,10 @@ def alg_bytes(cfg, n_rows, nrhs):
     return {"project": project, "expand": expand, "factor": factor, "total": factor + 16 * n_rows * nrhs}
 
 
-DMMA_MIN_RHS = 5  # the library's default HMAT_DMMA_MIN: from 5 rhs the FP64 tensor-core path runs
+# Roofline of a pass: FP64 tensor pipe when its arithmetic intensity (2 nb flops per
+# 8-byte factor entry, nb = the pass width) exceeds the ridge 37.07 TF / 7.3 TB/s
+# ~ 5 flop/B, i.e. from 32-wide passes (33+ rhs); narrower passes stream HBM.
+TENSOR_BOUND_RHS = 33
 FP64_PEAK_TFLOPS = 37.07  # scripts/fp64_peak.cu, DMMA m8n8k4, this pool (profiles/r01_fp64_peak.txt)
 # Read-only stream ceiling: scripts/hbm_read_peak.cu (bulk-TMA ring, random fp64 data,
 # 800 back-to-back launches under the 1000 W cap), profiles/r01_hbm_read_peak.txt.
@@ -552,7 +555,7 @@ def run_ours(args):
             per_kernel[ph] = {"avg_ms": ms / nl, "launches": nl, "alg_bytes_per_launch": ab[ph] / max(1, (nl // args.steps)),
                               "GBps": ab[ph] / (ms / nl * 1e-3) / 1e9 / max(1, (nl // args.steps))}
     dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_ms"])
-    if nrhs >= DMMA_MIN_RHS:
+    if nrhs >= TENSOR_BOUND_RHS:
         # many right-hand sides: a dense FP64 contraction on the DMMA tensor pipe
         fl = alg_flops(cfg, n, nrhs)
         for ph, d in per_kernel.items():

@@ -160,11 +160,11 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
  * the z of blocks whose parent spans ranks (Steps 2-4), then
  * y_t = sum U_ts z_ts + D_t x_t (Step 5, eq:prod-yuz / eq:prod-ydz,
  * PAPER.md:907-959), expand fused over all levels and the dense leaf blocks.
- * x, y: N_loc x nrhs column-major, device or host.  1-4 rhs
- * run on the SIMT streaming kernels; from 5 rhs, where W % 16 == 0 (W <= 224, or
- * <= 112 if W % 32 != 0), 64 | leaf_size and weak admissibility, on the FP64
- * tensor cores in passes of 64 rhs, the last one 16 or 32 wide when at most
- * 16 / 32 remain.  HMAT_ERR_INVALID: NULL H/x/y, nrhs < 1, x aliasing y.
+ * x, y: N_loc x nrhs column-major, device or host.  1-2 rhs
+ * run on the SIMT streaming kernels; from 3 rhs (HMAT_DMMA_MIN), where W % 16 == 0
+ * (W <= 224, or <= 112 if W % 32 != 0), 64 | leaf_size and weak admissibility, on
+ * the FP64 tensor cores in passes of 64 rhs, the last one 8, 16 or 32 wide when
+ * at most 8 / 16 / 32 remain (other shapes: SIMT passes of up to 4).  HMAT_ERR_INVALID: NULL H/x/y, nrhs < 1, x aliasing y.
  * With P > 1 a collective (same nrhs, same order on every rank); with the
  * EXTERNAL exchange use hmat_project / hmat_expand (HMAT_ERR_UNSUPPORTED). */
 hmat_status hmat_matvec(hmat_t H, const double* x, double* y, int nrhs);
@@ -391,10 +391,10 @@ typedef struct {
   int Rp, Re, tpr, nstage_p, nstage_e, grid_p, grid_e;
   int64_t smem_p, smem_e;
   int max_nr;                 /* widest SIMT pass of right-hand sides                */
-  int dmma;                   /* 1: the FP64 tensor-core path serves >= 5 rhs         */
-  /* tensor-core pass layouts, [0] = 16, [1] = 32, [2] = 64 rhs wide (ok = 0: unused) */
-  int dmma_ok[3], dmma_grid_p[3], dmma_grid_e[3], dmma_stages_p[3], dmma_stages_e[3];
-  int64_t dmma_smem_p[3], dmma_smem_e[3];
+  int dmma;                   /* 1: the FP64 tensor-core path serves >= HMAT_DMMA_MIN (3) rhs */
+  /* tensor-core pass layouts, [0] = 16, [1] = 32, [2] = 64, [3] = 8 rhs wide (ok = 0: unused) */
+  int dmma_ok[4], dmma_grid_p[4], dmma_grid_e[4], dmma_stages_p[4], dmma_stages_e[4];
+  int64_t dmma_smem_p[4], dmma_smem_e[4];
 } hmat_plan_info_t;
 
 /* Validates (depth, dim, leaf_size, rank, nranks, rank_id) exactly like

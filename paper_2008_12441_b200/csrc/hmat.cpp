@@ -61,7 +61,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.max_nr = env_int("HMAT_MAX_NR", o.max_nr);
   o.dmma_max_stages_p = env_int("HMAT_DMMA_STAGES_P", o.dmma_max_stages_p);
   o.dmma_off = env_int("HMAT_DMMA_OFF", 0);
-  o.dmma_min = env_int("HMAT_DMMA_MIN", 5);
+  o.dmma_min = env_int("HMAT_DMMA_MIN", 3);
   o.dbg = env_int("HMAT_DEBUG_SKIP", 0);
   o.expand_chunk = env_int("HMAT_EXPAND_CHUNK", -1);
   o.project_dyn = env_int("HMAT_PROJECT_DYN", 1);
@@ -73,6 +73,8 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dmma_ileave = env_int("HMAT_DMMA_ILEAVE", 1);
   o.aflush = env_int("HMAT_PROJECT_AFLUSH", 1);
   o.dmma_upol = env_int("HMAT_DMMA_UPOL", 1);
+  o.dmma8_ctas = env_int("HMAT_DMMA8_CTAS", 0);
+  o.dmma8_max_stages = env_int("HMAT_DMMA8_STAGES", o.dmma8_max_stages);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
@@ -344,6 +346,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (e = configure_all(p)) || (p.dmma_ok && (e = hmat::configure_dmma(64, p.dl[2].dsmem_p, p.dl[2].dsmem_e))) ||
       (p.dmma_ok && p.dl[1].ok && (e = hmat::configure_dmma(32, p.dl[1].dsmem_p, p.dl[1].dsmem_e))) ||
       (p.dmma_ok && p.dl[0].ok && (e = hmat::configure_dmma(16, p.dl[0].dsmem_p, p.dl[0].dsmem_e))) ||
+      (p.dmma_ok && p.dl[3].ok && (e = hmat::configure_dmma(8, p.dl[3].dsmem_p, p.dl[3].dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
   H->external = p.P > 1 && dist->exchange == HMAT_EXCHANGE_EXTERNAL;
@@ -1370,7 +1373,7 @@ hmat_status hmat_plan_query(int depth, int dim, int leaf_size, int rank, int nra
   info->smem_e = p.lay[0].smem_e;
   info->max_nr = p.max_nr;
   info->dmma = use_dmma(p, p.dmma_min) ? 1 : 0;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     const hmat::Plan::DmmaLayout& d = p.dl[i];
     info->dmma_ok[i] = p.dmma_ok && d.ok ? 1 : 0;
     info->dmma_grid_p[i] = d.dgrid_p;

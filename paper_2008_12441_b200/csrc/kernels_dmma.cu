@@ -39,6 +39,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // k-step kb = w/4, N-tile pair np = n/16, lane = (n%8)*4 + w%4, half = (n/8)%2.
 template <int NB>
 __device__ __forceinline__ int64_t zfrag(int w, int n) {
+  if constexpr (NB == 8)  // one N-tile: [k-step][lane], one double per lane
+    return (int64_t)(w >> 2) * 32 + (n & 7) * 4 + (w & 3);
   return ((((int64_t)(w >> 2) * (NB / 16) + (n >> 4)) * 32 + (n & 7) * 4 + (w & 3)) << 1) + ((n >> 3) & 1);
 }
 
@@ -274,10 +276,10 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 template <int KC, int NB>
 __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int NCW = kThreadsE / 32;
-  constexpr int WM = NB == 16 ? 8 : 4, WN = NCW / WM;  // warp grid over rows x rhs
+  constexpr int WM = NB <= 16 ? 8 : 4, WN = NCW / WM;  // warp grid over rows x rhs
   constexpr int MT = RE / 8 / WM;                      // M-tiles (8 rows) per warp
   constexpr int NTW = NB / 8 / WN;                     // N-tiles per warp (NTW / 2 fragment-major pairs)
-  static_assert(NTW % 2 == 0 && MT * WM * 8 == RE, "expand warp grid");
+  static_assert((NTW == 1 || NTW % 2 == 0) && MT * WM * 8 == RE, "expand warp grid");
   // level stages: KC columns of U (pitch AP = KC + 4); dense stages: KD columns
   // of D (pitch APD) and the KD x NB box of x (pitch XP): KD = 16 with KC = 16, else 32
   constexpr int KD = KC == 16 ? 16 : 32;
@@ -386,12 +388,17 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) av[mt] = As[(wm * 8 * MT + mt * 8 + g) * AP + ks * 4 + tq];
             // fragment-major Zt chunk: k-step ks, N-tile pairs wn*NTW/2 .. + NTW/2 - 1
+            // (NB = 8: the one N-tile, a double per lane)
+            if constexpr (NTW == 1) {
+              bv[0] = Bs[ks * 32 + lane];
+            } else {
 #pragma unroll
-            for (int np = 0; np < NTW / 2; ++np) {
-              const double2 v =
-                  reinterpret_cast<const double2*>(Bs)[(ks * (NB / 16) + wn * (NTW / 2) + np) * 32 + lane];
-              bv[np * 2] = v.x;
-              bv[np * 2 + 1] = v.y;
+              for (int np = 0; np < NTW / 2; ++np) {
+                const double2 v =
+                    reinterpret_cast<const double2*>(Bs)[(ks * (NB / 16) + wn * (NTW / 2) + np) * 32 + lane];
+                bv[np * 2] = v.x;
+                bv[np * 2 + 1] = v.y;
+              }
             }
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
@@ -531,6 +538,39 @@ void launch_p16(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
   }
 }
 
+// NB = 8: one rhs group (NT = 1); W % 32 == 0: MT = W / 32 over 4 column groups,
+// NW = 4; W % 16 == 0: MT = W / 16 over 2 column groups, NW = 2
+void launch_p8(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.W % 32 == 0) {
+    switch (a.W / 32) {
+      case 1: launch_p<1, 1, 4, 8>(a, grid, smem, s); break;
+      case 2: launch_p<2, 1, 4, 8>(a, grid, smem, s); break;
+      case 3: launch_p<3, 1, 4, 8>(a, grid, smem, s); break;
+      case 4: launch_p<4, 1, 4, 8>(a, grid, smem, s); break;
+      case 5: launch_p<5, 1, 4, 8>(a, grid, smem, s); break;
+      case 6: launch_p<6, 1, 4, 8>(a, grid, smem, s); break;
+      default: launch_p<7, 1, 4, 8>(a, grid, smem, s); break;
+    }
+  } else {
+    switch (a.W / 16) {
+      case 1: launch_p<1, 1, 2, 8>(a, grid, smem, s); break;
+      case 3: launch_p<3, 1, 2, 8>(a, grid, smem, s); break;
+      case 5: launch_p<5, 1, 2, 8>(a, grid, smem, s); break;
+      default: launch_p<7, 1, 2, 8>(a, grid, smem, s); break;
+    }
+  }
+}
+
+cudaError_t set_p8(int64_t smem) {
+  cudaError_t e;
+  if ((e = set_p<1, 1, 4, 8>(smem)) || (e = set_p<2, 1, 4, 8>(smem)) || (e = set_p<3, 1, 4, 8>(smem)) ||
+      (e = set_p<4, 1, 4, 8>(smem)) || (e = set_p<5, 1, 4, 8>(smem)) || (e = set_p<6, 1, 4, 8>(smem)) ||
+      (e = set_p<7, 1, 4, 8>(smem)) || (e = set_p<1, 1, 2, 8>(smem)) || (e = set_p<3, 1, 2, 8>(smem)) ||
+      (e = set_p<5, 1, 2, 8>(smem)) || (e = set_p<7, 1, 2, 8>(smem)))
+    return e;
+  return cudaSuccess;
+}
+
 cudaError_t set_p16(int64_t smem) {
   cudaError_t e;
   if ((e = set_p<1, 1, 8, 16>(smem)) || (e = set_p<2, 1, 8, 16>(smem)) || (e = set_p<3, 1, 8, 16>(smem)) ||
@@ -587,7 +627,9 @@ __global__ void peer_sum_kernel(const __grid_constant__ StreamArgs a, double* __
 }  // namespace
 
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
-  if (nb == 16)
+  if (nb == 8)
+    launch_p8(a, grid, smem, s);
+  else if (nb == 16)
     launch_p16(a, grid, smem, s);
   else if (nb == 32)
     launch_p_nb<32>(a, grid, smem, s);
@@ -597,7 +639,9 @@ cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t s
 }
 
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
-  if (nb == 16)
+  if (nb == 8)
+    launch_e<8>(a, grid, smem, s);
+  else if (nb == 16)
     launch_e<16>(a, grid, smem, s);
   else if (nb == 32)
     launch_e<32>(a, grid, smem, s);
@@ -616,6 +660,10 @@ cudaError_t launch_peer_sum(const StreamArgs& a, double* out, cudaStream_t s) {
 
 cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e) {
   cudaError_t e;
+  if (nb == 8) {
+    if ((e = set_p8(smem_p))) return e;
+    return set_e<8>(smem_e);
+  }
   if (nb == 16) {
     if ((e = set_p16(smem_p))) return e;
     return set_e<16>(smem_e);

@@ -228,11 +228,12 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   if (p.dmma_ok) {
     p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
     p.dnw = (p.W % 32 != 0 && opt.dmma_nw == 8) ? 8 : 16;
-    for (int li = 0; li < 3; ++li) {
+    for (int li = 0; li < 4; ++li) {
       Plan::DmmaLayout& d = p.dl[li];
-      d.nb = 16 << li;
-      // project warps: 64 / 32 wide as p.dnw; 16 wide: 8 (W % 32 == 0) or 4 (kernels_dmma.cu)
-      d.nw = d.nb == 16 ? (p.W % 32 == 0 ? 8 : 4) : p.dnw;
+      d.nb = li == 3 ? 8 : 16 << li;
+      // project warps: 64 / 32 wide as p.dnw; 16 wide: 8 (W % 32 == 0) or 4; 8 wide:
+      // 4 or 2 (kernels_dmma.cu)
+      d.nw = d.nb == 8 ? (p.W % 32 == 0 ? 4 : 2) : d.nb == 16 ? (p.W % 32 == 0 ? 8 : 4) : p.dnw;
       // V rows + the nb x columns (pitch dkr + 4 = 4 mod 16 doubles)
       d.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(d.nb) * (p.dkr + 4) * 8, 128);
       const int64_t kd = p.dkc == 16 ? 16 : 32;  // dense-stage columns (kernels_dmma.cu KD)
@@ -243,9 +244,26 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       // two stages do not fit (64 / 32 wide keep their measured budgets)
       int ctas = 16 / d.nw;
       for (;; --ctas) {
-        const int64_t pbudget = d.nb == 16 ? 227 * 1024 / ctas - 1024 : (p.dnw == 8 ? 112 * 1024 : 226 * 1024);
+        const int64_t pbudget = d.nb <= 16 ? 227 * 1024 / ctas - 1024 : (p.dnw == 8 ? 112 * 1024 : 226 * 1024);
         d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / d.dstage_p));
         if (d.dns_p >= 2 || ctas == 1) break;
+      }
+      if (d.nb == 8) {
+        // 8 wide: next to no math per stage, so the pass is a stream; a slot is
+        // refilled only when all (2 or 4) warps are done with it, so about
+        // ctas (stages - 1) stages per SM are in flight -- pick the split of the
+        // shared memory that maximises it (ties: more CTAs), or HMAT_DMMA8_CTAS
+        int best = -1;
+        for (int c = 16 / d.nw; c >= 1; --c) {
+          if (opt.dmma8_ctas > 0 && c != opt.dmma8_ctas) continue;
+          const int64_t budget = 227 * 1024 / c - 1024;
+          const int ns = static_cast<int>(std::min<int64_t>(opt.dmma8_max_stages, (budget - bar_bytes) / d.dstage_p));
+          if (ns >= 2 && c * (ns - 1) > best) {
+            best = c * (ns - 1);
+            ctas = c;
+            d.dns_p = ns;
+          }
+        }
       }
       d.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 16 ? 5 : 3, (112 * 1024 - bar_bytes) / d.dstage_e));
       d.dsmem_p = d.dns_p * d.dstage_p + bar_bytes;
@@ -253,7 +271,9 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas, depth > 0 ? p.N_loc / p.dkr : 0));
       d.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * 2, p.N_loc / kDmmaRE));
       // (a 32-wide project pass with W % 32 != 0 needs the 8-warp grid: kernels_dmma.cu)
-      const bool narrow_on = d.nb == kDmmaNB || (d.nb == 32 ? opt.dmma_narrow >= 1 : opt.dmma_narrow >= 2);
+      const bool narrow_on = d.nb == kDmmaNB || (d.nb == 32   ? opt.dmma_narrow >= 1
+                                                 : d.nb == 16 ? opt.dmma_narrow >= 2
+                                                              : opt.dmma_narrow >= 3);
       d.ok = d.dns_p >= 2 && d.dns_e >= 2 && narrow_on && (d.nb != 32 || p.W % 32 == 0 || p.dnw == 8);
       p.dgrid_p_max = std::max(p.dgrid_p_max, d.dgrid_p);
     }

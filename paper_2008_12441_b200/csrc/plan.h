@@ -82,7 +82,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 5, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per level stage (32; 48 at W = 48; else 16)
@@ -95,11 +95,11 @@ struct Plan {
     int dns_p = 0, dns_e = 0;
     int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
     int dgrid_p = 0, dgrid_e = 0;
-  } dl[3];
+  } dl[4];                          // pass widths 16, 32, 64, and (dl[3]) 8
   int dgrid_p_max = 0;              // partial-sum / ticket slots to allocate (max over dl)
   // the layout of a pass of `nr` right-hand sides: the narrowest that holds them
   const DmmaLayout& dmma_layout(int nr) const {
-    return nr <= 16 && dl[0].ok ? dl[0] : nr <= 32 && dl[1].ok ? dl[1] : dl[2];
+    return nr <= 8 && dl[3].ok ? dl[3] : nr <= 16 && dl[0].ok ? dl[0] : nr <= 32 && dl[1].ok ? dl[1] : dl[2];
   }
 };
 
@@ -116,7 +116,7 @@ struct PlanOptions {
   int adm = 0;                      // structure: 0 = weak, 1 = standard admissibility
   int peer = 0;                     // P > 1 with the in-kernel peer exchange (expand stages hold P z rows)
   // per-call switches, read once at hmat_create (HMAT_* environment)
-  int dmma_off = 0, dmma_min = 5;   // tensor-core path off / from this many rhs (measured crossover)
+  int dmma_off = 0, dmma_min = 3;   // tensor-core path off / from this many rhs (measured crossover, 8-wide passes)
   int dbg = 0;                      // diagnostics (HMAT_DEBUG_SKIP)
   int expand_chunk = -1;            // expand items per dynamic chunk (-1 = default, 0 = static)
   int project_dyn = 1;              // project's last level in dynamic chunks
@@ -125,7 +125,7 @@ struct PlanOptions {
   int max_nr = 4;                   // widest SIMT right-hand-side pass (1, 2, 4 or 8): 8-wide passes
                                     // measured slower than two 4-wide ones (c3: 16.7 vs 14.2 ms)
   int dmma_max_stages_p = 3;        // DMMA project: pipeline depth cap
-  int dmma_narrow = 2;              // DMMA narrow last passes: 0 = none, 1 = 32 wide, 2 = 32 or 16 wide
+  int dmma_narrow = 3;              // DMMA narrow last passes: 0 = none, 1 = 32 wide, 2 = 32 or 16, 3 = 32, 16 or 8 wide
   int dmma_kc = 0;                  // DMMA expand k-columns per level stage (0 = auto: 32 / 48 / 16)
   int pdl = 2;                      // PDL: 0 off, 1 expand after project, 2 also project after the previous kernel
   int lpar = 1;                     // project: level-parallel mode for small operators
@@ -134,6 +134,8 @@ struct PlanOptions {
   int project_chunk = 4;            // project: minimum stages per dynamic chunk of the last level
   int aflush = 1;                   // project: asynchronous node flushes (no CTA barrier per node)
   int dmma_upol = 1;                // tensor-core expand: L2 policy of the U / D boxes (0 first, 1 normal)
+  int dmma8_ctas = 0;               // 8-wide tensor-core project: CTAs per SM (0 = auto)
+  int dmma8_max_stages = 8;         // 8-wide tensor-core project: ring depth cap
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.

@@ -71,10 +71,10 @@ class hmat_plan_info_t(ctypes.Structure):
                 ("Rp", ctypes.c_int), ("Re", ctypes.c_int), ("tpr", ctypes.c_int), ("nstage_p", ctypes.c_int),
                 ("nstage_e", ctypes.c_int), ("grid_p", ctypes.c_int), ("grid_e", ctypes.c_int),
                 ("smem_p", ctypes.c_int64), ("smem_e", ctypes.c_int64),
-                ("max_nr", ctypes.c_int), ("dmma", ctypes.c_int), ("dmma_ok", ctypes.c_int * 3),
-                ("dmma_grid_p", ctypes.c_int * 3), ("dmma_grid_e", ctypes.c_int * 3),
-                ("dmma_stages_p", ctypes.c_int * 3), ("dmma_stages_e", ctypes.c_int * 3),
-                ("dmma_smem_p", ctypes.c_int64 * 3), ("dmma_smem_e", ctypes.c_int64 * 3)]
+                ("max_nr", ctypes.c_int), ("dmma", ctypes.c_int), ("dmma_ok", ctypes.c_int * 4),
+                ("dmma_grid_p", ctypes.c_int * 4), ("dmma_grid_e", ctypes.c_int * 4),
+                ("dmma_stages_p", ctypes.c_int * 4), ("dmma_stages_e", ctypes.c_int * 4),
+                ("dmma_smem_p", ctypes.c_int64 * 4), ("dmma_smem_e", ctypes.c_int64 * 4)]
 
 
 _H = ctypes.c_void_p

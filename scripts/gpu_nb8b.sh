@@ -1,0 +1,9 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_multirank.py tests/test_gpu_peer_ipc.py tests/test_abi.py tests/test_gpu_random_shapes.py -m gpu -x -q > gpurun_out/pytest_nb8.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_nb8.log
+S="WARM=20,REPS=10"
+timeout 900 python scripts/kernel_sweep.py c4 "$S,NRHS=8" "$S,NRHS=8,HMAT_DMMA8_CTAS=4" "$S,NRHS=8,HMAT_DMMA8_CTAS=6" "$S,NRHS=8,HMAT_DMMA8_CTAS=3" "$S,NRHS=4" "$S,NRHS=3" > gpurun_out/nb8b.log 2>&1
+timeout 900 python scripts/kernel_sweep.py c2 "WARM=100,REPS=50,NRHS=8" "WARM=100,REPS=50,NRHS=8,HMAT_DMMA8_CTAS=6" "WARM=100,REPS=50,NRHS=4" "WARM=100,REPS=50,NRHS=16" >> gpurun_out/nb8b.log 2>&1
+timeout 900 python scripts/kernel_sweep.py c3 "WARM=50,REPS=20,NRHS=8" "WARM=50,REPS=20,NRHS=8,HMAT_DMMA8_CTAS=2" "WARM=50,REPS=20,NRHS=4" "WARM=50,REPS=20,NRHS=16" >> gpurun_out/nb8b.log 2>&1
+cat gpurun_out/nb8b.log

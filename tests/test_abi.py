@@ -139,10 +139,10 @@ def test_c_example_runs(tmp_path):
 
 
 @pytest.mark.parametrize("L,d,b,r,dmma,narrow", [
-    (5, 3, 64, 32, 1, (1, 1, 1)),    # c5: W = 224, every pass width
-    (9, 2, 64, 16, 1, (1, 1, 1)),    # c4 shape: W = 48 (8-warp project grid)
-    (3, 3, 64, 8, 0, (0, 0, 0)),     # W = 56: not a multiple of 16 -> SIMT only
-    (3, 2, 32, 16, 0, (0, 0, 0)),    # leaf 32: not a multiple of the 64-row item
+    (5, 3, 64, 32, 1, (1, 1, 1, 1)),    # c5: W = 224, every pass width (16, 32, 64, 8)
+    (9, 2, 64, 16, 1, (1, 1, 1, 1)),    # c4 shape: W = 48 (8-warp project grid)
+    (3, 3, 64, 8, 0, (0, 0, 0, 0)),     # W = 56: not a multiple of 16 -> SIMT only
+    (3, 2, 32, 16, 0, (0, 0, 0, 0)),    # leaf 32: not a multiple of the 64-row item
 ])
 def test_plan_query_reports_tensor_core_layouts(L, d, b, r, dmma, narrow):
     """hmat_plan_query (host only) states which products the tensor-core path
@@ -150,7 +150,7 @@ def test_plan_query_reports_tensor_core_layouts(L, d, b, r, dmma, narrow):
     info = hm.hmat_plan_query(L, d, b, r)
     assert info.dmma == dmma and tuple(info.dmma_ok) == narrow
     assert info.max_nr == 4
-    for i in range(3):
+    for i in range(4):
         if info.dmma_ok[i]:
             assert 2 <= info.dmma_stages_p[i] and 2 <= info.dmma_stages_e[i]
             assert info.dmma_smem_p[i] <= 227 * 1024 and info.dmma_smem_e[i] <= 227 * 1024

@@ -77,6 +77,8 @@ CASES = [
     (HConfig("pdmma3", d=2, L=4, b=64, r=16, seed=309), 8, 64),  # tensor-core path, W = 48
     (HConfig("pdmma3", d=2, L=4, b=64, r=16, seed=309), 4, 7),   # 16-wide pass, W = 48
     (HConfig("pdmma", d=3, L=3, b=64, r=32, seed=305), 2, 12),   # 16-wide pass, W = 224
+    (HConfig("pdmma", d=3, L=3, b=64, r=32, seed=305), 8, 8),    # 8-wide pass, W = 224
+    (HConfig("pdmma3", d=2, L=4, b=64, r=16, seed=309), 8, 6),   # 8-wide pass, W = 48
 ]
 
 

@@ -158,11 +158,12 @@ DMMA = [HConfig("d3L2", d=3, L=2, b=64, r=32, seed=501), HConfig("d3L3", d=3, L=
 
 
 @pytest.mark.parametrize("cfg", DMMA, ids=lambda c: c.name)
-@pytest.mark.parametrize("nrhs", [5, 16, 17, 32, 33, 64, 70, 96])
+@pytest.mark.parametrize("nrhs", [5, 8, 9, 16, 17, 32, 33, 64, 70, 72, 96])
 def test_dmma_many_rhs(cfg, nrhs):
-    """FP64 tensor-core path (nrhs >= 5, W % 16 == 0, 64 | b): passes of 64
-    right-hand sides, the last one 16 or 32 wide when at most 16 / 32 remain
-    (5, 16 | 17, 32 | 70 = 64 + 6 | 96 = 64 + 32), ragged passes, vs the oracle."""
+    """FP64 tensor-core path (nrhs >= 3, W % 16 == 0, 64 | b): passes of 64
+    right-hand sides, the last one 8, 16 or 32 wide when at most 8 / 16 / 32
+    remain (5 | 8, 9 | 16, 17, 32 | 70 = 64 + 6, 72 = 64 + 8 | 96 = 64 + 32),
+    ragged passes, vs the oracle."""
     U, V, D, x = host_case(cfg, nrhs)
     ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
     h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
@@ -172,6 +173,24 @@ def test_dmma_many_rhs(cfg, nrhs):
         hm.hmat_destroy(h)
     assert_parity(gpu_matvec(cfg, U, V, D, x), ref)
 
+
+
+@pytest.mark.parametrize("cfg", [DMMA[0], DMMA[4], DMMA[6], DMMA[7]], ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 2, 3, 4])
+def test_dmma_8wide_pass_few_rhs(cfg, nrhs, monkeypatch):
+    """The 8-wide tensor-core pass (one N-tile: fragment-major Zt of one double
+    per lane) serving 1..4 rhs when the threshold is lowered (HMAT_DMMA_MIN)."""
+    monkeypatch.setenv("HMAT_DMMA_MIN", "1")
+    U, V, D, x = host_case(cfg, nrhs)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        assert hm.hmat_plan_query(cfg.L, cfg.d, cfg.b, cfg.r).dmma_ok[3] == 1
+        y = np.zeros((cfg.N, nrhs), order="F")
+        hm.hmat_matvec(h, np.asfortranarray(x.reshape(cfg.N, nrhs)), y, nrhs)
+        assert_parity(y, ref.reshape(cfg.N, nrhs))
+    finally:
+        hm.hmat_destroy(h)
 
 
 def _dev_cols(x):
