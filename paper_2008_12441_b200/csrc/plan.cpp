@@ -252,9 +252,12 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
         // 8 wide: next to no math per stage, so the pass is a stream; a slot is
         // refilled only when all (2 or 4) warps are done with it, so about
         // ctas (stages - 1) stages per SM are in flight -- pick the split of the
-        // shared memory that maximises it (ties: more CTAs), or HMAT_DMMA8_CTAS
+        // shared memory that maximises it (ties: more CTAs) among >= 3 CTAs per
+        // SM where they fit (c4, 8 rhs: 2 CTAs x 7 stages 12.0 ms, 3 x 4 10.7,
+        // 6 x 2 10.7), or HMAT_DMMA8_CTAS
         int best = -1;
         for (int c = 16 / d.nw; c >= 1; --c) {
+          if (opt.dmma8_ctas <= 0 && c < 3 && best >= 0) break;
           if (opt.dmma8_ctas > 0 && c != opt.dmma8_ctas) continue;
           const int64_t budget = 227 * 1024 / c - 1024;
           const int ns = static_cast<int>(std::min<int64_t>(opt.dmma8_max_stages, (budget - bar_bytes) / d.dstage_p));
