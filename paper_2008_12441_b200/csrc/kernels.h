@@ -88,6 +88,8 @@ struct StreamArgs {
   int skip_remote;           // standard H^T, P > 1: expand skips near-field blocks of remote neighbours
   int aflush;                // project: asynchronous node flushes (HMAT_PROJECT_AFLUSH)
   int dmma_upol;             // tensor-core expand: L2 policy of the U / D boxes (HMAT_DMMA_UPOL)
+  int64_t pchunk;            // tensor-core project: stages per chunk of the level interleave (0 = off)
+  double* accbuf;            // tensor-core project: [grid][L][W NB] running sums between chunks
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)
   int64_t exch;              // doubles of this pass's exchange levels
   int cross;                 // levels 1..cross are exchange levels

@@ -82,6 +82,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.project_chunk = opt.project_chunk;
   p.aflush = opt.aflush;
   p.dmma_upol = opt.dmma_upol;
+  p.dmma_pchunk = opt.dmma_pchunk;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;
@@ -268,7 +269,11 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
           }
         }
       }
-      d.dns_e = static_cast<int>(std::min<int64_t>(p.dkc == 16 ? 5 : 3, (112 * 1024 - bar_bytes) / d.dstage_e));
+      // expand ring: 5 stages of 16-column chunks, 3 of wider ones (64 / 32 rhs);
+      // narrow passes (<= 16 rhs) carry little math per stage, so deeper rings
+      // keep more bytes in flight (HMAT_DMMA_STAGES_E caps them)
+      const int cap_e = d.nb <= 16 && opt.dmma_stages_e_narrow > 0 ? opt.dmma_stages_e_narrow : (p.dkc == 16 ? 5 : 3);
+      d.dns_e = static_cast<int>(std::min<int64_t>(cap_e, (112 * 1024 - bar_bytes) / d.dstage_e));
       d.dsmem_p = d.dns_p * d.dstage_p + bar_bytes;
       d.dsmem_e = d.dns_e * d.dstage_e + bar_bytes;
       d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas, depth > 0 ? p.N_loc / p.dkr : 0));

@@ -82,7 +82,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1, dmma_pchunk = 32;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per level stage (32; 48 at W = 48; else 16)
@@ -136,6 +136,8 @@ struct PlanOptions {
   int dmma_upol = 1;                // tensor-core expand: L2 policy of the U / D boxes (0 first, 1 normal)
   int dmma8_ctas = 0;               // 8-wide tensor-core project: CTAs per SM (0 = auto)
   int dmma8_max_stages = 8;         // 8-wide tensor-core project: ring depth cap
+  int dmma_pchunk = 32;             // <= 16-wide tensor-core project: stages per level-interleaved chunk
+  int dmma_stages_e_narrow = 0;     // <= 16-wide tensor-core expand: ring depth cap (0: 5 / 3 as wider passes)
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.
