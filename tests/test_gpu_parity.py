@@ -534,3 +534,31 @@ def test_power_iteration_back_to_back_products(monkeypatch):
     for k in range(10):
         ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, ref)
     assert np.linalg.norm(outs[1] - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("cfg", [HConfig("ck48", d=2, L=5, b=64, r=16, seed=511),    # W = 48
+                                 HConfig("ck16", d=1, L=11, b=64, r=16, seed=512),   # W = 16
+                                 HConfig("ck80", d=1, L=10, b=128, r=80, seed=513),  # W = 80
+                                 HConfig("ck112", d=3, L=3, b=64, r=16, seed=514)],  # W = 112
+                         ids=lambda c: c.name)
+@pytest.mark.parametrize("chunk", [1, 3, 7])
+def test_dmma_project_level_chunks(cfg, chunk, monkeypatch):
+    """8-wide passes interleave the levels in chunks of HMAT_DMMA_PCHUNK stages of
+    each CTA's range, carrying the running sums between chunks (kernels_dmma.cu);
+    small chunks put chunk boundaries inside nodes of every level.  The result is
+    the oracle's and bit-identical to the unchunked level order (each level's
+    stages are summed in the same order)."""
+    U, V, D, x = host_case(cfg, 8)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    outs = []
+    for ch in (chunk, 0):
+        monkeypatch.setenv("HMAT_DMMA_PCHUNK", str(ch))
+        h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+        try:
+            y = np.zeros((cfg.N, 8), order="F")
+            hm.hmat_matvec(h, np.asfortranarray(x), y, 8)
+            outs.append(y)
+        finally:
+            hm.hmat_destroy(h)
+    assert_parity(outs[0], ref)
+    assert np.array_equal(outs[0], outs[1])
