@@ -638,7 +638,9 @@ def run_ours(args):
             "step_ms": {"mean": float(step_ms.mean()), "median": float(np.median(step_ms)),
                         "min": float(step_ms.min()), "max": float(step_ms.max()), "n": int(len(step_ms)),
                         "how": "a second pass of the K steps with a CUDA event after each step, max over ranks "
-                               f"per step; {nvec} distinct seeded x (PAPER.md:1129-1130 averages 128)"},
+                               f"per step; {nvec} distinct seeded x (PAPER.md:1129-1130 averages 128); the events "
+                               "between steps cost the cross-step launch overlap, so this pass runs a little slower "
+                               "than the plain one that gives `value`"},
             "factor_GBps": factor_gbps,
             "alg_GBps": ab["total"] * world / (ms_step * 1e-3) / 1e9,
             "roofline": roof,
