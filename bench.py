@@ -312,6 +312,31 @@ def cpu_baseline_record(cfg):
     }
 
 
+def environment():
+    """The report record's environment fields."""
+    import platform
+    env = {"host_cores": len(os.sched_getaffinity(0)), "glibc": "-".join(platform.libc_ver())}
+    try:
+        with open("/proc/cpuinfo") as f:
+            env["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    try:
+        import torch
+        env["torch"] = torch.__version__
+        env["cuda_runtime"] = torch.version.cuda
+        if torch.cuda.is_available():
+            env["gpu_name"] = torch.cuda.get_device_name()
+            v = torch.cuda.nccl.version()
+            env["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+        out = subprocess.run(["nvidia-smi", "--query-gpu=driver_version", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=10)
+        env["driver"] = out.stdout.strip().splitlines()[0] if out.returncode == 0 and out.stdout.strip() else None
+    except Exception:
+        pass
+    return env
+
+
 def workload_config(cfg):
     """The `config` object of both arms (same workload, same keys)."""
     return {"workload": workload_desc(cfg), "N": cfg.N, "nrhs": cfg.nrhs, "factor_bytes": cfg.factor_bytes,
@@ -617,6 +642,12 @@ def run_ours(args):
                 "read_stream_source": "scripts/hbm_read_peak.cu sustained bulk-TMA read ring (profiles/r01_hbm_read_peak.txt)"}
 
     value = 1e3 / ms_step  # matvecs/s of the whole job (one operator across all ranks)
+    # bytes of the packed cross-GPU exchange buffer per pass (0 at P = 1), per step
+    exch_width = min(nrhs, 64)
+    try:
+        exch_doubles = hm.hmat_exchange_size(h, exch_width) if world > 1 else 0
+    except Exception:
+        exch_doubles = 0
     # every rank's communicator spans the whole job (NCCL's own count for NCCL / TREE)
     cn = torch.tensor([comm_nranks], device="cuda")
     if world > 1:
@@ -651,6 +682,9 @@ def run_ours(args):
             "phase_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
             "profiled_ms_per_step": ms_prof_step,
             "setup_s": setup_s,
+            "vec_matvecs_per_s": value * nrhs,
+            "exchange_bytes_per_step": 8 * exch_doubles * ((nrhs + exch_width - 1) // exch_width),
+            "env": environment(),
         }
         print(json.dumps(line), flush=True)
     barrier()  # peer mailboxes are mapped by every rank: free them together

@@ -56,8 +56,10 @@ __device__ __forceinline__ bool peer_wait_flags(const StreamArgs& a) {
       __nanosleep(256);
       if (static_cast<int64_t>(dev::globaltimer_ns() - t0) > a.peer_timeout_ns) {
         // error word: bit 31 | missing rank << 16 | low 16 bits of the pass number
-        atomicCAS(a.err, 0u, 0x80000000u | (static_cast<unsigned int>(g) << 16) |
-                                 static_cast<unsigned int>(a.epoch & 0xffffu));
+        // (a plain store: atomics on host-mapped memory need platform support, and
+        // any waiter's report will do)
+        *reinterpret_cast<volatile unsigned int*>(a.err) =
+            0x80000000u | (static_cast<unsigned int>(g) << 16) | static_cast<unsigned int>(a.epoch & 0xffffu);
         __threadfence_system();
         return false;
       }
