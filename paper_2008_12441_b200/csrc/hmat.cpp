@@ -181,6 +181,7 @@ struct hmat_s {
   uint64_t epoch = 0;
   std::vector<void*> opened;  // IPC mappings to close
   int zt_cap = 1;         // rhs width of the z-buffer layout last written (zeroed at create)
+  int zt_nb_d = 0;        // tensor-core pass width of the DMMA z-buffer layout last written (0: never)
   bool prof = false;
   // per-CTA trace of the last project / expand launch (hmat_cta_trace)
   unsigned long long* trace = nullptr;
@@ -392,7 +393,8 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
   if (p.adm) {  // interaction-list slot tables for the project kernel's scatter
     int16_t code[3][8][hmat::kStdMaxSlots], slot[3][8][hmat::kStdMaxCodes];  // ~20 KB, per call
     hmat::std_slot_tables(code, slot);
-    if ((e = hmat::init_std_tables(&code[0][0][0], &slot[0][0][0])) != cudaSuccess)
+    if ((e = hmat::init_std_tables(&code[0][0][0], &slot[0][0][0])) != cudaSuccess ||
+        (p.dmma_ok && (e = hmat::init_std_tables_dmma(&code[0][0][0], &slot[0][0][0])) != cudaSuccess))
       return bail(cuda_fail(e, "init_std_tables"));
   }
   if (p.P > 1 && !H->external && !peer) {
@@ -458,14 +460,16 @@ hmat_status encode_map(CUtensorMap* m, int rank, const void* base, const uint64_
 
 bool use_dmma(const hmat::Plan& p, int nrhs) {
   if (!p.dmma_ok || p.dmma_off) return false;
-  return nrhs >= p.dmma_min;
+  // standard admissibility: one SIMT pass serves up to 4 rhs faster than the
+  // sliced tensor-core project (s2, 4 rhs: 9.9 vs 18.4 ms; 8 rhs: 19.9 vs 18.4)
+  return nrhs >= (p.adm ? std::max(p.dmma_min, 5) : p.dmma_min);
 }
 
 hmat_status ensure_dmma(hmat_s* H) {
   if (H->cnt_d) return HMAT_OK;
   const hmat::Plan& p = H->plan;
   const size_t zrow = size_t(p.W) * hmat::kDmmaNB * sizeof(double);
-  const size_t tickets = size_t(p.dgrid_p_max) * p.L * sizeof(int) + 256;
+  const size_t tickets = size_t(p.dgrid_p_max) * p.L * std::max(1, p.nslice) * sizeof(int) + 256;  // per slice
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zloc_d), std::max<size_t>(256, size_t(p.z_local_rows) * zrow)));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zex_d), std::max<size_t>(256, size_t(p.z_exch_rows) * zrow)));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->part_d),
@@ -860,7 +864,13 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       const uint32_t ubox[3] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaRE), 1};
       if ((st3 = encode_map(&a.tm_u, 3, a.U, dims, strides, ubox)) != HMAT_OK) return st3;
     }
-    {  // D-role panel [N_loc][Dp], box [64][KC+4]
+    if (p.adm) {  // the nd near-field D-role panels [nd][N_loc][Dp], box [1][64][KC+4]
+      const uint64_t dims[3] = {uint64_t(p.Dp), uint64_t(n), uint64_t(p.nd)};
+      const uint64_t strides[2] = {uint64_t(p.Dp) * 8, uint64_t(p.d_stride) * 8};
+      const uint32_t box[3] = {uint32_t((p.dkc == 16 ? 16 : 32) + 4), uint32_t(hmat::kDmmaRE), 1};
+      hmat_status st3 = encode_map(&a.tm_d, 3, a.D, dims, strides, box);
+      if (st3 != HMAT_OK) return st3;
+    } else {  // D-role panel [N_loc][Dp], box [64][KC+4]
       const uint64_t dims[2] = {uint64_t(p.Dp), uint64_t(n)};
       const uint64_t strides[1] = {uint64_t(p.Dp) * 8};
       const uint32_t box[2] = {uint32_t((p.dkc == 16 ? 16 : 32) + 4), uint32_t(hmat::kDmmaRE)};  // dense stage columns
@@ -869,10 +879,20 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     for (int c0 = 0; c0 < nrhs; c0 += hmat::kDmmaNB) {
       a.nr = nrhs - c0 < hmat::kDmmaNB ? nrhs - c0 : hmat::kDmmaNB;
+      a.wslice = p.wslice;
+      a.nslice = p.nslice;
       a.accbuf = H->accbuf_d;
       // the pass width: 32 when at most 32 rhs remain (half the work), else 64
       const hmat::Plan::DmmaLayout& dl = p.dmma_layout(a.nr);
       const int nb = dl.nb;
+      // standard admissibility: slots whose partner lies outside the domain are
+      // never written and must read as zero; a pass of another width leaves values
+      // at other positions of the fragment-major rows, so clear on a width change
+      if (p.adm && H->zt_nb_d != nb && (phases & kPhaseProject)) {
+        CUDA_TRY(cudaMemsetAsync(H->zloc_d, 0, std::max<size_t>(256, size_t(p.z_local_rows) * p.W * hmat::kDmmaNB * 8),
+                                 H->stream));
+        H->zt_nb_d = nb;
+      }
       a.dnw = dl.nw;
       // 8-wide passes on narrow panels: level-interleaved chunks, so x (nb/W of
       // the V bytes per level: 1/6 at W = 48) is re-read from L2, not DRAM

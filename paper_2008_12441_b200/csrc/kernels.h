@@ -86,6 +86,7 @@ struct StreamArgs {
   int early;                 // project: release a ring slot before the FMAs (HMAT_PROJECT_EARLY)
   int dmma_ileave;           // tensor-core expand: interleaved item order (HMAT_DMMA_ILEAVE)
   int skip_remote;           // standard H^T, P > 1: expand skips near-field blocks of remote neighbours
+  int wslice, nslice;        // tensor-core project: column slices of the panel (gridDim.y = nslice)
   int aflush;                // project: asynchronous node flushes (HMAT_PROJECT_AFLUSH)
   int dmma_upol;             // tensor-core expand: L2 policy of the U / D boxes (HMAT_DMMA_UPOL)
   int64_t pchunk;            // tensor-core project: stages per chunk of the level interleave (0 = off)
@@ -130,9 +131,10 @@ cudaError_t launch_expand(const StreamArgs& a, int nr_cap, int grid, int64_t sme
 // (PDL: its CTAs may start while that kernel's last CTAs finish; the kernel
 // calls griddepcontrol.wait before reading what the previous one wrote).
 template <typename Kernel>
-cudaError_t launch_pdl(Kernel kernel, const StreamArgs& a, int grid, int threads, int64_t smem, cudaStream_t s) {
+cudaError_t launch_pdl(Kernel kernel, const StreamArgs& a, int grid, int threads, int64_t smem, cudaStream_t s,
+                       int grid_y = 1) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.gridDim = dim3(static_cast<unsigned>(grid), static_cast<unsigned>(grid_y));
   cfg.blockDim = dim3(static_cast<unsigned>(threads));
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = s;
@@ -177,6 +179,9 @@ cudaError_t launch_std_tadd(double* y, int64_t ldy, double alpha, const double* 
                             int bpad, cudaStream_t s);
 // D^T of every dense leaf block (for H^T x); one-time helper.
 cudaError_t launch_transpose_leaf_blocks(const double* D, double* Dt, int64_t n_leaves, int b, int Dp, cudaStream_t s);
+// Standard admissibility on the tensor-core path: the slot tables of the
+// interaction lists (as init_std_tables) for kernels_dmma.cu's constant memory.
+cudaError_t init_std_tables_dmma(const int16_t* code, const int16_t* slot);
 // Opt the kernels into large dynamic shared memory (once per device).
 cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e);  // max over layouts
 

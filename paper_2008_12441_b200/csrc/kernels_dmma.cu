@@ -19,6 +19,7 @@
 // Pipelines, CTA splits and the deterministic ticketed reduction of node
 // partials are the same as in the single-vector kernels.
 #include "device_utils.cuh"
+#include "geometry.cuh"
 #include "kernels.h"
 #include "peer.cuh"
 
@@ -45,6 +46,31 @@ __device__ __forceinline__ int64_t zfrag(int w, int n) {
 }
 
 __device__ __forceinline__ int64_t owner_of(int64_t k, int64_t S, int64_t G) { return ((k + 1) * G - 1) / S; }
+
+// Standard admissibility: the interaction-list slot tables (the
+// same as kernels_project.cu's, written by init_std_tables_dmma).
+__constant__ int16_t c_std_code_d[3][8][kStdMaxSlots];
+__constant__ int16_t c_std_slot_d[3][8][kStdMaxCodes];
+
+// Column w = q r + aa of source node sg's z at `level`, standard admissibility:
+// target t = slot q of sg (child sigma of the parent's neighbour e), into t's
+// column qt r + aa (qt = slot of sg in t's list).  nullptr when the partner box
+// lies outside the domain (the block does not exist).
+template <int NB>
+__device__ __forceinline__ double* zt_column_std(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int level,
+                                                 int q, int aa) {
+  const int d = a.d, c = a.c;
+  const int tau = static_cast<int>(sg & (c - 1));
+  const int code = c_std_code_d[d - 1][tau][q];
+  const int e = code >> d, sigma = code & (c - 1);
+  int px[3];
+  geo::morton_decode(d, sg >> d, level - 1, px);
+  if (!((geo::near_mask(d, px, 1 << (level - 1)) >> e) & 1u)) return nullptr;
+  const int64_t t = geo::neighbour(d, px, e, level - 1) * c + sigma;
+  const int nd = d == 1 ? 3 : d == 2 ? 9 : 27;
+  const int qt = c_std_slot_d[d - 1][sigma][(nd - 1 - e) * c + tau];  // eps -> -eps, sigma <-> tau
+  return lv.zt + (t - lv.tbase) * (int64_t)a.W * NB + zfrag<NB>(qt * a.r + aa, 0);
+}
 
 // Column w = q r + aa of source node sg's z goes to target t = sib(sg, q), into
 // t's column qt r + aa (qt = slot of sg in t's list).  Returns the Zt block of t
@@ -87,8 +113,11 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t G = gridDim.x, bid = blockIdx.x;
-  const int W = a.W, Wp = a.Wp, L = a.L;
+  const int Wp = a.Wp, L = a.L;
   const int VP = a.vp;                     // smem pitch of V rows (= 4 mod 16)
+  // column slice of this CTA: [c0, c0 + WS) of the W panel columns (a panel wider
+  // than one CTA's register-resident node tile, standard admissibility: W = M r)
+  const int WS = a.wslice, c0 = static_cast<int>(blockIdx.y) * WS;
   const int64_t SL = a.N_loc / KR;
   const int64_t GL = G < SL ? G : SL;
   const int NS = a.nstage_p;
@@ -125,7 +154,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
   };
   auto issue = [&](int sl) {  // one thread: the next stage into slot sl
     dev::mbar_arrive_expect_tx(&full[sl], stage_tx);
-    dev::tma_load_3d(smem + sl * a.stage_bytes_p, &a.tm_v, 0, static_cast<int>(kr * KR), lr - 1, &full[sl],
+    dev::tma_load_3d(smem + sl * a.stage_bytes_p, &a.tm_v, c0, static_cast<int>(kr * KR), lr - 1, &full[sl],
                      pol_stream);
     dev::tma_load_2d(smem + sl * a.stage_bytes_p + vbytes, &a.tm_x, static_cast<int>(kr * KR), 0, &full[sl],
                      pol_keep);
@@ -229,15 +258,15 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           // column w = q r + aa; rhs n = 8 NT ng + 8 nt + 2 tq + h
-          const int w = (mg * MT + mt) * 8 + g;
+          const int w = c0 + (mg * MT + mt) * 8 + g;
           const int q = w / a.r;
-          double* zc = zt_column<NB>(a, lv, sg, q, w - q * a.r);
+          double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, w - q * a.r) : zt_column<NB>(a, lv, sg, q, w - q * a.r);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int n = (ng * NT + nt) * 8 + tq * 2 + h;
-              if (n < a.nr) zc[zfrag<NB>(0, n)] = acc[mt][nt][h];
+              if (n < a.nr && zc) zc[zfrag<NB>(0, n)] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -246,7 +275,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
         double* pp = a.part + (((int64_t)(l - 1) * G + bid) * 2 + myslot) * (int64_t)Wp * NB;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
-          const int w = (mg * MT + mt) * 8 + g;
+          const int w = c0 + (mg * MT + mt) * 8 + g;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -258,7 +287,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
         __threadfence();
         dev::named_bar_sync(1, CTP);
         const int64_t b0 = owner_of(sa, SL, GL), b1 = owner_of(sb - 1, SL, GL);
-        int* ticket = a.cnt + (int64_t)(l - 1) * G + b1;
+        int* ticket = a.cnt + ((int64_t)(l - 1) * G + b1) * gridDim.y + blockIdx.y;  // per column slice
         if (tid == 0) {
           const int prev = atomicAdd(ticket, 1);
           *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
@@ -270,14 +299,17 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
           // thread: rhs n = tid % NB, columns w = tid / NB, + CTP / NB, ... (CTP is a multiple of NB)
           const int n = tid % NB, wstep = CTP / NB;
           const int64_t zn = zfrag<NB>(0, n);
-          int w = tid / NB, q = w / a.r, aa = w - q * a.r;
+          int w = c0 + tid / NB, q = w / a.r, aa = w - q * a.r;
           const int64_t ps = (int64_t)Wp * NB;
           const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
           const double* p1 = a.part + (((int64_t)(l - 1) * G + b0 + 1) * 2) * ps;
-          for (; w < W; w += wstep) {
+          for (; w < c0 + WS; w += wstep) {
             const int64_t off = (int64_t)w * NB + n;
             const double v = dev::sum_cg(dev::ld_cg(p0 + off), p1 + off, 2 * ps, b1 - b0);
-            if (n < a.nr) zt_column<NB>(a, lv, sg, q, aa)[zn] = v;
+            if (n < a.nr) {
+              double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, aa) : zt_column<NB>(a, lv, sg, q, aa);
+              if (zc) zc[zn] = v;
+            }
             for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
           }
           if (tid == 0) *ticket = 0;
@@ -348,33 +380,55 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   // re-read (a.dmma_upol: 0 evict_first, 1 evict_normal)
   const uint64_t pol_stream = a.dmma_upol == 1 ? dev::policy_evict_normal() : dev::policy_evict_first();
   const uint64_t pol_keep = dev::policy_evict_last();
-  auto level_on = [&](int l) -> bool {
-    return l == L + 1 ? a.dense != 0 : ((a.level_mask >> (l - 1)) & 1ull) != 0;
+  // Dense stages: the leaf-diagonal block (weak, stage L + 1), or the 3^d
+  // near-field blocks of the tile's leaf (standard admissibility, stages L + 1 + e
+  // for the neighbours e inside the domain, one GPU).  nmask: the present ones.
+  const int ndn = a.adm ? a.nd : 1;
+  const int64_t lbase = a.row0 / b;
+  auto near_of = [&](int64_t item) -> uint32_t {
+    if (!a.adm) return 1u;
+    int x[3];
+    geo::morton_decode(a.d, lbase + item * RE / b, L, x);
+    return geo::near_mask(a.d, x, 1 << L);
   };
-  // refill cursor (item jr, level lr in 1..L+1 (L+1 = dense), chunk kcr): identical in every warp
+  auto level_on = [&](int l, uint32_t nmask) -> bool {
+    return l > L ? a.dense != 0 && ((nmask >> (l - L - 1)) & 1u) : ((a.level_mask >> (l - 1)) & 1ull) != 0;
+  };
+  // refill cursor (item jr, level lr in 1..L+ndn (> L: dense), chunk kcr): identical in every warp
   int64_t jr = j0;
   int lr = 1, kcr = 0;
+  uint32_t pmask = jr < j1 ? near_of(jr) : 1u;
   bool any = false;
-  for (int l = 1; l <= L + 1; ++l) any = any || level_on(l);
+  for (int l = 1; l <= L + ndn; ++l) any = any || level_on(l, a.adm ? 1u << ((a.nd - 1) / 2) : 1u);  // (self)
   if (!any) jr = j1;
-  while (jr < j1 && !level_on(lr)) ++lr;
+  while (jr < j1 && !level_on(lr, pmask)) ++lr;
   auto advance = [&]() {
-    if (++kcr < (lr == L + 1 ? kcd : kcw)) return;
+    if (++kcr < (lr > L ? kcd : kcw)) return;
     kcr = 0;
     do {
-      if (++lr > L + 1) {
+      if (++lr > L + ndn) {
         lr = 1;
         jr += jst;
+        pmask = jr < j1 ? near_of(jr) : 1u;
       }
-    } while (!level_on(lr));
+    } while (jr < j1 && !level_on(lr, pmask));
   };
   auto issue = [&](int sl) {  // one thread: stage (jr, lr, kcr) into slot sl
     unsigned char* st = smem + sl * a.stage_bytes_e;
     const int i0 = static_cast<int>(jr * RE);
-    if (lr == L + 1) {
+    if (lr > L) {
       dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes_d + NB * XP * 8));
-      dev::tma_load_2d(st, &a.tm_d, kcr * KD, i0, &full[sl], pol_stream);
-      dev::tma_load_2d(st + abytes_d, &a.tm_xe, (i0 / b) * b + kcr * KD, 0, &full[sl], pol_keep);
+      if (a.adm) {  // near-field block e: panel e of the D-role panels, x of neighbour leaf e
+        const int e = lr - L - 1;
+        int x[3];
+        geo::morton_decode(a.d, lbase + i0 / b, L, x);
+        const int64_t nleaf = geo::neighbour(a.d, x, e, L) - lbase;
+        dev::tma_load_3d(st, &a.tm_d, kcr * KD, i0, e, &full[sl], pol_stream);
+        dev::tma_load_2d(st + abytes_d, &a.tm_xe, static_cast<int>(nleaf * b) + kcr * KD, 0, &full[sl], pol_keep);
+      } else {
+        dev::tma_load_2d(st, &a.tm_d, kcr * KD, i0, &full[sl], pol_stream);
+        dev::tma_load_2d(st + abytes_d, &a.tm_xe, (i0 / b) * b + kcr * KD, 0, &full[sl], pol_keep);
+      }
     } else {
       const LevelArgs& lv = a.lv[lr];
       const double* zt = lv.zt + ((a.row0 + i0) / lv.m - lv.tbase) * (int64_t)W * NB;
@@ -411,9 +465,10 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int k = 0; k < NTW; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
-    for (int l = 1; l <= L + 1; ++l) {
-      const bool is_d = (l == L + 1);
-      if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+    const uint32_t cmask = near_of(j);
+    for (int l = 1; l <= L + ndn; ++l) {
+      const bool is_d = (l > L);
+      if (!level_on(l, cmask)) continue;
       const int nkc = is_d ? kcd : kcw;
       for (int kc = 0; kc < nkc; ++kc) {
         dev::mbar_wait(&full[slot], phase);
@@ -497,10 +552,11 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
 
 template <int MT, int NT, int NW, int NB>
 void launch_p(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  const int gy = a.nslice > 0 ? a.nslice : 1;  // column slices
   if (a.pdl_p)
-    launch_pdl(project_dmma_kernel<kDmmaKR, MT, NT, NW, NB>, a, grid, NW * 32, smem, s);
+    launch_pdl(project_dmma_kernel<kDmmaKR, MT, NT, NW, NB>, a, grid, NW * 32, smem, s, gy);
   else
-    project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<grid, NW * 32, smem, s>>>(a);
+    project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<dim3(grid, gy), NW * 32, smem, s>>>(a);
 }
 
 template <int MT, int NT, int NW, int NB>
@@ -516,8 +572,8 @@ cudaError_t set_p(int64_t smem) {
 template <int NB>
 void launch_p_nb(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
   constexpr int NT64 = NB == 64 ? 2 : 1;
-  if (a.W % 32 == 0) {
-    switch (a.W / 32) {
+  if (a.wslice % 32 == 0) {
+    switch (a.wslice / 32) {
       case 1: launch_p<1, NT64, 16, NB>(a, grid, smem, s); break;
       case 2: launch_p<2, NT64, 16, NB>(a, grid, smem, s); break;
       case 3: launch_p<3, NT64, 16, NB>(a, grid, smem, s); break;
@@ -527,14 +583,14 @@ void launch_p_nb(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
       default: launch_p<7, NT64, 16, NB>(a, grid, smem, s); break;
     }
   } else if (a.dnw == 8) {  // 2 column groups (W/16 M-tiles) x NB/8/NT rhs groups, 2 CTAs per SM
-    switch (a.W / 16) {
+    switch (a.wslice / 16) {
       case 1: launch_p<1, NT64, 8, NB>(a, grid, smem, s); break;
       case 3: launch_p<3, NT64, 8, NB>(a, grid, smem, s); break;
       case 5: launch_p<5, NT64, 8, NB>(a, grid, smem, s); break;
       default: launch_p<7, NT64, 8, NB>(a, grid, smem, s); break;
     }
   } else if constexpr (NB == 64) {  // (NB = 32 needs dnw = 8 here: plan.cpp)
-    switch (a.W / 16) {
+    switch (a.wslice / 16) {
       case 1: launch_p<1, 1, 16, 64>(a, grid, smem, s); break;
       case 3: launch_p<3, 1, 16, 64>(a, grid, smem, s); break;
       case 5: launch_p<5, 1, 16, 64>(a, grid, smem, s); break;
@@ -558,8 +614,8 @@ cudaError_t set_p_nb(int64_t smem) {
 // NB = 16: NT = 1 (2 rhs groups); W % 32 == 0: MT = W / 32 over 4 column groups,
 // NW = 8; W % 16 == 0: MT = W / 16 over 2 column groups, NW = 4
 void launch_p16(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  if (a.W % 32 == 0) {
-    switch (a.W / 32) {
+  if (a.wslice % 32 == 0) {
+    switch (a.wslice / 32) {
       case 1: launch_p<1, 1, 8, 16>(a, grid, smem, s); break;
       case 2: launch_p<2, 1, 8, 16>(a, grid, smem, s); break;
       case 3: launch_p<3, 1, 8, 16>(a, grid, smem, s); break;
@@ -569,7 +625,7 @@ void launch_p16(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
       default: launch_p<7, 1, 8, 16>(a, grid, smem, s); break;
     }
   } else {
-    switch (a.W / 16) {
+    switch (a.wslice / 16) {
       case 1: launch_p<1, 1, 4, 16>(a, grid, smem, s); break;
       case 3: launch_p<3, 1, 4, 16>(a, grid, smem, s); break;
       case 5: launch_p<5, 1, 4, 16>(a, grid, smem, s); break;
@@ -581,8 +637,8 @@ void launch_p16(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
 // NB = 8: one rhs group (NT = 1); W % 32 == 0: MT = W / 32 over 4 column groups,
 // NW = 4; W % 16 == 0: MT = W / 16 over 2 column groups, NW = 2
 void launch_p8(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  if (a.W % 32 == 0) {
-    switch (a.W / 32) {
+  if (a.wslice % 32 == 0) {
+    switch (a.wslice / 32) {
       case 1: launch_p<1, 1, 4, 8>(a, grid, smem, s); break;
       case 2: launch_p<2, 1, 4, 8>(a, grid, smem, s); break;
       case 3: launch_p<3, 1, 4, 8>(a, grid, smem, s); break;
@@ -592,7 +648,7 @@ void launch_p8(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
       default: launch_p<7, 1, 4, 8>(a, grid, smem, s); break;
     }
   } else {
-    switch (a.W / 16) {
+    switch (a.wslice / 16) {
       case 1: launch_p<1, 1, 2, 8>(a, grid, smem, s); break;
       case 3: launch_p<3, 1, 2, 8>(a, grid, smem, s); break;
       case 5: launch_p<5, 1, 2, 8>(a, grid, smem, s); break;
@@ -696,6 +752,12 @@ cudaError_t launch_peer_sum(const StreamArgs& a, double* out, cudaStream_t s) {
   if (grid > 148) grid = 148;
   peer_sum_kernel<<<static_cast<int>(grid), 256, 0, s>>>(a, out);
   return cudaGetLastError();
+}
+
+cudaError_t init_std_tables_dmma(const int16_t* code, const int16_t* slot) {
+  cudaError_t e = cudaMemcpyToSymbol(c_std_code_d, code, sizeof(int16_t) * 3 * 8 * kStdMaxSlots);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(c_std_slot_d, slot, sizeof(int16_t) * 3 * 8 * kStdMaxCodes);
 }
 
 cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e) {

@@ -222,19 +222,32 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   // expand k-chunk of a level stage: 32 columns (W % 32 == 0), the whole level at
   // W = 48 (the c2 / c4 shape: a third of the stages of 16-column chunks), else 16;
   // dense stages are 32 columns of D (kernels_dmma.cu KD)
-  p.dkc = opt.dmma_kc > 0 ? opt.dmma_kc : p.W % 32 == 0 ? 32 : p.W == 48 ? 48 : 16;
+  p.dkc = opt.dmma_kc > 0 ? opt.dmma_kc : p.W % 32 == 0 ? 32 : p.W % 48 == 0 ? 48 : 16;
   if (p.W % p.dkc != 0 || (p.dkc != 16 && p.dkc != 32 && p.dkc != 48)) p.dkc = p.W % 32 == 0 ? 32 : 16;
-  p.dmma_ok = p.adm == 0 && p.W % 16 == 0 && (p.W % 32 == 0 ? p.W <= 224 : p.W <= 112) &&
+  // The project's column slice: the whole panel (weak admissibility), or for the
+  // standard structure (W = M r, up to 1024 columns) the widest divisor WS of W
+  // one CTA's register-resident node tile takes (WS % 16 == 0, WS <= 224 if
+  // WS % 32 == 0, else <= 112); the slices are CTAs of a 2-D grid (one GPU only:
+  // the boundary exchange of P > 1 stays on the SIMT kernels).
+  int ws = p.W;
+  if (p.adm) {
+    ws = 0;
+    for (int cand = 16; cand <= 224 && cand <= p.W; cand += 16)
+      if (p.W % cand == 0 && (cand % 32 == 0 || cand <= 112)) ws = cand;
+  }
+  p.wslice = ws;
+  p.nslice = ws > 0 ? p.W / ws : 0;
+  p.dmma_ok = ws > 0 && (p.adm == 0 || p.P == 1) && p.W % 16 == 0 && (ws % 32 == 0 ? ws <= 224 : ws <= 112) &&
               leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
-    p.vp = p.Wp + ((4 - p.Wp % 16) + 16) % 16;
-    p.dnw = (p.W % 32 != 0 && opt.dmma_nw == 8) ? 8 : 16;
+    p.vp = ws + ((4 - ws % 16) + 16) % 16;
+    p.dnw = (ws % 32 != 0 && opt.dmma_nw == 8) ? 8 : 16;
     for (int li = 0; li < 4; ++li) {
       Plan::DmmaLayout& d = p.dl[li];
       d.nb = li == 3 ? 8 : 16 << li;
       // project warps: 64 / 32 wide as p.dnw; 16 wide: 8 (W % 32 == 0) or 4; 8 wide:
       // 4 or 2 (kernels_dmma.cu)
-      d.nw = d.nb == 8 ? (p.W % 32 == 0 ? 4 : 2) : d.nb == 16 ? (p.W % 32 == 0 ? 8 : 4) : p.dnw;
+      d.nw = d.nb == 8 ? (ws % 32 == 0 ? 4 : 2) : d.nb == 16 ? (ws % 32 == 0 ? 8 : 4) : p.dnw;
       // V rows + the nb x columns (pitch dkr + 4 = 4 mod 16 doubles)
       d.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(d.nb) * (p.dkr + 4) * 8, 128);
       const int64_t kd = p.dkc == 16 ? 16 : 32;  // dense-stage columns (kernels_dmma.cu KD)
@@ -282,7 +295,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       const bool narrow_on = d.nb == kDmmaNB || (d.nb == 32   ? opt.dmma_narrow >= 1
                                                  : d.nb == 16 ? opt.dmma_narrow >= 2
                                                               : opt.dmma_narrow >= 3);
-      d.ok = d.dns_p >= 2 && d.dns_e >= 2 && narrow_on && (d.nb != 32 || p.W % 32 == 0 || p.dnw == 8);
+      d.ok = d.dns_p >= 2 && d.dns_e >= 2 && narrow_on && (d.nb != 32 || ws % 32 == 0 || p.dnw == 8);
       p.dgrid_p_max = std::max(p.dgrid_p_max, d.dgrid_p);
     }
     if (!p.dl[2].ok) p.dmma_ok = false;

@@ -84,6 +84,7 @@ struct Plan {
   bool dmma_ok = false;
   int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1, dmma_pchunk = 32;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
+  int wslice = 0, nslice = 0;       // tensor-core project: column slice width / count (W = wslice nslice)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
   int dkc = kDmmaKC;                // expand: k-columns per level stage (32; 48 at W = 48; else 16)
   int dnw = 16;                     // project: warps per CTA (16 at 1 CTA/SM, or 8 at 2 CTAs/SM)

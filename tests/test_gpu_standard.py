@@ -143,11 +143,12 @@ def test_standard_3d_leaf64_caps_pass_width():
     assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
 
 
-def test_s2_full_size_sampled_rows():
+@pytest.mark.parametrize("nrhs", [1, 16])
+def test_s2_full_size_sampled_rows(nrhs):
     """The bench's s2 line at full size (N = 2^20, 27 interaction slots, 55.6 GB
     of factors), in the bench's launch configuration (device-generated panels,
-    default plan): sampled rows vs the oracle's row-restricted Def 2.4 walk with
-    on-demand factors."""
+    default plan; 16 rhs: the tensor-core passes, 9 project slices): sampled rows
+    vs the oracle's row-restricted Def 2.4 walk with on-demand factors."""
     from tests.helpers import device_operator
     cfg = hgen.EXTRA_CONFIGS["s2"]
     free, _ = torch.cuda.mem_get_info()
@@ -155,21 +156,23 @@ def test_s2_full_size_sampled_rows():
         pytest.skip(f"needs {cfg.factor_bytes / 1e9:.0f} GB of device memory")
     h = device_operator(cfg, hm)
     try:
-        x = torch.empty(cfg.N, dtype=torch.float64, device="cuda")
-        hgen.dev_fill_x(cfg, 1, 2, 0, cfg.N, x.data_ptr(), cfg.N)
-        y = torch.empty_like(x)
-        hm.hmat_matvec(h, x, y)
+        X = torch.empty(nrhs, cfg.N, dtype=torch.float64, device="cuda")
+        hgen.dev_fill_x(cfg, nrhs, 2, 0, cfg.N, X.data_ptr(), cfg.N)
+        Y = torch.empty_like(X)
+        hm.hmat_matvec(h, X.t(), Y.t(), nrhs)
         torch.cuda.synchronize()
-        xh = x.cpu().numpy()
+        if nrhs > 1:
+            assert hm.hmat_launches_per_matvec(h, nrhs) == 2
+        xh = X.t().cpu().numpy()
+        x, y = (xh[:, 0], Y[0]) if nrhs == 1 else (np.asfortranarray(xh), Y.t())
         n_side = 1 << cfg.L
         corner = [0, cfg.b - 1]                                      # domain corner leaf
         edge = [(n_side // 2) * cfg.b + 5]                           # a boundary leaf
         rows = np.array(sorted(set(corner + edge + [cfg.N // 2 + 17, cfg.N - 1] +
                                    list(np.random.default_rng(4).integers(0, cfg.N, 3)))))
-        ref = oracle.std_rows_generated(cfg, xh, rows)
-        yall = y.cpu().numpy()
-        got = yall[rows]
-        assert np.abs(got - ref).max() <= 1e-12 * np.abs(yall).max()
+        ref = oracle.std_rows_generated(cfg, x, rows)
+        got = y.cpu().numpy()[rows]
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
         assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
     finally:
         hm.hmat_destroy(h)
@@ -198,5 +201,60 @@ def test_standard_literal_order_parity(d, L, b, r, nrhs):
         hm.hmat_gemv(h, 1, 1.0, np.asfortranarray(x), 0.0, yt, nrhs)
         A = oracle.std_assemble_strict(d, L, b, r, U, V, Dc)
         assert_parity(yt, A.T @ x)
+    finally:
+        hm.hmat_destroy(h)
+
+
+STD_DMMA = [HConfig("stdT2", d=2, L=3, b=64, r=16, adm=1, seed=790),    # W = 432: 9 project slices of 48
+            HConfig("stdT2b", d=2, L=4, b=64, r=16, adm=1, seed=791),   # deeper: nodes split across CTAs
+            HConfig("stdT1", d=1, L=6, b=64, r=16, adm=1, seed=792),    # W = 48: one slice
+            HConfig("stdT2r", d=2, L=3, b=64, r=32, adm=1, seed=793)]   # W = 864: 9 slices of 96
+
+
+@pytest.mark.parametrize("cfg", STD_DMMA, ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [5, 8, 16, 33, 64, 70])
+def test_standard_tensor_core_passes(cfg, nrhs):
+    """Standard admissibility on the FP64 tensor cores (one GPU, W % 16 == 0,
+    64 | b): the project runs in column slices of the W = M r panel (a 2-D grid),
+    scattering z through the interaction-list slot tables; the expand streams the
+    3^d near-field blocks of each tile's leaf (skipping those outside the domain).
+    H and H^T vs the oracle's block loops; 2 launches per pass (the tensor-core
+    path ran)."""
+    U, V, Dn = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
+    try:
+        assert hm.hmat_launches_per_matvec(h, nrhs) == 2 * ((nrhs + 63) // 64)
+        xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        yd = torch.empty_like(xd)
+        hm.hmat_matvec(h, xd.t(), yd.t(), nrhs)
+        yt = torch.empty_like(xd)
+        hm.hmat_gemv(h, 1, 1.0, xd.t(), 0.0, yt.t(), nrhs)
+        torch.cuda.synchronize()
+        assert_parity(yd.t().cpu().numpy(), oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
+        assert_parity(yt.t().cpu().numpy(), oracle.std_matvec_t(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
+    finally:
+        hm.hmat_destroy(h)
+
+
+def test_standard_tensor_core_width_change_and_simt_agree():
+    """Passes of different widths on one handle (64, then 8, then 64 again) and
+    the SIMT kernels (HMAT_DMMA_OFF) give the same products: the z rows of slots
+    outside the domain stay zero across layout changes."""
+    cfg = STD_DMMA[0]
+    U, V, Dn = hgen.inputs(cfg)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
+    try:
+        outs = []
+        for nrhs in (64, 8, 64):
+            x = hgen.xblock(cfg, nrhs=nrhs, vec=nrhs)
+            xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+            yd = torch.empty_like(xd)
+            hm.hmat_matvec(h, xd.t(), yd.t(), nrhs)
+            torch.cuda.synchronize()
+            y = yd.t().cpu().numpy()
+            assert_parity(y, oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
+            outs.append(y)
+        assert np.array_equal(outs[0], outs[2])
     finally:
         hm.hmat_destroy(h)
