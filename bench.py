@@ -674,6 +674,9 @@ def run_ours(args):
                                "than the plain one that gives `value`"},
             "factor_GBps": factor_gbps,
             "alg_GBps": ab["total"] * world / (ms_step * 1e-3) / 1e9,
+            # the memory floor: every factor byte and x / y once at the read-stream ceiling
+            "floor_ms": alg_bytes(cfg, cfg.N, nrhs)["total"] / (HBM_READ_STREAM_GBS * 1e9) * 1e3 / world,
+            "frac_of_floor": alg_bytes(cfg, cfg.N, nrhs)["total"] / (HBM_READ_STREAM_GBS * 1e9) * 1e3 / world / ms_step,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -93,6 +93,16 @@ EXTRA_CONFIGS = {
     # diagonal blocks, 4 x 64 = 256 square, are dense; low-rank blocks at levels
     # 1..6): exactly the weak structure of depth 6 with leaf 256
     "c2strict": HConfig("c2strict", d=2, L=6, b=256, r=16, nrhs=1, seed=SEED_BASE + 13),
+    # the mid-rhs regime (2-16 rhs against the memory floor): the c2 / c4
+    # operators with 4, 8 and 16 right-hand sides, and s2 with 16 (the standard
+    # structure's tensor-core passes)
+    "c2r4": HConfig("c2r4", d=2, L=7, b=64, r=16, nrhs=4, seed=SEED_BASE + 2),
+    "c2r8": HConfig("c2r8", d=2, L=7, b=64, r=16, nrhs=8, seed=SEED_BASE + 2),
+    "c2r16": HConfig("c2r16", d=2, L=7, b=64, r=16, nrhs=16, seed=SEED_BASE + 2),
+    "c4r4": HConfig("c4r4", d=2, L=9, b=64, r=16, nrhs=4, seed=SEED_BASE + 4),
+    "c4r8": HConfig("c4r8", d=2, L=9, b=64, r=16, nrhs=8, seed=SEED_BASE + 4),
+    "c4r16": HConfig("c4r16", d=2, L=9, b=64, r=16, nrhs=16, seed=SEED_BASE + 4),
+    "s2r16": HConfig("s2r16", d=2, L=7, b=64, r=16, nrhs=16, seed=SEED_BASE + 12, adm=1),
 }
 
 _lib = None
