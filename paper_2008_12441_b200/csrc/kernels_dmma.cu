@@ -112,12 +112,18 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int64_t G = gridDim.x, bid = blockIdx.x;
+  // Column slices (a.nslice > 1, the standard structure's wide panels) are the
+  // fastest-varying part of the CTA index: the CTAs resident at any time hold all
+  // slices of neighbouring row ranges, so a stage's x rows are shared through L2
+  // by the slices instead of being swept once per slice.
+  const int NSL = a.nslice > 0 ? a.nslice : 1;
+  const int64_t G = gridDim.x / NSL, bid = blockIdx.x / NSL;
+  const int slice = static_cast<int>(blockIdx.x % NSL);
   const int Wp = a.Wp, L = a.L;
   const int VP = a.vp;                     // smem pitch of V rows (= 4 mod 16)
   // column slice of this CTA: [c0, c0 + WS) of the W panel columns (a panel wider
   // than one CTA's register-resident node tile, standard admissibility: W = M r)
-  const int WS = a.wslice, c0 = static_cast<int>(blockIdx.y) * WS;
+  const int WS = a.wslice, c0 = slice * WS;
   const int64_t SL = a.N_loc / KR;
   const int64_t GL = G < SL ? G : SL;
   const int NS = a.nstage_p;
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
   __syncthreads();
   if (a.pdl_p) dev::pdl_wait();  // the previous kernel (e.g. last product's expand) complete
   if (a.pdl) dev::pdl_launch_dependents();  // expand may launch as SMs free up
-  const dev::CtaTrace trace_scope(a.trace, bid);
+  const dev::CtaTrace trace_scope(a.trace, blockIdx.x);
   if (bid >= GL) return;
   advance();  // first stage
   for (int i = 0; i < NS && lr <= L; ++i) {
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
         __threadfence();
         dev::named_bar_sync(1, CTP);
         const int64_t b0 = owner_of(sa, SL, GL), b1 = owner_of(sb - 1, SL, GL);
-        int* ticket = a.cnt + ((int64_t)(l - 1) * G + b1) * gridDim.y + blockIdx.y;  // per column slice
+        int* ticket = a.cnt + ((int64_t)(l - 1) * G + b1) * NSL + slice;  // per column slice
         if (tid == 0) {
           const int prev = atomicAdd(ticket, 1);
           *flag = (prev == static_cast<int>(b1 - b0)) ? 1 : 0;
@@ -552,11 +558,11 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
 
 template <int MT, int NT, int NW, int NB>
 void launch_p(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  const int gy = a.nslice > 0 ? a.nslice : 1;  // column slices
+  const int gs = grid * (a.nslice > 0 ? a.nslice : 1);  // column slices fastest (kernel)
   if (a.pdl_p)
-    launch_pdl(project_dmma_kernel<kDmmaKR, MT, NT, NW, NB>, a, grid, NW * 32, smem, s, gy);
+    launch_pdl(project_dmma_kernel<kDmmaKR, MT, NT, NW, NB>, a, gs, NW * 32, smem, s);
   else
-    project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<dim3(grid, gy), NW * 32, smem, s>>>(a);
+    project_dmma_kernel<kDmmaKR, MT, NT, NW, NB><<<gs, NW * 32, smem, s>>>(a);
 }
 
 template <int MT, int NT, int NW, int NB>
