@@ -70,6 +70,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.pdl = env_int("HMAT_PDL", 2);
   o.lpar = env_int("HMAT_PROJECT_LPAR", 1);
   o.early = env_int("HMAT_PROJECT_EARLY", 1);
+  o.eshape = env_int("HMAT_EXPAND_SHAPE", 1);
   o.dmma_ileave = env_int("HMAT_DMMA_ILEAVE", 1);
   o.aflush = env_int("HMAT_PROJECT_AFLUSH", 1);
   o.dmma_upol = env_int("HMAT_DMMA_UPOL", 1);
@@ -784,6 +785,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   a.dbg = p.dbg;
   a.snake = p.snake;
   a.early = p.early;
+  a.eshape = p.eshape;
   a.dmma_ileave = p.dmma_ileave;
   a.aflush = p.aflush;
   a.dmma_upol = p.dmma_upol;

@@ -84,6 +84,7 @@ struct StreamArgs {
   unsigned int* err;         // host-mapped error word: a flag wait that timed out (peer.cuh)
   int64_t peer_timeout_ns;   // bound on a flag wait (HMAT_PEER_TIMEOUT_MS)
   int early;                 // project: release a ring slot before the FMAs (HMAT_PROJECT_EARLY)
+  int eshape;                // expand: compile-time consumer shapes, 1 rhs (HMAT_EXPAND_SHAPE)
   int dmma_ileave;           // tensor-core expand: interleaved item order (HMAT_DMMA_ILEAVE)
   int skip_remote;           // standard H^T, P > 1: expand skips near-field blocks of remote neighbours
   int wslice, nslice;        // tensor-core project: column slices of the panel (gridDim.y = nslice)

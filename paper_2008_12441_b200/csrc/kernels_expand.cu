@@ -42,7 +42,21 @@ __device__ __forceinline__ int level_order(const StreamArgs& a, int li) {
   return li <= nloc ? li + a.cross : li - nloc;
 }
 
-template <int NR>
+// Compile-time consumer shapes (1 rhs, weak admissibility, one dense stage,
+// no peer exchange): tpr threads per row, NJU U / NJD D column pairs per
+// thread.  The per-thread smem offsets are then a base register plus
+// immediates, so a U stage is NJU x (2 LDS.128 + 2 DFMA) and little else --
+// fewer issue slots and less power per byte streamed (the kernel runs under
+// the board's power cap next to project).  SH = 1: W = 48 (c1, c2, c4), SH = 2:
+// W = 224 (c3); both with b = 64.
+template <int SH>
+struct ExpShape {
+  static constexpr int TPR = SH == 1 ? 4 : 16;
+  static constexpr int NJU = SH == 1 ? 6 : 7;
+  static constexpr int NJD = SH == 1 ? 8 : 2;
+};
+
+template <int NR, int SH = 0>
 __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_constant__ StreamArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -342,6 +356,89 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     peeked = true;
     return true;
   };
+  if constexpr (SH != 0) {
+    using S = ExpShape<SH>;
+    constexpr int TPR = S::TPR, NJU = S::NJU, NJD = S::NJD;
+    constexpr int NPc = TPR * NJU, NPDc = TPR * NJD, REc = CT / TPR;
+    // Pair cp of row ri sits at byte (ri NP + cp) 16 of a U stage, pair cp of
+    // the z row at (Re NP + cp) 16 = the U offset + (Re - ri) NP 16; the same
+    // for D and the x segment.  Thread p of row ri reads pairs p + TPR n.  With
+    // TPR = 4 a quarter-warp phase of LDS.128 holds rows 2k and 2k + 1, whose
+    // pitches are multiples of 128 B: the odd row starts one pair group later
+    // (n = 1, ..., NJ - 1, then 0) so the phase's 8 reads hit 8 bank groups.
+    const int odd = TPR == 4 ? (ri & 1) : 0;
+    const uint32_t ub0 = (ri * NPc + p) * 16 + odd * TPR * 16;
+    const uint32_t ul = odd ? ub0 - TPR * 16 : ub0 + (NJU - 1) * TPR * 16;
+    const uint32_t zd = (REc - ri) * NPc * 16;
+    const uint32_t db0 = (ri * NPDc + p) * 16 + odd * TPR * 16;
+    const uint32_t dl = odd ? db0 - TPR * 16 : db0 + (NJD - 1) * TPR * 16;
+    const uint32_t xd = (REc - ri) * NPDc * 16;
+    const bool skip = a.dbg & 2;
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      if (++slot == NS) {
+        slot = 0;
+        phase ^= 1;
+      }
+    };
+    while (next_range()) {
+      for (int64_t j = cj0; j < cj1; ++j) {
+        double acc = 0.0, acc2 = 0.0;  // two chains: even / odd columns
+        for (int l = 1; l <= L; ++l) {
+          if (!((a.level_mask >> (l - 1)) & 1ull)) continue;
+          if (!peeked) dev::mbar_wait(&full[slot], phase);
+          peeked = false;
+          if (!skip) {
+            const unsigned char* st = smem + slot * a.stage_bytes_e;
+            const unsigned char* su = st + ub0;
+            const unsigned char* sz = su + zd;
+#pragma unroll
+            for (int n = 0; n < NJU - 1; ++n) {
+              const double2 u = *reinterpret_cast<const double2*>(su + n * TPR * 16);
+              const double2 z = *reinterpret_cast<const double2*>(sz + n * TPR * 16);
+              acc = fma(u.x, z.x, acc);
+              acc2 = fma(u.y, z.y, acc2);
+            }
+            const double2 u = *reinterpret_cast<const double2*>(st + ul);
+            const double2 z = *reinterpret_cast<const double2*>(st + ul + zd);
+            acc = fma(u.x, z.x, acc);
+            acc2 = fma(u.y, z.y, acc2);
+          }
+          release();
+        }
+        if (a.dense) {
+          if (!peeked) dev::mbar_wait(&full[slot], phase);
+          peeked = false;
+          if (!skip) {
+            const unsigned char* st = smem + slot * a.stage_bytes_e;
+            const unsigned char* sd = st + db0;
+            const unsigned char* sx = sd + xd;
+#pragma unroll
+            for (int n = 0; n < NJD - 1; ++n) {
+              const double2 dv = *reinterpret_cast<const double2*>(sd + n * TPR * 16);
+              const double2 xv = *reinterpret_cast<const double2*>(sx + n * TPR * 16);
+              acc = fma(dv.x, xv.x, acc);
+              acc2 = fma(dv.y, xv.y, acc2);
+            }
+            const double2 dv = *reinterpret_cast<const double2*>(st + dl);
+            const double2 xv = *reinterpret_cast<const double2*>(st + dl + xd);
+            acc = fma(dv.x, xv.x, acc);
+            acc2 = fma(dv.y, xv.y, acc2);
+          }
+          release();
+        }
+        acc += acc2;
+#pragma unroll
+        for (int off = TPR >> 1; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (p == 0) {
+          double* yp = a.y + j * REc + ri;  // y = alpha (H x) + beta y (GEMV)
+          *yp = a.beta == 0.0 ? a.alpha * acc : a.alpha * acc + a.beta * *yp;
+        }
+      }
+    }
+    return;
+  }
   while (next_range()) {
   leaf0 = (cj0 * Re / b) * b;
   in_leaf = (cj0 * Re - leaf0) / Re;
@@ -487,13 +584,38 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   }
 }
 
-template <int NR>
-cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+template <int NR, int SH>
+cudaError_t launch_sh(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
   if (!a.pdl) {
-    expand_kernel<NR><<<grid, kThreads, smem, s>>>(a);
+    expand_kernel<NR, SH><<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
   }
-  return launch_pdl(expand_kernel<NR>, a, grid, kThreads, smem, s);
+  return launch_pdl(expand_kernel<NR, SH>, a, grid, kThreads, smem, s);
+}
+
+template <int SH>
+bool shape_is(const StreamArgs& a) {
+  using S = ExpShape<SH>;
+  return a.tpr == S::TPR && a.Re * S::TPR == CT && a.W == a.Wp && a.Wp == 2 * S::TPR * S::NJU &&
+         a.b == a.Dp && a.Dp == 2 * S::TPR * S::NJD;
+}
+
+// compile-time consumer shape of this launch (ExpShape), 0 = generic
+int expand_shape(const StreamArgs& a, int nr_cap) {
+  if (nr_cap != 1 || a.adm || a.peer || a.ndc != 1 || !a.eshape) return 0;
+  if (shape_is<1>(a)) return 1;
+  if (shape_is<2>(a)) return 2;
+  return 0;
+}
+
+template <int NR>
+cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if constexpr (NR == 1) {
+    const int sh = expand_shape(a, NR);
+    if (sh == 1) return launch_sh<1, 1>(a, grid, smem, s);
+    if (sh == 2) return launch_sh<1, 2>(a, grid, smem, s);
+  }
+  return launch_sh<NR, 0>(a, grid, smem, s);
 }
 
 }  // namespace
@@ -511,6 +633,8 @@ cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e) {
   cudaError_t e = configure_project(smem_p);
   if (e != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
+  if ((e = cudaFuncSetAttribute(expand_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
+  if ((e = cudaFuncSetAttribute(expand_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   return cudaFuncSetAttribute(expand_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);

@@ -78,6 +78,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.pdl = opt.pdl;
   p.lpar = opt.lpar;
   p.early = opt.early;
+  p.eshape = opt.eshape;
   p.dmma_ileave = opt.dmma_ileave;
   p.project_chunk = opt.project_chunk;
   p.aflush = opt.aflush;

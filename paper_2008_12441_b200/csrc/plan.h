@@ -82,7 +82,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1, dmma_pchunk = 32;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, eshape = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1, dmma_pchunk = 32;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int wslice = 0, nslice = 0;       // tensor-core project: column slice width / count (W = wslice nslice)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
@@ -131,6 +131,7 @@ struct PlanOptions {
   int pdl = 2;                      // PDL: 0 off, 1 expand after project, 2 also project after the previous kernel
   int lpar = 1;                     // project: level-parallel mode for small operators
   int early = 1;                    // project: release a ring slot before the FMAs (1 rhs)
+  int eshape = 1;                   // expand: compile-time consumer shapes (1 rhs, ExpShape)
   int dmma_ileave = 1;              // tensor-core expand: interleaved item order over the CTAs
   int project_chunk = 4;            // project: minimum stages per dynamic chunk of the last level
   int aflush = 1;                   // project: asynchronous node flushes (no CTA barrier per node)
