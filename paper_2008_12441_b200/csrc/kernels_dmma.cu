@@ -351,7 +351,12 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 // the last of the 8 warps to finish a slot refills it.
 // KC: k-columns per stage (32, or 16 when W % 32 != 0); the staged U / D row
 // chunks and x columns have pitch KC + 4 (= 4 mod 16 doubles).
-template <int KC, int NB>
+// WF: weak admissibility with every level and the dense block active (the
+// plain product; a.level_mask full, a.dense): the stage sequence is then fixed
+// -- kcw chunks per level, kcd for the leaf block -- and the cursor walk and the
+// per-stage level checks compile away.  (Per stage and warp they outnumbered
+// the DMMAs of a narrow pass.)
+template <int KC, int NB, bool WF>
 __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_constant__ StreamArgs a) {
   constexpr int NCW = kThreadsE / 32;
   constexpr int WM = NB <= 16 ? 8 : 4, WN = NCW / WM;  // warp grid over rows x rhs
@@ -389,15 +394,16 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   // Dense stages: the leaf-diagonal block (weak, stage L + 1), or the 3^d
   // near-field blocks of the tile's leaf (standard admissibility, stages L + 1 + e
   // for the neighbours e inside the domain, one GPU).  nmask: the present ones.
-  const int ndn = a.adm ? a.nd : 1;
+  const int ndn = !WF && a.adm ? a.nd : 1;
   const int64_t lbase = a.row0 / b;
   auto near_of = [&](int64_t item) -> uint32_t {
-    if (!a.adm) return 1u;
+    if (WF || !a.adm) return 1u;
     int x[3];
     geo::morton_decode(a.d, lbase + item * RE / b, L, x);
     return geo::near_mask(a.d, x, 1 << L);
   };
   auto level_on = [&](int l, uint32_t nmask) -> bool {
+    if constexpr (WF) return true;
     return l > L ? a.dense != 0 && ((nmask >> (l - L - 1)) & 1u) : ((a.level_mask >> (l - 1)) & 1ull) != 0;
   };
   // refill cursor (item jr, level lr in 1..L+ndn (> L: dense), chunk kcr): identical in every warp
@@ -411,6 +417,13 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   auto advance = [&]() {
     if (++kcr < (lr > L ? kcd : kcw)) return;
     kcr = 0;
+    if constexpr (WF) {
+      if (++lr > L + 1) {
+        lr = 1;
+        jr += jst;
+      }
+      return;
+    }
     do {
       if (++lr > L + ndn) {
         lr = 1;
@@ -424,7 +437,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
     const int i0 = static_cast<int>(jr * RE);
     if (lr > L) {
       dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes_d + NB * XP * 8));
-      if (a.adm) {  // near-field block e: panel e of the D-role panels, x of neighbour leaf e
+      if (!WF && a.adm) {  // near-field block e: panel e of the D-role panels, x of neighbour leaf e
         const int e = lr - L - 1;
         int x[3];
         geo::morton_decode(a.d, lbase + i0 / b, L, x);
@@ -683,12 +696,22 @@ cudaError_t set_p16(int64_t smem) {
   return cudaSuccess;
 }
 
+template <int KC, int NB, bool WF>
+void launch_e_wf(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
+  if (a.pdl)
+    launch_pdl(expand_dmma_kernel<KC, NB, WF>, a, grid, kThreadsE, smem, s);
+  else
+    expand_dmma_kernel<KC, NB, WF><<<grid, kThreadsE, smem, s>>>(a);
+}
+
 template <int KC, int NB>
 void launch_e_kc(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
-  if (a.pdl)
-    launch_pdl(expand_dmma_kernel<KC, NB>, a, grid, kThreadsE, smem, s);
+  const uint64_t all_lv = a.L >= 64 ? ~0ull : (1ull << a.L) - 1;
+  const bool wf = !a.adm && a.dense && (a.level_mask & all_lv) == all_lv && !(a.dbg & 16);
+  if (wf)
+    launch_e_wf<KC, NB, true>(a, grid, smem, s);
   else
-    expand_dmma_kernel<KC, NB><<<grid, kThreadsE, smem, s>>>(a);
+    launch_e_wf<KC, NB, false>(a, grid, smem, s);
 }
 
 template <int NB>
@@ -701,13 +724,19 @@ void launch_e(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
     launch_e_kc<32, NB>(a, grid, smem, s);
 }
 
+template <int NB, bool WF>
+cudaError_t set_e_wf(int64_t smem) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, NB, WF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
+      (e = cudaFuncSetAttribute(expand_dmma_kernel<48, NB, WF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+    return e;
+  return cudaFuncSetAttribute(expand_dmma_kernel<32, NB, WF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 template <int NB>
 cudaError_t set_e(int64_t smem) {
-  cudaError_t e;
-  if ((e = cudaFuncSetAttribute(expand_dmma_kernel<16, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) ||
-      (e = cudaFuncSetAttribute(expand_dmma_kernel<48, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-    return e;
-  return cudaFuncSetAttribute(expand_dmma_kernel<32, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const cudaError_t e = set_e_wf<NB, false>(smem);
+  return e != cudaSuccess ? e : set_e_wf<NB, true>(smem);
 }
 
 // Wait for the P ranks' flags of this pass, then exchange[o] = sum over ranks g
