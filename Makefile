@@ -20,8 +20,17 @@ HMAT_HDR  := include/hmat.h $(CSRC)/plan.h $(CSRC)/kernels.h $(CSRC)/comm.h $(CS
 
 all: $(PKG)/libhmat.so oracle/liboracle.so gen/libhgen.so gen/libhgen_dev.so
 
-$(PKG)/libhmat.so: $(HMAT_SRC) $(HMAT_HDR)
-	$(NVCC) $(NVFLAGS) -shared -Iinclude -I$(NCCL_INC) $(HMAT_SRC) -o $@ -ldl 2> build_hmat.log || (cat build_hmat.log; false)
+# one object per translation unit (build/obj, git-ignored), so `make -j` compiles
+# the kernel files in parallel; ptxas -v output in build/obj/<file>.log
+OBJDIR    := build/obj
+HMAT_OBJ  := $(patsubst $(CSRC)/%,$(OBJDIR)/%.o,$(HMAT_SRC))
+
+$(OBJDIR)/%.o: $(CSRC)/% $(HMAT_HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Iinclude -I$(NCCL_INC) -c $< -o $@ 2> $@.log || (cat $@.log; false)
+
+$(PKG)/libhmat.so: $(HMAT_OBJ)
+	$(NVCC) $(ARCH) -shared $(HMAT_OBJ) -o $@ -ldl
 
 oracle/liboracle.so: oracle/hmat_oracle.c gen/hgen.h
 	gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared -Wall $< -o $@ -lm
@@ -33,6 +42,6 @@ gen/libhgen_dev.so: gen/hgen_device.cu gen/hgen.h
 	$(NVCC) $(ARCH) -O3 -fmad=false -std=c++17 -Xcompiler -fPIC -shared $< -o $@
 
 clean:
-	rm -f $(PKG)/libhmat.so oracle/liboracle.so gen/libhgen.so gen/libhgen_dev.so build_hmat.log
+	rm -rf $(PKG)/libhmat.so oracle/liboracle.so gen/libhgen.so gen/libhgen_dev.so $(OBJDIR)
 
 .PHONY: all clean

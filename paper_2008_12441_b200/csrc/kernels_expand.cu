@@ -48,13 +48,16 @@ __device__ __forceinline__ int level_order(const StreamArgs& a, int li) {
 // immediates, so a U stage is NJU x (2 LDS.128 + 2 DFMA) and little else --
 // fewer issue slots and less power per byte streamed (the kernel runs under
 // the board's power cap next to project).  SH = 1: W = 48 (c1, c2, c4), SH = 2:
-// W = 224 (c3); both with b = 64.
+// W = 224 (c3); both with b = 64.  SH = 3: standard admissibility in 2-D with
+// r = 16, b = 64, one GPU (s2): W = 27 r = 432, one row per warp (Re = 8), the
+// 3 x 3 near-field blocks in 3 dense stages of 3.
 template <int SH>
 struct ExpShape {
-  static constexpr int TPR = SH == 1 ? 4 : 16;
-  static constexpr int NJU = SH == 1 ? 6 : 7;
-  static constexpr int NJD = SH == 1 ? 8 : 2;
+  static constexpr int TPR = SH == 1 ? 4 : SH == 2 ? 16 : 32;
+  static constexpr int NJU = SH == 1 ? 6 : SH == 2 ? 7 : 0;
+  static constexpr int NJD = SH == 1 ? 8 : SH == 2 ? 2 : 1;
 };
+constexpr int kStd2NP = 27 * 16 / 2;  // SH = 3: U column pairs
 
 template <int NR, int SH = 0>
 __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_constant__ StreamArgs a) {
@@ -356,7 +359,91 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     peeked = true;
     return true;
   };
-  if constexpr (SH != 0) {
+  if constexpr (SH == 3) {
+    // one row per warp, lane p: U pairs p + 32 n (n < 6) and p + 192 (p < 24);
+    // D pair p of each present near-field block.  Consecutive lanes read
+    // consecutive 16-byte pairs of one row: conflict-free without rotation.
+    constexpr int NPc = kStd2NP, NFULL = NPc / 32, NTAIL = NPc - 32 * NFULL, REc = CT / 32, NPDc = 32;
+    const uint32_t ub0 = (ri * NPc + p) * 16;
+    const uint32_t zd = (REc - ri) * NPc * 16;
+    const bool tail = p < NTAIL;
+    const uint32_t db0 = (ri * NPDc + p) * 16;
+    const uint32_t xd = (REc - ri) * NPDc * 16;
+    const uint32_t dblk = static_cast<uint32_t>(REc * NPDc * 16 + a.xs_e * 8);
+    const bool skip = a.dbg & 2;
+    const int ipl2 = b / REc;
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) dev::mbar_arrive(&empty[slot]);
+      if (++slot == NS) {
+        slot = 0;
+        phase ^= 1;
+      }
+    };
+    while (next_range()) {
+      int64_t lf = (a.row0 + cj0 * REc) / b;  // the item's leaf
+      int il = static_cast<int>((cj0 * REc) % b) / REc;
+      int x2[3];
+      geo::morton_decode(2, lf, L, x2);
+      uint32_t nm = geo::near_mask(2, x2, 1 << L);
+      for (int64_t j = cj0; j < cj1; ++j) {
+        double acc = 0.0, acc2 = 0.0;
+        for (int l = 1; l <= L + 3; ++l) {
+          const bool is_d = l > L;
+          if (is_d ? !a.dense : !((a.level_mask >> (l - 1)) & 1ull)) continue;
+          if (!peeked) dev::mbar_wait(&full[slot], phase);
+          peeked = false;
+          if (!skip) {
+            const unsigned char* st = smem + slot * a.stage_bytes_e;
+            if (!is_d) {
+              const unsigned char* su = st + ub0;
+              const unsigned char* sz = su + zd;
+#pragma unroll
+              for (int n = 0; n < NFULL; ++n) {
+                const double2 u = *reinterpret_cast<const double2*>(su + n * 512);
+                const double2 z = *reinterpret_cast<const double2*>(sz + n * 512);
+                acc = fma(u.x, z.x, acc);
+                acc2 = fma(u.y, z.y, acc2);
+              }
+              if (tail) {
+                const double2 u = *reinterpret_cast<const double2*>(su + NFULL * 512);
+                const double2 z = *reinterpret_cast<const double2*>(sz + NFULL * 512);
+                acc = fma(u.x, z.x, acc);
+                acc2 = fma(u.y, z.y, acc2);
+              }
+            } else {
+              const uint32_t m3 = nm >> ((l - L - 1) * 3);
+              const unsigned char* sd = st + db0;
+#pragma unroll
+              for (int e = 0; e < 3; ++e) {
+                if ((m3 >> e) & 1u) {
+                  const double2 dv = *reinterpret_cast<const double2*>(sd + e * dblk);
+                  const double2 xv = *reinterpret_cast<const double2*>(sd + e * dblk + xd);
+                  acc = fma(dv.x, xv.x, acc);
+                  acc2 = fma(dv.y, xv.y, acc2);
+                }
+              }
+            }
+          }
+          release();
+        }
+        acc += acc2;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (p == 0) {
+          double* yp = a.y + j * REc + ri;  // y = alpha (H x) + beta y (GEMV)
+          *yp = a.beta == 0.0 ? a.alpha * acc : a.alpha * acc + a.beta * *yp;
+        }
+        if (++il == ipl2) {
+          il = 0;
+          ++lf;
+          geo::morton_decode(2, lf, L, x2);
+          nm = geo::near_mask(2, x2, 1 << L);
+        }
+      }
+    }
+    return;
+  } else if constexpr (SH != 0) {
     using S = ExpShape<SH>;
     constexpr int TPR = S::TPR, NJU = S::NJU, NJD = S::NJD;
     constexpr int NPc = TPR * NJU, NPDc = TPR * NJD, REc = CT / TPR;
@@ -602,7 +689,13 @@ bool shape_is(const StreamArgs& a) {
 
 // compile-time consumer shape of this launch (ExpShape), 0 = generic
 int expand_shape(const StreamArgs& a, int nr_cap) {
-  if (nr_cap != 1 || a.adm || a.peer || a.ndc != 1 || !a.eshape) return 0;
+  if (nr_cap != 1 || a.peer || !a.eshape) return 0;
+  if (a.adm)  // standard, 2-D, r = 16, b = 64, one GPU (no halo, nothing skipped)
+    return a.d == 2 && a.r == 16 && a.b == 64 && a.Dp == 64 && a.W == 2 * kStd2NP && a.Wp == a.W && a.tpr == 32 &&
+                   a.Re * 32 == CT && a.ndc == 3 && a.dgs == 3 && a.nd == 9 && !a.halo_of && !a.skip_remote
+               ? 3
+               : 0;
+  if (a.ndc != 1) return 0;
   if (shape_is<1>(a)) return 1;
   if (shape_is<2>(a)) return 2;
   return 0;
@@ -614,6 +707,7 @@ cudaError_t launch_nr(const StreamArgs& a, int grid, int64_t smem, cudaStream_t 
     const int sh = expand_shape(a, NR);
     if (sh == 1) return launch_sh<1, 1>(a, grid, smem, s);
     if (sh == 2) return launch_sh<1, 2>(a, grid, smem, s);
+    if (sh == 3) return launch_sh<1, 3>(a, grid, smem, s);
   }
   return launch_sh<NR, 0>(a, grid, smem, s);
 }
@@ -635,6 +729,7 @@ cudaError_t configure_kernels(int64_t smem_p, int64_t smem_e) {
   if ((e = cudaFuncSetAttribute(expand_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
+  if ((e = cudaFuncSetAttribute(expand_kernel<1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   if ((e = cudaFuncSetAttribute(expand_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e))) return e;
   return cudaFuncSetAttribute(expand_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);

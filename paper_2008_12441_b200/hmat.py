@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhmat.so")
+LIB_PATH = os.environ.get("HMAT_LIB_AB") or os.path.join(_HERE, "libhmat.so")  # (A/B experiments: another build)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "

@@ -22,7 +22,7 @@ def _built():
 def pytest_sessionstart(session):
     # Build the in-tree native artefacts if a fresh checkout lacks them.
     if not _built():
-        subprocess.run(["make", "-s", "-C", ROOT], check=False)
+        subprocess.run(["make", "-s", "-j8", "-C", ROOT], check=False)
 
 
 @pytest.fixture(scope="session")
