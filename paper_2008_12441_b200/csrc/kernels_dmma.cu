@@ -63,10 +63,9 @@ __device__ __forceinline__ double* zt_column_std(const StreamArgs& a, const Leve
   const int tau = static_cast<int>(sg & (c - 1));
   const int code = c_std_code_d[d - 1][tau][q];
   const int e = code >> d, sigma = code & (c - 1);
-  int px[3];
-  geo::morton_decode(d, sg >> d, level - 1, px);
-  if (!((geo::near_mask(d, px, 1 << (level - 1)) >> e) & 1u)) return nullptr;
-  const int64_t t = geo::neighbour(d, px, e, level - 1) * c + sigma;
+  const int64_t pt = geo::neighbour_k(d, sg >> d, e, level - 1);  // the parent's neighbour e
+  if (pt < 0) return nullptr;
+  const int64_t t = pt * c + sigma;
   const int nd = d == 1 ? 3 : d == 2 ? 9 : 27;
   const int qt = c_std_slot_d[d - 1][sigma][(nd - 1 - e) * c + tau];  // eps -> -eps, sigma <-> tau
   return lv.zt + (t - lv.tbase) * (int64_t)a.W * NB + zfrag<NB>(qt * a.r + aa, 0);
@@ -398,9 +397,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   const int64_t lbase = a.row0 / b;
   auto near_of = [&](int64_t item) -> uint32_t {
     if (WF || !a.adm) return 1u;
-    int x[3];
-    geo::morton_decode(a.d, lbase + item * RE / b, L, x);
-    return geo::near_mask(a.d, x, 1 << L);
+    return geo::near_mask_k(a.d, lbase + item * RE / b, L);
   };
   auto level_on = [&](int l, uint32_t nmask) -> bool {
     if constexpr (WF) return true;
@@ -439,9 +436,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
       dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes_d + NB * XP * 8));
       if (!WF && a.adm) {  // near-field block e: panel e of the D-role panels, x of neighbour leaf e
         const int e = lr - L - 1;
-        int x[3];
-        geo::morton_decode(a.d, lbase + i0 / b, L, x);
-        const int64_t nleaf = geo::neighbour(a.d, x, e, L) - lbase;
+        const int64_t nleaf = geo::neighbour_k(a.d, lbase + i0 / b, e, L) - lbase;
         dev::tma_load_3d(st, &a.tm_d, kcr * KD, i0, e, &full[sl], pol_stream);
         dev::tma_load_2d(st + abytes_d, &a.tm_xe, static_cast<int>(nleaf * b) + kcr * KD, 0, &full[sl], pol_keep);
       } else {

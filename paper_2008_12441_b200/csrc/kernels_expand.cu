@@ -110,9 +110,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       xld = a.ldx;
       if (!a.adm) return lane == 0 ? leaf0 : kNone;
       if (lane >= a.nd) return kNone;
-      int lx[3];
-      geo::morton_decode(a.d, leaf_idx, L, lx);
-      if (!((geo::near_mask(a.d, lx, 1 << L) >> lane) & 1u)) return kNone;
+      const int64_t nb = geo::neighbour_k(a.d, leaf_idx, lane, L);
+      if (nb < 0) return kNone;
       if (a.halo_of) {
         const int h = a.halo_of[(leaf_idx - a.row0 / b) * a.nd + lane];
         if (h >= 0 && a.skip_remote) return kNone;  // H^T: that product arrives in the exchange
@@ -122,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
           return (int64_t)h * NR * a.bpad;
         }
       }
-      return geo::neighbour(a.d, lx, lane, L) * b - a.row0;
+      return nb * b - a.row0;
     };
     int64_t src = kNone;
     bool peers_ready = false;
@@ -326,7 +325,6 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   const int64_t ipl = b / Re;
   int64_t leaf0 = 0, in_leaf = 0;
   int64_t leaf_idx = 0;
-  int lx[3] = {0, 0, 0};
   uint32_t nmask = 1u, hmask = 0u;  // neighbours present / read from the halo buffer (P > 1)
   const int64_t lbase = a.row0 / b;
   auto halo_mask = [&]() -> uint32_t {
@@ -337,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   };
   // H^T with P > 1: remote neighbours' blocks are skipped (added after the kernel)
   auto present = [&]() -> uint32_t {
-    const uint32_t m = geo::near_mask(a.d, lx, 1 << L);
+    const uint32_t m = geo::near_mask_k(a.d, leaf_idx, L);
     return a.skip_remote ? m & ~hmask : m;
   };
   int slot = 0;
@@ -383,9 +381,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     while (next_range()) {
       int64_t lf = (a.row0 + cj0 * REc) / b;  // the item's leaf
       int il = static_cast<int>((cj0 * REc) % b) / REc;
-      int x2[3];
-      geo::morton_decode(2, lf, L, x2);
-      uint32_t nm = geo::near_mask(2, x2, 1 << L);
+      uint32_t nm = geo::near_mask_k(2, lf, L);
       for (int64_t j = cj0; j < cj1; ++j) {
         double acc = 0.0, acc2 = 0.0;
         for (int l = 1; l <= L + 3; ++l) {
@@ -437,8 +433,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         if (++il == ipl2) {
           il = 0;
           ++lf;
-          geo::morton_decode(2, lf, L, x2);
-          nm = geo::near_mask(2, x2, 1 << L);
+          nm = geo::near_mask_k(2, lf, L);
         }
       }
     }
@@ -531,7 +526,6 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   in_leaf = (cj0 * Re - leaf0) / Re;
   leaf_idx = (a.row0 + leaf0) / b;
   if (a.adm) {
-    geo::morton_decode(a.d, leaf_idx, L, lx);
     hmask = halo_mask();
     nmask = present();
   }
@@ -613,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
             const unsigned char* se = st + (e - e0) * dblk;
             const double2* D2 = reinterpret_cast<const double2*>(se) + ri * NPD;
             const double* xs = reinterpret_cast<const double*>(se + Re * Dp * 8);
-            const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour(a.d, lx, e, L) * b - a.row0 : leaf0;
+            const int64_t src0 = (a.adm && (b & 1)) ? geo::neighbour_k(a.d, leaf_idx, e, L) * b - a.row0 : leaf0;
             // halo segments start 16-byte aligned (bpad even): no parity offset
             const bool halo = (hmask >> e) & 1u;
             int xo[NR];
@@ -662,7 +656,6 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
       leaf0 += b;
       if (a.adm) {
         ++leaf_idx;
-        geo::morton_decode(a.d, leaf_idx, L, lx);
         hmask = halo_mask();
         nmask = present();
       }

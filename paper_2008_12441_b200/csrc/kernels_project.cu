@@ -80,12 +80,7 @@ __device__ __forceinline__ void scatter_z_std(const StreamArgs& a, const LevelAr
 // nbr[e] for the parent of source node sg at `level` (threads 0..nd-1).
 __device__ __forceinline__ void std_parent_neighbours(const StreamArgs& a, int64_t sg, int level, int t,
                                                       int64_t* nbr) {
-  if (t < a.nd) {
-    int x[3];
-    geo::morton_decode(a.d, sg >> a.d, level - 1, x);
-    const uint32_t m = geo::near_mask(a.d, x, 1 << (level - 1));
-    nbr[t] = ((m >> t) & 1u) ? geo::neighbour(a.d, x, t, level - 1) : -1;
-  }
+  if (t < a.nd) nbr[t] = geo::neighbour_k(a.d, sg >> a.d, t, level - 1);
 }
 
 template <int NR>
