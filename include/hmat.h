@@ -164,8 +164,9 @@ hmat_status hmat_panel(hmat_t H, int kind, int level, double** ptr, int64_t* row
  * run on the SIMT streaming kernels; from 3 rhs (HMAT_DMMA_MIN), where W % 16 == 0
  * (W <= 224, or <= 112 if W % 32 != 0) and 64 | leaf_size, on the FP64 tensor
  * cores in passes of 64 rhs, the last one 8, 16 or 32 wide when at most 8 / 16 /
- * 32 remain; standard admissibility from 5 rhs on one GPU with W % 16 == 0 (any W
- * up to 1024: the project runs in column slices).  Other shapes: SIMT passes of up
+ * 32 remain; standard admissibility from 5 rhs with W % 16 == 0 (any W up to
+ * 1024: the project runs in column slices; with P > 1 the packed cross-rank buffer
+ * of the standard structure serves both paths).  Other shapes: SIMT passes of up
  * to 4.  HMAT_ERR_INVALID: NULL H/x/y, nrhs < 1, x aliasing y.
  * With P > 1 a collective (same nrhs, same order on every rank); with the
  * EXTERNAL exchange use hmat_project / hmat_expand (HMAT_ERR_UNSUPPORTED). */

@@ -472,7 +472,10 @@ hmat_status ensure_dmma(hmat_s* H) {
   const size_t zrow = size_t(p.W) * hmat::kDmmaNB * sizeof(double);
   const size_t tickets = size_t(p.dgrid_p_max) * p.L * std::max(1, p.nslice) * sizeof(int) + 256;  // per slice
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zloc_d), std::max<size_t>(256, size_t(p.z_local_rows) * zrow)));
-  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zex_d), std::max<size_t>(256, size_t(p.z_exch_rows) * zrow)));
+  // exchange levels, or (standard admissibility, P > 1) the packed cross-rank buffer of a 64-wide pass
+  const size_t zex_bytes = H->sx ? size_t(H->sx->doubles_max(hmat::kDmmaNB, p.r)) * sizeof(double)
+                                 : size_t(p.z_exch_rows) * zrow;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->zex_d), std::max<size_t>(256, zex_bytes)));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->part_d),
                       std::max<size_t>(256, size_t(p.dgrid_p_max) * p.L * 2 * p.Wp * hmat::kDmmaNB * sizeof(double))));
   CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&H->cnt_d), tickets));
@@ -925,19 +928,51 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
         lv.zt = (l <= p.cross ? H->zex_d : H->zloc_d) + p.zt_off[l] * p.W * nb;
         lv.tbase = p.zt_tbase[l];
       }
-      const size_t exch = size_t(p.z_exch_rows) * p.W * nb;
+      size_t exch = size_t(p.z_exch_rows) * p.W * nb;
       a.zex_base = H->zex_d;  // PEER: the project's last CTA pushes this region to every mailbox
+      if (H->sx) {  // standard admissibility, P > 1: the packed cross-rank buffer (std_exchange.h)
+        const hmat::StdExchange& X = *H->sx;
+        exch = size_t(trans ? X.doubles_t(nb, p.r) : X.doubles(nb, p.r));
+        a.skip_remote = trans ? 1 : 0;
+        a.xchg = H->zex_d;
+        a.halo_of = H->halo_of_d;
+        a.halo_base = X.halo_base(nb, p.r);
+        a.bpad = X.bpad;
+        for (int l = 2; l <= p.L; ++l) a.lv[l].xent = H->xent_d + X.src_off[l];
+        if (!trans && X.Hn > 0) {  // remote neighbours' x: [Hn nb][bpad], box [nb][KD + 4]
+          const uint64_t dims[2] = {uint64_t(X.bpad), uint64_t(X.Hn) * nb};
+          const uint64_t strides[1] = {uint64_t(X.bpad) * 8};
+          const uint32_t box[2] = {uint32_t((p.dkc == 16 ? 16 : 32) + 4), uint32_t(nb)};
+          hmat_status st3 = encode_map(&a.tm_xh, 2, H->zex_d + a.halo_base, dims, strides, box);
+          if (st3 != HMAT_OK) return st3;
+        }
+      }
+      auto before_project = [&]() -> cudaError_t {  // P > 1, standard: this rank's halo x (H^T: products)
+        if (!H->sx) return cudaSuccess;
+        if (trans)
+          return hmat::launch_std_tpack(H->zex_d + a.halo_base, H->D, p.d_stride, p.Dp, a.x, ldx, H->tpack_d,
+                                        int64_t(H->sx->tpack.size() / 3), nb, a.nr, p.b, a.bpad, H->stream);
+        return hmat::launch_std_pack_x(H->zex_d + a.halo_base, a.x, ldx, H->pack_d, int64_t(H->sx->pack.size() / 2),
+                                       nb, a.nr, p.b, a.bpad, H->stream);
+      };
+      auto before_expand = [&]() -> cudaError_t {
+        // PEER: the rank-ordered sum of the P mailbox slots into the exchange levels,
+        // when this pass ran a project (whose last CTA raised the flags)
+        if (H->peer) return dl.dgrid_p > 0 && level_mask ? hmat::launch_peer_sum(a, H->zex_d, H->stream) : cudaSuccess;
+        if (!H->sx) return cudaSuccess;  // standard, P > 1: the received z entries into Zt
+        return hmat::launch_std_unpack_z_dmma(H->zloc_d, H->zex_d, H->unpack_d, int64_t(H->sx->unpack.size() / 2), nb,
+                                              a.nr, p.W, p.r, H->stream);
+      };
+      auto after_expand = [&]() -> cudaError_t {  // standard H^T, P > 1: the incoming near-field products
+        if (!H->sx || !trans || !dense) return cudaSuccess;
+        return hmat::launch_std_tadd(a.y, n, alpha, H->zex_d + a.halo_base, H->tadd_leaf_d, H->tadd_off_d,
+                                     H->tadd_pair_d, int64_t(H->sx->tadd_leaf.size()), nb, a.nr, p.b, a.bpad,
+                                     H->stream);
+      };
       hmat_status st2 = pass(
           H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, nb, dl.dgrid_p, dl.dsmem_p, H->stream); },
           [&] { return hmat::launch_expand_dmma(a, nb, dl.dgrid_e, dl.dsmem_e, H->stream); }, dl.dgrid_p > 0,
-          dl.dgrid_p, dl.dgrid_e, [] { return cudaSuccess; },
-          // PEER: the rank-ordered sum of the P mailbox slots into the exchange levels,
-          // when this pass ran a project (whose last CTA raised the flags)
-          [&] {
-            return H->peer && dl.dgrid_p > 0 && level_mask ? hmat::launch_peer_sum(a, H->zex_d, H->stream)
-                                                            : cudaSuccess;
-          },
-          [] { return cudaSuccess; });
+          dl.dgrid_p, dl.dgrid_e, before_project, before_expand, after_expand);
       if (st2 != HMAT_OK) return st2;
     }
   }
@@ -1079,7 +1114,10 @@ hmat_status hmat_exchange_size_op(hmat_t H, int trans, int nrhs, int64_t* count)
   const hmat::Plan& p = H->plan;
   if (use_dmma(p, nrhs)) {
     if (nrhs > hmat::kDmmaNB) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
-    *count = p.P > 1 ? p.z_exch_rows * p.W * p.dmma_layout(nrhs).nb : 0;
+    const int nb = p.dmma_layout(nrhs).nb;
+    *count = p.P > 1 ? (H->sx ? (trans ? H->sx->doubles_t(nb, p.r) : H->sx->doubles(nb, p.r))
+                              : p.z_exch_rows * p.W * nb)
+                     : 0;
   } else {
     if (nrhs > p.max_nr) return fail(HMAT_ERR_INVALID, "more than one pass of right-hand sides");
     const int cap = nr_cap(nrhs);

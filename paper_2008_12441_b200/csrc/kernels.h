@@ -121,6 +121,9 @@ struct StreamArgs {
   alignas(64) CUtensorMap tm_xe;
   // SIMT expand with ndc > 1: 2-D map over the D-role panel [N_loc][Dp], box [Re][dc]
   alignas(64) CUtensorMap tm_dse;
+  // DMMA expand, standard admissibility, P > 1: 2-D map over the packed buffer's
+  // halo x [Hn NB][bpad] (row h NB + n: halo leaf h, rhs n), box [NB][KC+4]
+  alignas(64) CUtensorMap tm_xh;
 };
 
 // Launch one project pass (template NR chosen from args.nr).  grid = plan.grid_p.
@@ -150,6 +153,9 @@ cudaError_t launch_pdl(Kernel kernel, const StreamArgs& a, int grid, int threads
 // nb: the pass width (32 or 64 right-hand sides; plan.h DmmaLayout).
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
 cudaError_t launch_expand_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s);
+// standard admissibility, P > 1: received z entries [e][nb][r] -> fragment-major Zt rows
+cudaError_t launch_std_unpack_z_dmma(double* zt, const double* xchg, const int64_t* unpack, int64_t n_unpack, int nb,
+                                     int nr, int W, int r, cudaStream_t s);
 cudaError_t configure_dmma(int nb, int64_t smem_p, int64_t smem_e);
 // PEER exchange on the tensor-core path: wait for the P ranks' flags of this
 // pass, then out[0..a.exch) = the rank-ordered sum of this rank's P mailbox slots.

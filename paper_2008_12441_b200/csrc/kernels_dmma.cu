@@ -55,16 +55,26 @@ __constant__ int16_t c_std_slot_d[3][8][kStdMaxCodes];
 // Column w = q r + aa of source node sg's z at `level`, standard admissibility:
 // target t = slot q of sg (child sigma of the parent's neighbour e), into t's
 // column qt r + aa (qt = slot of sg in t's list).  nullptr when the partner box
-// lies outside the domain (the block does not exist).
+// lies outside the domain (the block does not exist).  P > 1: a pair with an
+// entry in the packed cross-rank buffer (std_exchange.h) goes there instead,
+// rhs n at + n r (xs = r; xs = 0: the fragment-major Zt column, + zfrag(0, n)).
 template <int NB>
 __device__ __forceinline__ double* zt_column_std(const StreamArgs& a, const LevelArgs& lv, int64_t sg, int level,
-                                                 int q, int aa) {
+                                                 int q, int aa, int& xs) {
+  xs = 0;
   const int d = a.d, c = a.c;
   const int tau = static_cast<int>(sg & (c - 1));
   const int code = c_std_code_d[d - 1][tau][q];
   const int e = code >> d, sigma = code & (c - 1);
   const int64_t pt = geo::neighbour_k(d, sg >> d, e, level - 1);  // the parent's neighbour e
   if (pt < 0) return nullptr;
+  if (lv.xent) {
+    const int32_t ent = lv.xent[(sg - lv.tbase) * (a.W / a.r) + q];
+    if (ent >= 0) {
+      xs = a.r;
+      return a.xchg + (int64_t)ent * NB * a.r + aa;
+    }
+  }
   const int64_t t = pt * c + sigma;
   const int nd = d == 1 ? 3 : d == 2 ? 9 : 27;
   const int qt = c_std_slot_d[d - 1][sigma][(nd - 1 - e) * c + tau];  // eps -> -eps, sigma <-> tau
@@ -265,13 +275,15 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
           // column w = q r + aa; rhs n = 8 NT ng + 8 nt + 2 tq + h
           const int w = c0 + (mg * MT + mt) * 8 + g;
           const int q = w / a.r;
-          double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, w - q * a.r) : zt_column<NB>(a, lv, sg, q, w - q * a.r);
+          int xs = 0;
+          double* zc =
+              a.adm ? zt_column_std<NB>(a, lv, sg, l, q, w - q * a.r, xs) : zt_column<NB>(a, lv, sg, q, w - q * a.r);
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int n = (ng * NT + nt) * 8 + tq * 2 + h;
-              if (n < a.nr && zc) zc[zfrag<NB>(0, n)] = acc[mt][nt][h];
+              if (n < a.nr && zc) zc[xs ? n * xs : zfrag<NB>(0, n)] = acc[mt][nt][h];
               acc[mt][nt][h] = 0.0;
             }
         }
@@ -312,8 +324,9 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
             const int64_t off = (int64_t)w * NB + n;
             const double v = dev::sum_cg(dev::ld_cg(p0 + off), p1 + off, 2 * ps, b1 - b0);
             if (n < a.nr) {
-              double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, aa) : zt_column<NB>(a, lv, sg, q, aa);
-              if (zc) zc[zn] = v;
+              int xs = 0;
+              double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, aa, xs) : zt_column<NB>(a, lv, sg, q, aa);
+              if (zc) zc[xs ? n * xs : zn] = v;
             }
             for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
           }
@@ -395,9 +408,18 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   // for the neighbours e inside the domain, one GPU).  nmask: the present ones.
   const int ndn = !WF && a.adm ? a.nd : 1;
   const int64_t lbase = a.row0 / b;
+  // (P > 1: a neighbour on another rank -- halo_of >= 0 -- is read from the
+  // packed buffer's halo x, map tm_xh; H^T skips it: its product arrives in the
+  // exchange and is added after the kernel)
   auto near_of = [&](int64_t item) -> uint32_t {
     if (WF || !a.adm) return 1u;
-    return geo::near_mask_k(a.d, lbase + item * RE / b, L);
+    uint32_t m = geo::near_mask_k(a.d, lbase + item * RE / b, L);
+    if (a.halo_of && a.skip_remote) {
+      const int32_t* ho = a.halo_of + (item * RE / b) * a.nd;
+      for (int e = 0; e < a.nd; ++e)
+        if (ho[e] >= 0) m &= ~(1u << e);
+    }
+    return m;
   };
   auto level_on = [&](int l, uint32_t nmask) -> bool {
     if constexpr (WF) return true;
@@ -436,9 +458,14 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
       dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes_d + NB * XP * 8));
       if (!WF && a.adm) {  // near-field block e: panel e of the D-role panels, x of neighbour leaf e
         const int e = lr - L - 1;
-        const int64_t nleaf = geo::neighbour_k(a.d, lbase + i0 / b, e, L) - lbase;
         dev::tma_load_3d(st, &a.tm_d, kcr * KD, i0, e, &full[sl], pol_stream);
-        dev::tma_load_2d(st + abytes_d, &a.tm_xe, static_cast<int>(nleaf * b) + kcr * KD, 0, &full[sl], pol_keep);
+        const int h = a.halo_of ? a.halo_of[(i0 / b) * a.nd + e] : -1;
+        if (h >= 0) {  // remote neighbour: its x from the halo region, rows h NB .. h NB + NB - 1
+          dev::tma_load_2d(st + abytes_d, &a.tm_xh, kcr * KD, h * NB, &full[sl], pol_keep);
+        } else {
+          const int64_t nleaf = geo::neighbour_k(a.d, lbase + i0 / b, e, L) - lbase;
+          dev::tma_load_2d(st + abytes_d, &a.tm_xe, static_cast<int>(nleaf * b) + kcr * KD, 0, &full[sl], pol_keep);
+        }
       } else {
         dev::tma_load_2d(st, &a.tm_d, kcr * KD, i0, &full[sl], pol_stream);
         dev::tma_load_2d(st + abytes_d, &a.tm_xe, (i0 / b) * b + kcr * KD, 0, &full[sl], pol_keep);
@@ -750,7 +777,39 @@ __global__ void peer_sum_kernel(const __grid_constant__ StreamArgs a, double* __
   }
 }
 
+// Standard admissibility, P > 1: received z entries [e][NB][r] of the packed
+// buffer -> this rank's fragment-major Zt rows (the SIMT path's
+// std_unpack_z_kernel for the tensor-core layout)
+template <int NB>
+__global__ void std_unpack_z_dmma_kernel(double* __restrict__ zt, const double* __restrict__ xchg,
+                                         const int64_t* __restrict__ unpack, int64_t n_unpack, int nr, int W, int r) {
+  const int64_t total = n_unpack * nr * r;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = o / ((int64_t)nr * r);
+    const int rem = static_cast<int>(o - it * nr * r);
+    const int n = rem / r, aa = rem - n * r;
+    const int64_t e = unpack[2 * it], rq = unpack[2 * it + 1];
+    const int64_t row = rq >> 8;
+    const int q = static_cast<int>(rq & 255);
+    zt[row * (int64_t)W * NB + zfrag<NB>(q * r + aa, n)] = xchg[(e * NB + n) * r + aa];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_std_unpack_z_dmma(double* zt, const double* xchg, const int64_t* unpack, int64_t n_unpack, int nb,
+                                     int nr, int W, int r, cudaStream_t s) {
+  if (n_unpack == 0) return cudaSuccess;
+  int64_t g = (n_unpack * nr * r + 255) / 256;
+  const int grid = static_cast<int>(g < 1 ? 1 : g > 148 * 16 ? 148 * 16 : g);
+  switch (nb) {
+    case 8: std_unpack_z_dmma_kernel<8><<<grid, 256, 0, s>>>(zt, xchg, unpack, n_unpack, nr, W, r); break;
+    case 16: std_unpack_z_dmma_kernel<16><<<grid, 256, 0, s>>>(zt, xchg, unpack, n_unpack, nr, W, r); break;
+    case 32: std_unpack_z_dmma_kernel<32><<<grid, 256, 0, s>>>(zt, xchg, unpack, n_unpack, nr, W, r); break;
+    default: std_unpack_z_dmma_kernel<64><<<grid, 256, 0, s>>>(zt, xchg, unpack, n_unpack, nr, W, r); break;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_project_dmma(const StreamArgs& a, int nb, int grid, int64_t smem, cudaStream_t s) {
   if (nb == 8)

@@ -238,7 +238,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   }
   p.wslice = ws;
   p.nslice = ws > 0 ? p.W / ws : 0;
-  p.dmma_ok = ws > 0 && (p.adm == 0 || p.P == 1) && p.W % 16 == 0 && (ws % 32 == 0 ? ws <= 224 : ws <= 112) &&
+  p.dmma_ok = ws > 0 && p.W % 16 == 0 && (ws % 32 == 0 ? ws <= 224 : ws <= 112) &&
               leaf % kDmmaRE == 0 && leaf % p.dkr == 0 && p.N_loc % kDmmaRE == 0;
   if (p.dmma_ok) {
     p.vp = ws + ((4 - ws % 16) + 16) % 16;

@@ -243,7 +243,20 @@ STD_CASES = [
 ]
 
 
-@pytest.mark.parametrize("cfg,P,nrhs", STD_CASES, ids=lambda v: getattr(v, "name", str(v)))
+# the tensor-core path (from 5 rhs; W = 27 r = 432 in 2-D, 3 r = 48 in 1-D):
+# cross-rank z entries scattered by the DMMA project into the packed buffer,
+# remote neighbours' x read by tensor TMA from its halo region, the received
+# entries unpacked into the fragment-major Zt (kernels_dmma.cu)
+STD_DMMA_CASES = [
+    (HConfig("sdm2", d=2, L=4, b=64, r=16, adm=1, seed=316), 2, 5),    # 8-wide pass
+    (HConfig("sdm2", d=2, L=4, b=64, r=16, adm=1, seed=316), 4, 12),   # 16-wide
+    (HConfig("sdm2", d=2, L=4, b=64, r=16, adm=1, seed=316), 8, 20),   # 32-wide
+    (HConfig("sdm2", d=2, L=4, b=64, r=16, adm=1, seed=316), 16, 64),  # one level-2 node per rank
+    (HConfig("sdm1", d=1, L=6, b=64, r=16, adm=1, seed=317), 8, 9),    # 1D: nodes spanning ranks
+]
+
+
+@pytest.mark.parametrize("cfg,P,nrhs", STD_CASES + STD_DMMA_CASES, ids=lambda v: getattr(v, "name", str(v)))
 def test_standard_sharded_split_phase_matches_oracle(cfg, P, nrhs):
     y, cnt = sharded_std_matvec(cfg, P, nrhs)
     U, V, Dn = hgen.inputs(cfg)
@@ -283,7 +296,7 @@ def sharded_std_gemv_t(cfg, P, nrhs, alpha, beta, y0):
 
 
 @pytest.mark.parametrize("cfg,P,nrhs", [STD_CASES[0], STD_CASES[1], STD_CASES[3], STD_CASES[4], STD_CASES[5],
-                                        STD_CASES[6], STD_CASES[8], STD_CASES[9]],
+                                        STD_CASES[6], STD_CASES[8], STD_CASES[9]] + STD_DMMA_CASES,
                          ids=lambda v: getattr(v, "name", str(v)))
 def test_standard_sharded_transpose_matches_oracle(cfg, P, nrhs):
     """Standard admissibility, H^T with P > 1 (PAPER.md:961-969 GEMV "T"): the
