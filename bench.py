@@ -574,7 +574,7 @@ def run_ours(args):
         for v, xv in enumerate(xh):
             xv.copy_(X[v % nvec])
         yh = torch.empty(nrhs, n, dtype=torch.float64).pin_memory()
-        e2e_steps = max(3, min(args.steps, 16))
+        e2e_steps = max(3, min(args.steps, 64))  # the timed steps K (fill and drain of the copy pipeline amortised over them)
         matvec(xh[0].t(), yh.t())
         barrier()
         torch.cuda.synchronize()
