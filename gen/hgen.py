@@ -94,8 +94,10 @@ EXTRA_CONFIGS = {
     # 1..6): exactly the weak structure of depth 6 with leaf 256
     "c2strict": HConfig("c2strict", d=2, L=6, b=256, r=16, nrhs=1, seed=SEED_BASE + 13),
     # the mid-rhs regime (2-16 rhs against the memory floor): the c2 / c4
-    # operators with 4, 8 and 16 right-hand sides, and s2 with 16 (the standard
+    # operators with 2, 4, 8 and 16 right-hand sides, and s2 with 16 (the standard
     # structure's tensor-core passes)
+    "c2r2": HConfig("c2r2", d=2, L=7, b=64, r=16, nrhs=2, seed=SEED_BASE + 2),
+    "c4r2": HConfig("c4r2", d=2, L=9, b=64, r=16, nrhs=2, seed=SEED_BASE + 4),
     "c2r4": HConfig("c2r4", d=2, L=7, b=64, r=16, nrhs=4, seed=SEED_BASE + 2),
     "c2r8": HConfig("c2r8", d=2, L=7, b=64, r=16, nrhs=8, seed=SEED_BASE + 2),
     "c2r16": HConfig("c2r16", d=2, L=7, b=64, r=16, nrhs=16, seed=SEED_BASE + 2),

@@ -10,7 +10,7 @@ timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "bench c4 rc=$?"
 timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref_c4.json 2> gpurun_out/bench_ref_c4.err; echo "ref c4 rc=$?"
-for c in c5 c1 c2 c3 s2 c2strict c2r4 c2r8 c2r16 c4r4 c4r8 c4r16 s2r16; do
+for c in c5 c1 c2 c3 s2 c2strict c2r2 c2r4 c2r8 c2r16 c4r2 c4r4 c4r8 c4r16 s2r16; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c rc=$?"
 done
 (cd scripts && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu && ./fp64_peak) > gpurun_out/fp64_peak.txt 2>&1; echo "fp64 rc=$?"
