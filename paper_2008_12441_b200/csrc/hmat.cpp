@@ -75,6 +75,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.aflush = env_int("HMAT_PROJECT_AFLUSH", 1);
   o.dmma_upol = env_int("HMAT_DMMA_UPOL", 1);
   o.dmma8_ctas = env_int("HMAT_DMMA8_CTAS", 0);
+  o.dmma8_nw = env_int("HMAT_DMMA8_NW", o.dmma8_nw);
   o.dmma_pchunk = env_int("HMAT_DMMA_PCHUNK", 32);
   o.dmma_stages_e_narrow = env_int("HMAT_DMMA_STAGES_E", 0);
   o.dmma8_max_stages = env_int("HMAT_DMMA8_STAGES", o.dmma8_max_stages);

@@ -688,6 +688,10 @@ void launch_p8(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
       case 6: launch_p<6, 1, 4, 8>(a, grid, smem, s); break;
       default: launch_p<7, 1, 4, 8>(a, grid, smem, s); break;
     }
+  } else if (a.dnw == 3 && a.wslice == 48) {
+    launch_p<2, 1, 3, 8>(a, grid, smem, s);
+  } else if (a.dnw == 6 && a.wslice == 48) {
+    launch_p<1, 1, 6, 8>(a, grid, smem, s);
   } else {
     switch (a.wslice / 16) {
       case 1: launch_p<1, 1, 2, 8>(a, grid, smem, s); break;
@@ -703,7 +707,8 @@ cudaError_t set_p8(int64_t smem) {
   if ((e = set_p<1, 1, 4, 8>(smem)) || (e = set_p<2, 1, 4, 8>(smem)) || (e = set_p<3, 1, 4, 8>(smem)) ||
       (e = set_p<4, 1, 4, 8>(smem)) || (e = set_p<5, 1, 4, 8>(smem)) || (e = set_p<6, 1, 4, 8>(smem)) ||
       (e = set_p<7, 1, 4, 8>(smem)) || (e = set_p<1, 1, 2, 8>(smem)) || (e = set_p<3, 1, 2, 8>(smem)) ||
-      (e = set_p<5, 1, 2, 8>(smem)) || (e = set_p<7, 1, 2, 8>(smem)))
+      (e = set_p<5, 1, 2, 8>(smem)) || (e = set_p<7, 1, 2, 8>(smem)) || (e = set_p<2, 1, 3, 8>(smem)) ||
+      (e = set_p<1, 1, 6, 8>(smem)))
     return e;
   return cudaSuccess;
 }

@@ -248,7 +248,10 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       d.nb = li == 3 ? 8 : 16 << li;
       // project warps: 64 / 32 wide as p.dnw; 16 wide: 8 (W % 32 == 0) or 4; 8 wide:
       // 4 or 2 (kernels_dmma.cu)
-      d.nw = d.nb == 8 ? (ws % 32 == 0 ? 4 : 2) : d.nb == 16 ? (ws % 32 == 0 ? 8 : 4) : p.dnw;
+      // 8 wide, W = 48: 3 warps of 16 columns (5 CTAs per SM: more warps in flight than
+      // 2 warps of 24; c2 4 rhs project 0.562 -> 0.533 ms, c4 8 rhs total unchanged)
+      const int nw8 = opt.dmma8_nw > 0 && ws == 48 && 48 % (8 * opt.dmma8_nw) == 0 ? opt.dmma8_nw : 2;
+      d.nw = d.nb == 8 ? (ws % 32 == 0 ? 4 : nw8) : d.nb == 16 ? (ws % 32 == 0 ? 8 : 4) : p.dnw;
       // V rows + the nb x columns (pitch dkr + 4 = 4 mod 16 doubles)
       d.dstage_p = round_up(int64_t(p.dkr) * p.vp * 8 + int64_t(d.nb) * (p.dkr + 4) * 8, 128);
       const int64_t kd = p.dkc == 16 ? 16 : 32;  // dense-stage columns (kernels_dmma.cu KD)

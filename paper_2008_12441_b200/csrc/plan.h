@@ -137,6 +137,7 @@ struct PlanOptions {
   int aflush = 1;                   // project: asynchronous node flushes (no CTA barrier per node)
   int dmma_upol = 1;                // tensor-core expand: L2 policy of the U / D boxes (0 first, 1 normal)
   int dmma8_ctas = 0;               // 8-wide tensor-core project: CTAs per SM (0 = auto)
+  int dmma8_nw = 3;                 // 8-wide tensor-core project, W = 48: warps per CTA (2, 3 or 6; other W % 32 != 0: 2)
   int dmma8_max_stages = 8;         // 8-wide tensor-core project: ring depth cap
   int dmma_pchunk = 32;             // <= 16-wide tensor-core project: stages per level-interleaved chunk
   int dmma_stages_e_narrow = 0;     // <= 16-wide tensor-core expand: ring depth cap (0: 5 / 3 as wider passes)
