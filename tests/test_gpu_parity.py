@@ -193,6 +193,25 @@ def test_dmma_8wide_pass_few_rhs(cfg, nrhs, monkeypatch):
         hm.hmat_destroy(h)
 
 
+@pytest.mark.parametrize("nw", ["2", "6"])
+@pytest.mark.parametrize("nrhs", [3, 8, 11])
+def test_dmma_8wide_project_warp_splits(nw, nrhs, monkeypatch):
+    """The 8-wide project's CTA shapes at W = 48 (HMAT_DMMA8_NW: 2 warps x 24
+    columns, 6 x 8; the default 3 x 16 runs everywhere else), with 3 and 8 rhs
+    (one 8-wide pass) and 11 (one 16-wide pass, unaffected)."""
+    monkeypatch.setenv("HMAT_DMMA8_NW", nw)
+    cfg = HConfig("nw48", d=2, L=4, b=64, r=16, seed=91)   # W = 48
+    U, V, D, x = host_case(cfg, nrhs)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        y = np.zeros((cfg.N, nrhs), order="F")
+        hm.hmat_matvec(h, np.asfortranarray(x.reshape(cfg.N, nrhs)), y, nrhs)
+        assert_parity(y, ref.reshape(cfg.N, nrhs))
+    finally:
+        hm.hmat_destroy(h)
+
+
 def _dev_cols(x):
     """host (N,) / (N, k) array -> device tensor with the same column-major layout."""
     if x.ndim == 1:
