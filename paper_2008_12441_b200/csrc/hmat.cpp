@@ -77,6 +77,7 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dmma8_ctas = env_int("HMAT_DMMA8_CTAS", 0);
   o.dmma8_nw = env_int("HMAT_DMMA8_NW", o.dmma8_nw);
   o.dmma_pchunk = env_int("HMAT_DMMA_PCHUNK", 32);
+  o.dmma_pchunk16 = env_int("HMAT_DMMA_PCHUNK16", 16);
   o.dmma_stages_e_narrow = env_int("HMAT_DMMA_STAGES_E", 0);
   o.dmma8_max_stages = env_int("HMAT_DMMA8_STAGES", o.dmma8_max_stages);
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
@@ -904,7 +905,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       // the V bytes per level: 1/6 at W = 48) is re-read from L2, not DRAM
       // (c4 8 rhs project 10.8 -> 10.0 ms, c2 0.66 -> 0.55 ms; at W = 224 or 16
       // rhs the chunk switches cost more than they save)
-      a.pchunk = nb == 8 && p.W <= 112 ? p.dmma_pchunk : 0;
+      // 16 wide: chunks of 16 stages, so the x rows of all CTAs' current chunks
+      // (592 x 16 x 32 rows x 16 rhs: 39 MB) stay in L2 (c4 16 rhs project 13.0 ->
+      // 12.0 ms, c2 0.80 -> 0.70 ms; 32-stage chunks: 78 MB, no gain)
+      a.pchunk = nb == 8 && p.W <= 112 ? p.dmma_pchunk : nb == 16 && p.W <= 112 ? p.dmma_pchunk16 : 0;
       a.nstage_p = dl.dns_p;
       a.stage_bytes_p = dl.dstage_p;
       a.bar_off_p = dl.dns_p * dl.dstage_p;

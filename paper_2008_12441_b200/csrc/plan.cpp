@@ -84,6 +84,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
   p.aflush = opt.aflush;
   p.dmma_upol = opt.dmma_upol;
   p.dmma_pchunk = opt.dmma_pchunk;
+  p.dmma_pchunk16 = opt.dmma_pchunk16;
   if (p.adm == 0) {
     p.M = p.c - 1;  // siblings (weak admissibility)
     p.nd = 1;

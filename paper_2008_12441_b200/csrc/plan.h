@@ -82,7 +82,7 @@ struct Plan {
   int max_nr = 1;                   // widest SIMT pass (<= kMaxNR) whose stages fit in smem
   // DMMA path (nrhs >= a threshold, W % 32 == 0, W <= 224, 64 | b)
   bool dmma_ok = false;
-  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, eshape = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1, dmma_pchunk = 32;  // from PlanOptions
+  int dmma_off = 0, dmma_min = 3, dbg = 0, expand_chunk = -1, project_dyn = 1, snake = 1, pdl = 2, lpar = 1, early = 1, eshape = 1, dmma_ileave = 1, project_chunk = 4, aflush = 1, dmma_upol = 1, dmma_pchunk = 32, dmma_pchunk16 = 16;  // from PlanOptions
   int vp = 0;                       // smem pitch of staged V rows (= 4 mod 16 doubles)
   int wslice = 0, nslice = 0;       // tensor-core project: column slice width / count (W = wslice nslice)
   int dkr = kDmmaKR;                // project: V rows (the GEMM's k) per stage
@@ -139,7 +139,8 @@ struct PlanOptions {
   int dmma8_ctas = 0;               // 8-wide tensor-core project: CTAs per SM (0 = auto)
   int dmma8_nw = 3;                 // 8-wide tensor-core project, W = 48: warps per CTA (2, 3 or 6; other W % 32 != 0: 2)
   int dmma8_max_stages = 8;         // 8-wide tensor-core project: ring depth cap
-  int dmma_pchunk = 32;             // <= 16-wide tensor-core project: stages per level-interleaved chunk
+  int dmma_pchunk = 32;             // 8-wide tensor-core project: stages per level-interleaved chunk
+  int dmma_pchunk16 = 16;           // 16-wide tensor-core project: the same (0 = level after level)
   int dmma_stages_e_narrow = 0;     // <= 16-wide tensor-core expand: ring depth cap (0: 5 / 3 as wider passes)
 };
 

@@ -561,21 +561,23 @@ def test_power_iteration_back_to_back_products(monkeypatch):
                                  HConfig("ck112", d=3, L=3, b=64, r=16, seed=514)],  # W = 112
                          ids=lambda c: c.name)
 @pytest.mark.parametrize("chunk", [1, 3, 7])
-def test_dmma_project_level_chunks(cfg, chunk, monkeypatch):
-    """8-wide passes interleave the levels in chunks of HMAT_DMMA_PCHUNK stages of
-    each CTA's range, carrying the running sums between chunks (kernels_dmma.cu);
+@pytest.mark.parametrize("width", [8, 16])
+def test_dmma_project_level_chunks(cfg, chunk, width, monkeypatch):
+    """8- and 16-wide passes interleave the levels in chunks of HMAT_DMMA_PCHUNK /
+    HMAT_DMMA_PCHUNK16 stages of each CTA's range, carrying the running sums between chunks (kernels_dmma.cu);
     small chunks put chunk boundaries inside nodes of every level.  The result is
     the oracle's and bit-identical to the unchunked level order (each level's
     stages are summed in the same order)."""
-    U, V, D, x = host_case(cfg, 8)
+    nrhs = 8 if width == 8 else 13  # one 8-wide / one 16-wide pass
+    U, V, D, x = host_case(cfg, nrhs)
     ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x)
     outs = []
     for ch in (chunk, 0):
-        monkeypatch.setenv("HMAT_DMMA_PCHUNK", str(ch))
+        monkeypatch.setenv("HMAT_DMMA_PCHUNK" if width == 8 else "HMAT_DMMA_PCHUNK16", str(ch))
         h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
         try:
-            y = np.zeros((cfg.N, 8), order="F")
-            hm.hmat_matvec(h, np.asfortranarray(x), y, 8)
+            y = np.zeros((cfg.N, nrhs), order="F")
+            hm.hmat_matvec(h, np.asfortranarray(x), y, nrhs)
             outs.append(y)
         finally:
             hm.hmat_destroy(h)
