@@ -441,15 +441,15 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
         lr = 1;
         jr += jst;
       }
-      return;
+    } else {
+      do {
+        if (++lr > L + ndn) {
+          lr = 1;
+          jr += jst;
+          pmask = jr < j1 ? near_of(jr) : 1u;
+        }
+      } while (jr < j1 && !level_on(lr, pmask));
     }
-    do {
-      if (++lr > L + ndn) {
-        lr = 1;
-        jr += jst;
-        pmask = jr < j1 ? near_of(jr) : 1u;
-      }
-    } while (jr < j1 && !level_on(lr, pmask));
   };
   auto issue = [&](int sl) {  // one thread: stage (jr, lr, kcr) into slot sl
     unsigned char* st = smem + sl * a.stage_bytes_e;

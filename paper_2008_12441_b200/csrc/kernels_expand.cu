@@ -519,8 +519,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         }
       }
     }
-    return;
-  }
+  } else {  // generic shapes
   while (next_range()) {
   leaf0 = (cj0 * Re / b) * b;
   in_leaf = (cj0 * Re - leaf0) / Re;
@@ -660,6 +659,7 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         nmask = present();
       }
     }
+  }
   }
   }
 }

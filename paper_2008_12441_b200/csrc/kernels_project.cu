@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 2) project_kernel(const __grid_const
             double v = 0.0;
             for (int g = 0; g < RG; ++g) v += red[((int64_t)g * NR + kk) * Wp + col];
             if (kk < a.nr) {
-              if (SH) scatter_z_c<NR, Sh::D, Sh::R>(a, lv, sg, col, kk, v);
+              if constexpr (SH != 0) scatter_z_c<NR, Sh::D, Sh::R>(a, lv, sg, col, kk, v);
               else if (a.adm) scatter_z_std<NR>(a, lv, sg, nbr, col, kk, v);
               else scatter_z<NR>(a, lv, sg, col, kk, v);
             }
