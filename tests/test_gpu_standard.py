@@ -258,3 +258,38 @@ def test_standard_tensor_core_width_change_and_simt_agree():
         assert np.array_equal(outs[0], outs[2])
     finally:
         hm.hmat_destroy(h)
+
+
+@pytest.mark.parametrize("cfg", STD_DMMA[:2], ids=lambda c: c.name)
+@pytest.mark.parametrize("nrhs", [1, 2])
+def test_standard_simt_2d_r16(cfg, nrhs):
+    """The SIMT path of the 2-D standard structure with r = 16, b = 64 (W = 432):
+    1 rhs runs the expand's compile-time consumer shape (one row per warp, three
+    near-field blocks per dense stage), 2 rhs the generic kernel.  H, H^T, and the
+    two parts on their own -- the low-rank levels (hmat_matvec_parts, dense off)
+    vs the oracle with the near-field blocks zeroed, the near field alone vs the
+    oracle with U, V zeroed."""
+    U, V, Dn = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs)
+    h = hm.hmat_create_standard(cfg.L, cfg.d, cfg.b, cfg.r, U, V, Dn)
+    try:
+        xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        outs = {}
+        for name in ("full", "trans", "lowrank", "near"):
+            yd = torch.full_like(xd, float("nan"))
+            if name == "full":
+                hm.hmat_matvec(h, xd.t(), yd.t(), nrhs)
+            elif name == "trans":
+                hm.hmat_gemv(h, 1, 1.0, xd.t(), 0.0, yd.t(), nrhs)
+            else:
+                hm.hmat_matvec_parts(h, xd.t(), yd.t(), (1 << 64) - 1 if name == "lowrank" else 0,
+                                     name == "near", nrhs)
+            torch.cuda.synchronize()
+            outs[name] = yd.t().cpu().numpy()
+        ref = lambda U_, V_, D_: oracle.std_matvec(cfg.d, cfg.L, cfg.b, cfg.r, U_, V_, D_, x)
+        assert_parity(outs["full"], ref(U, V, Dn))
+        assert_parity(outs["trans"], oracle.std_matvec_t(cfg.d, cfg.L, cfg.b, cfg.r, U, V, Dn, x))
+        assert_parity(outs["lowrank"], ref(U, V, np.zeros_like(Dn)))
+        assert_parity(outs["near"], ref(np.zeros_like(U), np.zeros_like(V), Dn))
+    finally:
+        hm.hmat_destroy(h)
