@@ -203,6 +203,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
   int slot = 0;
   uint32_t phase = 0;
   constexpr int NACC = MT * NT * 2;
+  // 8-wide passes with few fragments per stage: release a slot before its DMMAs
+  constexpr bool EARLY = NB == 8 && (MT + NT) * (KR / 4) <= 32;
   double* accb = a.accbuf + ((int64_t)bid * L * (NW * 32) + tid) * NACC;  // + (l-1) NW 32 NACC
   for (int64_t ck0 = k0; ck0 < k1; ck0 += CH) {
   const int64_t ck1 = ck0 + CH < k1 ? ck0 + CH : k1;
@@ -227,6 +229,38 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
       const double* Vs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p) + mg * 8 * MT + g;
       const double* Xs = reinterpret_cast<const double*>(smem + slot * a.stage_bytes_p + vbytes) +
                          (ng * 8 * NT + g) * XPP + tq;
+      if constexpr (EARLY) {
+        // 8 wide: the whole stage's fragments to registers, the slot handed back,
+        // then the DMMAs -- the slot is held for the loads only, so its refill
+        // (the pass is a stream: little math per byte) starts a DMMA chain earlier
+        double af[KR / 4][MT], bf[KR / 4][NT];
+#pragma unroll
+        for (int ks = 0; ks < KR / 4; ++ks) {
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) af[ks][mt] = Vs[(ks * 4 + tq) * VP + mt * 8];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) bf[ks][nt] = Xs[nt * 8 * XPP + ks * 4];
+        }
+        // every lane's loads are ordered before lane 0's release (syncwarp), and
+        // the last warp's acquire orders them all before its refill
+        __syncwarp();
+        if (lane == 0) {
+          const int prev = dev::atom_add_acq_rel_cta(&done[slot], 1);
+          if (prev == NCW - 1) {
+            done[slot] = 0;
+            if (lr <= L) {
+              dev::fence_proxy_async_smem();
+              issue(slot);
+            }
+          }
+        }
+#pragma unroll
+        for (int ks = 0; ks < KR / 4; ++ks)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[ks][mt], bf[ks][nt]);
+      } else {
 #pragma unroll
       for (int ks = 0; ks < KR / 4; ++ks) {
         double av[MT], bv[NT];
@@ -251,6 +285,7 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
             issue(slot);
           }
         }
+      }
       }
       if (lr <= L) advance();
       if (++slot == NS) {
