@@ -351,19 +351,46 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
           // thread: rhs n = tid % NB, columns w = tid / NB, + CTP / NB, ... (CTP is a multiple of NB)
           const int n = tid % NB, wstep = CTP / NB;
           const int64_t zn = zfrag<NB>(0, n);
-          int w = c0 + tid / NB, q = w / a.r, aa = w - q * a.r;
+          const int w0 = c0 + tid / NB;
+          const int nwt = w0 < c0 + WS ? (c0 + WS - w0 + wstep - 1) / wstep : 0;  // this thread's columns
           const int64_t ps = (int64_t)Wp * NB;
           const double* p0 = a.part + (((int64_t)(l - 1) * G + b0) * 2 + slot0) * ps;
           const double* p1 = a.part + (((int64_t)(l - 1) * G + b0 + 1) * 2) * ps;
-          for (; w < c0 + WS; w += wstep) {
-            const int64_t off = (int64_t)w * NB + n;
-            const double v = dev::sum_cg(dev::ld_cg(p0 + off), p1 + off, 2 * ps, b1 - b0);
-            if (n < a.nr) {
-              int xs = 0;
-              double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, aa, xs) : zt_column<NB>(a, lv, sg, q, aa);
-              if (zc) zc[xs ? n * xs : zn] = v;
+          const int64_t cnt = b1 - b0;
+          // 2 columns at a time, 8 partials deep: 16 loads in flight per thread (a
+          // node spanning ~100 CTAs -- the coarsest level of a small operator -- is
+          // otherwise a long serial chain of L2 round trips in one CTA); each
+          // column's sum keeps the CTA order
+          for (int j0 = 0; j0 < nwt; j0 += 2) {
+            double v[2];
+            int64_t off[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              off[u] = (int64_t)(w0 + (j0 + u) * wstep) * NB + n;
+              v[u] = j0 + u < nwt ? dev::ld_cg(p0 + off[u]) : 0.0;
             }
-            for (aa += wstep; aa >= a.r; aa -= a.r) ++q;
+            for (int64_t i = 0; i < cnt; i += 8) {
+              double t[2][8];
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                  t[u][s] = (j0 + u < nwt && i + s < cnt) ? dev::ld_cg(p1 + off[u] + (i + s) * 2 * ps) : 0.0;
+#pragma unroll
+              for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+                  if (i + s < cnt) v[u] += t[u][s];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              if (j0 + u < nwt && n < a.nr) {
+                const int w = w0 + (j0 + u) * wstep, q = w / a.r, aa = w - q * a.r;
+                int xs = 0;
+                double* zc = a.adm ? zt_column_std<NB>(a, lv, sg, l, q, aa, xs) : zt_column<NB>(a, lv, sg, q, aa);
+                if (zc) zc[xs ? n * xs : zn] = v[u];
+              }
+            }
           }
           if (tid == 0) *ticket = 0;
         }
