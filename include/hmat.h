@@ -34,7 +34,9 @@
  * VECTORS: x and y are N_loc x nrhs column-major with leading dimension N_loc
  * (block-row distributed exactly like the panels).  They may
  * be device pointers (on H's device) or host pointers; host vectors are copied
- * in/out by the call.  x and y must not alias.  y is overwritten.
+ * in/out by the call (a host y of a blocking call leaves in row chunks while the
+ * expand kernel computes the next ones: HMAT_Y_CHUNKS, default 4, launches the
+ * expand once per chunk).  x and y must not alias.  y is overwritten.
  *
  * STREAMS AND SYNCHRONISATION: work is enqueued on H's stream.  With device
  * x/y the call returns without waiting (like a BLAS handle); with a host x or

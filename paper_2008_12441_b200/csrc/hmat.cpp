@@ -145,6 +145,11 @@ struct hmat_s {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   bool comp_rec[2] = {false, false}, out_rec[2] = {false, false};
   int apar = 0;
+  // blocking host-y calls: expand in row chunks, each chunk's y copied out on
+  // s_y while the next chunk runs (HMAT_Y_CHUNKS)
+  int y_chunks = 4;
+  cudaStream_t s_y = nullptr;
+  cudaEvent_t ev_y[8] = {};
   hmat::Comm* comm = nullptr;
   // DMMA (many right-hand sides) buffers, allocated on first use
   double* zloc_d = nullptr;
@@ -224,6 +229,12 @@ void release(hmat_s* H) {
   }
   if (H->s_in) cudaStreamDestroy(H->s_in);
   if (H->s_out) cudaStreamDestroy(H->s_out);
+  if (H->s_y) {
+    cudaStreamSynchronize(H->s_y);
+    cudaStreamDestroy(H->s_y);
+  }
+  for (cudaEvent_t ev : H->ev_y)
+    if (ev) cudaEventDestroy(ev);
   cudaFree(H->zloc_d);
   cudaFree(H->zex_d);
   cudaFree(H->part_d);
@@ -357,6 +368,7 @@ hmat_status create_common(int depth, int dim, int leaf, int rank, const hmat_dis
       (p.dmma_ok && p.dl[3].ok && (e = hmat::configure_dmma(8, p.dl[3].dsmem_p, p.dl[3].dsmem_e))) ||
       (e = cudaStreamSynchronize(H->stream)))
     return bail(cuda_fail(e, "initialising device buffers"));
+  H->y_chunks = std::max(1, std::min(8, env_int("HMAT_Y_CHUNKS", 4)));
   H->external = p.P > 1 && dist->exchange == HMAT_EXCHANGE_EXTERNAL;
   H->tree = p.P > 1 && dist->exchange == HMAT_EXCHANGE_TREE;
   H->peer = peer;
@@ -803,6 +815,45 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   // or event wait of this call in between
   a.pdl_p = a.pdl && p.pdl >= 2 && p.P == 1 && !async_io ? 1 : 0;
 
+  // A blocking call with y in host memory: the expand runs in row chunks of
+  // whole leaves and each chunk's rows of y are copied out (on s_y) while the
+  // next chunk computes, so only the last chunk's copy follows the kernels.
+  // (Not with the standard structure's P > 1 exchange -- H^T adds to y after the
+  // expand -- nor under the per-kernel profiler or the peer exchange.)
+  const int ychunks =
+      (!y_dev && !async_io && phases == kPhaseAll && !H->peer && !H->sx && !H->prof) ? H->y_chunks : 1;
+  bool y_split = false;
+  auto expand_rows = [&](auto&& launch, int64_t item_rows, bool dmma, int c0, int nr) -> cudaError_t {
+    if (ychunks <= 1) return launch();
+    cudaError_t e;
+    if (!H->s_y) {
+      if ((e = cudaStreamCreateWithFlags(&H->s_y, cudaStreamNonBlocking))) return e;
+      for (cudaEvent_t& ev : H->ev_y)
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return e;
+    }
+    const int64_t units = n / p.b, per = (units + ychunks - 1) / ychunks;  // leaves (b is a multiple of item_rows)
+    int k = 0;
+    for (int64_t u0 = 0; u0 < units; u0 += per, ++k) {
+      const int64_t r0 = u0 * p.b, r1 = std::min(units, u0 + per) * p.b;
+      a.item0 = r0 / item_rows;
+      if (dmma)
+        a.e_items = (r1 - r0) / item_rows;
+      else
+        a.items_e = (r1 - r0) / item_rows;
+      if ((e = launch())) return e;
+      if ((e = cudaEventRecord(H->ev_y[k], H->stream)) || (e = cudaStreamWaitEvent(H->s_y, H->ev_y[k], 0)) ||
+          (e = cudaMemcpy2DAsync(y + int64_t(c0) * n + r0, size_t(n) * sizeof(double), yd + int64_t(c0) * n + r0,
+                                 size_t(n) * sizeof(double), size_t(r1 - r0) * sizeof(double), size_t(nr),
+                                 cudaMemcpyDeviceToHost, H->s_y)))
+        return e;
+    }
+    a.item0 = 0;
+    a.e_items = 0;
+    a.items_e = p.items_e;
+    y_split = true;
+    return cudaSuccess;
+  };
+
   // One pass of right-hand sides: [zero the exchange levels] project
   // [copy them out] [NCCL sum over ranks] [copy the caller's sum in] expand.
   auto pass = [&](double* zex, size_t exch, auto&& project, auto&& expand, bool has_project, int gp, int ge,
@@ -976,7 +1027,11 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       };
       hmat_status st2 = pass(
           H->zex_d, exch, [&] { return hmat::launch_project_dmma(a, nb, dl.dgrid_p, dl.dsmem_p, H->stream); },
-          [&] { return hmat::launch_expand_dmma(a, nb, dl.dgrid_e, dl.dsmem_e, H->stream); }, dl.dgrid_p > 0,
+          [&] {
+            return expand_rows([&] { return hmat::launch_expand_dmma(a, nb, dl.dgrid_e, dl.dsmem_e, H->stream); },
+                               hmat::kDmmaRE, true, c0, a.nr);
+          },
+          dl.dgrid_p > 0,
           dl.dgrid_p, dl.dgrid_e, before_project, before_expand, after_expand);
       if (st2 != HMAT_OK) return st2;
     }
@@ -1067,7 +1122,11 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     }
     hmat_status st2 = pass(
         H->zex, exch, [&] { return hmat::launch_project(a, cap, grid_p, ly.smem_p, H->stream); },
-        [&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, ly.grid_p > 0, grid_p,
+        [&] {
+          return expand_rows([&] { return hmat::launch_expand(a, cap, ly.grid_e, ly.smem_e, H->stream); }, p.Re, false,
+                             c0, nr);
+        },
+        ly.grid_p > 0, grid_p,
         ly.grid_e, pack_x, unpack_z, add_t);
     if (st2 != HMAT_OK) return st2;
   }
@@ -1083,13 +1142,14 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     CUDA_TRY(cudaGetLastError());
     return HMAT_OK;
   }
-  if (!y_dev && (phases & kPhaseExpand)) {
+  if (!y_dev && (phases & kPhaseExpand) && !y_split) {
     prof_begin(H, 3, &ep);
     CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->stream));
     prof_end(H, &ep);
   }
   if (host_io) {
     CUDA_TRY(cudaStreamSynchronize(H->stream));
+    if (y_split) CUDA_TRY(cudaStreamSynchronize(H->s_y));
     hmat_status sa = check_async(H);
     if (sa != HMAT_OK) return sa;
   }

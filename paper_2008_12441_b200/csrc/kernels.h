@@ -63,6 +63,8 @@ struct StreamArgs {
   int64_t dyn_chunk; // project: stages per chunk (a multiple of the level's node size)
   int* sched_p;      // project: [next chunk, CTAs done]
   int64_t stage_bytes_e, items_e;
+  int64_t item0;     // expand: first item of this launch (row chunks of a host-y product; 0 = from the start)
+  int64_t e_items;   // tensor-core expand: items of this launch (0 = all)
   int xs_p, xs_e;
   int vp;              // DMMA project: smem pitch of staged V rows
   int dkr;             // DMMA project: V rows per stage (32)

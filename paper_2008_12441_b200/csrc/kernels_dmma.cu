@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t G = gridDim.x, bid = blockIdx.x;
   const int W = a.W, b = a.b, L = a.L;
-  const int64_t items = a.N_loc / RE;
+  // items [ib, ib + items) of the shard (a row chunk of a host-y product, or all)
+  const int64_t ib = a.item0;
+  const int64_t items = a.e_items > 0 ? a.e_items : a.N_loc / RE;
   // item order: interleaved (CTA b takes items b, b + G, b + 2G, ...: the G CTAs
   // work on G consecutive tiles at any time, so the coarse levels' Zt chunks they
   // share stay in L2 -- a handful of nodes instead of one per CTA, which at c5
@@ -490,7 +492,7 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   // refill cursor (item jr, level lr in 1..L+ndn (> L: dense), chunk kcr): identical in every warp
   int64_t jr = j0;
   int lr = 1, kcr = 0;
-  uint32_t pmask = jr < j1 ? near_of(jr) : 1u;
+  uint32_t pmask = jr < j1 ? near_of(ib + jr) : 1u;
   bool any = false;
   for (int l = 1; l <= L + ndn; ++l) any = any || level_on(l, a.adm ? 1u << ((a.nd - 1) / 2) : 1u);  // (self)
   if (!any) jr = j1;
@@ -508,14 +510,14 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
         if (++lr > L + ndn) {
           lr = 1;
           jr += jst;
-          pmask = jr < j1 ? near_of(jr) : 1u;
+          pmask = jr < j1 ? near_of(ib + jr) : 1u;
         }
       } while (jr < j1 && !level_on(lr, pmask));
     }
   };
   auto issue = [&](int sl) {  // one thread: stage (jr, lr, kcr) into slot sl
     unsigned char* st = smem + sl * a.stage_bytes_e;
-    const int i0 = static_cast<int>(jr * RE);
+    const int i0 = static_cast<int>((ib + jr) * RE);
     if (lr > L) {
       dev::mbar_arrive_expect_tx(&full[sl], static_cast<uint32_t>(abytes_d + NB * XP * 8));
       if (!WF && a.adm) {  // near-field block e: panel e of the D-role panels, x of neighbour leaf e
@@ -562,13 +564,13 @@ __global__ void __launch_bounds__(kThreadsE, 2) expand_dmma_kernel(const __grid_
   int slot = 0;
   uint32_t phase = 0;
   for (int64_t j = j0; j < j1; j += jst) {
-    const int64_t i0 = j * RE;
+    const int64_t i0 = (ib + j) * RE;
     double acc[MT][NTW][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int k = 0; k < NTW; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
-    const uint32_t cmask = near_of(j);
+    const uint32_t cmask = near_of(ib + j);
     for (int l = 1; l <= L + ndn; ++l) {
       const bool is_d = (l > L);
       if (!level_on(l, cmask)) continue;

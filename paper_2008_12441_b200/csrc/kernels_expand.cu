@@ -65,7 +65,10 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t G = gridDim.x, bid = blockIdx.x;
-  const int64_t j0 = a.items_e * bid / G, j1 = a.items_e * (bid + 1) / G;
+  // items [item0, item0 + items_e) of the shard (item0 > 0: one of the row
+  // chunks of a host-y product, whose copy out overlaps the next chunk)
+  const int64_t ib = a.item0;
+  const int64_t j0 = ib + a.items_e * bid / G, j1 = ib + a.items_e * (bid + 1) / G;
   const int Re = a.Re, W = a.W, Wp = a.Wp, Dp = a.Dp, b = a.b, L = a.L;
   const int NS = a.nstage_e;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.bar_off_e);
@@ -158,8 +161,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
         return false;
       }
       chunk = c;
-      cj0 = int64_t(c) * a.chunk_e;
-      cj1 = cj0 + a.chunk_e < a.items_e ? cj0 + a.chunk_e : a.items_e;
+      cj0 = ib + int64_t(c) * a.chunk_e;
+      cj1 = cj0 + a.chunk_e < ib + a.items_e ? cj0 + a.chunk_e : ib + a.items_e;
       first_stage = true;
       return true;
     };
@@ -352,8 +355,8 @@ __global__ void __launch_bounds__(kThreads, 2) expand_kernel(const __grid_consta
     dev::mbar_wait(&full[slot], phase);
     const int c = chunk_q[slot];
     if (c < 0) return false;
-    cj0 = int64_t(c) * a.chunk_e;
-    cj1 = cj0 + a.chunk_e < a.items_e ? cj0 + a.chunk_e : a.items_e;
+    cj0 = ib + int64_t(c) * a.chunk_e;
+    cj1 = cj0 + a.chunk_e < ib + a.items_e ? cj0 + a.chunk_e : ib + a.items_e;
     peeked = true;
     return true;
   };
