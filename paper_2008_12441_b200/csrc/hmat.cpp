@@ -820,17 +820,21 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   // next chunk computes, so only the last chunk's copy follows the kernels.
   // (Not with the standard structure's P > 1 exchange -- H^T adds to y after the
   // expand -- nor under the per-kernel profiler or the peer exchange.)
-  const int ychunks =
-      (!y_dev && !async_io && phases == kPhaseAll && !H->peer && !H->sx && !H->prof) ? H->y_chunks : 1;
+  // (Also in the streaming mode: there the copies go to s_out, and the last
+  // product's copy-out -- the pipeline's drain -- overlaps its own expand.)
+  const int ychunks = (!y_dev && phases == kPhaseAll && !H->peer && !H->sx && !H->prof) ? H->y_chunks : 1;
   bool y_split = false;
   auto expand_rows = [&](auto&& launch, int64_t item_rows, bool dmma, int c0, int nr) -> cudaError_t {
     if (ychunks <= 1) return launch();
     cudaError_t e;
-    if (!H->s_y) {
+    cudaStream_t s_copy = async_io ? H->s_out : H->s_y;
+    if (!async_io && !H->s_y) {
       if ((e = cudaStreamCreateWithFlags(&H->s_y, cudaStreamNonBlocking))) return e;
+      s_copy = H->s_y;
+    }
+    if (!H->ev_y[0])
       for (cudaEvent_t& ev : H->ev_y)
         if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return e;
-    }
     const int64_t units = n / p.b, per = (units + ychunks - 1) / ychunks;  // leaves (b is a multiple of item_rows)
     int k = 0;
     for (int64_t u0 = 0; u0 < units; u0 += per, ++k) {
@@ -841,10 +845,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       else
         a.items_e = (r1 - r0) / item_rows;
       if ((e = launch())) return e;
-      if ((e = cudaEventRecord(H->ev_y[k], H->stream)) || (e = cudaStreamWaitEvent(H->s_y, H->ev_y[k], 0)) ||
+      if ((e = cudaEventRecord(H->ev_y[k], H->stream)) || (e = cudaStreamWaitEvent(s_copy, H->ev_y[k], 0)) ||
           (e = cudaMemcpy2DAsync(y + int64_t(c0) * n + r0, size_t(n) * sizeof(double), yd + int64_t(c0) * n + r0,
                                  size_t(n) * sizeof(double), size_t(r1 - r0) * sizeof(double), size_t(nr),
-                                 cudaMemcpyDeviceToHost, H->s_y)))
+                                 cudaMemcpyDeviceToHost, s_copy)))
         return e;
     }
     a.item0 = 0;
@@ -1134,8 +1138,10 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     CUDA_TRY(cudaEventRecord(H->ev_comp[par], H->stream));
     H->comp_rec[par] = true;
     if (!y_dev) {
-      CUDA_TRY(cudaStreamWaitEvent(H->s_out, H->ev_comp[par], 0));
-      CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->s_out));
+      if (!y_split) {  // (row-chunked: the chunks' copies are already queued on s_out)
+        CUDA_TRY(cudaStreamWaitEvent(H->s_out, H->ev_comp[par], 0));
+        CUDA_TRY(cudaMemcpyAsync(y, yd, size_t(n) * nrhs * sizeof(double), cudaMemcpyDefault, H->s_out));
+      }
       CUDA_TRY(cudaEventRecord(H->ev_out[par], H->s_out));
       H->out_rec[par] = true;
     }
