@@ -377,6 +377,41 @@ def test_host_async_streaming_mode():
         hm.hmat_destroy(h)
 
 
+@pytest.mark.parametrize("chunks", ["1", "3", "8"])
+@pytest.mark.parametrize("nrhs", [1, 2, 9, 70])
+def test_host_y_row_chunks_bitwise(chunks, nrhs, monkeypatch):
+    """A host y leaves in row chunks of whole leaves while the expand computes
+    the next ones (HMAT_Y_CHUNKS; the expand runs once per chunk over an item
+    range): y is bit-identical to the device-pointer product, for the SIMT (1, 2
+    rhs) and tensor-core (9: one 16-wide pass, 70: a 64- and an 8-wide pass)
+    kernels, in the blocking and the streaming mode."""
+    monkeypatch.setenv("HMAT_Y_CHUNKS", chunks)
+    cfg = HConfig("ych", d=2, L=4, b=64, r=16, seed=1402)   # 256 leaves
+    U, V, D = hgen.inputs(cfg)
+    x = hgen.xblock(cfg, nrhs=nrhs)
+    h = hm.hmat_create(cfg.L, cfg.d, cfg.b, cfg.r, U, V, D)
+    try:
+        xd = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+        yd = torch.empty_like(xd)
+        hm.hmat_matvec(h, xd.t(), yd.t(), nrhs)
+        torch.cuda.synchronize()
+        ref = yd.t().cpu().numpy()
+        xh = torch.from_numpy(np.ascontiguousarray(x.T)).pin_memory()
+        yh = torch.full_like(xh, float("nan")).pin_memory()
+        hm.hmat_matvec(h, xh.t(), yh.t(), nrhs)                       # blocking
+        assert np.array_equal(yh.t().numpy(), ref)
+        hm.hmat_set_host_async(h, True)                                # streaming
+        ys = [torch.full_like(xh, float("nan")).pin_memory() for _ in range(3)]
+        for y in ys:
+            hm.hmat_matvec(h, xh.t(), y.t(), nrhs)
+        hm.hmat_synchronize(h)
+        for y in ys:
+            assert np.array_equal(y.t().numpy(), ref)
+        assert_parity(ref, oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x))
+    finally:
+        hm.hmat_destroy(h)
+
+
 @pytest.mark.parametrize("snake", ["0", "1"])
 def test_project_stream_direction(snake, monkeypatch):
     """Project's per-level stream direction (HMAT_PROJECT_SNAKE): backwards even
