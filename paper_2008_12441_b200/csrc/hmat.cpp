@@ -822,7 +822,11 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
   // expand -- nor under the per-kernel profiler or the peer exchange.)
   // (Also in the streaming mode: there the copies go to s_out, and the last
   // product's copy-out -- the pipeline's drain -- overlaps its own expand.)
-  const int ychunks = (!y_dev && phases == kPhaseAll && !H->peer && !H->sx && !H->prof) ? H->y_chunks : 1;
+  // Only where the copy is worth the extra launches: from 4 MB of y (c1's 32 KB
+  // took 2.4x longer per call in 4 launches).
+  const bool y_big = size_t(n) * size_t(nrhs) * sizeof(double) >= (size_t(4) << 20);
+  const int ychunks =
+      (!y_dev && y_big && phases == kPhaseAll && !H->peer && !H->sx && !H->prof) ? H->y_chunks : 1;
   bool y_split = false;
   auto expand_rows = [&](auto&& launch, int64_t item_rows, bool dmma, int c0, int nr) -> cudaError_t {
     if (ychunks <= 1) return launch();
