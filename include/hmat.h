@@ -34,7 +34,7 @@
  * VECTORS: x and y are N_loc x nrhs column-major with leading dimension N_loc
  * (block-row distributed exactly like the panels).  They may
  * be device pointers (on H's device) or host pointers; host vectors are copied
- * in/out by the call (a host y of a blocking call leaves in row chunks while the
+ * in/out by the call (a host y of 4 MB or more leaves in row chunks while the
  * expand kernel computes the next ones: HMAT_Y_CHUNKS, default 4, launches the
  * expand once per chunk).  x and y must not alias.  y is overwritten.
  *
@@ -383,7 +383,9 @@ hmat_status hmat_cta_trace_read(hmat_t H, int kernel, int64_t* out, int max_ctas
  * rank (the steps of PAPER.md:652-663 as kernels): per pass of right-hand sides, project + expand, + pack / unpack with
  * standard admissibility and P > 1, + log2 P adds with the TREE exchange, + the
  * mailbox sum on the tensor-core path with the PEER exchange (NCCL's own kernels
- * and memsets not counted).  -1 for NULL H or nrhs < 1. */
+ * and memsets not counted), for device x / y (a host y of 4 MB or more adds
+ * HMAT_Y_CHUNKS - 1 expand launches per pass: VECTORS above).  -1 for NULL H or
+ * nrhs < 1. */
 int64_t hmat_launches_per_matvec(hmat_t H, int nrhs);
 
 /* Host-only description of a shard's plan (no GPU needed). */
