@@ -83,6 +83,9 @@ hmat::PlanOptions options_from_env(int num_sms) {
   o.dmma_nw = env_int("HMAT_DMMA_NW", o.dmma_nw);
   o.dmma_narrow = env_int("HMAT_DMMA_NARROW", o.dmma_narrow);
   o.dmma_kc = env_int("HMAT_DMMA_KC", 0);
+  o.dmma16_ctas = env_int("HMAT_DMMA16_CTAS", 0);
+  o.dmma16_max_stages = env_int("HMAT_DMMA16_STAGES", 0);
+  o.dmma_e_ctas = env_int("HMAT_DMMA_E_CTAS", 0);
   return o;
 }
 

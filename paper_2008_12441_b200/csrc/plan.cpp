@@ -261,10 +261,11 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
                             128);
       // project CTAs per SM: 16 warps' worth (1 CTA of 16, 2 of 8, 4 of 4), fewer if
       // two stages do not fit (64 / 32 wide keep their measured budgets)
-      int ctas = 16 / d.nw;
+      int ctas = d.nb == 16 && opt.dmma16_ctas > 0 ? std::min(opt.dmma16_ctas, 16 / d.nw) : 16 / d.nw;
+      const int cap_p = d.nb == 16 && opt.dmma16_max_stages > 0 ? opt.dmma16_max_stages : opt.dmma_max_stages_p;
       for (;; --ctas) {
         const int64_t pbudget = d.nb <= 16 ? 227 * 1024 / ctas - 1024 : (p.dnw == 8 ? 112 * 1024 : 226 * 1024);
-        d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, opt.dmma_max_stages_p), (pbudget - bar_bytes) / d.dstage_p));
+        d.dns_p = static_cast<int>(std::min<int64_t>(std::max(2, cap_p), (pbudget - bar_bytes) / d.dstage_p));
         if (d.dns_p >= 2 || ctas == 1) break;
       }
       if (d.nb == 8) {
@@ -291,11 +292,19 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       // narrow passes (<= 16 rhs) carry little math per stage, so deeper rings
       // keep more bytes in flight (HMAT_DMMA_STAGES_E caps them)
       const int cap_e = d.nb <= 16 && opt.dmma_stages_e_narrow > 0 ? opt.dmma_stages_e_narrow : (p.dkc == 16 ? 5 : 3);
-      d.dns_e = static_cast<int>(std::min<int64_t>(cap_e, (112 * 1024 - bar_bytes) / d.dstage_e));
+      // CTAs per SM: 2 (112 KB each), or at 16 wide under weak admissibility 3
+      // (A/B r02, ms per 16-rhs product, 2 -> 3 CTAs: c4 26.05 -> 25.37, c3 7.68 ->
+      // 7.48, c2 1.233 -> 1.223; not the standard structure: s2 10.34 -> 10.82);
+      // HMAT_DMMA_E_CTAS = 1..3 sets it for <= 16-wide passes
+      const int ctas_e = d.nb <= 16 && opt.dmma_e_ctas >= 1 && opt.dmma_e_ctas <= 3 ? opt.dmma_e_ctas
+                         : d.nb == 16 && !p.adm && opt.dmma_e_ctas == 0            ? 3
+                                                                                   : 2;
+      const int64_t ebudget = ctas_e == 2 ? 112 * 1024 : 227 * 1024 / ctas_e - 1024;
+      d.dns_e = static_cast<int>(std::min<int64_t>(cap_e, (ebudget - bar_bytes) / d.dstage_e));
       d.dsmem_p = d.dns_p * d.dstage_p + bar_bytes;
       d.dsmem_e = d.dns_e * d.dstage_e + bar_bytes;
       d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas, depth > 0 ? p.N_loc / p.dkr : 0));
-      d.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * 2, p.N_loc / kDmmaRE));
+      d.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas_e, p.N_loc / kDmmaRE));
       // (a 32-wide project pass with W % 32 != 0 needs the 8-warp grid: kernels_dmma.cu)
       const bool narrow_on = d.nb == kDmmaNB || (d.nb == 32   ? opt.dmma_narrow >= 1
                                                  : d.nb == 16 ? opt.dmma_narrow >= 2

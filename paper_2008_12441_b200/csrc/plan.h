@@ -142,6 +142,9 @@ struct PlanOptions {
   int dmma_pchunk = 32;             // 8-wide tensor-core project: stages per level-interleaved chunk
   int dmma_pchunk16 = 16;           // 16-wide tensor-core project: the same (0 = level after level)
   int dmma_stages_e_narrow = 0;     // <= 16-wide tensor-core expand: ring depth cap (0: 5 / 3 as wider passes)
+  int dmma16_ctas = 0;              // 16-wide tensor-core project: CTAs per SM (0 = auto: 16 warps' worth)
+  int dmma16_max_stages = 0;        // 16-wide tensor-core project: ring depth cap (0 = dmma_max_stages_p)
+  int dmma_e_ctas = 0;              // <= 16-wide tensor-core expand: CTAs per SM, 1-3 (0 = auto: 3 at 16 wide, weak; else 2)
 };
 
 // Validates arguments and fills `plan`.  Returns "" on success, else a message.
