@@ -163,7 +163,7 @@ class ClockSampler:
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, device):
         self.device = device
@@ -193,7 +193,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, smax, reasons = [], [], set()
+        sm, smax, reasons, pw, plim = [], [], set(), [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [s.strip() for s in ln.split(",")]
@@ -207,10 +207,16 @@ class ClockSampler:
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
+            for dst, i in ((pw, 3), (plim, 9)):  # board power draw / enforced limit, W
+                try:
+                    dst.append(float(f[i]))
+                except (ValueError, IndexError):
+                    pass
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": float(np.median(pw)) if pw else None,
+                "power_limit_w": max(plim) if plim else None}
 
 
 # --------------------------------------------------------------------------------------
@@ -642,6 +648,8 @@ def run_ours(args):
                 "read_stream_source": "scripts/hbm_read_peak.cu sustained bulk-TMA read ring (profiles/r01_hbm_read_peak.txt)"}
 
     value = 1e3 / ms_step  # matvecs/s of the whole job (one operator across all ranks)
+    if clk.get("power_w"):  # board energy per matvec (rank 0's GPU; median power x step time)
+        clk["j_per_matvec"] = clk["power_w"] * ms_step / 1e3
     # bytes of the packed cross-GPU exchange buffer per pass (0 at P = 1), per step
     exch_width = min(nrhs, 64)
     try:
