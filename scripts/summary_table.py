@@ -18,9 +18,11 @@ for c in ["c1", "c2", "c3", "c4", "c5", "s2", "c2strict", "c2r2", "c2r4", "c2r8"
                 f"{r['achieved']:,.1f} {r['unit']} | {r['peak']:,.1f} | {r['frac']:.3f} | "
                 f"{'%.3f' % rs if rs else '—'} | {ph['project']:.3f} | {ph['expand']:.3f} | "
                 f"{e['value']:,.1f} / {e['blocking']['value']:,.1f} | {cpu['value']:.4g} | "
-                f"{clk['sm_mhz']:.0f}, {', '.join(clk['reasons']) or '-'} |")
+                f"{clk['sm_mhz']:.0f}, {', '.join(clk['reasons']) or '-'} | "
+                f"{'%.0f W, %.1f J' % (clk['power_w'], clk['j_per_matvec']) if clk.get('j_per_matvec') else '—'} |")
 hdr = ("| cfg | matvec/s | ms/step | bound | dominant kernel | achieved | peak | frac | frac of 7.3 TB/s read stream "
-       "| project ms | expand ms | e2e streaming / blocking (matvec/s) | CPU oracle (matvec/s, all cores) | SM MHz, throttle |\n"
-       "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
+       "| project ms | expand ms | e2e streaming / blocking (matvec/s) | CPU oracle (matvec/s, all cores) | SM MHz, throttle "
+       "| board power, energy per matvec |\n"
+       "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
 print(hdr)
 print("\n".join(rows))

@@ -106,3 +106,31 @@ def test_reference_arm_same_config_and_sample_as_cpu_baseline():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["config"] == json.loads(json.dumps(bench.workload_config(CONFIGS["c2"])))
     assert "leading level-1 diagonal sub-H-matrix of c2" in line["cpu_baseline"]["sample"]
+
+
+def test_clock_sampler_reports_throttle_reasons_and_power():
+    """The clocks object of a bench line from nvidia-smi's CSV samples (the
+    ClockSampler query's column order): median SM clock, the throttle reasons
+    seen in any sample, median board power, the enforced limit."""
+    class _Proc:
+        def terminate(self):
+            pass
+
+        def wait(self, timeout=None):
+            pass
+
+    class _Thread:
+        def join(self, timeout=None):
+            pass
+
+    cs = bench.ClockSampler(0)
+    cs.proc, cs.t = _Proc(), _Thread()
+    assert cs.Q.split(",")[3] == "power.draw" and cs.Q.split(",")[9] == "power.limit"
+    cs.lines = ["0, 1500, 1965, 998.5, 0x4, Not Active, Not Active, Not Active, Active, 1000.00",
+                "0, 1540, 1965, 1001.5, 0x0, Not Active, Not Active, Not Active, Not Active, 1000.00",
+                "0, 1520, 1965, 990.0, 0x4, Not Active, Not Active, Not Active, Active, 1000.00",
+                "garbage"]
+    clk = cs.stop()
+    assert clk["sm_mhz"] == 1520.0 and clk["sm_max_mhz"] == 1965.0 and clk["samples"] == 3
+    assert clk["reasons"] == ["sw_power_cap"]
+    assert clk["power_w"] == 998.5 and clk["power_limit_w"] == 1000.0
