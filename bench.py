@@ -648,8 +648,13 @@ def run_ours(args):
                 "read_stream_source": "scripts/hbm_read_peak.cu sustained bulk-TMA read ring (profiles/r01_hbm_read_peak.txt)"}
 
     value = 1e3 / ms_step  # matvecs/s of the whole job (one operator across all ranks)
-    if clk.get("power_w"):  # board energy per matvec (rank 0's GPU; median power x step time)
+    # board energy per matvec (rank 0's GPU; median power x step time) -- only over a
+    # timed region of >= 2 s: nvidia-smi's power.draw is a 1-s average, which lags a
+    # shorter region (profiles/r02_power_probe.txt)
+    if clk.get("power_w") and ms_total >= 2000.0:
         clk["j_per_matvec"] = clk["power_w"] * ms_step / 1e3
+    elif clk.get("power_w"):
+        clk["power_note"] = "timed region < 2 s: power.draw (1-s average) lags it"
     # bytes of the packed cross-GPU exchange buffer per pass (0 at P = 1), per step
     exch_width = min(nrhs, 64)
     try:
