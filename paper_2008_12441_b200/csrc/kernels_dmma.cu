@@ -261,6 +261,8 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[ks][mt], bf[ks][nt]);
       } else {
+      // (diagnostics, HMAT_DEBUG_SKIP bit 5: the ring without the math -- wrong results)
+      if (!(a.dbg & 32))
 #pragma unroll
       for (int ks = 0; ks < KR / 4; ++ks) {
         double av[MT], bv[NT];
