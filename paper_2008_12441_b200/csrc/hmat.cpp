@@ -927,7 +927,8 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     if (p.L > 0) {  // V-role panels [L][N_loc][Wp], box [1][dkr][vp]
       const uint64_t dims[3] = {uint64_t(p.Wp), uint64_t(n), uint64_t(p.L)};
       const uint64_t strides[2] = {uint64_t(p.Wp) * 8, uint64_t(p.panel_stride) * 8};
-      const uint32_t box[3] = {uint32_t(p.vp), uint32_t(p.dkr), 1};
+      const bool vdiag = (p.dbg & 128) && p.nslice <= 1 && p.Wp <= p.vp;  // (bit 7: diagnostics, kernels_dmma.cu)
+      const uint32_t box[3] = {uint32_t(vdiag ? p.Wp : p.vp), uint32_t(p.dkr), 1};
       hmat_status st3 = encode_map(&a.tm_v, 3, a.V, dims, strides, box);
       if (st3 != HMAT_OK) return st3;
       const uint32_t ubox[3] = {uint32_t(p.dkc + 4), uint32_t(hmat::kDmmaRE), 1};

@@ -167,12 +167,17 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW) project_dmma_kernel(const __
     }
     kr = cb;
   };
+  const bool no_x = (a.dbg & 64) != 0;  // (diagnostics: the ring without its x boxes -- wrong results)
+  // (diagnostics, bit 7: V boxes exactly Wp wide, no out-of-bounds columns -- wrong
+  // results; unsliced panels only, where Wp <= vp and the box fits the slot)
+  const uint32_t vtx = static_cast<uint32_t>((a.dbg & 128) && NSL == 1 && Wp <= VP ? (int64_t)KR * Wp * 8 : vbytes);
   auto issue = [&](int sl) {  // one thread: the next stage into slot sl
-    dev::mbar_arrive_expect_tx(&full[sl], stage_tx);
+    dev::mbar_arrive_expect_tx(&full[sl], no_x ? vtx : stage_tx - static_cast<uint32_t>(vbytes) + vtx);
     dev::tma_load_3d(smem + sl * a.stage_bytes_p, &a.tm_v, c0, static_cast<int>(kr * KR), lr - 1, &full[sl],
                      pol_stream);
-    dev::tma_load_2d(smem + sl * a.stage_bytes_p + vbytes, &a.tm_x, static_cast<int>(kr * KR), 0, &full[sl],
-                     pol_keep);
+    if (!no_x)
+      dev::tma_load_2d(smem + sl * a.stage_bytes_p + vbytes, &a.tm_x, static_cast<int>(kr * KR), 0, &full[sl],
+                       pol_keep);
   };
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {

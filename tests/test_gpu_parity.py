@@ -590,6 +590,26 @@ def test_power_iteration_back_to_back_products(monkeypatch):
     assert np.linalg.norm(outs[1] - ref) <= 1e-11 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("width", [8, 16])
+@pytest.mark.parametrize("mask", [1 << 2, 1 << 4, 0b10100, 0b01011])
+def test_dmma_project_level_chunks_masked(mask, width, monkeypatch):
+    """Level-interleaved chunks with a level mask (hmat_matvec_parts): a single
+    active level (its next (chunk, level) is itself, whose running sums of the
+    chunk are saved only at the level's end) and non-adjacent levels; the
+    tensor-core project loads the next level's sums one level ahead.  Parity with
+    the oracle's parts and bit-identical to the unchunked order."""
+    cfg = HConfig("ckm", d=2, L=5, b=64, r=16, seed=515)                              # W = 48
+    nrhs = 8 if width == 8 else 13
+    U, V, D, x = host_case(cfg, nrhs)
+    ref = oracle.matvec(cfg.d, cfg.L, cfg.b, cfg.r, U, V, D, x, level_mask=mask, dense=False)
+    outs = []
+    for ch in (3, 0):
+        monkeypatch.setenv("HMAT_DMMA_PCHUNK" if width == 8 else "HMAT_DMMA_PCHUNK16", str(ch))
+        outs.append(gpu_matvec(cfg, U, V, D, x, level_mask=mask, dense=False))
+    assert_parity(outs[0], ref)
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("cfg", [HConfig("ck48", d=2, L=5, b=64, r=16, seed=511),    # W = 48
                                  HConfig("ck16", d=1, L=11, b=64, r=16, seed=512),   # W = 16
                                  HConfig("ck80", d=1, L=10, b=128, r=80, seed=513),  # W = 80
