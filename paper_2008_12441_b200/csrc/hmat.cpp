@@ -1062,10 +1062,14 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
     a.nr = nr;
     a.x = xd + c0 * ldx;
     a.y = yd + c0 * n;
-    // expand's dynamic chunks of 1 item (0 = static ranges: for standard
-    // admissibility, where the static ranges measured faster (s2: 4.0 vs 4.5 ms),
-    // and when an item has no stage at all, which the chunk protocol needs)
-    a.chunk_e = p.expand_chunk >= 0 ? p.expand_chunk : (p.adm ? 0 : 1);
+    // expand's dynamic chunks of 1 item, 2 for standard admissibility (s2: 3.81 ->
+    // 3.75 ms against static ranges, 3.89 with chunks of 1; A/B late r02); 0 =
+    // static ranges when an item may have no stage at all (the chunk protocol
+    // carries the chunk id in a chunk's first stage): no dense block and, under
+    // standard admissibility, no active level >= 2 (level 1 holds no blocks)
+    const uint64_t lv_all = p.L >= 64 ? ~0ull : (1ull << p.L) - 1;
+    const bool std_stage = dense || (level_mask & lv_all & ~1ull);
+    a.chunk_e = p.expand_chunk >= 0 ? p.expand_chunk : (p.adm ? (std_stage ? 2 : 0) : 1);
     if (!level_mask && !dense) a.chunk_e = 0;
     // project: the last active level in dynamic chunks of whole nodes (>= 4
     // stages), when it is local (no exchange) and has at least 2 chunks per CTA
