@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 rows = []
 for c in ["c1", "c2", "c3", "c4", "c5", "s2", "c2strict", "c2r2", "c2r4", "c2r8", "c2r16", "c4r2", "c4r4", "c4r8", "c4r16", "s2r16",
-          "c4_long", "c4r16_long"]:
+          "c4_long", "c4r8_long", "c4r16_long", "c5_long"]:
     p = os.path.join(ROOT, "profiles", f"{rnd}_bench_{c}.json")
     if not os.path.exists(p):
         continue
