@@ -638,6 +638,12 @@ def run_ours(args):
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(cfg.name, dom),
                 "peak_source": "measured FP64 DMMA m8n8k4 peak on this pool (profiles/r01_fp64_peak.txt)",
                 "per_kernel": per_kernel}
+        # the DMMA peak scales with the SM clock; under the board's power cap the
+        # timed region runs below the clock the peak was measured at (1965 MHz)
+        if clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+            at_clk = FP64_PEAK_TFLOPS * clk["sm_mhz"] / clk["sm_max_mhz"]
+            roof["peak_at_clock"] = at_clk
+            roof["frac_at_clock"] = achieved / at_clk
     else:
         peak, peak_src = measured_peaks()
         achieved = per_kernel[dom]["GBps"]
