@@ -974,6 +974,7 @@ hmat_status run(hmat_t H, int trans, double alpha, const double* x, double beta,
       a.pchunk = nb == 8 && p.W <= 112 ? p.dmma_pchunk : nb == 16 && p.W <= 112 ? p.dmma_pchunk16 : 0;
       a.nstage_p = dl.dns_p;
       a.stage_bytes_p = dl.dstage_p;
+      a.grid_e_gen = dl.dgrid_e_gen;
       a.bar_off_p = dl.dns_p * dl.dstage_p;
       a.nstage_e = dl.dns_e;
       a.stage_bytes_e = dl.dstage_e;

@@ -92,6 +92,7 @@ struct StreamArgs {
   int wslice, nslice;        // tensor-core project: column slices of the panel (gridDim.y = nslice)
   int aflush;                // project: asynchronous node flushes (HMAT_PROJECT_AFLUSH)
   int dmma_upol;             // tensor-core expand: L2 policy of the U / D boxes (HMAT_DMMA_UPOL)
+  int grid_e_gen;            // tensor-core expand: grid of the general variant (<= the plan's grid)
   int64_t pchunk;            // tensor-core project: stages per chunk of the level interleave (0 = off)
   double* accbuf;            // tensor-core project: [grid][L][W NB] running sums between chunks
   const double* zex_base;    // local exchange buffer (offsets of the exchange levels)

@@ -808,8 +808,8 @@ void launch_e_kc(const StreamArgs& a, int grid, int64_t smem, cudaStream_t s) {
   const bool wf = !a.adm && a.dense && (a.level_mask & all_lv) == all_lv && !(a.dbg & 16);
   if (wf)
     launch_e_wf<KC, NB, true>(a, grid, smem, s);
-  else
-    launch_e_wf<KC, NB, false>(a, grid, smem, s);
+  else  // (the general variant's ~100 registers fit 2 CTAs per SM: a grid of 3 per SM would run a second wave)
+    launch_e_wf<KC, NB, false>(a, a.grid_e_gen > 0 && a.grid_e_gen < grid ? a.grid_e_gen : grid, smem, s);
 }
 
 template <int NB>

@@ -305,6 +305,7 @@ std::string plan_build(int depth, int dim, int leaf, int rank, int P, int shard,
       d.dsmem_e = d.dns_e * d.dstage_e + bar_bytes;
       d.dgrid_p = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas, depth > 0 ? p.N_loc / p.dkr : 0));
       d.dgrid_e = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * ctas_e, p.N_loc / kDmmaRE));
+      d.dgrid_e_gen = static_cast<int>(std::min<int64_t>(int64_t(opt.num_sms) * std::min(ctas_e, 2), p.N_loc / kDmmaRE));
       // (a 32-wide project pass with W % 32 != 0 needs the 8-warp grid: kernels_dmma.cu)
       const bool narrow_on = d.nb == kDmmaNB || (d.nb == 32   ? opt.dmma_narrow >= 1
                                                  : d.nb == 16 ? opt.dmma_narrow >= 2

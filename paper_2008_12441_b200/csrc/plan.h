@@ -96,6 +96,8 @@ struct Plan {
     int dns_p = 0, dns_e = 0;
     int64_t dstage_p = 0, dstage_e = 0, dsmem_p = 0, dsmem_e = 0;
     int dgrid_p = 0, dgrid_e = 0;
+    int dgrid_e_gen = 0;            // expand grid of the general (not plain-product) variant: its
+                                    // registers fit 2 CTAs per SM, not 3 (kernels_dmma.cu)
   } dl[4];                          // pass widths 16, 32, 64, and (dl[3]) 8
   int dgrid_p_max = 0;              // partial-sum / ticket slots to allocate (max over dl)
   // the layout of a pass of `nr` right-hand sides: the narrowest that holds them
